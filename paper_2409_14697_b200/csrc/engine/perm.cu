@@ -1,0 +1,260 @@
+// Data-movement and reduction kernels (sm_100a): IMS, XRS slab swap / window
+// copies, norm, basis init, whole-slice diagonal tables.
+//
+//   k_ims          replaces imsSwap (proj/src/engine.cpp:86-101)
+//   k_slab_swap    replaces xrsFill + xrsDeliver for slices in one process
+//                  (proj/src/distributed.cpp:76-120): in-place pairwise swap, no buffer
+//   k_window_pack / k_window_unpack
+//                  the NCCL path's send pack / copy-back (distributed.cpp:76-120)
+//   k_norm_*       StateVector::norm (engine.cpp:12-16), deterministic tree order
+//   k_set_basis    initState (engine.cpp:18-28) after a memset
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace qkdev {
+
+struct PairSpec {
+    int s;
+    int out[40];
+    int in[40];
+};
+
+// x with bits out[j] <-> in[j] exchanged (a GF(2)-linear bit permutation).
+__device__ __forceinline__ uint64_t bitswapDev(uint64_t x, const PairSpec& p) {
+    for (int j = 0; j < p.s; j++) {
+        const uint64_t d = ((x >> p.out[j]) ^ (x >> p.in[j])) & 1u;
+        x ^= (d << p.out[j]) | (d << p.in[j]);
+    }
+    return x;
+}
+
+// In-place a[bitswap(i)] <- a[i].  Thread t owns x = t | (k << logT) for
+// k = 0..; bitswap is linear, so P(x) = P(t) ^ P(k << logT), and P(k << logT)
+// is advanced incrementally from a table of P(trailing-ones masks): a handful
+// of integer ops per element instead of 5 per pair.  Each orbit {x, P(x)} is
+// swapped once, by its smaller member (the reference swaps from the larger
+// one; the permutation is the same).
+__global__ void __launch_bounds__(256) k_ims(double2* __restrict__ a, int logN, int logT, const __grid_constant__ PairSpec p) {
+    __shared__ uint64_t steps[64];
+    const int hiBits = logN - logT;
+    if (threadIdx.x < hiBits + 1) {
+        const int j = threadIdx.x;  // mask of (j+1) trailing ones, shifted to the high part
+        const uint64_t m = (j + 1 >= 64) ? ~uint64_t(0) : ((uint64_t(1) << (j + 1)) - 1);
+        steps[j] = bitswapDev(m << logT, p);
+    }
+    __syncthreads();
+    const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    uint64_t px = bitswapDev(t, p);  // P(t | 0)
+    const uint64_t K = uint64_t(1) << hiBits;
+    uint64_t k = 0;
+    while (k < K) {
+        // 4 independent elements per trip for memory-level parallelism.
+        uint64_t xs[4], ys[4];
+        int n = 0;
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            if (k < K) {
+                xs[u] = t | (k << logT);
+                ys[u] = px;
+                n = u + 1;
+                const int tz = __ffsll((long long)(~k)) - 1;  // trailing ones of k
+                if (k + 1 < K) px ^= steps[tz];
+                k++;
+            }
+        }
+        double2 vx[4], vy[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+            if (u < n && xs[u] < ys[u]) {
+                vx[u] = a[xs[u]];
+                vy[u] = a[ys[u]];
+            }
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+            if (u < n && xs[u] < ys[u]) {
+                a[xs[u]] = vy[u];
+                a[ys[u]] = vx[u];
+            }
+    }
+}
+
+// Offsets of a slab element: o deposited around the (ascending) out positions.
+struct SlabSpec {
+    int s;
+    int outs[8];   // ascending
+};
+
+__device__ __forceinline__ uint64_t depositAround(uint64_t o, const SlabSpec& sp) {
+    for (int j = 0; j < sp.s; j++) {
+        const int p = sp.outs[j];
+        o = ((o >> p) << (p + 1)) | (o & ((uint64_t(1) << p) - 1));
+    }
+    return o;
+}
+
+// Swap slab elements pairwise: A[dep(o)] <-> B[dep(o)] for o < count, where A
+// and B already point at their slab's bit pattern (may be peer memory).
+__global__ void __launch_bounds__(256) k_slab_swap(double2* A, double2* B, uint64_t count, const __grid_constant__ SlabSpec sp) {
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t o = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; o < count; o += stride) {
+        const uint64_t i = depositAround(o, sp);
+        const double2 x = A[i], y = B[i];
+        A[i] = y;
+        B[i] = x;
+    }
+}
+
+// buf[o - w0] = S[dep(o)] for o in [w0, w0 + cnt)  (S points at the slab pattern)
+__global__ void __launch_bounds__(256) k_window_pack(double2* __restrict__ buf, const double2* __restrict__ S, uint64_t w0,
+                                                     uint64_t cnt, const __grid_constant__ SlabSpec sp) {
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t o = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; o < cnt; o += stride)
+        buf[o] = S[depositAround(w0 + o, sp)];
+}
+
+__global__ void __launch_bounds__(256) k_window_unpack(double2* __restrict__ S, const double2* __restrict__ buf,
+                                                       uint64_t w0, uint64_t cnt, const __grid_constant__ SlabSpec sp) {
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t o = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; o < cnt; o += stride)
+        S[depositAround(w0 + o, sp)] = buf[o];
+}
+
+// a[i] *= tab[sub(i)], sub bit (k-1-j) = bit tgt[j] of i: fused diagonals wider
+// than a tile (k > 13 when chunk_qbit > 13).
+struct DiagSpec {
+    int k;
+    int tgt[40];
+};
+__global__ void __launch_bounds__(256) k_diag_table(double2* __restrict__ a, const double2* __restrict__ tab, uint64_t n,
+                                                    const __grid_constant__ DiagSpec d) {
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        uint64_t sub = 0;
+        for (int j = 0; j < d.k; j++) sub |= ((i >> d.tgt[j]) & 1u) << (d.k - 1 - j);
+        const double2 c = __ldg(tab + sub), x = a[i];
+        a[i] = make_double2(fma(x.x, c.x, -x.y * c.y), fma(x.x, c.y, x.y * c.x));
+    }
+}
+
+// ---- norm: per-thread compensated sums, fixed-order tree per block, then one
+// block folds the partials in index order (bitwise deterministic).
+__device__ __forceinline__ void twoSum(double& s, double& c, double x) {
+    const double t = s + x;
+    const double bp = t - s;
+    c += (s - (t - bp)) + (x - bp);
+    s = t;
+}
+
+__global__ void __launch_bounds__(256) k_norm_partial(const double2* __restrict__ a, uint64_t n, double* __restrict__ part) {
+    __shared__ double ss[256], sc[256];
+    const uint64_t per = (n + gridDim.x - 1) / gridDim.x;
+    const uint64_t lo = per * blockIdx.x, hi = lo + per < n ? lo + per : n;
+    double s = 0, c = 0;
+    for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        const double2 x = a[i];
+        twoSum(s, c, fma(x.x, x.x, x.y * x.y));
+    }
+    ss[threadIdx.x] = s;
+    sc[threadIdx.x] = c;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) {
+            double s2 = ss[threadIdx.x], c2 = sc[threadIdx.x] + sc[threadIdx.x + w];
+            twoSum(s2, c2, ss[threadIdx.x + w]);
+            ss[threadIdx.x] = s2;
+            sc[threadIdx.x] = c2;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        part[2 * blockIdx.x] = ss[0];
+        part[2 * blockIdx.x + 1] = sc[0];
+    }
+}
+
+__global__ void k_norm_final(const double* __restrict__ part, int nb, double* __restrict__ out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double s = 0, c = 0;
+        for (int b = 0; b < nb; b++) {
+            twoSum(s, c, part[2 * b]);
+            c += part[2 * b + 1];
+        }
+        out[0] = s + c;
+    }
+}
+
+__global__ void k_set_basis(double2* a, uint64_t idx) { a[idx] = make_double2(1.0, 0.0); }
+
+// ---- launchers ----------------------------------------------------------------
+
+static unsigned gridFor(uint64_t work, unsigned threads, unsigned cap) {
+    uint64_t g = (work + threads - 1) / threads;
+    if (g > cap) g = cap;
+    return unsigned(g ? g : 1);
+}
+
+cudaError_t launchIms(double2* a, int logN, const int* outs, const int* ins, int s, cudaStream_t st) {
+    PairSpec p{};
+    p.s = s;
+    for (int j = 0; j < s; j++) {
+        p.out[j] = outs[j];
+        p.in[j] = ins[j];
+    }
+    // 2^logT threads, each walking 2^(logN-logT) elements.
+    int logT = logN < 20 ? logN : 20;
+    if (logT < 0) logT = 0;
+    const uint64_t T = uint64_t(1) << logT;
+    const unsigned threads = T < 256 ? unsigned(T) : 256u;
+    k_ims<<<unsigned(T / threads), threads, 0, st>>>(a, logN, logT, p);
+    return cudaGetLastError();
+}
+
+cudaError_t launchSlabSwap(double2* A, double2* B, uint64_t count, const int* outsSorted, int s, cudaStream_t st) {
+    SlabSpec sp{};
+    sp.s = s;
+    for (int j = 0; j < s; j++) sp.outs[j] = outsSorted[j];
+    k_slab_swap<<<gridFor(count, 256, 148 * 16), 256, 0, st>>>(A, B, count, sp);
+    return cudaGetLastError();
+}
+
+cudaError_t launchWindowPack(double2* buf, const double2* S, uint64_t w0, uint64_t cnt, const int* outsSorted, int s,
+                             cudaStream_t st) {
+    SlabSpec sp{};
+    sp.s = s;
+    for (int j = 0; j < s; j++) sp.outs[j] = outsSorted[j];
+    k_window_pack<<<gridFor(cnt, 256, 148 * 16), 256, 0, st>>>(buf, S, w0, cnt, sp);
+    return cudaGetLastError();
+}
+
+cudaError_t launchWindowUnpack(double2* S, const double2* buf, uint64_t w0, uint64_t cnt, const int* outsSorted, int s,
+                               cudaStream_t st) {
+    SlabSpec sp{};
+    sp.s = s;
+    for (int j = 0; j < s; j++) sp.outs[j] = outsSorted[j];
+    k_window_unpack<<<gridFor(cnt, 256, 148 * 16), 256, 0, st>>>(S, buf, w0, cnt, sp);
+    return cudaGetLastError();
+}
+
+cudaError_t launchDiagTable(double2* a, const double2* tab, uint64_t n, const int* tgt, int k, cudaStream_t st) {
+    DiagSpec d{};
+    d.k = k;
+    for (int j = 0; j < k; j++) d.tgt[j] = tgt[j];
+    k_diag_table<<<gridFor(n, 256, 148 * 16), 256, 0, st>>>(a, tab, n, d);
+    return cudaGetLastError();
+}
+
+constexpr int kNormBlocks = 1184;  // 148 SMs x 8
+
+cudaError_t launchNorm(const double2* a, uint64_t n, double* scratch, double* out, cudaStream_t st) {
+    k_norm_partial<<<kNormBlocks, 256, 0, st>>>(a, n, scratch);
+    k_norm_final<<<1, 32, 0, st>>>(scratch, kNormBlocks, out);
+    return cudaGetLastError();
+}
+size_t normScratchDoubles() { return 2 * kNormBlocks; }
+
+cudaError_t launchSetBasis(double2* a, uint64_t idx, cudaStream_t st) {
+    k_set_basis<<<1, 1, 0, st>>>(a, idx);
+    return cudaGetLastError();
+}
+
+}  // namespace qkdev

@@ -1,0 +1,898 @@
+// Runtime + C-ABI (include/qk.h): device-resident rank slices, program
+// compilation cache, the item dispatcher, XRS over NCCL or peer memory.
+//
+// Replaces the reference's L5/L6 drivers: simulateProgram
+// (proj/src/engine.cpp:283-297), spawnRanks / xrsSwap / planXrs
+// (proj/src/distributed.cpp:25-206).  There is no CPU fallback: every
+// amplitude update is a kernel from block_pass.cu / perm.cu; without a CUDA
+// device the calls fail with QK_ERR_SIM.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "qk.h"
+#include "quokka/circuit.hpp"
+#include "quokka/optimizer.hpp"
+#include "quokka/tools.hpp"
+#include "schedule.h"
+
+namespace qkdev {
+cudaError_t launchBlockPass(double2*, const double2*, const PassParams&, int, cudaStream_t);
+cudaError_t launchDenseGroup(double2*, const double2*, int, const int*, uint64_t, int, cudaStream_t);
+cudaError_t launchIms(double2*, int, const int*, const int*, int, cudaStream_t);
+cudaError_t launchSlabSwap(double2*, double2*, uint64_t, const int*, int, cudaStream_t);
+cudaError_t launchWindowPack(double2*, const double2*, uint64_t, uint64_t, const int*, int, cudaStream_t);
+cudaError_t launchWindowUnpack(double2*, const double2*, uint64_t, uint64_t, const int*, int, cudaStream_t);
+cudaError_t launchDiagTable(double2*, const double2*, uint64_t, const int*, int, cudaStream_t);
+cudaError_t launchNorm(const double2*, uint64_t, double*, double*, cudaStream_t);
+size_t normScratchDoubles();
+cudaError_t launchSetBasis(double2*, uint64_t, cudaStream_t);
+}  // namespace qkdev
+
+using quokka::ConfigError;
+using quokka::Index;
+using quokka::ParseError;
+using quokka::SimulationError;
+
+namespace {
+
+thread_local std::string g_lastError;
+
+void cuda(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw SimulationError(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+void nccl(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) throw SimulationError(std::string("NCCL error in ") + what + ": " + ncclGetErrorString(r));
+}
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return QK_OK;
+    } catch (const ParseError& e) {
+        g_lastError = e.what();
+        return QK_ERR_PARSE;
+    } catch (const ConfigError& e) {
+        g_lastError = e.what();
+        return QK_ERR_CONFIG;
+    } catch (const SimulationError& e) {
+        g_lastError = e.what();
+        return QK_ERR_SIM;
+    } catch (const std::exception& e) {
+        g_lastError = e.what();
+        return QK_ERR_SIM;
+    }
+}
+
+char* dupText(const std::string& s) {
+    char* p = static_cast<char*>(std::malloc(s.size() + 1));
+    std::memcpy(p, s.data(), s.size() + 1);
+    return p;
+}
+
+quokka::Config toConfig(const qk_config& c) {
+    quokka::Config q;
+    q.totalQubits = c.total_qubits;
+    q.rankQubits = c.rank_qubits;
+    q.bufferQubits = c.buffer_qubits;
+    q.chunkQubits = c.chunk_qubits;
+    q.fusionQubits = c.fusion_qubits;
+    q.cacheLineQubits = c.cache_line_qubits;
+    q.imsEnabled = c.ims != 0;
+    q.xrsEnabled = c.xrs != 0;
+    q.fusionEnabled = c.fusion != 0;
+    q.diagonalFusionEnabled = c.diagonal_fusion != 0;
+    return q;
+}
+
+qk_config fromConfig(const quokka::Config& q) {
+    qk_config c;
+    c.total_qubits = q.totalQubits;
+    c.rank_qubits = q.rankQubits;
+    c.buffer_qubits = q.bufferQubits;
+    c.chunk_qubits = q.chunkQubits;
+    c.fusion_qubits = q.fusionQubits;
+    c.cache_line_qubits = q.cacheLineQubits;
+    c.ims = q.imsEnabled;
+    c.xrs = q.xrsEnabled;
+    c.fusion = q.fusionEnabled;
+    c.diagonal_fusion = q.diagonalFusionEnabled;
+    return c;
+}
+
+// ---- XRS plan (distributed.cpp:25-71 semantics) ------------------------------
+
+struct XrsPlan {
+    std::vector<int> outs, insRel;  // ascending outs, rank-bit indices
+    int s = 0;
+    Index slabOffsets = 0, window = 0, rounds = 0;
+};
+
+XrsPlan planXrs(const quokka::SwapOp& op, int n, int R, int B) {
+    if (op.kind != quokka::SwapOp::CrossRank) throw SimulationError("xrsSwap needs a cross-rank swap op");
+    const int region = n - R;
+    XrsPlan p;
+    for (const auto& [o, i] : op.pairs) {
+        if (o < 0 || o >= region || i < region || i >= n)
+            throw SimulationError("cross-rank swap positions out of range");
+        p.outs.push_back(o);
+        p.insRel.push_back(i - region);
+    }
+    p.s = int(op.pairs.size());
+    if (B < p.s) throw SimulationError("exchange buffer smaller than one amplitude per slab");
+    p.slabOffsets = Index(1) << (region - p.s);
+    p.window = std::min(p.slabOffsets, Index(1) << (B - p.s));
+    p.rounds = (p.slabOffsets + p.window - 1) / p.window;
+    return p;
+}
+
+int ownSlab(int rank, const XrsPlan& p) {
+    int v = 0;
+    for (int j = 0; j < p.s; j++) v |= ((rank >> p.insRel[size_t(j)]) & 1) << j;
+    return v;
+}
+
+int partnerOf(int rank, int slab, const XrsPlan& p) {
+    for (int j = 0; j < p.s; j++) {
+        rank &= ~(1 << p.insRel[size_t(j)]);
+        rank |= ((slab >> j) & 1) << p.insRel[size_t(j)];
+    }
+    return rank;
+}
+
+Index slabBits(int slab, const XrsPlan& p) {
+    Index b = 0;
+    for (int j = 0; j < p.s; j++) b |= Index((slab >> j) & 1) << p.outs[size_t(j)];
+    return b;
+}
+
+// This rank's message schedule for one CSQS: per window round, for every slab
+// pa != own, send slab pa's window to the rank whose swapped bits equal pa and
+// receive that rank's slab `own` window into receive-buffer section `sec`,
+// which is copied back into slab pa (distributed.cpp:76-120).  The NCCL path
+// executes exactly this list; tests/test_xrs_plan.py executes it over gloo.
+std::vector<qk_xrs_msg> xrsMessages(const XrsPlan& p, int rank) {
+    std::vector<qk_xrs_msg> out;
+    if (p.s == 0) return out;
+    const int own = ownSlab(rank, p), slabs = 1 << p.s;
+    int round = 0;
+    for (Index w0 = 0; w0 < p.slabOffsets; w0 += p.window, round++) {
+        const Index cnt = std::min(p.window, p.slabOffsets - w0);
+        for (int pa = 0, sec = 0; pa < slabs; pa++) {
+            if (pa == own) continue;
+            out.push_back(qk_xrs_msg{round, partnerOf(rank, pa, p), pa, sec++, w0, cnt});
+        }
+    }
+    return out;
+}
+
+// The reference's RankStats accounting for one CSQS (distributed.cpp:87-93, 116-119).
+void accountXrs(const XrsPlan& p, qk_xrs_stats* st) {
+    if (!st) return;
+    const Index other = (Index(1) << p.s) - 1;
+    st->bytes_sent += other * p.slabOffsets * 16;
+    st->bytes_received += other * p.slabOffsets * 16;
+    st->peak_buffer_bytes = std::max<uint64_t>(st->peak_buffer_bytes, other * p.window * 16);
+    st->rounds += p.rounds;
+}
+
+// ---- compiled programs ----------------------------------------------------------
+
+struct CompiledItem {
+    enum Kind { Block, Ims, Xrs } kind = Block;
+    std::vector<qkeng::Step> steps;  // Block
+    std::vector<int> outs, ins;      // Ims / Xrs
+    double flopsPerAmp = 0;
+    uint64_t denseTargetsOff = 0;    // int offset into the device target table
+};
+
+struct Compiled {
+    int nLocal = 0;
+    std::vector<CompiledItem> items;
+    std::vector<double> gtab;     // host copy of device tables
+    std::vector<int> targets;     // dense-group target lists
+};
+
+struct DeviceTables {
+    double2* gtab = nullptr;
+    int* targets = nullptr;
+};
+
+}  // namespace
+
+struct qk_program {
+    quokka::Program prog;
+    std::mutex mu;
+    std::map<int, std::shared_ptr<Compiled>> compiled;            // by nLocal
+    std::map<std::pair<int, int>, DeviceTables> tables;           // (nLocal, device)
+    ~qk_program() {
+        for (auto& kv : tables) {
+            int prev = 0;
+            cudaGetDevice(&prev);
+            cudaSetDevice(kv.first.second);
+            cudaFree(kv.second.gtab);
+            cudaFree(kv.second.targets);
+            cudaSetDevice(prev);
+        }
+    }
+};
+
+struct qk_state {
+    int n = 0, R = 0, rank = 0, B = 0, device = 0, nLocal = 0;
+    uint64_t count = 0;
+    double2* amps = nullptr;
+    cudaStream_t stream = nullptr;
+    double* normScratch = nullptr;
+    double* normOut = nullptr;
+    double2* recvBuf = nullptr;
+    double2* packBuf = nullptr;
+    uint64_t bufAmps = 0;
+    ncclComm_t comm = nullptr;
+    bool profiling = false;
+    qk_run_stats last{};
+};
+
+namespace {
+
+struct DeviceGuard {
+    int prev = 0;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+std::shared_ptr<Compiled> compileFor(qk_program* p, int nLocal) {
+    std::lock_guard<std::mutex> lk(p->mu);
+    auto it = p->compiled.find(nLocal);
+    if (it != p->compiled.end()) return it->second;
+    auto c = std::make_shared<Compiled>();
+    c->nLocal = nLocal;
+    for (const quokka::ProgramItem& item : p->prog.items) {
+        CompiledItem ci;
+        if (item.type == quokka::ProgramItem::Block) {
+            ci.kind = CompiledItem::Block;
+            ci.steps = qkeng::compileBlock(item.block.gates, nLocal, c->gtab);
+            for (qkeng::Step& s : ci.steps) {
+                ci.flopsPerAmp += s.flopsPerAmp;
+                if (s.kind != qkeng::Step::Pass) {
+                    const uint64_t off = c->targets.size();
+                    c->targets.insert(c->targets.end(), s.targets.begin(), s.targets.end());
+                    s.targets.insert(s.targets.begin(), int(off));  // [0] = device offset
+                }
+            }
+        } else {
+            ci.kind = item.swap.kind == quokka::SwapOp::InMemory ? CompiledItem::Ims : CompiledItem::Xrs;
+            for (const auto& [o, i] : item.swap.pairs) {
+                ci.outs.push_back(o);
+                ci.ins.push_back(i);
+            }
+        }
+        c->items.push_back(std::move(ci));
+    }
+    p->compiled[nLocal] = c;
+    return c;
+}
+
+DeviceTables tablesFor(qk_program* p, const Compiled& c, int device) {
+    std::lock_guard<std::mutex> lk(p->mu);
+    auto key = std::make_pair(c.nLocal, device);
+    auto it = p->tables.find(key);
+    if (it != p->tables.end()) return it->second;
+    DeviceTables t;
+    DeviceGuard g(device);
+    const size_t gbytes = std::max<size_t>(16, c.gtab.size() * sizeof(double));
+    cuda(cudaMalloc(&t.gtab, gbytes), "cudaMalloc(gtab)");
+    if (!c.gtab.empty()) cuda(cudaMemcpy(t.gtab, c.gtab.data(), c.gtab.size() * sizeof(double), cudaMemcpyHostToDevice), "upload gtab");
+    const size_t tbytes = std::max<size_t>(4, c.targets.size() * sizeof(int));
+    cuda(cudaMalloc(&t.targets, tbytes), "cudaMalloc(targets)");
+    if (!c.targets.empty()) cuda(cudaMemcpy(t.targets, c.targets.data(), c.targets.size() * sizeof(int), cudaMemcpyHostToDevice), "upload targets");
+    p->tables[key] = t;
+    return t;
+}
+
+// Profiling: CUDA events on the state's stream around each launch class.
+struct Timer {
+    qk_state* st;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[3];
+    explicit Timer(qk_state* s) : st(s) {}
+    template <class F>
+    void time(int cls, F&& f) {
+        if (!st->profiling) {
+            f();
+            return;
+        }
+        cudaEvent_t a, b;
+        cuda(cudaEventCreate(&a), "event");
+        cuda(cudaEventCreate(&b), "event");
+        cuda(cudaEventRecord(a, st->stream), "event record");
+        f();
+        cuda(cudaEventRecord(b, st->stream), "event record");
+        ev[cls].emplace_back(a, b);
+    }
+    void collect(double out[3]) {
+        for (int c = 0; c < 3; c++) {
+            out[c] = 0;
+            for (auto& [a, b] : ev[c]) {
+                float ms = 0;
+                cudaEventSynchronize(b);
+                cudaEventElapsedTime(&ms, a, b);
+                out[c] += ms;
+                cudaEventDestroy(a);
+                cudaEventDestroy(b);
+            }
+            ev[c].clear();
+        }
+    }
+};
+
+void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_run_stats& rs) {
+    for (const qkeng::Step& s : ci.steps) {
+        if (s.kind == qkeng::Step::Pass) {
+            cuda(qkdev::launchBlockPass(st->amps, t.gtab, *s.pass, st->nLocal, st->stream), "block pass");
+        } else if (s.kind == qkeng::Step::DiagTable) {
+            cuda(qkdev::launchDiagTable(st->amps, t.gtab + s.matOff, st->count, s.targets.data() + 1, s.k, st->stream),
+                 "diag table");
+        } else {
+            uint64_t mask = 0;
+            for (size_t j = 1; j < s.targets.size(); j++) mask |= uint64_t(1) << s.targets[j];
+            cuda(qkdev::launchDenseGroup(st->amps, t.gtab + s.matOff, s.k, t.targets + s.targets[0], mask, st->nLocal,
+                                         st->stream),
+                 "dense group");
+        }
+        rs.kernel_launches++;
+        rs.block_launches++;
+    }
+    rs.block_bytes += 32.0 * double(st->count) * double(ci.steps.size());
+    rs.block_flops += ci.flopsPerAmp * double(st->count);
+}
+
+void runIms(qk_state* st, const std::vector<int>& outs, const std::vector<int>& ins, qk_run_stats& rs) {
+    if (outs.empty()) return;
+    cuda(qkdev::launchIms(st->amps, st->nLocal, outs.data(), ins.data(), int(outs.size()), st->stream), "ims");
+    rs.kernel_launches++;
+    rs.ims_launches++;
+    rs.ims_bytes += 32.0 * double(st->count) * (1.0 - std::ldexp(1.0, -int(outs.size())));
+}
+
+void ensureXrsBuffers(qk_state* st, uint64_t amps, bool pack) {
+    if (st->bufAmps < amps) {
+        DeviceGuard g(st->device);
+        cudaFree(st->recvBuf);
+        cudaFree(st->packBuf);
+        st->recvBuf = st->packBuf = nullptr;
+        cuda(cudaMalloc(&st->recvBuf, amps * sizeof(double2)), "cudaMalloc(recv buffer)");
+        st->bufAmps = amps;
+    }
+    if (pack && !st->packBuf) cuda(cudaMalloc(&st->packBuf, st->bufAmps * sizeof(double2)), "cudaMalloc(pack buffer)");
+}
+
+// NCCL XRS for this rank (one process per GPU): per window round, one grouped
+// ncclSend/ncclRecv per partner into a single receive buffer, then copy-back.
+void runXrsNccl(qk_state* st, const XrsPlan& p, qk_run_stats& rs) {
+    if (!st->comm) throw SimulationError("cross-rank swap needs a communicator (qk_comm_init) or qk_simulate_local");
+    if (p.s == 0) return;
+    const int region = st->nLocal, slabs = 1 << p.s, own = ownSlab(st->rank, p);
+    bool contiguous = true;  // AIO staging: outs are the top S in-rank positions
+    for (int j = 0; j < p.s; j++) contiguous &= p.outs[size_t(j)] == region - p.s + j;
+    (void)own;
+    ensureXrsBuffers(st, uint64_t(slabs - 1) * p.window, !contiguous);
+    const std::vector<qk_xrs_msg> msgs = xrsMessages(p, st->rank);
+    for (size_t a = 0; a < msgs.size();) {
+        size_t b = a;
+        while (b < msgs.size() && msgs[b].round == msgs[a].round) b++;  // one window round
+        if (!contiguous)
+            for (size_t m = a; m < b; m++) {
+                cuda(qkdev::launchWindowPack(st->packBuf + uint64_t(msgs[m].section) * msgs[m].count,
+                                             st->amps + slabBits(msgs[m].slab, p), msgs[m].w0, msgs[m].count,
+                                             p.outs.data(), p.s, st->stream),
+                     "xrs pack");
+                rs.kernel_launches++;
+            }
+        nccl(ncclGroupStart(), "ncclGroupStart");
+        for (size_t m = a; m < b; m++) {
+            const qk_xrs_msg& x = msgs[m];
+            const double2* src = contiguous ? st->amps + slabBits(x.slab, p) + x.w0
+                                            : st->packBuf + uint64_t(x.section) * x.count;
+            nccl(ncclSend(src, 2 * x.count, ncclDouble, x.peer, st->comm, st->stream), "ncclSend");
+            nccl(ncclRecv(st->recvBuf + uint64_t(x.section) * x.count, 2 * x.count, ncclDouble, x.peer, st->comm,
+                          st->stream),
+                 "ncclRecv");
+        }
+        nccl(ncclGroupEnd(), "ncclGroupEnd");
+        for (size_t m = a; m < b; m++) {
+            const qk_xrs_msg& x = msgs[m];
+            cuda(qkdev::launchWindowUnpack(st->amps + slabBits(x.slab, p), st->recvBuf + uint64_t(x.section) * x.count,
+                                           x.w0, x.count, p.outs.data(), p.s, st->stream),
+                 "xrs copy-back");
+            rs.kernel_launches++;
+        }
+        rs.xrs_rounds++;
+        a = b;
+    }
+    rs.xrs_bytes += 16.0 * double(st->count) * (1.0 - std::ldexp(1.0, -p.s));
+}
+
+// In-process XRS: every slab pair swapped in place by one kernel reading and
+// writing both slices (same device or peer-mapped).  No buffer, no copy-back.
+void runXrsLocal(qk_state** sl, int ns, const XrsPlan& p) {
+    for (int k = 0; k < ns; k++) cuda(cudaStreamSynchronize(sl[k]->stream), "xrs pre-sync");
+    const int slabs = 1 << p.s;
+    for (int r = 0; r < ns; r++) {
+        const int own = ownSlab(r, p);
+        for (int pa = 0; pa < slabs; pa++) {
+            if (pa == own) continue;
+            const int q = partnerOf(r, pa, p);
+            if (q < r) continue;  // each unordered slab pair once
+            DeviceGuard g(sl[r]->device);
+            cuda(qkdev::launchSlabSwap(sl[r]->amps + slabBits(pa, p), sl[q]->amps + slabBits(own, p), p.slabOffsets,
+                                       p.outs.data(), p.s, sl[r]->stream),
+                 "xrs slab swap");
+        }
+    }
+    for (int k = 0; k < ns; k++) cuda(cudaStreamSynchronize(sl[k]->stream), "xrs post-sync");
+}
+
+void checkProgramAgainst(const quokka::Program& prog, const quokka::Config& cfg, int n, int R) {
+    if (prog.nQubits != cfg.totalQubits || prog.rankQubits != cfg.rankQubits)
+        throw ConfigError("program and config disagree on the qubit split");
+    if (n != cfg.totalQubits || R != cfg.rankQubits) throw ConfigError("state and config disagree on the qubit split");
+    const int region = cfg.rankRegion();
+    // Validate every item up front (distributed.cpp:149-164): nothing throws mid-run.
+    for (const quokka::ProgramItem& it : prog.items) {
+        if (it.type == quokka::ProgramItem::Block) {
+            for (const quokka::Gate& g : it.block.gates)
+                for (int q : g.qubits())
+                    if (q < 0 || q >= prog.chunkQubits)
+                        throw SimulationError("block gate " + std::to_string(g.id) + " reaches outside the chunk");
+        } else if (it.swap.kind == quokka::SwapOp::InMemory) {
+            for (const auto& [a, b] : it.swap.pairs)
+                if (a < 0 || b < 0 || a >= region || b >= region)
+                    throw SimulationError("in-memory swap reaches into the rank bits");
+        } else {
+            if (R == 0) throw SimulationError("cross-rank swap in a single-rank run; use the multi-rank engine");
+            planXrs(it.swap, cfg.totalQubits, cfg.rankQubits, cfg.bufferQubits);
+        }
+    }
+}
+
+void setBasis(qk_state* st, Index global) {
+    if (global >= (Index(1) << st->n)) throw SimulationError("initial basis state out of range");
+    cuda(cudaMemsetAsync(st->amps, 0, st->count * sizeof(double2), st->stream), "memset");
+    if ((global >> st->nLocal) == Index(st->rank))
+        cuda(qkdev::launchSetBasis(st->amps, global & (st->count - 1), st->stream), "set basis");
+}
+
+}  // namespace
+
+// ================================================================ C-ABI ======
+
+extern "C" {
+
+const char* qk_last_error(void) { return g_lastError.c_str(); }
+void qk_free(void* p) { std::free(p); }
+
+int qk_device_count(int* count) {
+    return guard([&] { cuda(cudaGetDeviceCount(count), "cudaGetDeviceCount"); });
+}
+
+int qk_create(int n, int R, int rank, int B, int device, qk_state** out) {
+    return guard([&] {
+        if (n < 1 || n > 40) throw SimulationError("qubit count " + std::to_string(n) + " out of range");
+        if (R < 0 || R >= n) throw ConfigError("rank_qbit must leave at least one in-rank qubit");
+        if (rank < 0 || rank >= (1 << R)) throw ConfigError("rank out of range");
+        int ndev = 0;
+        cuda(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+        if (device < 0 || device >= ndev) throw SimulationError("no such CUDA device");
+        auto st = std::make_unique<qk_state>();
+        st->n = n;
+        st->R = R;
+        st->rank = rank;
+        st->nLocal = n - R;
+        st->B = B < 0 ? std::min(n - R, 28) : B;
+        st->device = device;
+        st->count = uint64_t(1) << st->nLocal;
+        DeviceGuard g(device);
+        cuda(cudaStreamCreateWithFlags(&st->stream, cudaStreamNonBlocking), "stream");
+        cuda(cudaMalloc(&st->amps, st->count * sizeof(double2)), "cudaMalloc(state)");
+        cuda(cudaMalloc(&st->normScratch, qkdev::normScratchDoubles() * sizeof(double)), "cudaMalloc(norm)");
+        cuda(cudaMalloc(&st->normOut, sizeof(double)), "cudaMalloc(norm)");
+        setBasis(st.get(), Index(rank) << st->nLocal);
+        *out = st.release();
+    });
+}
+
+int qk_destroy(qk_state* st) {
+    return guard([&] {
+        if (!st) return;
+        DeviceGuard g(st->device);
+        cudaStreamSynchronize(st->stream);
+        if (st->comm) ncclCommDestroy(st->comm);
+        cudaFree(st->amps);
+        cudaFree(st->normScratch);
+        cudaFree(st->normOut);
+        cudaFree(st->recvBuf);
+        cudaFree(st->packBuf);
+        cudaStreamDestroy(st->stream);
+        delete st;
+    });
+}
+
+int qk_set_basis(qk_state* st, uint64_t global) {
+    return guard([&] {
+        DeviceGuard g(st->device);
+        setBasis(st, global);
+    });
+}
+
+int qk_upload(qk_state* st, uint64_t off, uint64_t cnt, const double* host) {
+    return guard([&] {
+        if (off + cnt > st->count) throw SimulationError("upload range outside the slice");
+        DeviceGuard g(st->device);
+        cuda(cudaMemcpyAsync(st->amps + off, host, cnt * sizeof(double2), cudaMemcpyHostToDevice, st->stream), "upload");
+        cuda(cudaStreamSynchronize(st->stream), "upload sync");
+    });
+}
+
+int qk_download(qk_state* st, uint64_t off, uint64_t cnt, double* host) {
+    return guard([&] {
+        if (off + cnt > st->count) throw SimulationError("download range outside the slice");
+        DeviceGuard g(st->device);
+        cuda(cudaMemcpyAsync(host, st->amps + off, cnt * sizeof(double2), cudaMemcpyDeviceToHost, st->stream), "download");
+        cuda(cudaStreamSynchronize(st->stream), "download sync");
+    });
+}
+
+int qk_norm(qk_state* st, double* out) {
+    return guard([&] {
+        DeviceGuard g(st->device);
+        cuda(qkdev::launchNorm(st->amps, st->count, st->normScratch, st->normOut, st->stream), "norm");
+        cuda(cudaMemcpyAsync(out, st->normOut, sizeof(double), cudaMemcpyDeviceToHost, st->stream), "norm copy");
+        cuda(cudaStreamSynchronize(st->stream), "norm sync");
+    });
+}
+
+int qk_synchronize(qk_state* st) {
+    return guard([&] { cuda(cudaStreamSynchronize(st->stream), "synchronize"); });
+}
+
+int qk_stream(qk_state* st, void** s) {
+    return guard([&] { *s = st->stream; });
+}
+
+int qk_set_profiling(qk_state* st, int on) {
+    return guard([&] { st->profiling = on != 0; });
+}
+
+int qk_apply_block(qk_state* st, const qk_gate* gates, int ngates, int chunk) {
+    return guard([&] {
+        quokka::Program p;
+        p.nQubits = st->n;
+        p.rankQubits = st->R;
+        p.chunkQubits = chunk;
+        quokka::GateBlock blk;
+        for (int i = 0; i < ngates; i++) {
+            const qk_gate& g = gates[i];
+            if (g.kind < QK_H || g.kind > QK_FUSED_DENSE) throw SimulationError("unknown gate kind");
+            quokka::Gate q;
+            q.kind = static_cast<quokka::GateKind>(g.kind);
+            q.id = long(g.id);
+            const int nq = g.nqubits;
+            if (nq < 1 || nq > 16) throw SimulationError("bad gate arity");
+            const bool fused = g.kind == QK_FUSED_DIAG || g.kind == QK_FUSED_DENSE;
+            if (!fused && quokka::kindArity(q.kind) != nq) throw SimulationError("gate arity does not match its kind");
+            if ((g.kind == QK_CX || g.kind == QK_CP)) {
+                q.controls = {g.qubits[0]};
+                q.targets = {g.qubits[1]};
+            } else {
+                q.targets.assign(g.qubits, g.qubits + nq);
+            }
+            for (int j = 0; j < quokka::kindParamCount(q.kind); j++) q.params.push_back(g.params[j]);
+            if (fused) {
+                if (!g.payload) throw SimulationError("fused gate without payload");
+                const size_t e = size_t(1) << (g.kind == QK_FUSED_DIAG ? nq : 2 * nq);
+                for (size_t j = 0; j < e; j++) q.payload.emplace_back(g.payload[2 * j], g.payload[2 * j + 1]);
+            }
+            for (int qq : q.qubits())
+                if (qq < 0 || qq >= chunk)
+                    throw SimulationError("block gate " + std::to_string(q.id) + " reaches outside the chunk");
+            blk.gates.push_back(std::move(q));
+        }
+        if (chunk < 1 || chunk > st->nLocal) throw SimulationError("chunk size out of range");
+        p.items.push_back(quokka::ProgramItem::makeBlock(std::move(blk)));
+        qk_program prog;
+        prog.prog = std::move(p);
+        DeviceGuard g(st->device);
+        auto c = compileFor(&prog, st->nLocal);
+        DeviceTables t = tablesFor(&prog, *c, st->device);
+        qk_run_stats rs{};
+        runBlock(st, c->items[0], t, rs);
+        cuda(cudaStreamSynchronize(st->stream), "apply block");
+    });
+}
+
+int qk_apply_gate(qk_state* st, const qk_gate* gate) {
+    return qk_apply_block(st, gate, 1, st->nLocal);
+}
+
+int qk_ims_swap(qk_state* st, const int* outs, const int* ins, int s, int /*cacheLineQubits*/) {
+    return guard([&] {
+        for (int j = 0; j < s; j++)
+            if (outs[j] < 0 || ins[j] < 0 || outs[j] >= st->nLocal || ins[j] >= st->nLocal)
+                throw SimulationError("in-memory swap position outside the slice");
+        DeviceGuard g(st->device);
+        qk_run_stats rs{};
+        runIms(st, std::vector<int>(outs, outs + s), std::vector<int>(ins, ins + s), rs);
+        cuda(cudaStreamSynchronize(st->stream), "ims");
+    });
+}
+
+int qk_xrs_swap_local(qk_state** sl, int ns, const int* outs, const int* ins, int s, qk_xrs_stats* stats) {
+    return guard([&] {
+        if (ns < 1) throw SimulationError("no slices");
+        const int n = sl[0]->n, R = sl[0]->R, B = sl[0]->B;
+        if (ns != (1 << R)) throw SimulationError("slice count does not match the rank count");
+        for (int k = 0; k < ns; k++)
+            if (sl[k]->rank != k || sl[k]->n != n || sl[k]->R != R) throw SimulationError("slices are not ranks 0..2^R-1");
+        quokka::SwapOp op;
+        op.kind = quokka::SwapOp::CrossRank;
+        for (int j = 0; j < s; j++) op.pairs.emplace_back(outs[j], ins[j]);
+        const XrsPlan p = planXrs(op, n, R, B);
+        if (stats)
+            for (int k = 0; k < ns; k++) accountXrs(p, &stats[k]);
+        if (p.s) runXrsLocal(sl, ns, p);
+    });
+}
+
+int qk_comm_unique_id(unsigned char id[128]) {
+    return guard([&] {
+        ncclUniqueId u;
+        nccl(ncclGetUniqueId(&u), "ncclGetUniqueId");
+        static_assert(sizeof(u) == 128, "nccl id size");
+        std::memcpy(id, &u, 128);
+    });
+}
+
+int qk_comm_init(qk_state* st, const unsigned char id[128], int nranks, int rank) {
+    return guard([&] {
+        if (nranks != (1 << st->R) || rank != st->rank) throw ConfigError("communicator does not match the rank split");
+        ncclUniqueId u;
+        std::memcpy(&u, id, 128);
+        DeviceGuard g(st->device);
+        nccl(ncclCommInitRank(&st->comm, nranks, u, rank), "ncclCommInitRank");
+    });
+}
+
+int qk_xrs_swap(qk_state* st, const int* outs, const int* ins, int s, qk_xrs_stats* stats) {
+    return guard([&] {
+        quokka::SwapOp op;
+        op.kind = quokka::SwapOp::CrossRank;
+        for (int j = 0; j < s; j++) op.pairs.emplace_back(outs[j], ins[j]);
+        const XrsPlan p = planXrs(op, st->n, st->R, st->B);
+        accountXrs(p, stats);
+        DeviceGuard g(st->device);
+        qk_run_stats rs{};
+        runXrsNccl(st, p, rs);
+        cuda(cudaStreamSynchronize(st->stream), "xrs");
+    });
+}
+
+int qk_xrs_plan(int n, int R, int B, int rank, const int* outs, const int* ins, int s, qk_xrs_msg* msgs, int cap,
+                int* nmsgs) {
+    return guard([&] {
+        quokka::SwapOp op;
+        op.kind = quokka::SwapOp::CrossRank;
+        for (int j = 0; j < s; j++) op.pairs.emplace_back(outs[j], ins[j]);
+        const XrsPlan p = planXrs(op, n, R, B);
+        const std::vector<qk_xrs_msg> m = xrsMessages(p, rank);
+        *nmsgs = int(m.size());
+        if (int(m.size()) > cap) throw SimulationError("message buffer too small");
+        std::copy(m.begin(), m.end(), msgs);
+    });
+}
+
+int qk_xrs_slab_index(int n, int R, const int* outs, int s, int slab, uint64_t offset, uint64_t* index) {
+    return guard([&] {
+        quokka::SwapOp op;
+        op.kind = quokka::SwapOp::CrossRank;
+        for (int j = 0; j < s; j++) op.pairs.emplace_back(outs[j], n - R + j);
+        XrsPlan p = planXrs(op, n, R, n - R);
+        Index o = offset;
+        for (int j = 0; j < s; j++) {  // deposit around the ascending out positions
+            const int q = p.outs[size_t(j)];
+            o = ((o >> q) << (q + 1)) | (o & ((Index(1) << q) - 1));
+        }
+        *index = o | slabBits(slab, p);
+    });
+}
+
+int qk_config_parse(const char* text, qk_config* out) {
+    return guard([&] {
+        std::istringstream in(text);
+        *out = fromConfig(quokka::parseConfig(in));
+    });
+}
+
+int qk_config_finalize(qk_config* cfg) {
+    return guard([&] {
+        quokka::Config c = toConfig(*cfg);
+        c.finalize();
+        *cfg = fromConfig(c);
+    });
+}
+
+int qk_config_serialize(const qk_config* cfg, char** text) {
+    return guard([&] { *text = dupText(quokka::serializeConfig(toConfig(*cfg))); });
+}
+
+int qk_program_parse(const char* text, const qk_config* cfg, int lenient, qk_program** out) {
+    return guard([&] {
+        std::istringstream in(text);
+        auto p = std::make_unique<qk_program>();
+        p->prog = quokka::parseProgram(in, toConfig(*cfg), lenient != 0);
+        *out = p.release();
+    });
+}
+
+int qk_program_optimize(const char* circuit, const qk_config* cfg, qk_program** out) {
+    return guard([&] {
+        const quokka::Config c = toConfig(*cfg);
+        std::istringstream in(circuit);
+        const quokka::Circuit circ = quokka::parseCircuit(in, c.totalQubits);
+        auto p = std::make_unique<qk_program>();
+        p->prog = quokka::aioOptimize(circ, c);
+        *out = p.release();
+    });
+}
+
+int qk_program_serialize(const qk_program* p, char** text) {
+    return guard([&] { *text = dupText(quokka::serializeProgram(p->prog)); });
+}
+
+int qk_program_counts(const qk_program* p, int64_t* blocks, int64_t* sqs, int64_t* csqs, int64_t* gates) {
+    return guard([&] {
+        if (blocks) *blocks = int64_t(p->prog.blockCount());
+        if (sqs) *sqs = int64_t(p->prog.swapCount(quokka::SwapOp::InMemory));
+        if (csqs) *csqs = int64_t(p->prog.swapCount(quokka::SwapOp::CrossRank));
+        if (gates) *gates = int64_t(p->prog.gateCount());
+    });
+}
+
+int qk_program_final_layout(const qk_program* p, int* physToLog) {
+    return guard([&] {
+        for (int i = 0; i < p->prog.finalLayout.size(); i++) physToLog[i] = p->prog.finalLayout.physToLog[size_t(i)];
+    });
+}
+
+int qk_program_destroy(qk_program* p) {
+    return guard([&] { delete p; });
+}
+
+int qk_circuit_roundtrip(const char* text, int n, char** out) {
+    return guard([&] {
+        std::istringstream in(text);
+        *out = dupText(quokka::serializeCircuit(quokka::parseCircuit(in, n)));
+    });
+}
+
+int qk_circuit_generate(const char* kind, int n, int64_t a, uint64_t seed, char** text) {
+    return guard([&] {
+        const std::string k = kind;
+        quokka::Circuit c;
+        if (k == "qft") c = quokka::genQft(n);
+        else if (k == "qaoa") c = quokka::genQaoa(n, int(a), seed);
+        else if (k == "bv") c = quokka::genBv(n, seed);
+        else if (k == "bvones") c = quokka::genBvAllOnes(n);
+        else if (k == "random") c = quokka::genRandom(n, int(a), seed);
+        else if (k == "grover") c = quokka::genGrover(n, seed, int(a));
+        else if (k.rfind("bench:", 0) == 0) {
+            int found = -1;
+            for (int kk = 0; kk <= static_cast<int>(quokka::GateKind::RZZ); kk++)
+                if (k.substr(6) == quokka::kindName(static_cast<quokka::GateKind>(kk))) found = kk;
+            if (found < 0) throw ConfigError("unknown gate kind '" + k.substr(6) + "'");
+            c = quokka::genGateBench(static_cast<quokka::GateKind>(found), n);
+        } else {
+            throw ConfigError("unknown generator '" + k + "'");
+        }
+        *text = dupText(quokka::serializeCircuit(c));
+    });
+}
+
+int qk_simulate(qk_state* st, const qk_program* cp, const qk_config* cfg, uint64_t initial, qk_run_stats* stats) {
+    return guard([&] {
+        qk_program* p = const_cast<qk_program*>(cp);
+        const quokka::Config c = toConfig(*cfg);
+        checkProgramAgainst(p->prog, c, st->n, st->R);
+        if (c.bufferQubits != st->B) st->B = c.bufferQubits;
+        DeviceGuard g(st->device);
+        auto comp = compileFor(p, st->nLocal);
+        const DeviceTables t = tablesFor(p, *comp, st->device);
+        qk_run_stats rs{};
+        Timer timer(st);
+        cudaEvent_t e0, e1;
+        cuda(cudaEventCreate(&e0), "event");
+        cuda(cudaEventCreate(&e1), "event");
+        cuda(cudaEventRecord(e0, st->stream), "event");
+        setBasis(st, initial);
+        for (const CompiledItem& it : comp->items) {
+            if (it.kind == CompiledItem::Block) timer.time(0, [&] { runBlock(st, it, t, rs); });
+            else if (it.kind == CompiledItem::Ims) timer.time(1, [&] { runIms(st, it.outs, it.ins, rs); });
+            else {
+                quokka::SwapOp op;
+                op.kind = quokka::SwapOp::CrossRank;
+                for (size_t j = 0; j < it.outs.size(); j++) op.pairs.emplace_back(it.outs[j], it.ins[j]);
+                const XrsPlan plan = planXrs(op, st->n, st->R, st->B);
+                timer.time(2, [&] { runXrsNccl(st, plan, rs); });
+            }
+        }
+        cuda(cudaEventRecord(e1, st->stream), "event");
+        cuda(cudaEventSynchronize(e1), "simulate");
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        double cls[3];
+        timer.collect(cls);
+        rs.block_ms = cls[0];
+        rs.ims_ms = cls[1];
+        rs.xrs_ms = cls[2];
+        rs.total_ms = ms;
+        st->last = rs;
+        if (stats) *stats = rs;
+    });
+}
+
+int qk_simulate_local(qk_state** sl, int ns, const qk_program* cp, const qk_config* cfg, uint64_t initial,
+                      qk_xrs_stats* stats) {
+    return guard([&] {
+        qk_program* p = const_cast<qk_program*>(cp);
+        const quokka::Config c = toConfig(*cfg);
+        if (ns < 1 || ns != (1 << c.rankQubits)) throw SimulationError("slice count does not match the rank count");
+        for (int k = 0; k < ns; k++) {
+            if (sl[k]->rank != k) throw SimulationError("slices must be ranks 0..2^R-1 in order");
+            checkProgramAgainst(p->prog, c, sl[k]->n, sl[k]->R);
+        }
+        if (initial >= (Index(1) << c.totalQubits)) throw SimulationError("initial basis state out of range");
+        auto comp = compileFor(p, sl[0]->nLocal);
+        std::vector<DeviceTables> tabs;
+        for (int k = 0; k < ns; k++) {
+            sl[k]->B = c.bufferQubits;
+            tabs.push_back(tablesFor(p, *comp, sl[k]->device));
+            DeviceGuard g(sl[k]->device);
+            setBasis(sl[k], initial);
+        }
+        if (stats)
+            for (int k = 0; k < ns; k++) stats[k] = qk_xrs_stats{};
+        for (const CompiledItem& it : comp->items) {
+            if (it.kind == CompiledItem::Xrs) {
+                quokka::SwapOp op;
+                op.kind = quokka::SwapOp::CrossRank;
+                for (size_t j = 0; j < it.outs.size(); j++) op.pairs.emplace_back(it.outs[j], it.ins[j]);
+                const XrsPlan plan = planXrs(op, c.totalQubits, c.rankQubits, c.bufferQubits);
+                if (stats)
+                    for (int k = 0; k < ns; k++) accountXrs(plan, &stats[k]);
+                if (plan.s) runXrsLocal(sl, ns, plan);
+                continue;
+            }
+            for (int k = 0; k < ns; k++) {
+                DeviceGuard g(sl[k]->device);
+                qk_run_stats rs{};
+                if (it.kind == CompiledItem::Block) runBlock(sl[k], it, tabs[size_t(k)], rs);
+                else runIms(sl[k], it.outs, it.ins, rs);
+            }
+        }
+        for (int k = 0; k < ns; k++) cuda(cudaStreamSynchronize(sl[k]->stream), "simulate local");
+    });
+}
+
+}  // extern "C"

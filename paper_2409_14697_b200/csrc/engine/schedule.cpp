@@ -1,0 +1,465 @@
+// Host-side compiler from a GateBlock to fused-pass programs (pass_program.h).
+//
+// Semantics: applying the returned steps in order equals applying the
+// block's gates in order to every chunk (proj/src/engine.cpp:262-281): gates
+// only ever address index bits, and a tile that contains all bits a gate
+// touches is closed under it, so tiling the slice by any superset of the
+// chunk bits gives the same result as the reference's 2^C chunk loop.
+//
+// Per pass the scheduler:
+//   1. picks ct tile bits = the union of the pass's gate qubits padded with the
+//      lowest physical bits (coalesced 128-B+ rows);
+//   2. walks the gates keeping a slot->tile-bit map; a gate that needs a qubit
+//      in a register slot (1-qubit dense, CX target, dense U_k) but finds it in
+//      the thread index starts a new segment = one shared-memory exchange, with
+//      the next register set chosen by look-ahead over the following gates;
+//   3. lowers each gate to a register op, a per-thread scalar update (diagonals
+//      on thread-index bits) or a relabel (SWAP never moves data).
+// H's 1/sqrt2 is not multiplied per gate: every H scales all amplitudes by
+// the same factor, so the product is folded into one exact power-of-two (x
+// 1/sqrt2) scale applied at the next exchange / store.
+#include "schedule.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+namespace qkeng {
+
+using namespace qkdev;
+using quokka::Amp;
+using quokka::Gate;
+using quokka::GateKind;
+using quokka::SimulationError;
+
+double referenceFlopsPerAmp(const Gate& g) {
+    switch (g.kind) {
+        case GateKind::H:
+        case GateKind::U:
+        case GateKind::X:
+        case GateKind::RX:
+        case GateKind::RY:
+            return 14;
+        case GateKind::RZ:
+        case GateKind::RZZ:
+        case GateKind::CP:
+        case GateKind::FusedDiag:
+            return 6;
+        case GateKind::CX:
+        case GateKind::SWAP:
+            return 0;
+        case GateKind::FusedDense:
+            return 8.0 * double(1 << g.targets.size()) - 2;
+    }
+    return 0;
+}
+
+namespace {
+
+bool denseInRegs(const Gate& g) {
+    return g.kind == GateKind::FusedDense && g.targets.size() >= 2 && g.targets.size() <= 4;
+}
+
+// Tile bits that must sit in register slots when `g` runs.
+std::vector<int> regNeeds(const Gate& g) {
+    switch (g.kind) {
+        case GateKind::H:
+        case GateKind::U:
+        case GateKind::X:
+        case GateKind::RX:
+        case GateKind::RY:
+        case GateKind::CX:
+            return {g.targets[0]};
+        case GateKind::FusedDense:
+            if (g.targets.size() == 1) return {g.targets[0]};
+            return g.targets;
+        default:
+            return {};
+    }
+}
+
+void appendComplex(std::vector<double>& v, const std::vector<Amp>& xs) {
+    for (const Amp& a : xs) {
+        v.push_back(a.real());
+        v.push_back(a.imag());
+    }
+}
+
+class PassBuilder {
+public:
+    PassBuilder(const std::vector<Gate>& tg, const std::vector<Gate>& orig, const std::vector<int>& tilePhys,
+                std::vector<double>& gtab)
+        : tg_(tg), orig_(orig), gtab_(gtab), ct_(int(tilePhys.size())) {
+        tilePhys_ = tilePhys;
+    }
+
+    // Compile gates [i, ...) into one PassParams; returns the next gate index.
+    size_t build(size_t i, Step& step) {
+        auto P = std::make_shared<PassParams>();
+        std::memset(P.get(), 0, sizeof(PassParams));
+        P_ = P.get();
+        P_->ct = ct_;
+        for (int j = 0; j < ct_; j++) {
+            P_->tile_phys[j] = int8_t(tilePhys_[size_t(j)]);
+            P_->tile_mask |= uint64_t(1) << tilePhys_[size_t(j)];
+        }
+        nops_ = ncoef_ = ncontrib_ = 0;
+        seg_ = 0;
+        hcount_ = 0;
+        dirty_ = false;
+        chooseMap(i);
+        std::memcpy(P_->map_in[0], map_, sizeof map_);
+
+        const size_t first = i;
+        double flops = 0;
+        while (i < tg_.size()) {
+            if (kMaxOps - nops_ < 4 || kMaxCoef - ncoef_ < 8 || kMaxContrib - ncontrib_ < 16 + ct_ ||
+                kMaxSegs - seg_ < 3)
+                break;
+            if (!satisfied(tg_[i])) {
+                flush();
+                P_->seg_end[seg_] = uint16_t(nops_);
+                std::memcpy(P_->map_out[seg_], map_, sizeof map_);
+                seg_++;
+                chooseMap(i);
+                std::memcpy(P_->map_in[seg_], map_, sizeof map_);
+            }
+            lower(tg_[i], orig_[i]);
+            flops += referenceFlopsPerAmp(orig_[i]);
+            i++;
+        }
+        flush();
+        P_->seg_end[seg_] = uint16_t(nops_);
+        std::memcpy(P_->map_out[seg_], map_, sizeof map_);
+        P_->nsegs = seg_ + 1;
+        P_->nops = nops_;
+        step.kind = Step::Pass;
+        step.pass = P;
+        step.flopsPerAmp = flops;
+        step.gates = int(i - first);
+        return i;
+    }
+
+private:
+    bool satisfied(const Gate& g) const {
+        if (denseInRegs(g)) {
+            const int k = int(g.targets.size());
+            for (int j = 0; j < k; j++)
+                if (inv_[g.targets[size_t(j)]] != k - 1 - j) return false;
+            return true;
+        }
+        for (int b : regNeeds(g))
+            if (inv_[b] >= kRegBits) return false;
+        return true;
+    }
+
+    // Choose which tile bits occupy the register slots from gate i onward.
+    void chooseMap(size_t i) {
+        int slotBit[kRegBits];
+        std::fill(slotBit, slotBit + kRegBits, -1);
+        std::vector<int> regs;  // tile bits at time i
+        if (i < tg_.size() && denseInRegs(tg_[i])) {
+            const Gate& g = tg_[i];
+            const int k = int(g.targets.size());
+            for (int j = 0; j < k; j++) slotBit[k - 1 - j] = g.targets[size_t(j)];
+            for (int j = 0; j < k; j++) regs.push_back(g.targets[size_t(j)]);
+        }
+        // Look ahead: add needed bits in order of first use while they fit.
+        std::vector<int> origin(static_cast<size_t>(ct_));  // current bit -> bit at time i (SWAP relabels)
+        for (int b = 0; b < ct_; b++) origin[size_t(b)] = b;
+        std::vector<char> inSet(size_t(ct_), 0);
+        for (int b : regs) inSet[size_t(b)] = 1;
+        for (size_t j = i; j < tg_.size() && int(regs.size()) <= kRegBits; j++) {
+            const Gate& g = tg_[j];
+            if (g.kind == GateKind::SWAP) {
+                const int a = g.targets[0], b = g.targets[1];
+                std::swap(origin[size_t(a)], origin[size_t(b)]);
+                std::swap(inSet[size_t(a)], inSet[size_t(b)]);
+                continue;
+            }
+            if (j > i && denseInRegs(g)) break;
+            std::vector<int> need;
+            for (int b : regNeeds(g))
+                if (!inSet[size_t(b)]) need.push_back(b);
+            if (need.empty()) continue;
+            if (regs.size() + need.size() > size_t(kRegBits)) break;
+            for (int b : need) {
+                inSet[size_t(b)] = 1;
+                regs.push_back(origin[size_t(b)]);
+            }
+        }
+        // Fill with the highest remaining tile bits (keeps low bits in lanes).
+        std::vector<char> used(size_t(ct_), 0);
+        for (int b : regs) used[size_t(b)] = 1;
+        for (int b = ct_ - 1; b >= 0 && int(regs.size()) < kRegBits; b--)
+            if (!used[size_t(b)]) {
+                used[size_t(b)] = 1;
+                regs.push_back(b);
+            }
+        // Assign register slots (canonical dense slots already fixed).
+        size_t r = 0;
+        for (int s = 0; s < kRegBits; s++) {
+            if (slotBit[s] >= 0) continue;
+            while (r < regs.size() && std::find(slotBit, slotBit + kRegBits, regs[r]) != slotBit + kRegBits) r++;
+            slotBit[s] = regs[r++];
+        }
+        // Thread bits ascending; lane bits 0..2 with distinct residues mod 3
+        // (conflict-free swizzled exchange).
+        std::vector<int> rest;
+        for (int b = 0; b < ct_; b++)
+            if (std::find(slotBit, slotBit + kRegBits, b) == slotBit + kRegBits) rest.push_back(b);
+        std::vector<int> lanes;
+        for (int want = 0; want < 3 && !rest.empty(); want++) {
+            size_t pick = rest.size();
+            for (size_t q = 0; q < rest.size(); q++) {
+                bool clash = false;
+                for (int l : lanes) clash |= (l % 3) == (rest[q] % 3);
+                if (!clash) {
+                    pick = q;
+                    break;
+                }
+            }
+            if (pick == rest.size()) break;
+            lanes.push_back(rest[pick]);
+            rest.erase(rest.begin() + long(pick));
+        }
+        lanes.insert(lanes.end(), rest.begin(), rest.end());
+        std::memset(map_, 0, sizeof map_);
+        for (int s = 0; s < kRegBits; s++) map_[s] = uint8_t(slotBit[s]);
+        for (size_t t = 0; t < lanes.size(); t++) map_[kRegBits + t] = uint8_t(lanes[t]);
+        for (int s = 0; s < ct_; s++) inv_[map_[s]] = s;
+    }
+
+    uint32_t addCoef(const std::vector<Amp>& xs) {
+        const uint32_t at = uint32_t(ncoef_);
+        for (const Amp& a : xs) {
+            P_->coef[2 * ncoef_] = a.real();
+            P_->coef[2 * ncoef_ + 1] = a.imag();
+            ncoef_++;
+        }
+        return at;
+    }
+
+    uint32_t addTable(const std::vector<Amp>& xs) {
+        const uint32_t at = uint32_t(gtab_.size() / 2);
+        appendComplex(gtab_, xs);
+        return at;
+    }
+
+    void emit(OpType t, int a = 0, int b = 0, int k = 0, uint32_t c = 0, uint16_t c16 = 0) {
+        DevOp& o = P_->ops[nops_++];
+        o.type = t;
+        o.a = uint8_t(a);
+        o.b = uint8_t(b);
+        o.k = uint8_t(k);
+        o.c = c;
+        o.c16 = c16;
+    }
+
+    void flush() {
+        if (hcount_ == 0 && !dirty_) return;
+        // (1/sqrt2)^h exactly: a power of two, times 1/sqrt2 when h is odd.
+        const double root = 1.0 / std::sqrt(2.0);
+        const double scale = std::ldexp(hcount_ % 2 ? root : 1.0, -(hcount_ / 2));
+        emit(OP_FLUSH, 0, 0, 0, addCoef({Amp(scale, 0.0)}));
+        hcount_ = 0;
+        dirty_ = false;
+    }
+
+    // Diagonal over (q0 = sub-index MSB, q1) with entries d[4].
+    void diag2(int q0, int q1, const std::vector<Amp>& d) {
+        const int s0 = inv_[q0], s1 = inv_[q1];
+        const uint32_t c = addCoef(d);
+        if (s0 < kRegBits && s1 < kRegBits) emit(OP_DIAG2_RR, s0, s1, 0, c);
+        else if (s0 < kRegBits) emit(OP_DIAG2_RT, s0, s1 - kRegBits, 0, c);
+        else if (s1 < kRegBits) emit(OP_DIAG2_RT, s1, s0 - kRegBits, 1, c);
+        else {
+            emit(OP_DIAG2_TT, s0 - kRegBits, s1 - kRegBits, 0, c);
+            dirty_ = true;
+        }
+    }
+
+    void diag1(int q, const std::vector<Amp>& d) {
+        const int s = inv_[q];
+        const uint32_t c = addCoef(d);
+        if (s < kRegBits) emit(OP_DIAG1_R, s, 0, 0, c);
+        else {
+            emit(OP_DIAG1_T, s - kRegBits, 0, 0, c);
+            dirty_ = true;
+        }
+    }
+
+    void lower(const Gate& g, const Gate& orig) {
+        switch (g.kind) {
+            case GateKind::H:
+                emit(OP_H, inv_[g.targets[0]]);
+                hcount_++;
+                return;
+            case GateKind::X:
+                emit(OP_X, inv_[g.targets[0]]);
+                return;
+            case GateKind::U:
+            case GateKind::RX:
+            case GateKind::RY:
+                emit(OP_MAT1, inv_[g.targets[0]], 0, 0, addCoef(quokka::gateMatrix(orig)));
+                return;
+            case GateKind::CX: {
+                const int t = inv_[g.targets[0]], c = inv_[g.controls[0]];
+                if (c < kRegBits) emit(OP_CX_RR, t, c);
+                else emit(OP_CX_RT, t, c - kRegBits);
+                return;
+            }
+            case GateKind::SWAP: {  // relabel only
+                const int a = g.targets[0], b = g.targets[1], sa = inv_[a], sb = inv_[b];
+                map_[sa] = uint8_t(b);
+                map_[sb] = uint8_t(a);
+                inv_[a] = sb;
+                inv_[b] = sa;
+                return;
+            }
+            case GateKind::RZ:
+                diag1(g.targets[0], quokka::gateDiagonal(orig));
+                return;
+            case GateKind::CP: {
+                const int sa = inv_[g.controls[0]], sb = inv_[g.targets[0]];
+                const uint32_t c = addCoef({quokka::gateDiagonal(orig)[3]});
+                if (sa < kRegBits && sb < kRegBits) emit(OP_CPHASE_RR, std::min(sa, sb), std::max(sa, sb), 0, c);
+                else if (sa < kRegBits) emit(OP_CPHASE_RT, sa, sb - kRegBits, 0, c);
+                else if (sb < kRegBits) emit(OP_CPHASE_RT, sb, sa - kRegBits, 0, c);
+                else {
+                    emit(OP_CPHASE_TT, sa - kRegBits, sb - kRegBits, 0, c);
+                    dirty_ = true;
+                }
+                return;
+            }
+            case GateKind::RZZ: {
+                const std::vector<int> qs = g.qubits();
+                diag2(qs[0], qs[1], quokka::gateDiagonal(orig));
+                return;
+            }
+            case GateKind::FusedDiag: {
+                const int k = int(g.targets.size());
+                if (k == 1) return diag1(g.targets[0], orig.payload);
+                if (k == 2) return diag2(g.targets[0], g.targets[1], orig.payload);
+                const uint16_t c16 = uint16_t(ncontrib_);
+                for (int s = 0; s < ct_; s++) P_->contrib[ncontrib_ + s] = 0;
+                for (int j = 0; j < k; j++)
+                    P_->contrib[ncontrib_ + inv_[g.targets[size_t(j)]]] = uint16_t(1u << (k - 1 - j));
+                ncontrib_ += ct_;
+                emit(OP_DTABLE, 0, 0, k, addTable(orig.payload), c16);
+                return;
+            }
+            case GateKind::FusedDense: {
+                const int k = int(g.targets.size());
+                if (k == 1) {
+                    emit(OP_MAT1, inv_[g.targets[0]], 0, 0, addCoef(orig.payload));
+                    return;
+                }
+                emit(OP_DENSE, 0, 0, k, addTable(orig.payload));
+                return;
+            }
+        }
+    }
+
+    const std::vector<Gate>& tg_;
+    const std::vector<Gate>& orig_;
+    std::vector<double>& gtab_;
+    std::vector<int> tilePhys_;
+    int ct_;
+    PassParams* P_ = nullptr;
+    int nops_ = 0, ncoef_ = 0, ncontrib_ = 0, seg_ = 0, hcount_ = 0;
+    bool dirty_ = false;
+    uint8_t map_[16] = {};
+    int inv_[16] = {};
+};
+
+Gate remapQubits(const Gate& g, const int* tileOf) {
+    Gate t;
+    t.kind = g.kind;
+    t.id = g.id;
+    for (int q : g.targets) t.targets.push_back(tileOf[q]);
+    for (int q : g.controls) t.controls.push_back(tileOf[q]);
+    return t;
+}
+
+void compileGroup(const std::vector<Gate>& gates, uint64_t used, int ct, int nLocal, std::vector<double>& gtab,
+                  std::vector<Step>& out) {
+    // Tile bits: every bit the group touches, padded with the lowest others.
+    uint64_t tile = used;
+    for (int b = 0; b < nLocal && __builtin_popcountll(tile) < ct; b++) tile |= uint64_t(1) << b;
+    std::vector<int> phys;
+    int tileOf[64];
+    std::fill(tileOf, tileOf + 64, -1);
+    for (int b = 0; b < nLocal; b++)
+        if ((tile >> b) & 1) {
+            tileOf[b] = int(phys.size());
+            phys.push_back(b);
+        }
+    std::vector<Gate> tg;
+    for (const Gate& g : gates) tg.push_back(remapQubits(g, tileOf));
+    PassBuilder pb(tg, gates, phys, gtab);
+    size_t i = 0;
+    while (i < gates.size()) {
+        Step st;
+        i = pb.build(i, st);
+        out.push_back(std::move(st));
+    }
+}
+
+}  // namespace
+
+std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::vector<double>& gtab) {
+    std::vector<Step> steps;
+    for (const Gate& g : gates)
+        for (int q : g.qubits())
+            if (q < 0 || q >= nLocal)
+                throw SimulationError("gate " + std::to_string(g.id) + " reaches outside the local slice");
+
+    auto denseStep = [&](const std::vector<Amp>& m, const std::vector<int>& targets, double flops) {
+        Step s;
+        s.kind = Step::DenseGroup;
+        s.k = int(targets.size());
+        s.matOff = gtab.size() / 2;
+        appendComplex(gtab, m);
+        s.targets = targets;
+        s.flopsPerAmp = flops;
+        s.gates = 1;
+        steps.push_back(std::move(s));
+    };
+
+    if (nLocal < kRegBits) {  // too small for a register tile: every gate as a dense group
+        for (const Gate& g : gates) denseStep(quokka::gateMatrix(g), g.qubits(), referenceFlopsPerAmp(g));
+        return steps;
+    }
+    const int ct = std::min(kMaxTileBits, nLocal);
+    std::vector<Gate> group;
+    uint64_t used = 0;
+    auto close = [&] {
+        if (!group.empty()) compileGroup(group, used, ct, nLocal, gtab, steps);
+        group.clear();
+        used = 0;
+    };
+    for (const Gate& g : gates) {
+        if (g.kind == GateKind::FusedDense && g.targets.size() > size_t(kRegBits)) {
+            close();
+            denseStep(g.payload, g.targets, referenceFlopsPerAmp(g));
+            continue;
+        }
+        if (g.kind == GateKind::FusedDiag && g.targets.size() > size_t(ct)) {  // wider than a tile
+            close();
+            denseStep(g.payload, g.targets, referenceFlopsPerAmp(g));
+            steps.back().kind = Step::DiagTable;
+            continue;
+        }
+        if (g.kind == GateKind::FusedDense && g.targets.size() > size_t(kMaxTileBits))
+            throw SimulationError("fused dense gate " + std::to_string(g.id) + " wider than 13 qubits");
+        const uint64_t m = g.depMask();
+        if (__builtin_popcountll(used | m) > ct) close();
+        group.push_back(g);
+        used |= m;
+    }
+    close();
+    return steps;
+}
+
+}  // namespace qkeng

@@ -1,0 +1,35 @@
+// Host-side compiler: GateBlock (physical positions) -> device steps.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <vector>
+
+#include "pass_program.h"
+#include "quokka/gates.hpp"
+
+namespace qkeng {
+
+struct Step {
+    enum Kind { Pass, DenseGroup, DiagTable } kind = Pass;
+    std::shared_ptr<qkdev::PassParams> pass;  // Kind::Pass
+    // Kind::DenseGroup / DiagTable: matrix (or diagonal) at gtab offset `matOff`,
+    // targets (j -> sub-index bit k-1-j)
+    int k = 0;
+    uint64_t matOff = 0;
+    std::vector<int> targets;
+    // algorithmic accounting: reference-formula flops per amplitude
+    double flopsPerAmp = 0;
+    int gates = 0;
+};
+
+// Appends device tables (fused-diagonal payloads, dense matrices) to `gtab`
+// (interleaved complex) and returns the steps that apply `gates` in order to a
+// slice of 2^nLocal amplitudes.  Throws SimulationError if a gate reaches a
+// position >= nLocal.
+std::vector<Step> compileBlock(const std::vector<quokka::Gate>& gates, int nLocal, std::vector<double>& gtab);
+
+// Reference-formula flops per amplitude for one gate.
+double referenceFlopsPerAmp(const quokka::Gate& g);
+
+}  // namespace qkeng

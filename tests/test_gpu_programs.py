@@ -1,0 +1,150 @@
+"""Whole-program parity on the GPU: final amplitudes vs the reference CPU
+simulator within 1e-10 max abs per amplitude, norm within 1e-12 (the north
+star's bar), plus closed-form KATs at sizes the CPU oracle cannot hold."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+from oracle import config_text
+
+pytestmark = pytest.mark.gpu
+
+G = np.load(os.path.join(GOLDEN, "golden_states.npz"))
+P = json.load(open(os.path.join(GOLDEN, "golden_programs.json")))
+TOL = 1e-10
+
+
+def run(qk, prog_text, cfg_text, initial=0):
+    cfg = qk.Config.parse(cfg_text)
+    prog = qk.Program.parse(prog_text, cfg)
+    if cfg.rank_qubits == 0:
+        st, p2l = qk.simulate_program(prog, initial)
+        return st, p2l, None
+    return qk.spawn_ranks(prog, initial)
+
+
+@pytest.mark.parametrize("name", sorted(k for k in P if "program" in P[k]))
+@pytest.mark.parametrize("initial", [0, 5])
+def test_golden_programs(qk, name, initial):
+    case = P[name]
+    st, p2l, stats = run(qk, case["program"], case["config"], initial)
+    want = G[f"{name}/init{initial}/state"].view(np.complex128)
+    assert np.max(np.abs(st - want)) < TOL
+    assert abs(np.sum(np.abs(st) ** 2) - 1.0) < 1e-12
+    assert p2l == list(G[f"{name}/init{initial}/phys_to_log"])
+    if stats is not None:
+        assert np.array_equal(np.array(stats, dtype=np.uint64), G[f"{name}/init{initial}/stats"])
+
+
+def test_random_programs_vs_reference(ref, qk):
+    # acceptance.cpp:67-96: random circuits x every flag combination x 1/2/4 ranks
+    rng = np.random.default_rng(9000)
+    for i in range(48):
+        n = int(rng.integers(4, 13))
+        r = i % 3
+        c = min(3 + int(rng.integers(0, 3)), n - r)
+        flags = i % 16
+        cfg_text = config_text(n, r, c, ims=flags & 1, xrs=(flags >> 1) & 1, fusion=(flags >> 2) & 1,
+                               diag=(flags >> 3) & 1)
+        circ = ref.gen("random", n, int(rng.integers(10, 61)), 31000 + i)
+        try:
+            prog = ref.optimize(circ, cfg_text)
+        except Exception:
+            continue
+        want, wl, wstats, _ = ref.simulate(prog, cfg_text, n, r, 0, 2)
+        st, p2l, stats = run(qk, prog, cfg_text)
+        assert np.max(np.abs(st - want.view(np.complex128))) < TOL, i
+        assert p2l == wl
+        if r:
+            assert np.array_equal(np.array(stats, dtype=np.uint64), wstats)
+
+
+@pytest.mark.parametrize("flags", [dict(), dict(c=12, fusion=0, diag=0), dict(c=13, fusion=0, diag=0)])
+def test_qft20_vs_reference(ref, qk, flags):
+    n = 20
+    cfg_text = config_text(n, 0, **flags)
+    prog = ref.optimize(ref.gen("qft", n), cfg_text)
+    for initial in (0, 0xA5A5A):
+        want, wl, _, _ = ref.simulate(prog, cfg_text, n, 0, initial, 8)
+        st, p2l, _ = run(qk, prog, cfg_text, initial)
+        assert np.max(np.abs(st - want.view(np.complex128))) < TOL
+        assert p2l == wl
+
+
+def test_qft24_vs_reference_unfused(ref, qk):
+    n = 24
+    cfg_text = config_text(n, 0, 12, fusion=0, diag=0)
+    prog = ref.optimize(ref.gen("qft", n), cfg_text)
+    want, wl, _, _ = ref.simulate(prog, cfg_text, n, 0, 0xA5A5A5, 8)
+    st, p2l, _ = run(qk, prog, cfg_text, 0xA5A5A5)
+    assert np.max(np.abs(st - want.view(np.complex128))) < TOL
+    assert abs(np.sum(np.abs(st) ** 2) - 1.0) < 1e-12
+
+
+def qft_expected(n, x, phys_to_log, idx):
+    """Closed form of genQft(n)|x> (no final swaps) at physical indices idx."""
+    logical = np.zeros_like(idx)
+    for p, l in enumerate(phys_to_log):
+        logical |= ((idx >> p) & 1) << l
+    rev = int(format(x, f"0{n}b")[::-1], 2)
+    ph = (rev * logical) % (1 << n)
+    return 2.0 ** (-n / 2) * np.exp(2j * np.pi * ph / (1 << n))
+
+
+@pytest.mark.parametrize("n", [26, 28])
+def test_qft_closed_form(qk, n):
+    cfg = qk.Config.make(n, 0, chunk=13, fusion=0, diag=0)
+    prog = qk.Program.optimize(qk.generate("qft", n), cfg)
+    x = 0x2C3B5A1 & ((1 << n) - 1)
+    st = qk.State(n)
+    st.simulate(prog, x)
+    p2l = prog.final_layout()
+    rng = np.random.default_rng(n)
+    for off in (0, (1 << n) - (1 << 20), int(rng.integers(0, (1 << n) - (1 << 20)))):
+        got = st.download(off, 1 << 20)
+        want = qft_expected(n, x, p2l, np.arange(off, off + (1 << 20), dtype=np.int64))
+        assert np.max(np.abs(got - want)) < TOL
+    assert abs(st.norm() - 1.0) < 1e-12
+
+
+def test_bv_closed_form(qk):
+    n = 26
+    cfg = qk.Config.make(n, 0, chunk=12)
+    prog = qk.Program.optimize(qk.generate("bvones", n), cfg)
+    st = qk.State(n)
+    st.simulate(prog, 0)
+    p2l = prog.final_layout()
+    l2p = {l: p for p, l in enumerate(p2l)}
+    secret = (1 << (n - 1)) - 1
+    idx = lambda logical: sum(((logical >> l) & 1) << l2p[l] for l in range(n))  # noqa: E731
+    a = st.download(idx(secret), 1)[0]
+    b = st.download(idx(secret | (1 << (n - 1))), 1)[0]
+    assert abs(a - 1 / np.sqrt(2)) < TOL and abs(b + 1 / np.sqrt(2)) < TOL
+    assert abs(st.norm() - 1.0) < 1e-12
+
+
+def test_grover_closed_form(qk):
+    n = 20
+    m = (n + 2) // 2
+    marked = 0x2A5 & ((1 << m) - 1)
+    circ = qk.generate("grover", n, 0, marked)
+    cfg = qk.Config.make(n, 0, chunk=12, fusion=0, diag=0)
+    prog = qk.Program.optimize(circ, cfg)
+    st, p2l = qk.simulate_program(prog)
+    k = int(np.floor(np.pi / 4 * np.sqrt(2 ** m)))
+    th = np.arcsin(2 ** (-m / 2))
+    logical = np.zeros(1 << n, dtype=np.complex128)
+    idx = np.arange(1 << n)
+    lg = np.zeros_like(idx)
+    for p, l in enumerate(p2l):
+        lg |= ((idx >> p) & 1) << l
+    logical[lg] = st
+    sign = (-1) ** k
+    data = logical[: 1 << m]
+    assert abs(data[marked] - sign * np.sin((2 * k + 1) * th)) < TOL
+    others = np.delete(data, marked)
+    assert np.max(np.abs(others - sign * np.cos((2 * k + 1) * th) / np.sqrt(2 ** m - 1))) < TOL
+    assert np.max(np.abs(logical[1 << m:])) < TOL  # ancillas back at |0>
