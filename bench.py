@@ -1,0 +1,344 @@
+#!/usr/bin/env python3
+"""Benchmark: QFT state-vector simulation, weak-scaled 2^33 amplitudes per GPU
+(33 qubits @ 1 GPU ... 36 qubits @ 8 GPUs), BASELINE.json's headline metric
+"circuit sim time (s)".
+
+One step = one full simulation of the program (initState + every block / IMS /
+XRS item) on resident HBM state — exactly what the reference times
+(proj/tools/main.cpp:126-145: wall from initState to the last item; parse and
+optimize excluded).  Lower is better.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...   (one process per GPU)
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "circuit sim time (s) and roofline fraction, 33q@1 GPU to 36q@8 GPU vs CPU ref"
+PER_GPU_QUBITS = 33
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--circuit", default="qft", help="qft | bvones | qaoa | random | grover")
+    ap.add_argument("--per-gpu-qubits", type=int, default=PER_GPU_QUBITS)
+    ap.add_argument("--chunk", type=int, default=13)
+    ap.add_argument("--cpu-sample-qubits", type=int, default=25)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def circuit_args(kind, n):
+    return {"qft": (0, 0), "bvones": (0, 0), "qaoa": (1, 1), "random": (400, 7), "grover": (1, 5)}[kind]
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.proc = None
+        self.gpu = gpu_index
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            os.makedirs(os.path.dirname(self.path), exist_ok=True)
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=self.fh, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8 and parts[0].replace(".", "").isdigit():
+                rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = sorted(float(r[0]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(rows[0][1]), "reasons": reasons,
+                "samples": len(rows), "power_w_max": max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())}
+
+
+# ------------------------------------------------------------------ peaks
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return d.get("hbm_gbs", 6650.0), "measured"
+    return 6650.0, "fallback"
+
+
+def ncu_traffic():
+    path = os.path.join(ROOT, "profiles", "block_pass_traffic.json")
+    if os.path.exists(path):
+        return json.load(open(path))
+    return None
+
+
+# ------------------------------------------------------------------ CPU baseline
+
+def cpu_reference_sample(kind, n_target, chunk, n_sample, threads):
+    """Reference simulateProgram (oracle/_ref, the unmodified reference build) on
+    the same circuit family at n_sample qubits with the same config family,
+    scaled to n_target by amplitude-passes: the reference's cost per item is
+    linear in the slice size (every block / IMS item sweeps every amplitude)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import Ref, config_text
+    import paper_2409_14697_b200 as qk
+    ref = Ref()
+    a, seed = circuit_args(kind, n_sample)
+    cfg_s = config_text(n_sample, 0, min(chunk, n_sample), fusion=0, diag=0)
+    prog_s = ref.optimize(ref.gen(kind, n_sample, a, seed), cfg_s)
+    t0 = time.perf_counter()
+    _, _, _, sec = ref.simulate(prog_s, cfg_s, n_sample, 0, 0, threads)
+    wall = time.perf_counter() - t0
+    # amplitude-passes of the sample and of the target program
+    def passes(text):
+        blocks = swaps = 0
+        lines = text.splitlines()
+        i = 0
+        while i < len(lines):
+            k = int(lines[i])
+            if lines[i + 1].startswith(("SQS", "CSQS")):
+                swaps += 1
+            else:
+                blocks += 1
+            i += 1 + k
+        return blocks + swaps
+    a2, seed2 = circuit_args(kind, n_target)
+    cfg_t = qk.Config.make(n_target, 0, chunk=chunk, fusion=0, diag=0)
+    prog_t = qk.Program.optimize(qk.generate(kind, n_target, a2, seed2), cfg_t).text()
+    scale = (2.0 ** n_target * passes(prog_t)) / (2.0 ** n_sample * passes(prog_s))
+    return sec * scale, sec, wall, scale, passes(prog_s), passes(prog_t)
+
+
+# ------------------------------------------------------------------ main
+
+def main():
+    args = parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and world > 1:
+        args.gpus = world
+    R = int(round(math.log2(max(1, args.gpus))))
+    n = args.per_gpu_qubits + R
+    kind = args.circuit
+
+    if args.impl == "reference":
+        return run_reference(args, rank, n, R, kind)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2409_14697_b200 as qk
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    a, seed = circuit_args(kind, n)
+    circ = qk.generate(kind, n, a, seed)
+    cfg = qk.Config.make(n, R, chunk=args.chunk, fusion=0, diag=0)
+    t0 = time.perf_counter()
+    prog = qk.Program.optimize(circ, cfg)
+    opt_s = time.perf_counter() - t0
+    counts = prog.counts()
+    prog_text = prog.text()
+
+    st = qk.State(n, R, rank, cfg.buffer_qubits, local_rank)
+    if world > 1:
+        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(qk.comm_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        st.comm_init(bytes(uid.cpu().numpy().tobytes()), world, rank)
+
+    ext = torch.cuda.ExternalStream(st.stream())
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        st.simulate(prog, 0)
+    barrier()
+
+    st.set_profiling(True)
+    stats = []
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        ev0.record(ext)
+        for _ in range(args.steps):
+            stats.append(st.simulate(prog, 0))
+        ev1.record(ext)
+        barrier()
+    st.set_profiling(False)
+    dev_ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([dev_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    clocks = clk.summary()
+
+    # End to end through the C-ABI with host buffers: program text -> parse ->
+    # device tables (H2D) -> simulate -> norm + 2^20-amplitude window (D2H).
+    import numpy as np
+    window = 1 << 20
+    host = torch.empty(window * 2, dtype=torch.float64).pin_memory().numpy().view(np.complex128)
+    e2e = []
+    for _ in range(max(1, min(args.steps, 3))):
+        barrier()
+        t1 = time.perf_counter()
+        p2 = qk.Program.parse(prog_text, cfg)
+        st.simulate(p2, 0)
+        nrm = st.norm()
+        st.download(0, window, out=host)
+        barrier()
+        e2e.append(time.perf_counter() - t1)
+        del p2
+    e2e_s = sorted(e2e)[len(e2e) // 2]
+    et = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+    e2e_s = float(et.item())
+
+    # Roofline of the dominant kernel (the fused block pass): algorithmic
+    # 32 B/amplitude per launch over its event-timed average.
+    s0 = stats[-1]
+    amps = 1 << (n - R)
+    peak, peak_src = measured_peaks()
+    blk_launch_ms = s0["block_ms"] / max(1, s0["block_launches"])
+    blk_gbs = 32.0 * amps / (blk_launch_ms * 1e-3) / 1e9
+    ims_launch_ms = s0["ims_ms"] / max(1, s0["ims_launches"]) if s0["ims_launches"] else 0.0
+    traffic = ncu_traffic()
+    # program-level roofline: T_roof = sum over items, HBM-bound
+    t_roof = (s0["block_bytes"] + s0["ims_bytes"]) / (peak * 1e9) + s0["xrs_bytes"] / 770e9
+
+    out = {
+        "metric": METRIC,
+        "value": round(ms_per_step / 1e3, 6),
+        "unit": "s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_per_step, 3),
+        "higher_is_better": False,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "c128 (fp64 complex)",
+        "data": "synthetic: generated circuit, |0> initial state",
+        "config": {"workload": f"{kind.upper()}-{n} ({kind}, {n} qubits, {1 << R} GPU(s), 2^{n - R} amps/GPU)",
+                   "n_qubits": n, "rank_qubits": R, "chunk_qubits": args.chunk, "fusion": 0,
+                   "diagonal_fusion": 0, "program": counts, "optimize_s": round(opt_s, 3),
+                   "l2": f"state {16 * amps / 2**30:.0f} GiB/GPU >> 126 MB L2: inputs larger than L2, no flush"},
+        "e2e": {"value": round(e2e_s, 6), "unit": "s", "h2d_bytes_per_step": len(prog_text.encode()),
+                "d2h_bytes_per_step": window * 16 + 8,
+                "path": "qk_program_parse + qk_simulate + qk_norm + qk_download(2^20 amps) via C-ABI"},
+        "gpu_launches": int(sum(x["kernel_launches"] for x in stats)),
+        "roofline": {"bound": "hbm", "kernel": "k_block_pass", "achieved": round(blk_gbs, 1),
+                     "peak": peak, "unit": "GB/s", "frac": round(blk_gbs / peak, 4),
+                     "peak_source": peak_src, "traffic": traffic,
+                     "algorithmic_bytes_per_launch": 32 * amps, "avg_launch_ms": round(blk_launch_ms, 3)},
+        "breakdown": {"block_ms": round(s0["block_ms"], 2), "ims_ms": round(s0["ims_ms"], 2),
+                      "xrs_ms": round(s0["xrs_ms"], 2), "block_launches": s0["block_launches"],
+                      "ims_launches": s0["ims_launches"], "xrs_rounds": s0["xrs_rounds"],
+                      "ims_avg_launch_ms": round(ims_launch_ms, 3),
+                      "ims_gbs": round(s0["ims_bytes"] / max(1e-9, s0["ims_ms"] * 1e-3) / 1e9, 1)
+                      if s0["ims_ms"] else None,
+                      "program_roofline_s": round(t_roof, 4),
+                      "program_roofline_frac": round(t_roof / (ms_per_step / 1e3), 4),
+                      "norm": nrm},
+        "clocks": clocks,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            threads = os.cpu_count() or 1
+            v, sec, wall, scale, ps, pt = cpu_reference_sample(kind, n, args.chunk, args.cpu_sample_qubits, threads)
+            out["cpu_baseline"] = {"value": round(v, 3), "unit": "s", "cores": threads, "kind": "reference",
+                                   "sample": f"reference simulateProgram (oracle/_ref) on {kind.upper()}-"
+                                             f"{args.cpu_sample_qubits} (C={min(args.chunk, args.cpu_sample_qubits)}, "
+                                             f"unfused, {ps} items) = {sec:.3f} s, scaled x{scale:.1f} by "
+                                             f"amplitude-passes to the {n}-qubit program ({pt} items)"}
+        except Exception as e:  # noqa: BLE001
+            out["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    st.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_reference(args, rank, n, R, kind):
+    """--impl reference: the reference's own CPU implementation (oracle/_ref =
+    /root/reference/proj/src compiled unmodified) on the host cores, rank 0 only."""
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, sec, wall, scale, ps, pt = cpu_reference_sample(kind, n, args.chunk, args.cpu_sample_qubits, threads)
+        if i >= args.warmup:
+            vals.append(v)
+    v = sum(vals) / len(vals)
+    out = {
+        "impl": "reference",
+        "metric": METRIC, "value": round(v, 3), "unit": "s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(v * 1e3, 1), "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "c128 (fp64 complex)",
+        "data": "synthetic: generated circuit, |0> initial state",
+        "config": {"workload": f"{kind.upper()}-{n} ({kind}, {n} qubits, {1 << R} GPU(s) equivalent)",
+                   "n_qubits": n, "chunk_qubits": args.chunk, "fusion": 0, "diagonal_fusion": 0},
+        "cpu_baseline": {"value": round(v, 3), "unit": "s", "cores": threads, "kind": "reference",
+                         "sample": f"reference simulateProgram on {kind.upper()}-{args.cpu_sample_qubits} "
+                                   f"({ps} items) x{scale:.1f} amplitude-pass scale to {n} qubits ({pt} items)"},
+        "e2e": {"value": round(v, 3), "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -170,7 +170,7 @@ def test_xrs_sweep_bitexact(ref, qk):
     for n in range(4, 11):
         for r in range(1, min(3, n - 1) + 1):
             region = n - r
-            for s in range(1, r + 1):
+            for s in range(1, min(r, region) + 1):
                 for b in sorted({s, (s + region) // 2, region}):
                     outs = sorted(int(x) for x in rng.choice(region, s, replace=False))
                     ins = sorted(int(x) for x in rng.choice(np.arange(region, n), s, replace=False))
