@@ -114,6 +114,7 @@ def lib():
         "qk_set_profiling": ([P, I], I),
         "qk_apply_block": ([P, C.POINTER(_Gate), I, I], I),
         "qk_apply_gate": ([P, C.POINTER(_Gate)], I),
+        "qk_debug_compile_block": ([C.POINTER(_Gate), I, I, C.POINTER(P)], I),
         "qk_ims_swap": ([P, C.POINTER(I), C.POINTER(I), I, I], I),
         "qk_xrs_swap_local": ([C.POINTER(P), I, C.POINTER(I), C.POINTER(I), I, C.POINTER(_XrsStats)], I),
         "qk_xrs_plan": ([I, I, I, I, C.POINTER(I), C.POINTER(I), I, C.POINTER(_XrsMsg), I,
@@ -394,6 +395,13 @@ def apply_block(state: State, gates, chunk_qubits: int) -> None:
     """applyBlock (engine.cpp:262-281) on a device slice."""
     arr, keep = _gate_array(gates)
     _check(lib().qk_apply_block(state._h, arr, len(keep), chunk_qubits))
+
+
+def debug_compile_block(gates, n_local: int) -> dict:
+    """The scheduler's pass programs for a block (host only; test hook)."""
+    import json
+    arr, keep = _gate_array(gates)
+    return json.loads(_text(lib().qk_debug_compile_block, arr, len(keep), n_local))
 
 
 def apply_gate(state: State, gate) -> None:

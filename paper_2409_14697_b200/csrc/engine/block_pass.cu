@@ -4,7 +4,7 @@
 // diag1/diag2 + inline CX/SWAP/D_k/U_k loops (proj/src/engine.cpp:189-281,
 // proj/src/kernels.cpp:16-48): instead of one sweep of a 2^C chunk per gate,
 // one CTA streams a 2^ct-amplitude tile from HBM ONCE, applies a whole run of
-// gates with the amplitudes held in registers (16 per thread), re-deals
+// gates with the amplitudes held in registers (2^rb per thread), re-deals
 // register bits through a swizzled shared-memory exchange only when a gate
 // needs a qubit that currently sits in the thread index, and writes the tile
 // back ONCE.  HBM traffic per pass: 32 B per amplitude, independent of the
@@ -45,131 +45,111 @@ __device__ __forceinline__ double2 coefAt(const PassParams& P, uint32_t i) {
     return make_double2(P.coef[2 * i], P.coef[2 * i + 1]);
 }
 
-using Regs = double2[kRegAmps];
+// ---- register-slot gate bodies (K, J compile-time slots, NA amplitudes) -----
 
-// ---- register-slot gate bodies (K, J compile-time slots) -------------------
-
-template <int K>
-__device__ __forceinline__ void opH(Regs& a) {
+template <int NA, int K>
+__device__ __forceinline__ void opH(double2 (&a)[NA]) {
+    if constexpr ((1 << K) < NA) {
 #pragma unroll
-    for (int s = 0; s < kRegAmps; s++)
-        if (!(s & (1 << K))) {
-            const double2 x = a[s], y = a[s | (1 << K)];
-            a[s] = cadd(x, y);
-            a[s | (1 << K)] = csub(x, y);
-        }
-}
-
-template <int K>
-__device__ __forceinline__ void opX(Regs& a) {
-#pragma unroll
-    for (int s = 0; s < kRegAmps; s++)
-        if (!(s & (1 << K))) {
-            const double2 t = a[s];
-            a[s] = a[s | (1 << K)];
-            a[s | (1 << K)] = t;
-        }
-}
-
-template <int K>
-__device__ __forceinline__ void opMat1(Regs& a, double2 m0, double2 m1, double2 m2, double2 m3) {
-#pragma unroll
-    for (int s = 0; s < kRegAmps; s++)
-        if (!(s & (1 << K))) {
-            const double2 x = a[s], y = a[s | (1 << K)];
-            a[s] = cmac(cmul(m0, x), m1, y);
-            a[s | (1 << K)] = cmac(cmul(m2, x), m3, y);
-        }
-}
-
-template <int K>
-__device__ __forceinline__ void opDiag1(Regs& a, double2 d0, double2 d1) {
-#pragma unroll
-    for (int s = 0; s < kRegAmps; s++) a[s] = cmul(a[s], (s & (1 << K)) ? d1 : d0);
-}
-
-// target slot K, control slot J
-template <int K, int J>
-__device__ __forceinline__ void opCxRR(Regs& a) {
-    if constexpr (K != J) {
-#pragma unroll
-        for (int s = 0; s < kRegAmps; s++)
-            if ((s & (1 << J)) && !(s & (1 << K))) {
-                const double2 t = a[s];
-                a[s] = a[s | (1 << K)];
-                a[s | (1 << K)] = t;
+        for (int s = 0; s < NA; s++)
+            if (!(s & (1 << K))) {
+                const double2 x = a[s], y = a[s | (1 << K)];
+                a[s] = cadd(x, y);
+                a[s | (1 << K)] = csub(x, y);
             }
+    }
+}
+
+__device__ __forceinline__ double selD(bool p, double x, double y) {
+    double r;
+    asm("{ .reg .pred q; setp.ne.u32 q, %3, 0; selp.f64 %0, %1, %2, q; }" : "=d"(r) : "d"(x), "d"(y), "r"(int(p)));
+    return r;
+}
+
+// Controlled swap of the slot-K pairs: a data-dependent select per pair, never
+// a register renaming (renaming inside the op switch makes ptxas copy the
+// whole register array every iteration).  cond(s) = control bit of s (slot
+// control: (s & cm) == cv) and thread-level condition `thr`.
+template <int NA, int K>
+__device__ __forceinline__ void opCx(double2 (&a)[NA], uint32_t cm, uint32_t cv, bool thr) {
+    if constexpr ((1 << K) < NA) {
+#pragma unroll
+        for (int s = 0; s < NA; s++)
+            if (!(s & (1 << K))) {
+                const bool c = thr && ((uint32_t(s) & cm) == cv);
+                const double2 x = a[s], y = a[s | (1 << K)];
+                a[s] = make_double2(selD(c, y.x, x.x), selD(c, y.y, x.y));
+                a[s | (1 << K)] = make_double2(selD(c, x.x, y.x), selD(c, x.y, y.y));
+            }
+    }
+}
+
+template <int NA, int K>
+__device__ __forceinline__ void opMat1(double2 (&a)[NA], double2 m0, double2 m1, double2 m2, double2 m3) {
+    if constexpr ((1 << K) < NA) {
+#pragma unroll
+        for (int s = 0; s < NA; s++)
+            if (!(s & (1 << K))) {
+                const double2 x = a[s], y = a[s | (1 << K)];
+                a[s] = cmac(cmul(m0, x), m1, y);
+                a[s | (1 << K)] = cmac(cmul(m2, x), m3, y);
+            }
+    }
+}
+
+template <int NA, int K>
+__device__ __forceinline__ void opDiag1(double2 (&a)[NA], double2 d0, double2 d1) {
+    if constexpr ((1 << K) < NA) {
+#pragma unroll
+        for (int s = 0; s < NA; s++) a[s] = cmul(a[s], (s & (1 << K)) ? d1 : d0);
+    }
+}
+
+// amplitudes whose slot-K bit is 1 *= e
+template <int NA, int K>
+__device__ __forceinline__ void opPhaseSlot(double2 (&a)[NA], double2 e) {
+    if constexpr ((1 << K) < NA) {
+#pragma unroll
+        for (int s = 0; s < NA; s++)
+            if (s & (1 << K)) a[s] = cmul(a[s], e);
     }
 }
 
 // MSB slot K, LSB slot J
-template <int K, int J>
-__device__ __forceinline__ void opDiag2RR(Regs& a, const double2 (&d)[4]) {
-    if constexpr (K != J) {
+template <int NA, int K, int J>
+__device__ __forceinline__ void opDiag2RR(double2 (&a)[NA], const double2 (&d)[4]) {
+    if constexpr (K != J && (1 << K) < NA && (1 << J) < NA) {
 #pragma unroll
-        for (int s = 0; s < kRegAmps; s++) a[s] = cmul(a[s], d[(((s >> K) & 1) << 1) | ((s >> J) & 1)]);
+        for (int s = 0; s < NA; s++) a[s] = cmul(a[s], d[(((s >> K) & 1) << 1) | ((s >> J) & 1)]);
     }
 }
 
-template <int K, int J>
-__device__ __forceinline__ void opCphaseRR(Regs& a, double2 e) {
-    if constexpr (K != J) {
+// amplitudes whose (slot K, slot J) bits equal (pat >> 1, pat & 1) *= e;
+// K < J, pattern already adjusted by the scheduler for any operand order.
+template <int NA, int K, int J>
+__device__ __forceinline__ void opCphaseRR(double2 (&a)[NA], double2 e, uint32_t pat) {
+    if constexpr (K < J && (1 << J) < NA) {
+        // Four candidate patterns; multiply only the matching quarter of the registers.
 #pragma unroll
-        for (int s = 0; s < kRegAmps; s++)
-            if ((s & (1 << K)) && (s & (1 << J))) a[s] = cmul(a[s], e);
-    }
-}
-
-template <int K>
-__device__ __forceinline__ void opCphaseR(Regs& a, double2 e) {
+        for (uint32_t p = 0; p < 4; p++)
+            if (p == pat) {
 #pragma unroll
-    for (int s = 0; s < kRegAmps; s++)
-        if (s & (1 << K)) a[s] = cmul(a[s], e);
-}
-
-template <int K, int J>
-__device__ __forceinline__ void opSwapRR(Regs& a) {
-    if constexpr (K < J) {
-#pragma unroll
-        for (int s = 0; s < kRegAmps; s++)
-            if ((s & (1 << K)) && !(s & (1 << J))) {
-                const int t = s ^ (1 << K) ^ (1 << J);
-                const double2 x = a[s];
-                a[s] = a[t];
-                a[t] = x;
+                for (int s = 0; s < NA; s++)
+                    if ((((s >> K) & 1) << 1 | ((s >> J) & 1)) == int(p)) a[s] = cmul(a[s], e);
             }
     }
 }
 
-// Fused dense 2^KK x 2^KK in canonical slots (target j at slot KK-1-j).
-// KK = 2 runs from registers; the matrix streams from the L1-cached table.
-template <int KK>
-__device__ __forceinline__ void opDenseReg(Regs& a, const double2* __restrict__ M) {
-    constexpr int D = 1 << KK, G = kRegAmps >> KK;
-#pragma unroll
-    for (int g = 0; g < G; g++) {
-        double2 out[D];
-#pragma unroll
-        for (int r = 0; r < D; r++) {
-            double2 acc = make_double2(0.0, 0.0);
-#pragma unroll
-            for (int s = 0; s < D; s++) acc = cmac(acc, __ldg(M + r * D + s), a[g * D + s]);
-            out[r] = acc;
-        }
-#pragma unroll
-        for (int r = 0; r < D; r++) a[g * D + r] = out[r];
-    }
-}
-
-// KK = 3, 4: inputs parked in this thread's column of shared memory
-// (layout [slot][thread], conflict-free), outputs accumulated into registers.
-template <int KK>
-__device__ __forceinline__ void opDenseSmem(Regs& a, const double2* __restrict__ M, double2* sm, int nt) {
-    constexpr int D = 1 << KK, G = kRegAmps >> KK;
+// Fused dense 2^KK x 2^KK in canonical slots (target j at slot KK-1-j):
+// inputs parked in this thread's column of shared memory (layout
+// [slot][thread], conflict-free), outputs accumulated back into registers.
+template <int NA, int KK>
+__device__ __forceinline__ void opDense(double2 (&a)[NA], const double2* __restrict__ M, double2* sm, int nt) {
+    constexpr int D = 1 << KK, G = NA >> KK;
     const int tid = threadIdx.x;
     __syncthreads();  // others may still read the exchange buffer
 #pragma unroll
-    for (int s = 0; s < kRegAmps; s++) sm[s * nt + tid] = a[s];
+    for (int s = 0; s < NA; s++) sm[s * nt + tid] = a[s];
 #pragma unroll
     for (int g = 0; g < G; g++)
 #pragma unroll
@@ -181,62 +161,112 @@ __device__ __forceinline__ void opDenseSmem(Regs& a, const double2* __restrict__
         }
 }
 
-#define QK_SLOT1(v, F, ...)               \
-    switch (v) {                          \
-        case 0: F<0>(__VA_ARGS__); break; \
-        case 1: F<1>(__VA_ARGS__); break; \
-        case 2: F<2>(__VA_ARGS__); break; \
-        default: F<3>(__VA_ARGS__); break; \
+#define QK_SLOT1(v, F, NA_, ...)                \
+    switch (v) {                                \
+        case 0: F<NA_, 0>(__VA_ARGS__); break;  \
+        case 1: F<NA_, 1>(__VA_ARGS__); break;  \
+        case 2: F<NA_, 2>(__VA_ARGS__); break;  \
+        case 3: F<NA_, 3>(__VA_ARGS__); break;  \
+        default: F<NA_, 4>(__VA_ARGS__); break; \
     }
-#define QK_SLOT2_INNER(K, w, F, ...)         \
-    switch (w) {                             \
-        case 0: F<K, 0>(__VA_ARGS__); break; \
-        case 1: F<K, 1>(__VA_ARGS__); break; \
-        case 2: F<K, 2>(__VA_ARGS__); break; \
-        default: F<K, 3>(__VA_ARGS__); break; \
+#define QK_SLOT2_INNER(K, w, F, NA_, ...)          \
+    switch (w) {                                   \
+        case 0: F<NA_, K, 0>(__VA_ARGS__); break;  \
+        case 1: F<NA_, K, 1>(__VA_ARGS__); break;  \
+        case 2: F<NA_, K, 2>(__VA_ARGS__); break;  \
+        case 3: F<NA_, K, 3>(__VA_ARGS__); break;  \
+        default: F<NA_, K, 4>(__VA_ARGS__); break; \
     }
-#define QK_SLOT2(v, w, F, ...)                                 \
-    switch (v) {                                               \
-        case 0: QK_SLOT2_INNER(0, w, F, __VA_ARGS__) break;    \
-        case 1: QK_SLOT2_INNER(1, w, F, __VA_ARGS__) break;    \
-        case 2: QK_SLOT2_INNER(2, w, F, __VA_ARGS__) break;    \
-        default: QK_SLOT2_INNER(3, w, F, __VA_ARGS__) break;   \
+#define QK_SLOT2(v, w, F, NA_, ...)                                \
+    switch (v) {                                                   \
+        case 0: QK_SLOT2_INNER(0, w, F, NA_, __VA_ARGS__) break;   \
+        case 1: QK_SLOT2_INNER(1, w, F, NA_, __VA_ARGS__) break;   \
+        case 2: QK_SLOT2_INNER(2, w, F, NA_, __VA_ARGS__) break;   \
+        case 3: QK_SLOT2_INNER(3, w, F, NA_, __VA_ARGS__) break;   \
+        default: QK_SLOT2_INNER(4, w, F, NA_, __VA_ARGS__) break;  \
     }
+
+template <int RB>
+__device__ __forceinline__ uint64_t slotOffset(int s, const uint64_t (&st)[RB]) {
+    uint64_t o = 0;
+#pragma unroll
+    for (int k = 0; k < RB; k++) o |= ((s >> k) & 1) ? st[k] : 0;
+    return o;
+}
+template <int RB>
+__device__ __forceinline__ uint32_t slotOffset(int s, const uint32_t (&st)[RB]) {
+    uint32_t o = 0;
+#pragma unroll
+    for (int k = 0; k < RB; k++) o ^= ((s >> k) & 1) ? st[k] : 0;
+    return o;
+}
 
 // Global offset of this thread's slot-0 amplitude and per-slot strides under map m.
-template <int CT>
+template <int CT, int RB>
 __device__ __forceinline__ void globalLayout(const PassParams& P, const uint8_t* m, uint32_t tid, uint64_t& off,
-                                             uint64_t (&stride)[kRegBits]) {
+                                             uint64_t (&stride)[RB]) {
     off = 0;
 #pragma unroll
-    for (int j = 0; j < CT - kRegBits; j++) off |= uint64_t((tid >> j) & 1u) << P.tile_phys[m[kRegBits + j]];
+    for (int j = 0; j < CT - RB; j++) off |= uint64_t((tid >> j) & 1u) << P.tile_phys[m[RB + j]];
 #pragma unroll
-    for (int k = 0; k < kRegBits; k++) stride[k] = uint64_t(1) << P.tile_phys[m[k]];
+    for (int k = 0; k < RB; k++) stride[k] = uint64_t(1) << P.tile_phys[m[k]];
 }
 
-template <int CT>
-__device__ __forceinline__ void smemLayout(const uint8_t* m, uint32_t tid, uint32_t& u, uint32_t (&su)[kRegBits]) {
+template <int CT, int RB>
+__device__ __forceinline__ void smemLayout(const uint8_t* m, uint32_t tid, uint32_t& u, uint32_t (&su)[RB]) {
     uint32_t t = 0;
 #pragma unroll
-    for (int j = 0; j < CT - kRegBits; j++) t |= ((tid >> j) & 1u) << m[kRegBits + j];
+    for (int j = 0; j < CT - RB; j++) t |= ((tid >> j) & 1u) << m[RB + j];
     u = swz(t);
 #pragma unroll
-    for (int k = 0; k < kRegBits; k++) su[k] = swz(1u << m[k]);
+    for (int k = 0; k < RB; k++) su[k] = swz(1u << m[k]);
 }
 
-__device__ __forceinline__ uint64_t slotOffset(int s, const uint64_t (&st)[kRegBits]) {
-    return ((s & 1) ? st[0] : 0) | ((s & 2) ? st[1] : 0) | ((s & 4) ? st[2] : 0) | ((s & 8) ? st[3] : 0);
-}
-__device__ __forceinline__ uint32_t slotOffset(int s, const uint32_t (&st)[kRegBits]) {
-    return ((s & 1) ? st[0] : 0) ^ ((s & 2) ? st[1] : 0) ^ ((s & 4) ? st[2] : 0) ^ ((s & 8) ? st[3] : 0);
+__host__ __device__ constexpr int lowBit(int x) { return (x & 1) ? 0 : 1 + lowBit(x >> 1); }
+
+// a[s] *= scale * P * prod_{k: bit k of s} R[k]; done as (low 2 slots) x (high slots)
+// factor tables so each amplitude costs ~2 complex multiplies.
+template <int RB>
+__device__ __forceinline__ void flushAll(double2 (&a)[1 << RB], double2 P, double scale, double2 (&R)[RB]) {
+    constexpr int NA = 1 << RB;
+    const double2 base = make_double2(P.x * scale, P.y * scale);
+    if constexpr (RB < 2) {
+#pragma unroll
+        for (int s = 0; s < NA; s++) {
+            double2 f = base;
+            if (s & 1) f = cmul(f, R[0]);
+            a[s] = cmul(a[s], f);
+        }
+    } else {
+        double2 lo[4];
+        lo[0] = base;
+        lo[1] = cmul(base, R[0]);
+        lo[2] = cmul(base, R[1]);
+        lo[3] = cmul(lo[1], R[1]);
+        constexpr int NH = NA >> 2;
+        double2 hi[NH];
+        hi[0] = make_double2(1.0, 0.0);
+#pragma unroll
+        for (int h = 1; h < NH; h++) {
+            const int low = lowBit(h);
+            hi[h] = (h & (h - 1)) ? cmul(hi[h & (h - 1)], R[2 + low]) : R[2 + low];
+        }
+#pragma unroll
+        for (int h = 0; h < NH; h++)
+#pragma unroll
+            for (int l = 0; l < 4; l++) a[h * 4 + l] = cmul(a[h * 4 + l], h ? cmul(lo[l], hi[h]) : lo[l]);
+    }
+#pragma unroll
+    for (int k = 0; k < RB; k++) R[k] = make_double2(1.0, 0.0);
 }
 
 }  // namespace
 
-template <int CT>
-__global__ void __launch_bounds__(1 << (CT - kRegBits), 1)
+template <int CT, int RB>
+__global__ void __launch_bounds__(1 << (CT - RB), 1)
     k_block_pass(double2* __restrict__ state, const double2* __restrict__ gtab, const __grid_constant__ PassParams P) {
-    constexpr int NT = 1 << (CT - kRegBits);
+    constexpr int NT = 1 << (CT - RB);
+    constexpr int NA = 1 << RB;
     extern __shared__ double2 sm[];
     const uint32_t tid = threadIdx.x;
 
@@ -248,123 +278,152 @@ __global__ void __launch_bounds__(1 << (CT - kRegBits), 1)
         base = ((base >> p) << (p + 1)) | (base & ((uint64_t(1) << p) - 1));
     }
 
-    Regs a;
+    double2 a[NA];
     {
-        uint64_t off, st[kRegBits];
-        globalLayout<CT>(P, P.map_in[0], tid, off, st);
-        off += base;
+        uint64_t off, st[RB];
+        globalLayout<CT, RB>(P, P.map_in[0], tid, off, st);
+        off |= base;
 #pragma unroll
-        for (int s = 0; s < kRegAmps; s++) a[s] = state[off | slotOffset(s, st)];
+        for (int s = 0; s < NA; s++) a[s] = __ldcs(state + (off | slotOffset<RB>(s, st)));
     }
 
-    double2 scal = make_double2(1.0, 0.0);  // pending per-thread factor (thread-bit-only diagonals)
-    int op = 0;
-    for (int sg = 0; sg < P.nsegs; sg++) {
-        if (sg > 0) {  // re-deal register bits through shared memory
-            uint32_t u, su[kRegBits];
-            __syncthreads();
-            smemLayout<CT>(P.map_out[sg - 1], tid, u, su);
+    double2 Pt = make_double2(1.0, 0.0);  // pending per-thread scalar
+    double2 R[RB];                         // pending per-slot phases (amplitudes with slot bit 1)
 #pragma unroll
-            for (int s = 0; s < kRegAmps; s++) sm[u ^ slotOffset(s, su)] = a[s];
-            __syncthreads();
-            smemLayout<CT>(P.map_in[sg], tid, u, su);
-#pragma unroll
-            for (int s = 0; s < kRegAmps; s++) a[s] = sm[u ^ slotOffset(s, su)];
-        }
-        const int end = P.seg_end[sg];
-        for (; op < end; op++) {
+    for (int k = 0; k < RB; k++) R[k] = make_double2(1.0, 0.0);
+
+    // One flat loop over the ops (a nested segment loop makes ptxas re-copy
+    // the whole register array at every iteration).
+    const int nops = P.nops;
+    for (int op = 0; op < nops; op++) {
+        {
             const DevOp o = P.ops[op];
             switch (o.type) {
-                case OP_H: QK_SLOT1(o.a, opH, a) break;
-                case OP_X: QK_SLOT1(o.a, opX, a) break;
+                case OP_EXCHANGE: {  // re-deal register bits through shared memory
+                    uint32_t u, su[RB];
+                    __syncthreads();
+                    smemLayout<CT, RB>(P.map_out[o.c - 1], tid, u, su);
+                    u ^= swz(P.xmask_out[o.c - 1]);  // flipped slots (X relabels)
+#pragma unroll
+                    for (int s = 0; s < NA; s++) sm[u ^ slotOffset<RB>(s, su)] = a[s];
+                    __syncthreads();
+                    smemLayout<CT, RB>(P.map_in[o.c], tid, u, su);
+#pragma unroll
+                    for (int s = 0; s < NA; s++) a[s] = sm[u ^ slotOffset<RB>(s, su)];
+                    break;
+                }
+                case OP_H: QK_SLOT1(o.a, opH, NA, a) break;
                 case OP_MAT1: {
                     const double2 m0 = coefAt(P, o.c), m1 = coefAt(P, o.c + 1), m2 = coefAt(P, o.c + 2),
                                   m3 = coefAt(P, o.c + 3);
-                    QK_SLOT1(o.a, opMat1, a, m0, m1, m2, m3)
+                    QK_SLOT1(o.a, opMat1, NA, a, m0, m1, m2, m3)
                     break;
                 }
-                case OP_CX_RR: QK_SLOT2(o.a, o.b, opCxRR, a) break;
-                case OP_CX_RT:
-                    if ((tid >> o.b) & 1u) QK_SLOT1(o.a, opX, a)
+                case OP_CX: {
+                    const uint32_t pol = (o.k >> 1) & 1u;
+                    uint32_t cm = 0, cv = 0;
+                    bool thr = true;
+                    if (o.k & 1u) thr = (((tid >> o.b) & 1u) ^ pol) != 0;
+                    else {
+                        cm = 1u << o.b;
+                        cv = (1u ^ pol) << o.b;
+                    }
+                    QK_SLOT1(o.a, opCx, NA, a, cm, cv, thr)
                     break;
+                }
                 case OP_DIAG1_R: {
                     const double2 d0 = coefAt(P, o.c), d1 = coefAt(P, o.c + 1);
-                    QK_SLOT1(o.a, opDiag1, a, d0, d1)
+                    QK_SLOT1(o.a, opDiag1, NA, a, d0, d1)
                     break;
                 }
-                case OP_DIAG1_T:
-                    scal = cmul(scal, coefAt(P, o.c + ((tid >> o.a) & 1u)));
-                    break;
                 case OP_DIAG2_RR: {
                     const double2 d[4] = {coefAt(P, o.c), coefAt(P, o.c + 1), coefAt(P, o.c + 2), coefAt(P, o.c + 3)};
-                    QK_SLOT2(o.a, o.b, opDiag2RR, a, d)
+                    QK_SLOT2(o.a, o.b, opDiag2RR, NA, a, d)
                     break;
                 }
-                case OP_DIAG2_RT: {
-                    const uint32_t tb = (tid >> o.b) & 1u;
-                    // thread bit MSB: entries (2tb, 2tb+1); thread bit LSB: (tb, 2+tb)
-                    const double2 d0 = coefAt(P, o.c + (o.k ? 2 * tb : tb));
-                    const double2 d1 = coefAt(P, o.c + (o.k ? 2 * tb + 1 : 2 + tb));
-                    QK_SLOT1(o.a, opDiag1, a, d0, d1)
-                    break;
-                }
-                case OP_DIAG2_TT:
-                    scal = cmul(scal, coefAt(P, o.c + ((((tid >> o.a) & 1u) << 1) | ((tid >> o.b) & 1u))));
-                    break;
                 case OP_CPHASE_RR: {
                     const double2 e = coefAt(P, o.c);
-                    QK_SLOT2(o.a, o.b, opCphaseRR, a, e)
+                    const uint32_t pat = o.k;
+                    QK_SLOT2(o.a, o.b, opCphaseRR, NA, a, e, pat)
                     break;
                 }
-                case OP_CPHASE_RT:
-                    if ((tid >> o.b) & 1u) {
-                        const double2 e = coefAt(P, o.c);
-                        QK_SLOT1(o.a, opCphaseR, a, e)
-                    }
+                case OP_PEND_R: {
+                    const double2 e = coefAt(P, o.c);
+#pragma unroll
+                    for (int k = 0; k < RB; k++)
+                        if (k == o.a) R[k] = cmul(R[k], e);
                     break;
-                case OP_CPHASE_TT:
-                    if (((tid >> o.a) & (tid >> o.b)) & 1u) scal = cmul(scal, coefAt(P, o.c));
+                }
+                case OP_PEND_RT: {
+                    const double2 e = coefAt(P, o.c + ((tid >> o.b) & 1u));
+#pragma unroll
+                    for (int k = 0; k < RB; k++)
+                        if (k == o.a) R[k] = cmul(R[k], e);
+                    break;
+                }
+                case OP_SCAL: Pt = cmul(Pt, coefAt(P, o.c)); break;
+                case OP_SCAL_T: Pt = cmul(Pt, coefAt(P, o.c + ((tid >> o.a) & 1u))); break;
+                case OP_SCAL_TT:
+                    Pt = cmul(Pt, coefAt(P, o.c + ((((tid >> o.a) & 1u) << 1) | ((tid >> o.b) & 1u))));
+                    break;
+                case OP_FLUSH_SLOT: {
+                    double2 e = R[0];
+#pragma unroll
+                    for (int k = 1; k < RB; k++)
+                        if (k == o.a) e = R[k];
+                    QK_SLOT1(o.a, opPhaseSlot, NA, a, e)
+#pragma unroll
+                    for (int k = 0; k < RB; k++)
+                        if (k == o.a) R[k] = make_double2(1.0, 0.0);
+                    break;
+                }
+                case OP_FLUSH:
+                    flushAll<RB>(a, Pt, P.coef[2 * o.c], R);
+                    Pt = make_double2(1.0, 0.0);
                     break;
                 case OP_DTABLE: {
                     const uint16_t* cb = &P.contrib[o.c16];
+                    const uint32_t flipx = o.x16;
                     uint32_t sub = 0;
 #pragma unroll
-                    for (int j = kRegBits; j < CT; j++)
-                        if ((tid >> (j - kRegBits)) & 1u) sub |= cb[j];
-                    const uint32_t c0 = cb[0], c1 = cb[1], c2 = cb[2], c3 = cb[3];
+                    for (int j = RB; j < CT; j++)
+                        if ((tid >> (j - RB)) & 1u) sub |= cb[j];
+                    uint32_t cr[RB];
+#pragma unroll
+                    for (int k = 0; k < RB; k++) cr[k] = cb[k];
                     const double2* tab = gtab + o.c;
 #pragma unroll
-                    for (int s = 0; s < kRegAmps; s++) {
-                        const uint32_t i = sub | ((s & 1) ? c0 : 0) | ((s & 2) ? c1 : 0) | ((s & 4) ? c2 : 0) |
-                                           ((s & 8) ? c3 : 0);
-                        a[s] = cmul(a[s], __ldg(tab + i));
+                    for (int s = 0; s < NA; s++) {
+                        uint32_t i = sub;
+#pragma unroll
+                        for (int k = 0; k < RB; k++) i |= ((s >> k) & 1) ? cr[k] : 0u;
+                        a[s] = cmul(a[s], __ldg(tab + (i ^ flipx)));
                     }
                     break;
                 }
                 case OP_DENSE:
-                    if (o.k == 2) opDenseReg<2>(a, gtab + o.c);
-                    else if (o.k == 3) opDenseSmem<3>(a, gtab + o.c, sm, NT);
-                    else opDenseSmem<4>(a, gtab + o.c, sm, NT);
+                    if constexpr (RB >= 2) {
+                        if (o.k == 2) opDense<NA, 2>(a, gtab + o.c, sm, NT);
+                        else if constexpr (RB >= 3) {
+                            if (o.k == 3) opDense<NA, 3>(a, gtab + o.c, sm, NT);
+                            else if constexpr (RB >= 4) opDense<NA, 4>(a, gtab + o.c, sm, NT);
+                        }
+                    }
                     break;
-                case OP_FLUSH: {
-                    const double2 f = make_double2(scal.x * P.coef[2 * o.c], scal.y * P.coef[2 * o.c]);
-#pragma unroll
-                    for (int s = 0; s < kRegAmps; s++) a[s] = cmul(a[s], f);
-                    scal = make_double2(1.0, 0.0);
-                    break;
-                }
-                case OP_SWAP_RR: QK_SLOT2(o.a, o.b, opSwapRR, a) break;
                 default: break;
             }
         }
     }
 
     {
-        uint64_t off, st[kRegBits];
-        globalLayout<CT>(P, P.map_out[P.nsegs - 1], tid, off, st);
-        off += base;
+        uint64_t off, st[RB];
+        globalLayout<CT, RB>(P, P.map_out[P.nsegs - 1], tid, off, st);
+        off |= base;
+        const uint32_t xm = P.xmask_out[P.nsegs - 1];  // flipped slots (X relabels)
 #pragma unroll
-        for (int s = 0; s < kRegAmps; s++) state[off | slotOffset(s, st)] = a[s];
+        for (int j = 0; j < CT; j++) off ^= uint64_t((xm >> j) & 1u) << P.tile_phys[j];
+#pragma unroll
+        for (int s = 0; s < NA; s++) __stcs(state + (off ^ slotOffset<RB>(s, st)), a[s]);
     }
 }
 
@@ -405,18 +464,21 @@ __global__ void k_dense_group(double2* __restrict__ state, const double2* __rest
 template <int CT>
 static cudaError_t launchCT(double2* state, const double2* gtab, const PassParams& P, uint64_t ctas,
                             cudaStream_t stream) {
-    constexpr int NT = 1 << (CT - kRegBits);
+    constexpr int RB = regBitsFor(CT);
+    constexpr int NT = 1 << (CT - RB);
     const size_t smem = sizeof(double2) << CT;
     if (smem > 48 * 1024) {  // per-device attribute; cheap to re-apply
-        cudaError_t e = cudaFuncSetAttribute(k_block_pass<CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        cudaError_t e = cudaFuncSetAttribute(k_block_pass<CT, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             int(smem));
         if (e != cudaSuccess) return e;
     }
-    k_block_pass<CT><<<dim3(unsigned(ctas)), NT, smem, stream>>>(state, gtab, P);
+    k_block_pass<CT, RB><<<dim3(unsigned(ctas)), NT, smem, stream>>>(state, gtab, P);
     return cudaGetLastError();
 }
 
 cudaError_t launchBlockPass(double2* state, const double2* gtab, const PassParams& P, int nLocal,
                             cudaStream_t stream) {
+    if (P.rb != regBitsFor(P.ct)) return cudaErrorInvalidValue;
     const uint64_t ctas = uint64_t(1) << (nLocal - P.ct);
     switch (P.ct) {
         case 4: return launchCT<4>(state, gtab, P, ctas, stream);

@@ -4,12 +4,21 @@
 // One "pass" = one read + one write of the whole slice in HBM.  The kernel
 // runs one CTA per tile of 2^ct amplitudes; a tile is the set of indices that
 // vary over `ct` chosen physical bits (`tile_phys`, ascending) with all other
-// bits fixed by the CTA index.  Inside the CTA each thread keeps 16 amplitudes
-// in registers: 4 tile bits are "register slots" (0..3) and the remaining
-// ct-4 tile bits are thread-index bits (slots 4..ct-1: lane bits first, then
-// warp bits).  `maps[seg][slot]` = tile bit held by that slot.  Gates run
-// in registers; a segment boundary is a shared-memory exchange that re-deals
-// which tile bits sit in registers.
+// bits fixed by the CTA index.  Inside the CTA each thread keeps 2^rb
+// amplitudes in registers: rb tile bits are "register slots" (0..rb-1) and the
+// remaining ct-rb tile bits are thread-index bits (slots rb..ct-1: lane bits
+// first, then warp bits).  `map_*[seg][slot]` = tile bit held by that slot.
+// Gates run in registers; a segment boundary is a shared-memory exchange that
+// re-deals which tile bits sit in registers.  X gates never move data: the
+// scheduler tracks which slots hold a flipped bit and `xmask_out` corrects the
+// exchange / store addresses (register renaming inside the op loop would make
+// ptxas copy the whole register array every iteration).
+//
+// Diagonal factors that depend on thread-index bits are not applied to the
+// registers when they occur: each thread accumulates them into one scalar P
+// and one "pending phase" R[a] per register slot (applied to the amplitudes
+// whose slot-a bit is 1).  They are flushed into the registers only when a
+// non-diagonal op touches slot a, or at an exchange / the final store.
 //
 // The struct is passed BY VALUE as a __grid_constant__ kernel parameter
 // (CUDA >= 12.1 allows 32 764 B), so every op/coefficient read is a uniform
@@ -21,49 +30,53 @@
 
 namespace qkdev {
 
-constexpr int kRegBits = 4;                 // register slots per thread
-constexpr int kRegAmps = 1 << kRegBits;     // amplitudes per thread
+constexpr int kMaxRegBits = 5;              // register slots per thread (rb <= 5)
 constexpr int kMaxTileBits = 13;            // 2^13 x 16 B = 128 KiB of smem
-constexpr int kMaxOps = 640;
-constexpr int kMaxCoef = 900;               // complex coefficients (double2)
+constexpr int kMaxOps = 700;
+constexpr int kMaxCoef = 860;               // complex coefficients (double2)
 constexpr int kMaxSegs = 96;
 constexpr int kMaxContrib = 512;            // uint16 words for fused-diagonal index maps
 
+// Register bits used for a tile of ct bits: 16 amplitudes per thread up to
+// ct = 12 (<= 256 threads, no register cap), 32 per thread at ct = 13 (256
+// threads x <= 255 registers: the 2^13-amplitude tile never spills).
+constexpr int regBitsFor(int ct) { return ct >= 13 ? 5 : (ct < 4 ? ct : 4); }
+
 enum OpType : uint8_t {
     OP_MAT1 = 0,      // a = slot; coef[c..c+3] = 2x2 row-major
-    OP_H,             // a = slot; butterfly without the 1/sqrt2 (folded into the flush scale)
-    OP_X,             // a = slot; register swap
-    OP_CX_RR,         // a = target slot, b = control slot
-    OP_CX_RT,         // a = target slot, b = control thread bit
-    OP_DIAG1_R,       // a = slot; coef[c], coef[c+1]
-    OP_DIAG1_T,       // a = thread bit; coef[c], coef[c+1] -> per-thread scalar
-    OP_DIAG2_RR,      // a = MSB slot, b = LSB slot; coef[c..c+3]
-    OP_DIAG2_RT,      // a = slot, b = thread bit, k = 1 if the thread bit is the MSB; coef[c..c+3]
-    OP_DIAG2_TT,      // a = MSB thread bit, b = LSB thread bit; coef[c..c+3]
-    OP_CPHASE_RR,     // a, b = slots; coef[c] applied where both bits are 1
-    OP_CPHASE_RT,     // a = slot, b = thread bit; coef[c]
-    OP_CPHASE_TT,     // a, b = thread bits; coef[c]
+    OP_H,             // a = slot; butterfly without 1/sqrt2 (folded into the final scale)
+    OP_CX,            // a = target slot; k bit0: control is thread bit b (else slot b); k bit1: control polarity
+    OP_DIAG1_R,       // a = slot; coef[c], coef[c+1] applied directly
+    OP_DIAG2_RR,      // a = MSB slot, b = LSB slot; coef[c..c+3] applied directly
+    OP_CPHASE_RR,     // a = MSB slot, b = LSB slot; coef[c] where (bit a, bit b) == pattern k
+    OP_PEND_R,        // R[a] *= coef[c]
+    OP_PEND_RT,       // R[a] *= coef[c + bit_b(thread)]
+    OP_SCAL,          // P *= coef[c]
+    OP_SCAL_T,        // P *= coef[c + bit_a(thread)]
+    OP_SCAL_TT,       // P *= coef[c + 2 bit_a(thread) + bit_b(thread)]
+    OP_FLUSH_SLOT,    // amplitudes with slot-a bit 1 *= R[a]; R[a] = 1
+    OP_FLUSH,         // all amplitudes *= P * coef[c].x * prod_{a: bit a} R[a]; reset
     OP_DTABLE,        // fused diagonal: k targets; contrib[c16 .. c16+ct) index map; table at gtab + c
     OP_DENSE,         // fused dense 2^k (k <= 4): targets in canonical slots; matrix at gtab + c
-    OP_FLUSH,         // multiply every amplitude by (per-thread scalar) * coef[c].x; reset scalar
-    OP_SWAP_RR,       // a, b = slots: register permutation (SWAP when mapping relabel is not allowed)
+    OP_EXCHANGE,      // shared-memory exchange: map_out[c-1] -> map_in[c] (segment c starts)
 };
 
 struct DevOp {
     uint8_t type, a, b, k;
     uint32_t c;       // coefficient index (coef[]) or gtab offset (in double2 units)
     uint16_t c16;     // contrib[] offset for OP_DTABLE
-    uint16_t pad;
+    uint16_t x16;     // OP_DTABLE: XOR applied to the table index (flipped slots)
 };
 
 struct PassParams {
     int32_t ct;                       // tile bits
+    int32_t rb;                       // register bits (must equal regBitsFor(ct))
     int32_t nsegs;
     int32_t nops;
-    int32_t pad0;
-    uint64_t tile_mask;               // physical tile bits (for the CTA base deposit)
+    uint64_t tile_mask;               // physical tile bits
     int8_t tile_phys[16];             // physical bit of tile bit j (ascending)
     uint16_t seg_end[kMaxSegs];       // ops [seg_end[s-1], seg_end[s]) run in segment s
+    uint16_t xmask_out[kMaxSegs];     // tile-index XOR of the data at segment end (X gates are relabels)
     uint8_t map_in[kMaxSegs][16];     // mapping at segment start (load / exchange-read)
     uint8_t map_out[kMaxSegs][16];    // mapping at segment end (exchange-write / store)
     DevOp ops[kMaxOps];

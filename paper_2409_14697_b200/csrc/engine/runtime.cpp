@@ -443,6 +443,91 @@ void runXrsLocal(qk_state** sl, int ns, const XrsPlan& p) {
     for (int k = 0; k < ns; k++) cuda(cudaStreamSynchronize(sl[k]->stream), "xrs post-sync");
 }
 
+
+// qk_gate[] -> quokka::Gate list (matrix order: controls first), validating
+// arity and the chunk bound (engine.cpp:264-268).
+std::vector<quokka::Gate> gatesFromC(const qk_gate* gates, int ngates, int bound) {
+    std::vector<quokka::Gate> out;
+    for (int i = 0; i < ngates; i++) {
+        const qk_gate& g = gates[i];
+        if (g.kind < QK_H || g.kind > QK_FUSED_DENSE) throw SimulationError("unknown gate kind");
+        quokka::Gate q;
+        q.kind = static_cast<quokka::GateKind>(g.kind);
+        q.id = long(g.id);
+        const int nq = g.nqubits;
+        if (nq < 1 || nq > 16) throw SimulationError("bad gate arity");
+        const bool fused = g.kind == QK_FUSED_DIAG || g.kind == QK_FUSED_DENSE;
+        if (!fused && quokka::kindArity(q.kind) != nq) throw SimulationError("gate arity does not match its kind");
+        if (g.kind == QK_CX || g.kind == QK_CP) {
+            q.controls = {g.qubits[0]};
+            q.targets = {g.qubits[1]};
+        } else {
+            q.targets.assign(g.qubits, g.qubits + nq);
+        }
+        for (int j = 0; j < quokka::kindParamCount(q.kind); j++) q.params.push_back(g.params[j]);
+        if (fused) {
+            if (!g.payload) throw SimulationError("fused gate without payload");
+            const size_t e = size_t(1) << (g.kind == QK_FUSED_DIAG ? nq : 2 * nq);
+            for (size_t j = 0; j < e; j++) q.payload.emplace_back(g.payload[2 * j], g.payload[2 * j + 1]);
+        }
+        for (int qq : q.qubits())
+            if (qq < 0 || qq >= bound)
+                throw SimulationError("block gate " + std::to_string(q.id) + " reaches outside the chunk");
+        out.push_back(std::move(q));
+    }
+    return out;
+}
+
+// JSON dump of the compiled steps (scheduler test hook: tests/emulator.py
+// replays the pass programs on the CPU to check the scheduler without a GPU).
+std::string stepsJson(const std::vector<qkeng::Step>& steps, const std::vector<double>& gtab) {
+    std::ostringstream o;
+    o.precision(17);
+    o << "{\"gtab\":[";
+    for (size_t i = 0; i < gtab.size(); i++) o << (i ? "," : "") << gtab[i];
+    o << "],\"steps\":[";
+    for (size_t si = 0; si < steps.size(); si++) {
+        const qkeng::Step& s = steps[si];
+        o << (si ? "," : "") << "{\"kind\":" << int(s.kind) << ",\"k\":" << s.k << ",\"mat\":" << s.matOff
+          << ",\"targets\":[";
+        for (size_t j = 0; j < s.targets.size(); j++) o << (j ? "," : "") << s.targets[j];
+        o << "]";
+        if (s.kind == qkeng::Step::Pass) {
+            const qkdev::PassParams& P = *s.pass;
+            o << ",\"ct\":" << P.ct << ",\"rb\":" << P.rb << ",\"nsegs\":" << P.nsegs << ",\"tile_phys\":[";
+            for (int j = 0; j < P.ct; j++) o << (j ? "," : "") << int(P.tile_phys[j]);
+            o << "],\"map_in\":[";
+            for (int g = 0; g < P.nsegs; g++) {
+                o << (g ? "," : "") << "[";
+                for (int j = 0; j < P.ct; j++) o << (j ? "," : "") << int(P.map_in[g][j]);
+                o << "]";
+            }
+            o << "],\"map_out\":[";
+            for (int g = 0; g < P.nsegs; g++) {
+                o << (g ? "," : "") << "[";
+                for (int j = 0; j < P.ct; j++) o << (j ? "," : "") << int(P.map_out[g][j]);
+                o << "]";
+            }
+            o << "],\"xmask_out\":[";
+            for (int g = 0; g < P.nsegs; g++) o << (g ? "," : "") << P.xmask_out[g];
+            o << "],\"ops\":[";
+            for (int i = 0; i < P.nops; i++) {
+                const qkdev::DevOp& d = P.ops[i];
+                o << (i ? "," : "") << "[" << int(d.type) << "," << int(d.a) << "," << int(d.b) << "," << int(d.k)
+                  << "," << d.c << "," << d.c16 << "," << d.x16 << "]";
+            }
+            o << "],\"coef\":[";
+            for (int i = 0; i < 2 * qkdev::kMaxCoef; i++) o << (i ? "," : "") << P.coef[i];
+            o << "],\"contrib\":[";
+            for (int i = 0; i < qkdev::kMaxContrib; i++) o << (i ? "," : "") << P.contrib[i];
+            o << "]";
+        }
+        o << "}";
+    }
+    o << "]}";
+    return o.str();
+}
+
 void checkProgramAgainst(const quokka::Program& prog, const quokka::Config& cfg, int n, int R) {
     if (prog.nQubits != cfg.totalQubits || prog.rankQubits != cfg.rankQubits)
         throw ConfigError("program and config disagree on the qubit split");
@@ -581,33 +666,7 @@ int qk_apply_block(qk_state* st, const qk_gate* gates, int ngates, int chunk) {
         p.rankQubits = st->R;
         p.chunkQubits = chunk;
         quokka::GateBlock blk;
-        for (int i = 0; i < ngates; i++) {
-            const qk_gate& g = gates[i];
-            if (g.kind < QK_H || g.kind > QK_FUSED_DENSE) throw SimulationError("unknown gate kind");
-            quokka::Gate q;
-            q.kind = static_cast<quokka::GateKind>(g.kind);
-            q.id = long(g.id);
-            const int nq = g.nqubits;
-            if (nq < 1 || nq > 16) throw SimulationError("bad gate arity");
-            const bool fused = g.kind == QK_FUSED_DIAG || g.kind == QK_FUSED_DENSE;
-            if (!fused && quokka::kindArity(q.kind) != nq) throw SimulationError("gate arity does not match its kind");
-            if ((g.kind == QK_CX || g.kind == QK_CP)) {
-                q.controls = {g.qubits[0]};
-                q.targets = {g.qubits[1]};
-            } else {
-                q.targets.assign(g.qubits, g.qubits + nq);
-            }
-            for (int j = 0; j < quokka::kindParamCount(q.kind); j++) q.params.push_back(g.params[j]);
-            if (fused) {
-                if (!g.payload) throw SimulationError("fused gate without payload");
-                const size_t e = size_t(1) << (g.kind == QK_FUSED_DIAG ? nq : 2 * nq);
-                for (size_t j = 0; j < e; j++) q.payload.emplace_back(g.payload[2 * j], g.payload[2 * j + 1]);
-            }
-            for (int qq : q.qubits())
-                if (qq < 0 || qq >= chunk)
-                    throw SimulationError("block gate " + std::to_string(q.id) + " reaches outside the chunk");
-            blk.gates.push_back(std::move(q));
-        }
+        blk.gates = gatesFromC(gates, ngates, chunk);
         if (chunk < 1 || chunk > st->nLocal) throw SimulationError("chunk size out of range");
         p.items.push_back(quokka::ProgramItem::makeBlock(std::move(blk)));
         qk_program prog;
@@ -618,6 +677,14 @@ int qk_apply_block(qk_state* st, const qk_gate* gates, int ngates, int chunk) {
         qk_run_stats rs{};
         runBlock(st, c->items[0], t, rs);
         cuda(cudaStreamSynchronize(st->stream), "apply block");
+    });
+}
+
+int qk_debug_compile_block(const qk_gate* gates, int ngates, int nLocal, char** json) {
+    return guard([&] {
+        std::vector<double> gtab;
+        const std::vector<qkeng::Step> steps = qkeng::compileBlock(gatesFromC(gates, ngates, nLocal), nLocal, gtab);
+        *json = dupText(stepsJson(steps, gtab));
     });
 }
 

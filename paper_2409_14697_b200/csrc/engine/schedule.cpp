@@ -13,11 +13,13 @@
 //      in a register slot (1-qubit dense, CX target, dense U_k) but finds it in
 //      the thread index starts a new segment = one shared-memory exchange, with
 //      the next register set chosen by look-ahead over the following gates;
-//   3. lowers each gate to a register op, a per-thread scalar update (diagonals
-//      on thread-index bits) or a relabel (SWAP never moves data).
+//   3. lowers each gate to a register op, a deferred per-thread factor
+//      (diagonals touching thread-index bits: one scalar multiply per thread
+//      instead of a sweep over the registers), or a relabel (SWAP never moves
+//      data).
 // H's 1/sqrt2 is not multiplied per gate: every H scales all amplitudes by
 // the same factor, so the product is folded into one exact power-of-two (x
-// 1/sqrt2) scale applied at the next exchange / store.
+// 1/sqrt2) scale applied with the next full flush.
 #include "schedule.h"
 
 #include <algorithm>
@@ -56,26 +58,34 @@ double referenceFlopsPerAmp(const Gate& g) {
 
 namespace {
 
-bool denseInRegs(const Gate& g) {
-    return g.kind == GateKind::FusedDense && g.targets.size() >= 2 && g.targets.size() <= 4;
+bool denseInRegs(const Gate& g, int rb) {
+    return g.kind == GateKind::FusedDense && g.targets.size() >= 2 && int(g.targets.size()) <= std::min(4, rb);
+}
+
+// 1-qubit matrices that are diagonal (e.g. U(0,0,lambda) = T) run as diagonals.
+bool diagonalMatrix(const std::vector<Amp>& m) { return m.size() == 4 && m[1] == Amp(0) && m[2] == Amp(0); }
+
+bool oneQubitDense(const Gate& g, const Gate& orig) {
+    switch (g.kind) {
+        case GateKind::H:
+        case GateKind::X:
+            return true;
+        case GateKind::U:
+        case GateKind::RX:
+        case GateKind::RY:
+            return !diagonalMatrix(quokka::gateMatrix(orig));
+        case GateKind::FusedDense:
+            return g.targets.size() == 1 && !diagonalMatrix(orig.payload);
+        default:
+            return false;
+    }
 }
 
 // Tile bits that must sit in register slots when `g` runs.
-std::vector<int> regNeeds(const Gate& g) {
-    switch (g.kind) {
-        case GateKind::H:
-        case GateKind::U:
-        case GateKind::X:
-        case GateKind::RX:
-        case GateKind::RY:
-        case GateKind::CX:
-            return {g.targets[0]};
-        case GateKind::FusedDense:
-            if (g.targets.size() == 1) return {g.targets[0]};
-            return g.targets;
-        default:
-            return {};
-    }
+std::vector<int> regNeeds(const Gate& g, const Gate& orig) {
+    if (oneQubitDense(g, orig) || g.kind == GateKind::CX) return {g.targets[0]};
+    if (g.kind == GateKind::FusedDense && g.targets.size() > 1) return g.targets;
+    return {};
 }
 
 void appendComplex(std::vector<double>& v, const std::vector<Amp>& xs) {
@@ -85,11 +95,16 @@ void appendComplex(std::vector<double>& v, const std::vector<Amp>& xs) {
     }
 }
 
+Amp ratio(Amp num, Amp den) {
+    if (den == Amp(0.0, 0.0)) throw SimulationError("diagonal gate with a zero entry cannot be deferred");
+    return num / den;
+}
+
 class PassBuilder {
 public:
     PassBuilder(const std::vector<Gate>& tg, const std::vector<Gate>& orig, const std::vector<int>& tilePhys,
                 std::vector<double>& gtab)
-        : tg_(tg), orig_(orig), gtab_(gtab), ct_(int(tilePhys.size())) {
+        : tg_(tg), orig_(orig), gtab_(gtab), ct_(int(tilePhys.size())), rb_(regBitsFor(int(tilePhys.size()))) {
         tilePhys_ = tilePhys;
     }
 
@@ -99,6 +114,7 @@ public:
         std::memset(P.get(), 0, sizeof(PassParams));
         P_ = P.get();
         P_->ct = ct_;
+        P_->rb = rb_;
         for (int j = 0; j < ct_; j++) {
             P_->tile_phys[j] = int8_t(tilePhys_[size_t(j)]);
             P_->tile_mask |= uint64_t(1) << tilePhys_[size_t(j)];
@@ -106,31 +122,32 @@ public:
         nops_ = ncoef_ = ncontrib_ = 0;
         seg_ = 0;
         hcount_ = 0;
-        dirty_ = false;
+        pendScalar_ = false;
+        std::fill(pendSlot_, pendSlot_ + kMaxRegBits, false);
+        flips_ = 0;
         chooseMap(i);
         std::memcpy(P_->map_in[0], map_, sizeof map_);
 
         const size_t first = i;
         double flops = 0;
         while (i < tg_.size()) {
-            if (kMaxOps - nops_ < 4 || kMaxCoef - ncoef_ < 8 || kMaxContrib - ncontrib_ < 16 + ct_ ||
+            if (kMaxOps - nops_ < 12 || kMaxCoef - ncoef_ < 12 || kMaxContrib - ncontrib_ < 16 + ct_ ||
                 kMaxSegs - seg_ < 3)
                 break;
-            if (!satisfied(tg_[i])) {
-                flush();
-                P_->seg_end[seg_] = uint16_t(nops_);
-                std::memcpy(P_->map_out[seg_], map_, sizeof map_);
+            if (!satisfied(tg_[i], orig_[i])) {
+                flushAll();
+                closeSegment();
                 seg_++;
                 chooseMap(i);
                 std::memcpy(P_->map_in[seg_], map_, sizeof map_);
+                emit(OP_EXCHANGE, 0, 0, 0, uint32_t(seg_));
             }
             lower(tg_[i], orig_[i]);
             flops += referenceFlopsPerAmp(orig_[i]);
             i++;
         }
-        flush();
-        P_->seg_end[seg_] = uint16_t(nops_);
-        std::memcpy(P_->map_out[seg_], map_, sizeof map_);
+        flushAll();
+        closeSegment();
         P_->nsegs = seg_ + 1;
         P_->nops = nops_;
         step.kind = Step::Pass;
@@ -141,24 +158,38 @@ public:
     }
 
 private:
-    bool satisfied(const Gate& g) const {
-        if (denseInRegs(g)) {
+    bool isReg(int slot) const { return slot < rb_; }
+    // Slot holds its tile bit inverted (an X was applied as a relabel).
+    int flip(int slot) const { return int((flips_ >> slot) & 1u); }
+
+    void closeSegment() {
+        P_->seg_end[seg_] = uint16_t(nops_);
+        std::memcpy(P_->map_out[seg_], map_, sizeof map_);
+        uint32_t xm = 0;
+        for (int s = 0; s < ct_; s++)
+            if (flip(s)) xm |= 1u << map_[s];
+        P_->xmask_out[seg_] = uint16_t(xm);
+        flips_ = 0;  // the exchange / store writes the data at its true index
+    }
+
+    bool satisfied(const Gate& g, const Gate& orig) const {
+        if (denseInRegs(g, rb_)) {
             const int k = int(g.targets.size());
             for (int j = 0; j < k; j++)
                 if (inv_[g.targets[size_t(j)]] != k - 1 - j) return false;
             return true;
         }
-        for (int b : regNeeds(g))
-            if (inv_[b] >= kRegBits) return false;
+        for (int b : regNeeds(g, orig))
+            if (!isReg(inv_[b])) return false;
         return true;
     }
 
     // Choose which tile bits occupy the register slots from gate i onward.
     void chooseMap(size_t i) {
-        int slotBit[kRegBits];
-        std::fill(slotBit, slotBit + kRegBits, -1);
+        int slotBit[kMaxRegBits];
+        std::fill(slotBit, slotBit + kMaxRegBits, -1);
         std::vector<int> regs;  // tile bits at time i
-        if (i < tg_.size() && denseInRegs(tg_[i])) {
+        if (i < tg_.size() && denseInRegs(tg_[i], rb_)) {
             const Gate& g = tg_[i];
             const int k = int(g.targets.size());
             for (int j = 0; j < k; j++) slotBit[k - 1 - j] = g.targets[size_t(j)];
@@ -167,9 +198,9 @@ private:
         // Look ahead: add needed bits in order of first use while they fit.
         std::vector<int> origin(static_cast<size_t>(ct_));  // current bit -> bit at time i (SWAP relabels)
         for (int b = 0; b < ct_; b++) origin[size_t(b)] = b;
-        std::vector<char> inSet(size_t(ct_), 0);
+        std::vector<char> inSet(static_cast<size_t>(ct_), 0);
         for (int b : regs) inSet[size_t(b)] = 1;
-        for (size_t j = i; j < tg_.size() && int(regs.size()) <= kRegBits; j++) {
+        for (size_t j = i; j < tg_.size() && int(regs.size()) <= rb_; j++) {
             const Gate& g = tg_[j];
             if (g.kind == GateKind::SWAP) {
                 const int a = g.targets[0], b = g.targets[1];
@@ -177,37 +208,38 @@ private:
                 std::swap(inSet[size_t(a)], inSet[size_t(b)]);
                 continue;
             }
-            if (j > i && denseInRegs(g)) break;
+            if (j > i && denseInRegs(g, rb_)) break;
             std::vector<int> need;
-            for (int b : regNeeds(g))
+            for (int b : regNeeds(g, orig_[j]))
                 if (!inSet[size_t(b)]) need.push_back(b);
             if (need.empty()) continue;
-            if (regs.size() + need.size() > size_t(kRegBits)) break;
+            if (regs.size() + need.size() > size_t(rb_)) break;
             for (int b : need) {
                 inSet[size_t(b)] = 1;
                 regs.push_back(origin[size_t(b)]);
             }
         }
         // Fill with the highest remaining tile bits (keeps low bits in lanes).
-        std::vector<char> used(size_t(ct_), 0);
+        std::vector<char> used(static_cast<size_t>(ct_), 0);
         for (int b : regs) used[size_t(b)] = 1;
-        for (int b = ct_ - 1; b >= 0 && int(regs.size()) < kRegBits; b--)
+        for (int b = ct_ - 1; b >= 0 && int(regs.size()) < rb_; b--)
             if (!used[size_t(b)]) {
                 used[size_t(b)] = 1;
                 regs.push_back(b);
             }
         // Assign register slots (canonical dense slots already fixed).
         size_t r = 0;
-        for (int s = 0; s < kRegBits; s++) {
+        auto taken = [&](int b) { return std::find(slotBit, slotBit + rb_, b) != slotBit + rb_; };
+        for (int s = 0; s < rb_; s++) {
             if (slotBit[s] >= 0) continue;
-            while (r < regs.size() && std::find(slotBit, slotBit + kRegBits, regs[r]) != slotBit + kRegBits) r++;
+            while (r < regs.size() && taken(regs[r])) r++;
             slotBit[s] = regs[r++];
         }
         // Thread bits ascending; lane bits 0..2 with distinct residues mod 3
         // (conflict-free swizzled exchange).
         std::vector<int> rest;
         for (int b = 0; b < ct_; b++)
-            if (std::find(slotBit, slotBit + kRegBits, b) == slotBit + kRegBits) rest.push_back(b);
+            if (!taken(b)) rest.push_back(b);
         std::vector<int> lanes;
         for (int want = 0; want < 3 && !rest.empty(); want++) {
             size_t pick = rest.size();
@@ -225,8 +257,8 @@ private:
         }
         lanes.insert(lanes.end(), rest.begin(), rest.end());
         std::memset(map_, 0, sizeof map_);
-        for (int s = 0; s < kRegBits; s++) map_[s] = uint8_t(slotBit[s]);
-        for (size_t t = 0; t < lanes.size(); t++) map_[kRegBits + t] = uint8_t(lanes[t]);
+        for (int s = 0; s < rb_; s++) map_[s] = uint8_t(slotBit[s]);
+        for (size_t t = 0; t < lanes.size(); t++) map_[size_t(rb_) + t] = uint8_t(lanes[t]);
         for (int s = 0; s < ct_; s++) inv_[map_[s]] = s;
     }
 
@@ -256,60 +288,121 @@ private:
         o.c16 = c16;
     }
 
-    void flush() {
-        if (hcount_ == 0 && !dirty_) return;
+    void flushSlot(int slot) {
+        if (isReg(slot) && pendSlot_[slot]) {
+            emit(OP_FLUSH_SLOT, slot);
+            pendSlot_[slot] = false;
+        }
+    }
+
+    void flushAll() {
+        bool any = hcount_ > 0 || pendScalar_;
+        for (int s = 0; s < rb_; s++) any |= pendSlot_[s];
+        if (!any) return;
         // (1/sqrt2)^h exactly: a power of two, times 1/sqrt2 when h is odd.
         const double root = 1.0 / std::sqrt(2.0);
         const double scale = std::ldexp(hcount_ % 2 ? root : 1.0, -(hcount_ / 2));
         emit(OP_FLUSH, 0, 0, 0, addCoef({Amp(scale, 0.0)}));
         hcount_ = 0;
-        dirty_ = false;
+        pendScalar_ = false;
+        std::fill(pendSlot_, pendSlot_ + kMaxRegBits, false);
     }
 
-    // Diagonal over (q0 = sub-index MSB, q1) with entries d[4].
-    void diag2(int q0, int q1, const std::vector<Amp>& d) {
-        const int s0 = inv_[q0], s1 = inv_[q1];
-        const uint32_t c = addCoef(d);
-        if (s0 < kRegBits && s1 < kRegBits) emit(OP_DIAG2_RR, s0, s1, 0, c);
-        else if (s0 < kRegBits) emit(OP_DIAG2_RT, s0, s1 - kRegBits, 0, c);
-        else if (s1 < kRegBits) emit(OP_DIAG2_RT, s1, s0 - kRegBits, 1, c);
-        else {
-            emit(OP_DIAG2_TT, s0 - kRegBits, s1 - kRegBits, 0, c);
-            dirty_ = true;
-        }
+    void scalar(const std::vector<Amp>& d, OpType t, int a = 0, int b = 0) {
+        emit(t, a, b, 0, addCoef(d));
+        pendScalar_ = true;
+    }
+    void pending(int slot, const std::vector<Amp>& r, OpType t, int b = 0) {
+        emit(t, slot, b, 0, addCoef(r));
+        pendSlot_[slot] = true;
     }
 
-    void diag1(int q, const std::vector<Amp>& d) {
+    // amplitude *= d[logical bit q].  Slot semantics are physical: a flipped
+    // slot holds the logical bit inverted, so the entry pair swaps.
+    void diag1(int q, std::vector<Amp> d) {
         const int s = inv_[q];
-        const uint32_t c = addCoef(d);
-        if (s < kRegBits) emit(OP_DIAG1_R, s, 0, 0, c);
-        else {
-            emit(OP_DIAG1_T, s - kRegBits, 0, 0, c);
-            dirty_ = true;
+        if (flip(s)) std::swap(d[0], d[1]);
+        if (!isReg(s)) return scalar({d[0], d[1]}, OP_SCAL_T, s - rb_);
+        if (d[0] != Amp(1.0, 0.0)) scalar({d[0]}, OP_SCAL);
+        pending(s, {ratio(d[1], d[0])}, OP_PEND_R);
+    }
+
+    // amplitude *= d[2 bit(q0) + bit(q1)] (logical bits).
+    void diag2(int q0, int q1, const std::vector<Amp>& dl) {
+        const int s0 = inv_[q0], s1 = inv_[q1], f0 = flip(s0), f1 = flip(s1);
+        std::vector<Amp> d(4);  // physical entries
+        for (int b0 = 0; b0 < 2; b0++)
+            for (int b1 = 0; b1 < 2; b1++) d[size_t(2 * b0 + b1)] = dl[size_t(2 * (b0 ^ f0) + (b1 ^ f1))];
+        if (isReg(s0) && isReg(s1)) {
+            // one non-unit entry: multiply only that quarter (CP-like)
+            int nonUnit = -1, count = 0;
+            for (int e = 0; e < 4; e++)
+                if (d[size_t(e)] != Amp(1.0, 0.0)) {
+                    nonUnit = e;
+                    count++;
+                }
+            if (count == 0) return;
+            const int lo = std::min(s0, s1), hi = std::max(s0, s1);
+            if (count == 1) {
+                // pattern over (slot lo, slot hi)
+                const int b0 = nonUnit >> 1, b1 = nonUnit & 1;
+                const int pat = s0 == lo ? (b0 << 1 | b1) : (b1 << 1 | b0);
+                emit(OP_CPHASE_RR, lo, hi, pat, addCoef({d[size_t(nonUnit)]}));
+            } else {
+                emit(OP_DIAG2_RR, s0, s1, 0, addCoef(d));
+            }
+        } else if (isReg(s0)) {  // factor = d[2 r + t]
+            const int t = s1 - rb_;
+            scalar({d[0], d[1]}, OP_SCAL_T, t);
+            pending(s0, {ratio(d[2], d[0]), ratio(d[3], d[1])}, OP_PEND_RT, t);
+        } else if (isReg(s1)) {  // factor = d[2 t + r]
+            const int t = s0 - rb_;
+            scalar({d[0], d[2]}, OP_SCAL_T, t);
+            pending(s1, {ratio(d[1], d[0]), ratio(d[3], d[2])}, OP_PEND_RT, t);
+        } else {
+            scalar(d, OP_SCAL_TT, s0 - rb_, s1 - rb_);
         }
+    }
+
+    void mat1(int q, std::vector<Amp> m) {
+        const int s = inv_[q];
+        if (flip(s)) m = {m[3], m[2], m[1], m[0]};  // X M X
+        flushSlot(s);
+        emit(OP_MAT1, s, 0, 0, addCoef(m));
     }
 
     void lower(const Gate& g, const Gate& orig) {
         switch (g.kind) {
-            case GateKind::H:
-                emit(OP_H, inv_[g.targets[0]]);
+            case GateKind::H: {
+                const int s = inv_[g.targets[0]];
+                flushSlot(s);
+                emit(OP_H, s);
                 hcount_++;
+                if (flip(s)) {  // H on a flipped slot leaves it unflipped with the |1> half negated
+                    flips_ ^= 1u << s;
+                    pending(s, {Amp(-1.0, 0.0)}, OP_PEND_R);
+                }
                 return;
-            case GateKind::X:
-                emit(OP_X, inv_[g.targets[0]]);
+            }
+            case GateKind::X:  // relabel: no data moves
+                flips_ ^= 1u << inv_[g.targets[0]];
                 return;
             case GateKind::U:
             case GateKind::RX:
-            case GateKind::RY:
-                emit(OP_MAT1, inv_[g.targets[0]], 0, 0, addCoef(quokka::gateMatrix(orig)));
-                return;
+            case GateKind::RY: {
+                const std::vector<Amp> m = quokka::gateMatrix(orig);
+                if (diagonalMatrix(m)) return diag1(g.targets[0], {m[0], m[3]});
+                return mat1(g.targets[0], m);
+            }
             case GateKind::CX: {
                 const int t = inv_[g.targets[0]], c = inv_[g.controls[0]];
-                if (c < kRegBits) emit(OP_CX_RR, t, c);
-                else emit(OP_CX_RT, t, c - kRegBits);
+                flushSlot(t);
+                const int pol = flip(c);  // physical control value that means logical 1 is (1 ^ pol)
+                if (isReg(c)) emit(OP_CX, t, c, pol << 1);
+                else emit(OP_CX, t, c - rb_, 1 | (pol << 1));
                 return;
             }
-            case GateKind::SWAP: {  // relabel only
+            case GateKind::SWAP: {  // relabel only (pending factors and flips stay with their slots' data)
                 const int a = g.targets[0], b = g.targets[1], sa = inv_[a], sb = inv_[b];
                 map_[sa] = uint8_t(b);
                 map_[sb] = uint8_t(a);
@@ -320,18 +413,9 @@ private:
             case GateKind::RZ:
                 diag1(g.targets[0], quokka::gateDiagonal(orig));
                 return;
-            case GateKind::CP: {
-                const int sa = inv_[g.controls[0]], sb = inv_[g.targets[0]];
-                const uint32_t c = addCoef({quokka::gateDiagonal(orig)[3]});
-                if (sa < kRegBits && sb < kRegBits) emit(OP_CPHASE_RR, std::min(sa, sb), std::max(sa, sb), 0, c);
-                else if (sa < kRegBits) emit(OP_CPHASE_RT, sa, sb - kRegBits, 0, c);
-                else if (sb < kRegBits) emit(OP_CPHASE_RT, sb, sa - kRegBits, 0, c);
-                else {
-                    emit(OP_CPHASE_TT, sa - kRegBits, sb - kRegBits, 0, c);
-                    dirty_ = true;
-                }
+            case GateKind::CP:
+                diag2(g.controls[0], g.targets[0], quokka::gateDiagonal(orig));
                 return;
-            }
             case GateKind::RZZ: {
                 const std::vector<int> qs = g.qubits();
                 diag2(qs[0], qs[1], quokka::gateDiagonal(orig));
@@ -342,20 +426,32 @@ private:
                 if (k == 1) return diag1(g.targets[0], orig.payload);
                 if (k == 2) return diag2(g.targets[0], g.targets[1], orig.payload);
                 const uint16_t c16 = uint16_t(ncontrib_);
+                uint32_t x = 0;
                 for (int s = 0; s < ct_; s++) P_->contrib[ncontrib_ + s] = 0;
-                for (int j = 0; j < k; j++)
-                    P_->contrib[ncontrib_ + inv_[g.targets[size_t(j)]]] = uint16_t(1u << (k - 1 - j));
+                for (int j = 0; j < k; j++) {
+                    const int s = inv_[g.targets[size_t(j)]];
+                    P_->contrib[ncontrib_ + s] = uint16_t(1u << (k - 1 - j));
+                    if (flip(s)) x |= 1u << (k - 1 - j);
+                }
                 ncontrib_ += ct_;
                 emit(OP_DTABLE, 0, 0, k, addTable(orig.payload), c16);
+                P_->ops[nops_ - 1].x16 = uint16_t(x);
                 return;
             }
             case GateKind::FusedDense: {
                 const int k = int(g.targets.size());
                 if (k == 1) {
-                    emit(OP_MAT1, inv_[g.targets[0]], 0, 0, addCoef(orig.payload));
-                    return;
+                    if (diagonalMatrix(orig.payload)) return diag1(g.targets[0], {orig.payload[0], orig.payload[3]});
+                    return mat1(g.targets[0], orig.payload);
                 }
-                emit(OP_DENSE, 0, 0, k, addTable(orig.payload));
+                // canonical slots: sub-index bit b <-> slot b; flipped slots permute the matrix
+                const uint32_t f = flips_ & ((1u << k) - 1);
+                const size_t dim = size_t(1) << k;
+                std::vector<Amp> m(dim * dim);
+                for (size_t r = 0; r < dim; r++)
+                    for (size_t c = 0; c < dim; c++) m[r * dim + c] = orig.payload[(r ^ f) * dim + (c ^ f)];
+                for (int s = 0; s < k; s++) flushSlot(s);
+                emit(OP_DENSE, 0, 0, k, addTable(m));
                 return;
             }
         }
@@ -365,10 +461,12 @@ private:
     const std::vector<Gate>& orig_;
     std::vector<double>& gtab_;
     std::vector<int> tilePhys_;
-    int ct_;
+    int ct_, rb_;
     PassParams* P_ = nullptr;
     int nops_ = 0, ncoef_ = 0, ncontrib_ = 0, seg_ = 0, hcount_ = 0;
-    bool dirty_ = false;
+    bool pendScalar_ = false;
+    bool pendSlot_[kMaxRegBits] = {};
+    uint32_t flips_ = 0;  // slots (register and thread) holding an inverted bit
     uint8_t map_[16] = {};
     int inv_[16] = {};
 };
@@ -427,11 +525,12 @@ std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::
         steps.push_back(std::move(s));
     };
 
-    if (nLocal < kRegBits) {  // too small for a register tile: every gate as a dense group
+    if (nLocal < 4) {  // too small for a register tile: every gate as a dense group
         for (const Gate& g : gates) denseStep(quokka::gateMatrix(g), g.qubits(), referenceFlopsPerAmp(g));
         return steps;
     }
     const int ct = std::min(kMaxTileBits, nLocal);
+    const int rb = regBitsFor(ct);
     std::vector<Gate> group;
     uint64_t used = 0;
     auto close = [&] {
@@ -440,7 +539,9 @@ std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::
         used = 0;
     };
     for (const Gate& g : gates) {
-        if (g.kind == GateKind::FusedDense && g.targets.size() > size_t(kRegBits)) {
+        if (g.kind == GateKind::FusedDense && g.targets.size() > size_t(std::min(4, rb))) {
+            if (g.targets.size() > size_t(kMaxTileBits))
+                throw SimulationError("fused dense gate " + std::to_string(g.id) + " wider than 13 qubits");
             close();
             denseStep(g.payload, g.targets, referenceFlopsPerAmp(g));
             continue;
@@ -451,8 +552,6 @@ std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::
             steps.back().kind = Step::DiagTable;
             continue;
         }
-        if (g.kind == GateKind::FusedDense && g.targets.size() > size_t(kMaxTileBits))
-            throw SimulationError("fused dense gate " + std::to_string(g.id) + " wider than 13 qubits");
         const uint64_t m = g.depMask();
         if (__builtin_popcountll(used | m) > ct) close();
         group.push_back(g);

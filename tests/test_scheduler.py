@@ -1,0 +1,100 @@
+"""Host scheduler (CPU): the pass programs compiled for a block, replayed by
+the numpy kernel emulator (tests/emulator.py), reproduce the reference's
+applyBlock (the plain-C oracle) — register maps, deferred diagonal factors,
+X relabels, exchanges and multi-CTA tiles are all exercised without a GPU."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+from emulator import run_steps
+from oracle import config_text
+
+P = json.load(open(os.path.join(GOLDEN, "golden_programs.json")))
+G = np.load(os.path.join(GOLDEN, "golden_states.npz"))
+
+
+def emulate(qk, lines, n, st):
+    out = st.view(np.complex128).copy()
+    run_steps(out, n, qk.debug_compile_block(lines, n))
+    return out
+
+
+@pytest.mark.parametrize("name", ["mixed", "random5_0", "random5_1", "random5_2"])
+def test_golden_blocks(qk, name):
+    case = P[f"block/{name}"]
+    got = emulate(qk, case["lines"], case["n"], G[f"block/{name}/in"])
+    assert np.max(np.abs(got - G[f"block/{name}/out"].view(np.complex128))) < 1e-12
+
+
+@pytest.mark.parametrize("n,chunk", [(4, 4), (6, 3), (9, 9), (11, 7), (13, 13), (14, 12)])
+def test_random_blocks(qk, port, n, chunk):
+    rng = np.random.default_rng(n * 31 + chunk)
+    for seed in range(3):
+        lines = [ln for ln in qk.generate("random", chunk, 80, 1000 * n + seed).splitlines() if ln.strip()]
+        st = rng.standard_normal(2 << n)
+        want = st.copy()
+        port.apply_block(want, n, lines, chunk)
+        assert np.max(np.abs(emulate(qk, lines, n, st) - want.view(np.complex128))) < 1e-12, seed
+
+
+def test_x_heavy_sequences(qk, port):
+    # X relabels interleaved with every other kind (flipped slots everywhere)
+    n = 11
+    rng = np.random.default_rng(5)
+    kinds = ["H", "X", "U", "RZ", "CP", "RZZ", "CX", "SWAP", "RX"]
+    for trial in range(6):
+        lines = []
+        for gid in range(60):
+            k = kinds[int(rng.integers(len(kinds)))] if gid % 3 else "X"
+            q = [int(x) for x in rng.choice(n, 2, replace=False)]
+            if k in ("H", "X"):
+                lines.append(f"{k} {q[0]} {gid}")
+            elif k in ("RZ", "RX"):
+                lines.append(f"{k} {q[0]} {gid} {rng.normal():.6f}")
+            elif k == "U":
+                lines.append(f"U {q[0]} {gid} 0.3 {rng.normal():.6f} -0.2")
+            elif k in ("CP", "RZZ"):
+                lines.append(f"{k} {q[0]} {q[1]} {gid} {rng.normal():.6f}")
+            else:
+                lines.append(f"{k} {q[0]} {q[1]} {gid}")
+        st = rng.standard_normal(2 << n)
+        want = st.copy()
+        port.apply_block(want, n, lines, n)
+        assert np.max(np.abs(emulate(qk, lines, n, st) - want.view(np.complex128))) < 1e-12, trial
+
+
+@pytest.mark.parametrize("f", [2, 3, 4, 5])
+def test_fused_blocks(qk, port, ref, f):
+    n = 10
+    for kind, a in (("qaoa", 2), ("random", 90), ("qft", 0), ("bvones", 0)):
+        prog = ref.optimize(ref.gen(kind, n, a, 17), config_text(n, 0, 8, f))
+        lines = prog.splitlines()
+        i = 0
+        rng = np.random.default_rng(f)
+        while i < len(lines):
+            k = int(lines[i])
+            body = lines[i + 1:i + 1 + k]
+            i += 1 + k
+            if body[0].startswith("SQS"):
+                continue
+            st = rng.standard_normal(2 << n)
+            want = st.copy()
+            port.apply_block(want, n, body, 8)
+            assert np.max(np.abs(emulate(qk, body, n, st) - want.view(np.complex128))) < 1e-11, kind
+
+
+def test_pass_capacity_split(qk, port):
+    # > kMaxOps gates in one block: the scheduler splits into several passes
+    n = 9
+    lines = [ln for ln in qk.generate("random", n, 1500, 3).splitlines() if ln.strip()]
+    prog = qk.debug_compile_block(lines, n)
+    assert len(prog["steps"]) >= 2
+    st = np.random.default_rng(1).standard_normal(2 << n)
+    want = st.copy()
+    port.apply_block(want, n, lines, n)
+    out = st.view(np.complex128).copy()
+    run_steps(out, n, prog)
+    assert np.max(np.abs(out - want.view(np.complex128))) < 1e-11
