@@ -99,6 +99,8 @@ int qk_apply_block(qk_state* st, const qk_gate* gates, int ngates, int chunk_qub
 /* Scheduler test hook (host only, no device): the compiled pass programs of a
  * block for a 2^n_local slice, as JSON (tests/emulator.py replays them). */
 int qk_debug_compile_block(const qk_gate* gates, int ngates, int n_local, char** json);
+/* ... and of a whole program (device item list: blocks, IMS, XRS). */
+int qk_debug_compile_program(const qk_program* p, int n_local, char** json);
 /* engine.cpp:258-260 applyGate (whole slice, any position < N-R). */
 int qk_apply_gate(qk_state* st, const qk_gate* gate);
 /* engine.cpp:86-101 imsSwap: a[bitswap(i)] <- a[i], in place.  cache_line_qubits

@@ -115,6 +115,7 @@ def lib():
         "qk_apply_block": ([P, C.POINTER(_Gate), I, I], I),
         "qk_apply_gate": ([P, C.POINTER(_Gate)], I),
         "qk_debug_compile_block": ([C.POINTER(_Gate), I, I, C.POINTER(P)], I),
+        "qk_debug_compile_program": ([P, I, C.POINTER(P)], I),
         "qk_ims_swap": ([P, C.POINTER(I), C.POINTER(I), I, I], I),
         "qk_xrs_swap_local": ([C.POINTER(P), I, C.POINTER(I), C.POINTER(I), I, C.POINTER(_XrsStats)], I),
         "qk_xrs_plan": ([I, I, I, I, C.POINTER(I), C.POINTER(I), I, C.POINTER(_XrsMsg), I,
@@ -221,6 +222,12 @@ class Program:
 
     def text(self) -> str:
         return _text(lib().qk_program_serialize, self._h)
+
+    def debug_compile(self, n_local: int | None = None) -> dict:
+        """Device item list the engine runs (host only; test hook)."""
+        import json
+        n_local = self.cfg.total_qubits - self.cfg.rank_qubits if n_local is None else n_local
+        return json.loads(_text(lib().qk_debug_compile_program, self._h, n_local))
 
     def counts(self):
         v = [C.c_int64() for _ in range(4)]

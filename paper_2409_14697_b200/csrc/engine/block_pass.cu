@@ -41,6 +41,15 @@ __device__ __forceinline__ uint32_t swz(uint32_t u) {
     return u ^ (((u >> 3) ^ (u >> 6) ^ (u >> 9) ^ (u >> 12)) & 7u);
 }
 
+// Bits of t selected by mask m, compacted (PEXT over the 8 thread-index bits).
+__device__ __forceinline__ uint32_t pext8(uint32_t t, uint32_t m) {
+    uint32_t r = 0, i = 0;
+#pragma unroll
+    for (int j = 0; j < 8; j++)
+        if ((m >> j) & 1u) r |= ((t >> j) & 1u) << i++;
+    return r;
+}
+
 __device__ __forceinline__ double2 coefAt(const PassParams& P, uint32_t i) {
     return make_double2(P.coef[2 * i], P.coef[2 * i + 1]);
 }
@@ -161,6 +170,21 @@ __device__ __forceinline__ void opDense(double2 (&a)[NA], const double2* __restr
         }
 }
 
+// R[K] *= e (pending phase of slot K)
+template <int RB, int K>
+__device__ __forceinline__ void mulSlot(double2 (&R)[RB], double2 e) {
+    if constexpr (K < RB) R[K] = cmul(R[K], e);
+}
+
+// amplitudes with slot-K bit 1 *= R[K]; R[K] = 1
+template <int RB, int K>
+__device__ __forceinline__ void flushSlot(double2 (&a)[1 << RB], double2 (&R)[RB]) {
+    if constexpr (K < RB) {
+        opPhaseSlot<(1 << RB), K>(a, R[K]);
+        R[K] = make_double2(1.0, 0.0);
+    }
+}
+
 #define QK_SLOT1(v, F, NA_, ...)                \
     switch (v) {                                \
         case 0: F<NA_, 0>(__VA_ARGS__); break;  \
@@ -262,8 +286,8 @@ __device__ __forceinline__ void flushAll(double2 (&a)[1 << RB], double2 P, doubl
 
 }  // namespace
 
-template <int CT, int RB>
-__global__ void __launch_bounds__(1 << (CT - RB), 1)
+template <int CT, int RB, int MINB>
+__global__ void __launch_bounds__(1 << (CT - RB), MINB)
     k_block_pass(double2* __restrict__ state, const double2* __restrict__ gtab, const __grid_constant__ PassParams P) {
     constexpr int NT = 1 << (CT - RB);
     constexpr int NA = 1 << RB;
@@ -355,17 +379,37 @@ __global__ void __launch_bounds__(1 << (CT - RB), 1)
                     break;
                 }
                 case OP_PEND_RT: {
-                    const double2 e = coefAt(P, o.c + ((tid >> o.b) & 1u));
+                    const uint32_t tb = (tid >> o.b) & 1u;
+                    const double2 e0 = coefAt(P, o.c), e1 = coefAt(P, o.c + 1);  // uniform loads, then select
+                    const double2 e = make_double2(tb ? e1.x : e0.x, tb ? e1.y : e0.y);
+#pragma unroll
+                    for (int k = 0; k < RB; k++)
+                        if (k == o.a) R[k] = cmul(R[k], e);
+                    break;
+                }
+                case OP_SCAL_TAB: Pt = cmul(Pt, __ldg(gtab + o.c + pext8(tid, o.b))); break;
+                case OP_PEND_TAB: {
+                    const double2 e = __ldg(gtab + o.c + pext8(tid, o.b));
 #pragma unroll
                     for (int k = 0; k < RB; k++)
                         if (k == o.a) R[k] = cmul(R[k], e);
                     break;
                 }
                 case OP_SCAL: Pt = cmul(Pt, coefAt(P, o.c)); break;
-                case OP_SCAL_T: Pt = cmul(Pt, coefAt(P, o.c + ((tid >> o.a) & 1u))); break;
-                case OP_SCAL_TT:
-                    Pt = cmul(Pt, coefAt(P, o.c + ((((tid >> o.a) & 1u) << 1) | ((tid >> o.b) & 1u))));
+                case OP_SCAL_T: {
+                    const uint32_t tb = (tid >> o.a) & 1u;
+                    const double2 e0 = coefAt(P, o.c), e1 = coefAt(P, o.c + 1);
+                    Pt = cmul(Pt, make_double2(tb ? e1.x : e0.x, tb ? e1.y : e0.y));
                     break;
+                }
+                case OP_SCAL_TT: {
+                    const uint32_t i = (((tid >> o.a) & 1u) << 1) | ((tid >> o.b) & 1u);
+                    const double2 e0 = coefAt(P, o.c), e1 = coefAt(P, o.c + 1), e2 = coefAt(P, o.c + 2),
+                                  e3 = coefAt(P, o.c + 3);
+                    const double2 lo = (i & 1u) ? e1 : e0, hi = (i & 1u) ? e3 : e2;
+                    Pt = cmul(Pt, (i & 2u) ? hi : lo);
+                    break;
+                }
                 case OP_FLUSH_SLOT: {
                     double2 e = R[0];
 #pragma unroll
@@ -461,18 +505,21 @@ __global__ void k_dense_group(double2* __restrict__ state, const double2* __rest
 
 // ---- launchers --------------------------------------------------------------
 
-template <int CT>
+// CT <= 12: 16 amplitudes per thread, two CTAs per SM at CT = 12 (128 KiB of
+// smem, 128 registers); CT = 13: RB = 5 (256 threads x 255 registers, one CTA
+// per SM) or RB = 4 (512 threads x 128 registers).
+template <int CT, int RB = (CT < 4 ? CT : 4)>
 static cudaError_t launchCT(double2* state, const double2* gtab, const PassParams& P, uint64_t ctas,
                             cudaStream_t stream) {
-    constexpr int RB = regBitsFor(CT);
     constexpr int NT = 1 << (CT - RB);
+    constexpr int MINB = (CT == 12 && RB == 4) ? 2 : 1;
     const size_t smem = sizeof(double2) << CT;
     if (smem > 48 * 1024) {  // per-device attribute; cheap to re-apply
-        cudaError_t e = cudaFuncSetAttribute(k_block_pass<CT, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             int(smem));
+        cudaError_t e = cudaFuncSetAttribute(k_block_pass<CT, RB, MINB>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         if (e != cudaSuccess) return e;
     }
-    k_block_pass<CT, RB><<<dim3(unsigned(ctas)), NT, smem, stream>>>(state, gtab, P);
+    k_block_pass<CT, RB, MINB><<<dim3(unsigned(ctas)), NT, smem, stream>>>(state, gtab, P);
     return cudaGetLastError();
 }
 
@@ -480,6 +527,8 @@ cudaError_t launchBlockPass(double2* state, const double2* gtab, const PassParam
                             cudaStream_t stream) {
     if (P.rb != regBitsFor(P.ct)) return cudaErrorInvalidValue;
     const uint64_t ctas = uint64_t(1) << (nLocal - P.ct);
+    if (P.ct == 13) return P.rb == 5 ? launchCT<13, 5>(state, gtab, P, ctas, stream)
+                                     : launchCT<13, 4>(state, gtab, P, ctas, stream);
     switch (P.ct) {
         case 4: return launchCT<4>(state, gtab, P, ctas, stream);
         case 5: return launchCT<5>(state, gtab, P, ctas, stream);
@@ -490,7 +539,6 @@ cudaError_t launchBlockPass(double2* state, const double2* gtab, const PassParam
         case 10: return launchCT<10>(state, gtab, P, ctas, stream);
         case 11: return launchCT<11>(state, gtab, P, ctas, stream);
         case 12: return launchCT<12>(state, gtab, P, ctas, stream);
-        case 13: return launchCT<13>(state, gtab, P, ctas, stream);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -40,7 +40,10 @@ constexpr int kMaxContrib = 512;            // uint16 words for fused-diagonal i
 // Register bits used for a tile of ct bits: 16 amplitudes per thread up to
 // ct = 12 (<= 256 threads, no register cap), 32 per thread at ct = 13 (256
 // threads x <= 255 registers: the 2^13-amplitude tile never spills).
-constexpr int regBitsFor(int ct) { return ct >= 13 ? 5 : (ct < 4 ? ct : 4); }
+// Tuning knobs (host; schedule.cpp): QK_MAX_TILE_BITS = 12|13 (default 13),
+// QK_RB13 = 4|5 register bits at ct = 13 (default 5).
+int maxTileBits();
+int regBitsFor(int ct);
 
 enum OpType : uint8_t {
     OP_MAT1 = 0,      // a = slot; coef[c..c+3] = 2x2 row-major
@@ -59,6 +62,8 @@ enum OpType : uint8_t {
     OP_DTABLE,        // fused diagonal: k targets; contrib[c16 .. c16+ct) index map; table at gtab + c
     OP_DENSE,         // fused dense 2^k (k <= 4): targets in canonical slots; matrix at gtab + c
     OP_EXCHANGE,      // shared-memory exchange: map_out[c-1] -> map_in[c] (segment c starts)
+    OP_SCAL_TAB,      // P *= gtab[c + pext(thread, b)]      (b = thread-bit mask)
+    OP_PEND_TAB,      // R[a] *= gtab[c + pext(thread, b)]
 };
 
 struct DevOp {

@@ -10,6 +10,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -252,17 +253,87 @@ struct DeviceGuard {
     ~DeviceGuard() { cudaSetDevice(prev); }
 };
 
+bool lazyIms() {
+    static const bool on = [] {
+        const char* v = std::getenv("QK_LAZY_IMS");
+        return !(v && v[0] == '0');
+    }();
+    return on;
+}
+
+// IMS pair sets that move the data at memory bit mem[p] to bit p for every p:
+// each cycle of the bit permutation is a product of two reflections
+// (c_i -> c_{-i}, then c_i -> c_{1-i}), so at most two IMS passes.
+std::vector<std::vector<std::pair<int, int>>> materializePairs(const std::vector<int>& mem) {
+    const int n = int(mem.size());
+    std::vector<int> dest(static_cast<size_t>(n));  // data at bit b must go to bit dest[b]
+    for (int p = 0; p < n; p++) dest[size_t(mem[size_t(p)])] = p;
+    std::vector<std::pair<int, int>> t1, t2;
+    std::vector<char> seen(static_cast<size_t>(n), 0);
+    for (int s = 0; s < n; s++) {
+        if (seen[size_t(s)] || dest[size_t(s)] == s) continue;
+        std::vector<int> cyc;  // cyc[i+1] = dest[cyc[i]]
+        for (int b = s; !seen[size_t(b)]; b = dest[size_t(b)]) {
+            seen[size_t(b)] = 1;
+            cyc.push_back(b);
+        }
+        const int k = int(cyc.size());
+        for (int i = 1; i < k - i; i++) t1.emplace_back(cyc[size_t(i)], cyc[size_t(k - i)]);
+        for (int i = 0; i < k; i++) {
+            const int j = ((1 - i) % k + k) % k;
+            if (i < j) t2.emplace_back(cyc[size_t(i)], cyc[size_t(j)]);
+        }
+    }
+    std::vector<std::vector<std::pair<int, int>>> out;
+    for (auto* t : {&t1, &t2}) {
+        if (t->empty()) continue;
+        for (auto& pr : *t)
+            if (pr.first > pr.second) std::swap(pr.first, pr.second);
+        std::sort(t->begin(), t->end());
+        out.push_back(*t);
+    }
+    return out;
+}
+
 std::shared_ptr<Compiled> compileFor(qk_program* p, int nLocal) {
     std::lock_guard<std::mutex> lk(p->mu);
     auto it = p->compiled.find(nLocal);
     if (it != p->compiled.end()) return it->second;
     auto c = std::make_shared<Compiled>();
     c->nLocal = nLocal;
+    // Lazy in-memory swaps: an SQS only relabels which memory bit holds which
+    // program position (mem[p]); the following blocks address their qubits
+    // through `mem`, so the SQS costs no HBM pass.  The relabeling is
+    // materialized (<= 2 IMS passes) only before a cross-rank swap and at the
+    // end, so the final state is in the program's physical order.
+    std::vector<int> mem(static_cast<size_t>(nLocal));
+    for (int b = 0; b < nLocal; b++) mem[size_t(b)] = b;
+    const bool lazy = lazyIms();
+    auto materialize = [&] {
+        for (const auto& pairs : materializePairs(mem)) {
+            CompiledItem ci;
+            ci.kind = CompiledItem::Ims;
+            for (const auto& [o, i] : pairs) {
+                ci.outs.push_back(o);
+                ci.ins.push_back(i);
+            }
+            c->items.push_back(std::move(ci));
+        }
+        for (int b = 0; b < nLocal; b++) mem[size_t(b)] = b;
+    };
     for (const quokka::ProgramItem& item : p->prog.items) {
         CompiledItem ci;
         if (item.type == quokka::ProgramItem::Block) {
             ci.kind = CompiledItem::Block;
-            ci.steps = qkeng::compileBlock(item.block.gates, nLocal, c->gtab);
+            std::vector<quokka::Gate> gates;
+            for (const quokka::Gate& g : item.block.gates) {
+                quokka::Gate m = g;
+                m.constituents.clear();
+                for (int& q : m.targets) q = mem[size_t(q)];
+                for (int& q : m.controls) q = mem[size_t(q)];
+                gates.push_back(std::move(m));
+            }
+            ci.steps = qkeng::compileBlock(gates, nLocal, c->gtab);
             for (qkeng::Step& s : ci.steps) {
                 ci.flopsPerAmp += s.flopsPerAmp;
                 if (s.kind != qkeng::Step::Pass) {
@@ -271,7 +342,11 @@ std::shared_ptr<Compiled> compileFor(qk_program* p, int nLocal) {
                     s.targets.insert(s.targets.begin(), int(off));  // [0] = device offset
                 }
             }
+        } else if (item.swap.kind == quokka::SwapOp::InMemory && lazy) {
+            for (const auto& [o, i] : item.swap.pairs) std::swap(mem[size_t(o)], mem[size_t(i)]);
+            continue;
         } else {
+            if (item.swap.kind == quokka::SwapOp::CrossRank) materialize();
             ci.kind = item.swap.kind == quokka::SwapOp::InMemory ? CompiledItem::Ims : CompiledItem::Xrs;
             for (const auto& [o, i] : item.swap.pairs) {
                 ci.outs.push_back(o);
@@ -280,6 +355,7 @@ std::shared_ptr<Compiled> compileFor(qk_program* p, int nLocal) {
         }
         c->items.push_back(std::move(ci));
     }
+    materialize();
     p->compiled[nLocal] = c;
     return c;
 }
@@ -685,6 +761,30 @@ int qk_debug_compile_block(const qk_gate* gates, int ngates, int nLocal, char** 
         std::vector<double> gtab;
         const std::vector<qkeng::Step> steps = qkeng::compileBlock(gatesFromC(gates, ngates, nLocal), nLocal, gtab);
         *json = dupText(stepsJson(steps, gtab));
+    });
+}
+
+int qk_debug_compile_program(const qk_program* cp, int nLocal, char** json) {
+    return guard([&] {
+        qk_program* p = const_cast<qk_program*>(cp);
+        auto c = compileFor(p, nLocal);
+        std::ostringstream o;
+        o << "{\"items\":[";
+        for (size_t i = 0; i < c->items.size(); i++) {
+            const CompiledItem& it = c->items[i];
+            o << (i ? "," : "") << "{\"kind\":" << int(it.kind) << ",\"pairs\":[";
+            for (size_t j = 0; j < it.outs.size(); j++) o << (j ? "," : "") << "[" << it.outs[j] << "," << it.ins[j] << "]";
+            o << "]";
+            if (it.kind == CompiledItem::Block) {
+                std::vector<qkeng::Step> steps = it.steps;
+                for (qkeng::Step& s : steps)
+                    if (s.kind != qkeng::Step::Pass) s.targets.erase(s.targets.begin());
+                o << ",\"block\":" << stepsJson(steps, c->gtab);
+            }
+            o << "}";
+        }
+        o << "]}";
+        *json = dupText(o.str());
     });
 }
 

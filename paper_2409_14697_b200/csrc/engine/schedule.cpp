@@ -24,7 +24,31 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
+
+namespace qkdev {
+
+namespace {
+int envInt(const char* name, int dflt, int lo, int hi) {
+    const char* v = std::getenv(name);
+    if (!v) return dflt;
+    const int x = std::atoi(v);
+    return (x >= lo && x <= hi) ? x : dflt;
+}
+}  // namespace
+
+int maxTileBits() {
+    static const int v = envInt("QK_MAX_TILE_BITS", kMaxTileBits, 4, kMaxTileBits);
+    return v;
+}
+
+int regBitsFor(int ct) {
+    static const int rb13 = envInt("QK_RB13", 5, 4, 5);
+    return ct >= 13 ? rb13 : (ct < 4 ? ct : 4);
+}
+
+}  // namespace qkdev
 
 namespace qkeng {
 
@@ -125,13 +149,16 @@ public:
         pendScalar_ = false;
         std::fill(pendSlot_, pendSlot_ + kMaxRegBits, false);
         flips_ = 0;
+        batchReset();
         chooseMap(i);
         std::memcpy(P_->map_in[0], map_, sizeof map_);
 
         const size_t first = i;
         double flops = 0;
         while (i < tg_.size()) {
-            if (kMaxOps - nops_ < 12 || kMaxCoef - ncoef_ < 12 || kMaxContrib - ncontrib_ < 16 + ct_ ||
+            const int queued = int(regOps_.size());  // ops still held in the diagonal batch
+            if (kMaxOps - nops_ - queued < 16 || kMaxCoef - ncoef_ - 4 * queued < 16 ||
+                kMaxContrib - ncontrib_ < 16 + ct_ ||
                 kMaxSegs - seg_ < 3)
                 break;
             if (!satisfied(tg_[i], orig_[i])) {
@@ -296,6 +323,7 @@ private:
     }
 
     void flushAll() {
+        emitBatch();
         bool any = hcount_ > 0 || pendScalar_;
         for (int s = 0; s < rb_; s++) any |= pendSlot_[s];
         if (!any) return;
@@ -317,14 +345,91 @@ private:
         pendSlot_[slot] = true;
     }
 
+    // ---- diagonal batches -------------------------------------------------
+    // Consecutive diagonal gates commute, so a run of them (CP / RZ / RZZ /
+    // diagonal U / D_1 / D_2) is folded on the host into at most: one
+    // per-thread scalar table (factors of thread-index bits), one per-slot
+    // pending-phase table per register slot (factors of slot bit x thread
+    // bits), and register-only factors.  Tables are indexed by the compacted
+    // thread bits they depend on (<= 256 entries, L1-resident).  A 42-gate
+    // controlled-phase block becomes ~7 device ops instead of 42.
+    int nthr() const { return 1 << (ct_ - rb_); }
+
+    void batchReset() {
+        batchAny_ = false;
+        tabP_.assign(size_t(nthr()), Amp(1.0, 0.0));
+        maskP_ = 0;
+        usedP_ = false;
+        for (int s = 0; s < kMaxRegBits; s++) {
+            tabR_[s].assign(size_t(nthr()), Amp(1.0, 0.0));
+            maskR_[s] = 0;
+            usedR_[s] = false;
+        }
+        regOps_.clear();
+    }
+
+    // table over thread index t: t -> f(t)
+    template <class F>
+    void mulP(uint32_t mask, F f) {
+        for (int t = 0; t < nthr(); t++) tabP_[size_t(t)] *= f(t);
+        maskP_ |= mask;
+        usedP_ = batchAny_ = true;
+    }
+    template <class F>
+    void mulR(int s, uint32_t mask, F f) {
+        for (int t = 0; t < nthr(); t++) tabR_[s][size_t(t)] *= f(t);
+        maskR_[s] |= mask;
+        usedR_[s] = batchAny_ = true;
+    }
+
+    // compacted table over the bits of `mask` (the factor does not depend on others)
+    uint32_t compactTable(const std::vector<Amp>& full, uint32_t mask) {
+        std::vector<Amp> out;
+        const int bits = __builtin_popcount(mask);
+        for (int i = 0; i < (1 << bits); i++) {
+            int t = 0, r = 0;
+            for (int j = 0; j < 8; j++)
+                if ((mask >> j) & 1) t |= ((i >> r++) & 1) << j;
+            out.push_back(full[size_t(t)]);
+        }
+        return addTable(out);
+    }
+
+    static bool allOne(const std::vector<Amp>& v) {
+        for (const Amp& a : v)
+            if (a != Amp(1.0, 0.0)) return false;
+        return true;
+    }
+
+    void emitBatch() {
+        if (!batchAny_) return;
+        usedP_ = usedP_ && !allOne(tabP_);
+        for (int s = 0; s < rb_; s++) usedR_[s] = usedR_[s] && !allOne(tabR_[s]);
+        if (usedP_) {
+            emit(OP_SCAL_TAB, 0, int(maskP_), 0, compactTable(tabP_, maskP_));
+            pendScalar_ = true;
+        }
+        for (int s = 0; s < rb_; s++)
+            if (usedR_[s]) {
+                emit(OP_PEND_TAB, s, int(maskR_[s]), 0, compactTable(tabR_[s], maskR_[s]));
+                pendSlot_[s] = true;
+            }
+        for (const auto& op : regOps_) emit(op.t, op.a, op.b, op.k, addCoef(op.coef));
+        batchReset();
+    }
+
     // amplitude *= d[logical bit q].  Slot semantics are physical: a flipped
     // slot holds the logical bit inverted, so the entry pair swaps.
     void diag1(int q, std::vector<Amp> d) {
         const int s = inv_[q];
         if (flip(s)) std::swap(d[0], d[1]);
-        if (!isReg(s)) return scalar({d[0], d[1]}, OP_SCAL_T, s - rb_);
-        if (d[0] != Amp(1.0, 0.0)) scalar({d[0]}, OP_SCAL);
-        pending(s, {ratio(d[1], d[0])}, OP_PEND_R);
+        if (!isReg(s)) {
+            const int tb = s - rb_;
+            return mulP(1u << tb, [&](int t) { return d[size_t((t >> tb) & 1)]; });
+        }
+        if (d[0] != Amp(1.0, 0.0)) mulP(0, [&](int) { return d[0]; });
+        const Amp r = ratio(d[1], d[0]);
+        mulR(s, 0, [&](int) { return r; });
     }
 
     // amplitude *= d[2 bit(q0) + bit(q1)] (logical bits).
@@ -342,31 +447,32 @@ private:
                     count++;
                 }
             if (count == 0) return;
+            batchAny_ = true;
             const int lo = std::min(s0, s1), hi = std::max(s0, s1);
-            if (count == 1) {
-                // pattern over (slot lo, slot hi)
+            if (count == 1) {  // pattern over (slot lo, slot hi)
                 const int b0 = nonUnit >> 1, b1 = nonUnit & 1;
                 const int pat = s0 == lo ? (b0 << 1 | b1) : (b1 << 1 | b0);
-                emit(OP_CPHASE_RR, lo, hi, pat, addCoef({d[size_t(nonUnit)]}));
+                regOps_.push_back({OP_CPHASE_RR, lo, hi, pat, {d[size_t(nonUnit)]}});
             } else {
-                emit(OP_DIAG2_RR, s0, s1, 0, addCoef(d));
+                regOps_.push_back({OP_DIAG2_RR, s0, s1, 0, d});
             }
-        } else if (isReg(s0)) {  // factor = d[2 r + t]
-            const int t = s1 - rb_;
-            scalar({d[0], d[1]}, OP_SCAL_T, t);
-            pending(s0, {ratio(d[2], d[0]), ratio(d[3], d[1])}, OP_PEND_RT, t);
-        } else if (isReg(s1)) {  // factor = d[2 t + r]
-            const int t = s0 - rb_;
-            scalar({d[0], d[2]}, OP_SCAL_T, t);
-            pending(s1, {ratio(d[1], d[0]), ratio(d[3], d[2])}, OP_PEND_RT, t);
+        } else if (isReg(s0) || isReg(s1)) {
+            // factor(r, t): r = register slot bit, t = thread bit
+            const bool regIsMsb = isReg(s0);
+            const int rs = regIsMsb ? s0 : s1, tb = (regIsMsb ? s1 : s0) - rb_;
+            auto at = [&](int r, int t) { return regIsMsb ? d[size_t(2 * r + t)] : d[size_t(2 * t + r)]; };
+            mulP(1u << tb, [&](int t) { return at(0, (t >> tb) & 1); });
+            mulR(rs, 1u << tb, [&](int t) { return ratio(at(1, (t >> tb) & 1), at(0, (t >> tb) & 1)); });
         } else {
-            scalar(d, OP_SCAL_TT, s0 - rb_, s1 - rb_);
+            const int ta = s0 - rb_, tb = s1 - rb_;
+            mulP((1u << ta) | (1u << tb), [&](int t) { return d[size_t(2 * ((t >> ta) & 1) + ((t >> tb) & 1))]; });
         }
     }
 
     void mat1(int q, std::vector<Amp> m) {
         const int s = inv_[q];
         if (flip(s)) m = {m[3], m[2], m[1], m[0]};  // X M X
+        emitBatch();
         flushSlot(s);
         emit(OP_MAT1, s, 0, 0, addCoef(m));
     }
@@ -375,6 +481,7 @@ private:
         switch (g.kind) {
             case GateKind::H: {
                 const int s = inv_[g.targets[0]];
+                emitBatch();
                 flushSlot(s);
                 emit(OP_H, s);
                 hcount_++;
@@ -396,6 +503,7 @@ private:
             }
             case GateKind::CX: {
                 const int t = inv_[g.targets[0]], c = inv_[g.controls[0]];
+                emitBatch();
                 flushSlot(t);
                 const int pol = flip(c);  // physical control value that means logical 1 is (1 ^ pol)
                 if (isReg(c)) emit(OP_CX, t, c, pol << 1);
@@ -450,6 +558,7 @@ private:
                 std::vector<Amp> m(dim * dim);
                 for (size_t r = 0; r < dim; r++)
                     for (size_t c = 0; c < dim; c++) m[r * dim + c] = orig.payload[(r ^ f) * dim + (c ^ f)];
+                emitBatch();
                 for (int s = 0; s < k; s++) flushSlot(s);
                 emit(OP_DENSE, 0, 0, k, addTable(m));
                 return;
@@ -466,6 +575,19 @@ private:
     int nops_ = 0, ncoef_ = 0, ncontrib_ = 0, seg_ = 0, hcount_ = 0;
     bool pendScalar_ = false;
     bool pendSlot_[kMaxRegBits] = {};
+    // current diagonal batch
+    struct RegOp {
+        OpType t;
+        int a, b, k;
+        std::vector<Amp> coef;
+    };
+    bool batchAny_ = false, usedP_ = false;
+    std::vector<Amp> tabP_;
+    uint32_t maskP_ = 0;
+    std::vector<Amp> tabR_[kMaxRegBits];
+    uint32_t maskR_[kMaxRegBits] = {};
+    bool usedR_[kMaxRegBits] = {};
+    std::vector<RegOp> regOps_;
     uint32_t flips_ = 0;  // slots (register and thread) holding an inverted bit
     uint8_t map_[16] = {};
     int inv_[16] = {};
@@ -529,7 +651,7 @@ std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::
         for (const Gate& g : gates) denseStep(quokka::gateMatrix(g), g.qubits(), referenceFlopsPerAmp(g));
         return steps;
     }
-    const int ct = std::min(kMaxTileBits, nLocal);
+    const int ct = std::min(maxTileBits(), nLocal);
     const int rb = regBitsFor(ct);
     std::vector<Gate> group;
     uint64_t used = 0;

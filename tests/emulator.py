@@ -6,7 +6,17 @@ against the oracle without a GPU.  Never used by the product."""
 import numpy as np
 
 OPS = ["MAT1", "H", "CX", "DIAG1_R", "DIAG2_RR", "CPHASE_RR", "PEND_R", "PEND_RT", "SCAL", "SCAL_T",
-       "SCAL_TT", "FLUSH_SLOT", "FLUSH", "DTABLE", "DENSE", "EXCHANGE"]
+       "SCAL_TT", "FLUSH_SLOT", "FLUSH", "DTABLE", "DENSE", "EXCHANGE", "SCAL_TAB", "PEND_TAB"]
+
+
+def pext8(t, m):
+    r = np.zeros_like(t)
+    i = 0
+    for j in range(8):
+        if (m >> j) & 1:
+            r |= ((t >> j) & 1) << i
+            i += 1
+    return r
 
 
 def swz(u):
@@ -132,6 +142,10 @@ def _run_pass(state, n, P, gt):
                 R[:, oa] *= coef[oc]
             elif name == "PEND_RT":
                 R[:, oa] *= coef[oc + bit(tid, ob)]
+            elif name == "SCAL_TAB":
+                Pt *= gt[oc + pext8(tid, ob)]
+            elif name == "PEND_TAB":
+                R[:, oa] *= gt[oc + pext8(tid, ob)]
             elif name == "SCAL":
                 Pt *= coef[oc]
             elif name == "SCAL_T":

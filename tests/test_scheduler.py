@@ -98,3 +98,51 @@ def test_pass_capacity_split(qk, port):
     out = st.view(np.complex128).copy()
     run_steps(out, n, prog)
     assert np.max(np.abs(out - want.view(np.complex128))) < 1e-11
+
+
+def run_compiled(qk, port, prog, n, initial):
+    """Replay the engine's compiled item list (lazy IMS included) on the CPU."""
+    st = np.zeros(1 << n, dtype=np.complex128)
+    st[initial] = 1
+    for it in prog.debug_compile(n)["items"]:
+        if it["kind"] == 0:
+            run_steps(st, n, it["block"])
+        elif it["kind"] == 1:
+            f = st.view(np.float64)
+            port.ims_swap(f, n, [tuple(p) for p in it["pairs"]])
+        else:
+            raise AssertionError("cross-rank item in a single-rank program")
+    return st
+
+
+@pytest.mark.parametrize("name", sorted(k for k in P if "program" in P[k] and P[k]["r"] == 0))
+def test_compiled_programs_match_golden(qk, port, name):
+    case = P[name]
+    prog = qk.Program.parse(case["program"], qk.Config.parse(case["config"]))
+    for initial in (0, 5):
+        got = run_compiled(qk, port, prog, case["n"], initial)
+        want = G[f"{name}/init{initial}/state"].view(np.complex128)
+        assert np.max(np.abs(got - want)) < 1e-10
+
+
+def test_lazy_ims_removes_swap_passes(qk):
+    n = 16
+    cfg = qk.Config.make(n, 0, chunk=8, fusion=0, diag=0)
+    prog = qk.Program.optimize(qk.generate("qft", n), cfg)
+    items = prog.debug_compile()["items"]
+    ims = [it for it in items if it["kind"] == 1]
+    assert prog.counts()["sqs"] > 2 and len(ims) <= 2  # only the final materialization
+
+
+def test_random_programs_lazy(qk, port, ref):
+    rng = np.random.default_rng(77)
+    for i in range(12):
+        n = int(rng.integers(5, 11))
+        c = int(rng.integers(3, n + 1))
+        cfg_text = config_text(n, 0, c, fusion=i % 2, diag=(i // 2) % 2)
+        circ = ref.gen("random", n, 70, 500 + i)
+        prog_text = ref.optimize(circ, cfg_text)
+        want, _, _, _ = ref.simulate(prog_text, cfg_text, n, 0, 3, 1)
+        prog = qk.Program.parse(prog_text, qk.Config.parse(cfg_text))
+        got = run_compiled(qk, port, prog, n, 3)
+        assert np.max(np.abs(got - want.view(np.complex128))) < 1e-10, i
