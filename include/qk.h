@@ -99,6 +99,12 @@ int qk_apply_block(qk_state* st, const qk_gate* gates, int ngates, int chunk_qub
 /* Scheduler test hook (host only, no device): the compiled pass programs of a
  * block for a 2^n_local slice, as JSON (tests/emulator.py replays them). */
 int qk_debug_compile_block(const qk_gate* gates, int ngates, int n_local, char** json);
+/* Slices with >= v local qubits run straight-line specialized pass kernels
+ * (NVRTC, cached by pass content); smaller ones the pass interpreter; -1 = never. */
+int qk_set_jit_min_qubits(int v);
+/* Generate + NVRTC-compile the specialized kernels of a block (host only);
+ * returns their CUDA source. */
+int qk_debug_jit_compile(const qk_gate* gates, int ngates, int n_local, char** source);
 /* ... and of a whole program (device item list: blocks, IMS, XRS). */
 int qk_debug_compile_program(const qk_program* p, int n_local, char** json);
 /* engine.cpp:258-260 applyGate (whole slice, any position < N-R). */

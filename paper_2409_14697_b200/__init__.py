@@ -116,6 +116,8 @@ def lib():
         "qk_apply_gate": ([P, C.POINTER(_Gate)], I),
         "qk_debug_compile_block": ([C.POINTER(_Gate), I, I, C.POINTER(P)], I),
         "qk_debug_compile_program": ([P, I, C.POINTER(P)], I),
+        "qk_debug_jit_compile": ([C.POINTER(_Gate), I, I, C.POINTER(P)], I),
+        "qk_set_jit_min_qubits": ([I], I),
         "qk_ims_swap": ([P, C.POINTER(I), C.POINTER(I), I, I], I),
         "qk_xrs_swap_local": ([C.POINTER(P), I, C.POINTER(I), C.POINTER(I), I, C.POINTER(_XrsStats)], I),
         "qk_xrs_plan": ([I, I, I, I, C.POINTER(I), C.POINTER(I), I, C.POINTER(_XrsMsg), I,
@@ -409,6 +411,17 @@ def debug_compile_block(gates, n_local: int) -> dict:
     import json
     arr, keep = _gate_array(gates)
     return json.loads(_text(lib().qk_debug_compile_block, arr, len(keep), n_local))
+
+
+def set_jit_min_qubits(v: int) -> None:
+    """Slices with >= v local qubits use straight-line specialized pass kernels."""
+    _check(lib().qk_set_jit_min_qubits(v))
+
+
+def debug_jit_compile(gates, n_local: int) -> str:
+    """Generate and NVRTC-compile a block's specialized kernels (host only)."""
+    arr, keep = _gate_array(gates)
+    return _text(lib().qk_debug_jit_compile, arr, len(keep), n_local)
 
 
 def apply_gate(state: State, gate) -> None:

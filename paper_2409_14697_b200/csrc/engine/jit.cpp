@@ -1,0 +1,506 @@
+// Straight-line pass specialization: PassParams -> CUDA C++ -> NVRTC cubin.
+//
+// Emits exactly the semantics of k_block_pass (block_pass.cu) for one
+// PassParams, with everything the interpreter decides at run time resolved
+// at generation time: the op switch disappears, coefficients become
+// literals, register swaps (CX with a register control) become variable
+// renames, and deferred factors that are statically untouched are skipped.
+// The whole pass is one basic block per segment, so ptxas schedules the
+// independent amplitude updates of consecutive gates together (ILP the
+// interpreter's per-op dispatch cannot give).
+#include "jit.h"
+
+#include <dlfcn.h>
+#include <nvrtc.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <mutex>
+#include <sstream>
+#include <thread>
+
+#include "quokka/common.hpp"
+
+namespace qkjit {
+
+using qkdev::DevOp;
+using qkdev::PassParams;
+using quokka::SimulationError;
+
+namespace {
+
+std::string lit(double v) {
+    char buf[40];
+    std::snprintf(buf, sizeof buf, "%a", v);
+    return buf;
+}
+
+std::string c2(double re, double im) { return "C2(" + lit(re) + "," + lit(im) + ")"; }
+
+uint32_t swzHost(uint32_t u) { return u ^ (((u >> 3) ^ (u >> 6) ^ (u >> 9) ^ (u >> 12)) & 7u); }
+
+const char* kPrologue = R"(
+#include <cuda_runtime.h>
+typedef unsigned long long u64;
+typedef unsigned int u32;
+#define C2(r, i) make_double2((r), (i))
+static __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+static __device__ __forceinline__ double2 cmac(double2 acc, double2 m, double2 x) {
+    acc.x = fma(m.x, x.x, acc.x); acc.x = fma(-m.y, x.y, acc.x);
+    acc.y = fma(m.x, x.y, acc.y); acc.y = fma(m.y, x.x, acc.y);
+    return acc;
+}
+static __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+static __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+static __device__ __forceinline__ double2 csel(bool c, double2 x, double2 y) {
+    return make_double2(c ? x.x : y.x, c ? x.y : y.y);
+}
+static __device__ __forceinline__ u32 swz(u32 u) { return u ^ (((u >> 3) ^ (u >> 6) ^ (u >> 9) ^ (u >> 12)) & 7u); }
+)";
+
+class Gen {
+public:
+    explicit Gen(const PassParams& P) : P_(P), ct_(P.ct), rb_(P.rb), na_(1 << P.rb), nt_(1 << (P.ct - P.rb)) {
+        for (int s = 0; s < na_; s++) nm_.push_back(s);
+    }
+
+    std::string run(const std::string& name) {
+        const int minb = (ct_ == 12 && rb_ == 4) ? 2 : 1;
+        o_ << kPrologue;
+        o_ << "extern \"C\" __global__ void __launch_bounds__(" << nt_ << "," << minb << ") " << name
+           << "(double2* __restrict__ st, const double2* __restrict__ gt) {\n";
+        o_ << "  extern __shared__ double2 sm[];\n  const u32 tid = threadIdx.x;\n  u64 base = blockIdx.x;\n";
+        for (int j = 0; j < ct_; j++) {
+            const int p = P_.tile_phys[j];
+            o_ << "  base = ((base >> " << p << ") << " << (p + 1) << ") | (base & " << ((uint64_t(1) << p) - 1)
+               << "ull);\n";
+        }
+        // load (map_in[0], no flips)
+        o_ << "  { const u64 off = base | " << threadGlobal(P_.map_in[0]) << ";\n";
+        for (int s = 0; s < na_; s++)
+            o_ << "  a" << s << " = __ldcs(st + (off | " << regGlobal(P_.map_in[0], s) << "ull));\n";
+        o_ << "  }\n";
+        std::string decl = "  double2 ";
+        for (int s = 0; s < na_; s++) decl += (s ? ", a" : "a") + std::to_string(s);
+        // declarations must precede use: splice them in front of the load
+        std::string body = o_.str();
+        const size_t at = body.find("  { const u64 off = base |");
+        body.insert(at, decl + ";\n  double2 P = C2(1.0, 0.0);\n" + pendDecl());
+        o_.str("");
+        o_ << body;
+
+        for (int i = 0; i < P_.nops; i++) op(P_.ops[i]);
+
+        // store (map_out[last] with flips)
+        const int last = P_.nsegs - 1;
+        uint64_t gx = 0;
+        for (int j = 0; j < ct_; j++)
+            if ((P_.xmask_out[last] >> j) & 1) gx |= uint64_t(1) << P_.tile_phys[j];
+        o_ << "  { const u64 off = (base | " << threadGlobal(P_.map_out[last]) << ") ^ " << gx << "ull;\n";
+        for (int s = 0; s < na_; s++)
+            o_ << "  __stcs(st + (off ^ " << regGlobal(P_.map_out[last], s) << "ull), a" << nm_[size_t(s)] << ");\n";
+        o_ << "  }\n}\n";
+        return o_.str();
+    }
+
+private:
+    std::string pendDecl() {
+        std::string d;
+        for (int k = 0; k < rb_; k++) d += "  double2 R" + std::to_string(k) + " = C2(1.0, 0.0);\n";
+        return d;
+    }
+    std::string tb(int j) const { return "((tid >> " + std::to_string(j) + ") & 1u)"; }
+
+    // thread part of the global offset under map m
+    std::string threadGlobal(const uint8_t* m) const {
+        std::string e = "(u64)0";
+        for (int j = 0; j < ct_ - rb_; j++)
+            e += " | ((u64)" + tb(j) + " << " + std::to_string(int(P_.tile_phys[m[rb_ + j]])) + ")";
+        return "(" + e + ")";
+    }
+    uint64_t regGlobal(const uint8_t* m, int s) const {
+        uint64_t o = 0;
+        for (int k = 0; k < rb_; k++)
+            if ((s >> k) & 1) o |= uint64_t(1) << P_.tile_phys[m[k]];
+        return o;
+    }
+    std::string threadSmem(const uint8_t* m) const {
+        std::string e = "0u";
+        for (int j = 0; j < ct_ - rb_; j++) e += " | (" + tb(j) + " << " + std::to_string(int(m[rb_ + j])) + ")";
+        return "(" + e + ")";
+    }
+    uint32_t regSmem(const uint8_t* m, int s) const {
+        uint32_t u = 0;
+        for (int k = 0; k < rb_; k++)
+            if ((s >> k) & 1) u |= 1u << m[k];
+        return swzHost(u);
+    }
+
+    std::string lc(uint32_t i) const { return c2(P_.coef[2 * i], P_.coef[2 * i + 1]); }
+    std::string A(int s) const { return "a" + std::to_string(nm_[size_t(s)]); }
+
+    void mulAmp(int s, const std::string& e) { o_ << "  " << A(s) << " = cmul(" << A(s) << ", " << e << ");\n"; }
+
+    std::string pext(uint32_t mask) const {
+        std::string e = "0u";
+        int r = 0;
+        for (int j = 0; j < 8; j++)
+            if ((mask >> j) & 1) e += " | (" + tb(j) + " << " + std::to_string(r++) + ")";
+        return "(" + e + ")";
+    }
+
+    void op(const DevOp& d) {
+        const int a = d.a, b = d.b, K = 1 << d.a;
+        switch (d.type) {
+            case qkdev::OP_H:
+                for (int s = 0; s < na_; s++)
+                    if (!(s & K))
+                        o_ << "  { const double2 x = " << A(s) << ", y = " << A(s | K) << "; " << A(s)
+                           << " = cadd(x, y); " << A(s | K) << " = csub(x, y); }\n";
+                return;
+            case qkdev::OP_MAT1:
+                for (int s = 0; s < na_; s++)
+                    if (!(s & K))
+                        o_ << "  { const double2 x = " << A(s) << ", y = " << A(s | K) << "; " << A(s) << " = cmac(cmul("
+                           << lc(d.c) << ", x), " << lc(d.c + 1) << ", y); " << A(s | K) << " = cmac(cmul("
+                           << lc(d.c + 2) << ", x), " << lc(d.c + 3) << ", y); }\n";
+                return;
+            case qkdev::OP_CX: {
+                const int pol = (d.k >> 1) & 1;
+                if (d.k & 1) {  // thread-bit control: selects
+                    o_ << "  { const bool c = (" << tb(b) << " ^ " << pol << "u) != 0u;\n";
+                    for (int s = 0; s < na_; s++)
+                        if (!(s & K))
+                            o_ << "    { const double2 x = " << A(s) << ", y = " << A(s | K) << "; " << A(s)
+                               << " = csel(c, y, x); " << A(s | K) << " = csel(c, x, y); }\n";
+                    o_ << "  }\n";
+                } else {  // register control: pure rename
+                    for (int s = 0; s < na_; s++)
+                        if (!(s & K) && ((s >> b) & 1) == (1 ^ pol)) std::swap(nm_[size_t(s)], nm_[size_t(s | K)]);
+                }
+                return;
+            }
+            case qkdev::OP_DIAG1_R:
+                for (int s = 0; s < na_; s++) mulAmp(s, lc(d.c + ((s >> a) & 1)));
+                return;
+            case qkdev::OP_DIAG2_RR:
+                for (int s = 0; s < na_; s++) mulAmp(s, lc(d.c + ((((s >> a) & 1) << 1) | ((s >> b) & 1))));
+                return;
+            case qkdev::OP_CPHASE_RR:
+                for (int s = 0; s < na_; s++)
+                    if (((((s >> a) & 1) << 1) | ((s >> b) & 1)) == d.k) mulAmp(s, lc(d.c));
+                return;
+            case qkdev::OP_PEND_R:
+                o_ << "  R" << a << " = cmul(R" << a << ", " << lc(d.c) << ");\n";
+                dirtyR_[a] = true;
+                return;
+            case qkdev::OP_PEND_RT:
+                o_ << "  R" << a << " = cmul(R" << a << ", " << tb(b) << " ? " << lc(d.c + 1) << " : " << lc(d.c)
+                   << ");\n";
+                dirtyR_[a] = true;
+                return;
+            case qkdev::OP_SCAL:
+                o_ << "  P = cmul(P, " << lc(d.c) << ");\n";
+                dirtyP_ = true;
+                return;
+            case qkdev::OP_SCAL_T:
+                o_ << "  P = cmul(P, " << tb(a) << " ? " << lc(d.c + 1) << " : " << lc(d.c) << ");\n";
+                dirtyP_ = true;
+                return;
+            case qkdev::OP_SCAL_TT:
+                o_ << "  { const u32 i = (" << tb(a) << " << 1) | " << tb(b) << "; P = cmul(P, i == 0u ? " << lc(d.c)
+                   << " : i == 1u ? " << lc(d.c + 1) << " : i == 2u ? " << lc(d.c + 2) << " : " << lc(d.c + 3)
+                   << "); }\n";
+                dirtyP_ = true;
+                return;
+            case qkdev::OP_SCAL_TAB:
+                o_ << "  P = cmul(P, __ldg(gt + " << d.c << "u + " << pext(d.b) << "));\n";
+                dirtyP_ = true;
+                return;
+            case qkdev::OP_PEND_TAB:
+                o_ << "  R" << a << " = cmul(R" << a << ", __ldg(gt + " << d.c << "u + " << pext(d.b) << "));\n";
+                dirtyR_[a] = true;
+                return;
+            case qkdev::OP_FLUSH_SLOT:
+                if (!dirtyR_[a]) return;
+                for (int s = 0; s < na_; s++)
+                    if (s & K) mulAmp(s, "R" + std::to_string(a));
+                o_ << "  R" << a << " = C2(1.0, 0.0);\n";
+                dirtyR_[a] = false;
+                return;
+            case qkdev::OP_FLUSH:
+                flush(P_.coef[2 * d.c]);
+                return;
+            case qkdev::OP_DTABLE: {
+                const uint16_t* cb = &P_.contrib[d.c16];
+                std::string sub = "0u";
+                for (int j = rb_; j < ct_; j++)
+                    if (cb[j]) sub += " | (" + tb(j - rb_) + " ? " + std::to_string(cb[j]) + "u : 0u)";
+                o_ << "  { const u32 sub = " << sub << ";\n";
+                for (int s = 0; s < na_; s++) {
+                    uint32_t cs = 0;
+                    for (int k = 0; k < rb_; k++)
+                        if ((s >> k) & 1) cs |= cb[k];
+                    o_ << "  " << A(s) << " = cmul(" << A(s) << ", __ldg(gt + " << d.c << "u + ((sub | " << cs << "u) ^ "
+                       << d.x16 << "u)));\n";
+                }
+                o_ << "  }\n";
+                return;
+            }
+            case qkdev::OP_DENSE: {
+                const int D = 1 << d.k;
+                for (int g = 0; g < na_ / D; g++) {
+                    o_ << "  {\n";
+                    for (int s = 0; s < D; s++) o_ << "    const double2 x" << s << " = " << A(g * D + s) << ";\n";
+                    for (int r = 0; r < D; r++) {
+                        o_ << "    { double2 acc = C2(0.0, 0.0);";
+                        for (int s = 0; s < D; s++)
+                            o_ << " acc = cmac(acc, __ldg(gt + " << (d.c + uint32_t(r * D + s)) << "u), x" << s << ");";
+                        o_ << " " << A(g * D + r) << " = acc; }\n";
+                    }
+                    o_ << "  }\n";
+                }
+                return;
+            }
+            case qkdev::OP_EXCHANGE: {
+                const uint8_t* mo = P_.map_out[d.c - 1];
+                const uint8_t* mi = P_.map_in[d.c];
+                o_ << "  __syncthreads();\n  { const u32 u = swz(" << threadSmem(mo) << ") ^ "
+                   << swzHost(P_.xmask_out[d.c - 1]) << "u;\n";
+                for (int s = 0; s < na_; s++) o_ << "  sm[u ^ " << regSmem(mo, s) << "u] = " << A(s) << ";\n";
+                o_ << "  }\n  __syncthreads();\n  { const u32 u = swz(" << threadSmem(mi) << ");\n";
+                for (int s = 0; s < na_; s++) nm_[size_t(s)] = s;
+                for (int s = 0; s < na_; s++) o_ << "  " << A(s) << " = sm[u ^ " << regSmem(mi, s) << "u];\n";
+                o_ << "  }\n";
+                return;
+            }
+            default:
+                throw SimulationError("jit: unknown op");
+        }
+    }
+
+    // a[s] *= scale * P * prod_{k: bit k of s} R[k], touching only dirty factors.
+    void flush(double scale) {
+        bool anyR = false;
+        for (int k = 0; k < rb_; k++) anyR |= dirtyR_[k];
+        if (!anyR && !dirtyP_) {
+            if (scale != 1.0)
+                for (int s = 0; s < na_; s++)
+                    o_ << "  " << A(s) << " = make_double2(" << A(s) << ".x * " << lit(scale) << ", " << A(s) << ".y * "
+                       << lit(scale) << ");\n";
+            return;
+        }
+        o_ << "  {\n    const double2 f0 = " << (dirtyP_ ? "make_double2(P.x * " + lit(scale) + ", P.y * " + lit(scale) + ")"
+                                                         : c2(scale, 0.0))
+           << ";\n";
+        // f_s = f_{s without its highest set bit} * R_high ; computed on the fly per s
+        for (int s = 1; s < na_; s++) {
+            int hi = 31 - __builtin_clz(unsigned(s));
+            const int rest = s & ~(1 << hi);
+            if (dirtyR_[hi]) o_ << "    const double2 f" << s << " = cmul(f" << rest << ", R" << hi << ");\n";
+            else o_ << "    const double2 f" << s << " = f" << rest << ";\n";
+        }
+        for (int s = 0; s < na_; s++) mulAmp(s, "f" + std::to_string(s));
+        o_ << "  }\n  P = C2(1.0, 0.0);\n";
+        for (int k = 0; k < rb_; k++)
+            if (dirtyR_[k]) o_ << "  R" << k << " = C2(1.0, 0.0);\n";
+        dirtyP_ = false;
+        for (int k = 0; k < rb_; k++) dirtyR_[k] = false;
+    }
+
+    const PassParams& P_;
+    int ct_, rb_, na_, nt_;
+    std::vector<int> nm_;
+    bool dirtyP_ = false;
+    bool dirtyR_[qkdev::kMaxRegBits] = {};
+    std::ostringstream o_;
+};
+
+// ---- compile / load / launch -------------------------------------------------
+
+uint64_t hashPass(const PassParams& P) {
+    uint64_t h = 1469598103934665603ull;
+    const unsigned char* p = reinterpret_cast<const unsigned char*>(&P);
+    for (size_t i = 0; i < sizeof(PassParams); i++) {
+        h ^= p[i];
+        h *= 1099511628211ull;
+    }
+    return h;
+}
+
+// Driver API through dlopen: the library must load on hosts without libcuda.
+struct Driver {
+    using Res = int;
+    Res (*moduleLoadData)(void**, const void*) = nullptr;
+    Res (*moduleGetFunction)(void**, void*, const char*) = nullptr;
+    Res (*funcSetAttribute)(void*, int, int) = nullptr;
+    Res (*launchKernel)(void*, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, void*, void**,
+                        void**) = nullptr;
+    bool ok = false;
+    Driver() {
+        void* h = dlopen("libcuda.so.1", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return;
+        moduleLoadData = reinterpret_cast<decltype(moduleLoadData)>(dlsym(h, "cuModuleLoadData"));
+        moduleGetFunction = reinterpret_cast<decltype(moduleGetFunction)>(dlsym(h, "cuModuleGetFunction"));
+        funcSetAttribute = reinterpret_cast<decltype(funcSetAttribute)>(dlsym(h, "cuFuncSetAttribute"));
+        launchKernel = reinterpret_cast<decltype(launchKernel)>(dlsym(h, "cuLaunchKernel"));
+        ok = moduleLoadData && moduleGetFunction && funcSetAttribute && launchKernel;
+    }
+};
+
+Driver& driver() {
+    static Driver d;
+    return d;
+}
+
+struct Entry {
+    std::vector<char> cubin;
+    std::map<int, void*> func;  // device -> CUfunction
+};
+
+std::mutex g_mu;
+std::map<uint64_t, Entry> g_cache;
+
+std::string kernelName(uint64_t h) {
+    char buf[40];
+    std::snprintf(buf, sizeof buf, "qk_pass_%016llx", static_cast<unsigned long long>(h));
+    return buf;
+}
+
+std::string cacheDir() {
+    const char* d = std::getenv("QK_JIT_CACHE");
+    return d ? d : "/tmp/qk_jit_cache";
+}
+
+std::vector<char> cubinFor(const PassParams& P, uint64_t h) {
+    const std::string path = cacheDir() + "/" + kernelName(h) + ".cubin";
+    {
+        std::ifstream in(path, std::ios::binary);
+        if (in) return std::vector<char>((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+    }
+    std::vector<char> bin = compileToCubin(generatePassSource(P, kernelName(h)), kernelName(h));
+    std::string mk = "mkdir -p '" + cacheDir() + "'";
+    if (std::system(mk.c_str()) == 0) {
+        const std::string tmp = path + ".tmp" + std::to_string(reinterpret_cast<uintptr_t>(&bin));
+        std::ofstream out(tmp, std::ios::binary);
+        out.write(bin.data(), std::streamsize(bin.size()));
+        out.close();
+        std::rename(tmp.c_str(), path.c_str());
+    }
+    return bin;
+}
+
+void* functionFor(const PassParams& P, uint64_t h, int device) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    Entry& e = g_cache[h];
+    auto it = e.func.find(device);
+    if (it != e.func.end()) return it->second;
+    if (e.cubin.empty()) throw SimulationError("jit: pass not prepared");
+    Driver& d = driver();
+    if (!d.ok) throw SimulationError("jit: libcuda.so.1 not available");
+    void* mod = nullptr;
+    void* fn = nullptr;
+    if (d.moduleLoadData(&mod, e.cubin.data()) != 0) throw SimulationError("jit: cuModuleLoadData failed");
+    if (d.moduleGetFunction(&fn, mod, kernelName(h).c_str()) != 0) throw SimulationError("jit: cuModuleGetFunction failed");
+    const int smem = int(sizeof(double2) << P.ct);
+    if (smem > 48 * 1024 && d.funcSetAttribute(fn, 8 /*CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES*/, smem) != 0)
+        throw SimulationError("jit: cuFuncSetAttribute failed");
+    e.func[device] = fn;
+    return fn;
+}
+
+}  // namespace
+
+std::string generatePassSource(const PassParams& P, const std::string& name) { return Gen(P).run(name); }
+
+std::vector<char> compileToCubin(const std::string& src, const std::string& name) {
+    nvrtcProgram prog;
+    if (nvrtcCreateProgram(&prog, src.c_str(), (name + ".cu").c_str(), 0, nullptr, nullptr) != NVRTC_SUCCESS)
+        throw SimulationError("jit: nvrtcCreateProgram failed");
+    const char* opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-default-device", "-lineinfo",
+                          "-I/usr/local/cuda/include"};
+    const nvrtcResult r = nvrtcCompileProgram(prog, 5, opts);
+    if (r != NVRTC_SUCCESS) {
+        size_t n = 0;
+        nvrtcGetProgramLogSize(prog, &n);
+        std::string log(n, '\0');
+        nvrtcGetProgramLog(prog, &log[0]);
+        nvrtcDestroyProgram(&prog);
+        throw SimulationError("jit: NVRTC failed: " + log.substr(0, 2000));
+    }
+    size_t n = 0;
+    nvrtcGetCUBINSize(prog, &n);
+    std::vector<char> bin(n);
+    nvrtcGetCUBIN(prog, bin.data());
+    nvrtcDestroyProgram(&prog);
+    return bin;
+}
+
+namespace {
+std::atomic<int>& minQubitsVar() {
+    static std::atomic<int> v{[] {
+        const char* e = std::getenv("QK_JIT_MIN_QUBITS");
+        return e ? std::atoi(e) : 22;
+    }()};
+    return v;
+}
+}  // namespace
+
+int minQubits() { return minQubitsVar().load(); }
+void setMinQubits(int v) { minQubitsVar().store(v); }
+
+void prepare(const std::vector<const PassParams*>& passes, int device) {
+    std::vector<std::pair<uint64_t, const PassParams*>> todo;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        std::map<uint64_t, bool> seen;
+        for (const PassParams* P : passes) {
+            const uint64_t h = hashPass(*P);
+            if (seen[h] || !g_cache[h].cubin.empty()) continue;
+            seen[h] = true;
+            todo.emplace_back(h, P);
+        }
+    }
+    std::atomic<size_t> next{0};
+    std::string err;
+    std::mutex errMu;
+    auto worker = [&] {
+        for (size_t i; (i = next++) < todo.size();) {
+            try {
+                std::vector<char> bin = cubinFor(*todo[i].second, todo[i].first);
+                std::lock_guard<std::mutex> lk(g_mu);
+                g_cache[todo[i].first].cubin = std::move(bin);
+            } catch (const std::exception& e) {
+                std::lock_guard<std::mutex> lk(errMu);
+                err = e.what();
+            }
+        }
+    };
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    std::vector<std::thread> ts;
+    for (unsigned t = 0; t < std::min<unsigned>(hw, unsigned(todo.size())); t++) ts.emplace_back(worker);
+    for (auto& t : ts) t.join();
+    if (!err.empty()) throw SimulationError(err);
+    for (const PassParams* P : passes) functionFor(*P, hashPass(*P), device);
+}
+
+cudaError_t launch(const PassParams& P, double2* state, const double2* gtab, int nLocal, cudaStream_t stream) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    void* fn = functionFor(P, hashPass(P), dev);
+    const unsigned ctas = unsigned(uint64_t(1) << (nLocal - P.ct));
+    const unsigned nt = 1u << (P.ct - P.rb);
+    const unsigned smem = unsigned(sizeof(double2) << P.ct);
+    void* args[] = {&state, &gtab};
+    if (driver().launchKernel(fn, ctas, 1, 1, nt, 1, 1, smem, stream, args, nullptr) != 0)
+        return cudaErrorLaunchFailure;
+    return cudaSuccess;
+}
+
+}  // namespace qkjit

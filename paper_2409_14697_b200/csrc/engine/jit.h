@@ -1,0 +1,38 @@
+// Straight-line specialization of fused passes (NVRTC -> sm_100a cubin).
+//
+// The pass interpreter (block_pass.cu) dispatches every op at run time; for
+// large slices the same PassParams is instead emitted as one straight-line
+// kernel (ops unrolled, coefficients as literals, register swaps as renames)
+// and compiled once per distinct pass with NVRTC.  Same semantics op for op;
+// tests/test_gpu_jit.py checks the two against each other and the oracle.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "pass_program.h"
+
+namespace qkjit {
+
+// CUDA C++ source of a kernel named `name` applying P (exported for tests).
+std::string generatePassSource(const qkdev::PassParams& P, const std::string& name);
+
+// Compiles (or fetches from the process / disk cache) every pass for
+// `device`, in parallel.  Throws SimulationError on NVRTC / driver failures.
+void prepare(const std::vector<const qkdev::PassParams*>& passes, int device);
+
+// Launch the specialized kernel of P (prepare()d for the current device).
+cudaError_t launch(const qkdev::PassParams& P, double2* state, const double2* gtab, int nLocal,
+                   cudaStream_t stream);
+
+// Slices with at least this many local qubits use specialized kernels
+// (QK_JIT_MIN_QUBITS, default 22; -1 disables).
+int minQubits();
+void setMinQubits(int v);
+
+// NVRTC compile of a source to a cubin (used by tests on the CPU too).
+std::vector<char> compileToCubin(const std::string& src, const std::string& name);
+
+}  // namespace qkjit

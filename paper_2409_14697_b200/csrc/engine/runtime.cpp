@@ -23,6 +23,7 @@
 #include "quokka/circuit.hpp"
 #include "quokka/optimizer.hpp"
 #include "quokka/tools.hpp"
+#include "jit.h"
 #include "schedule.h"
 
 namespace qkdev {
@@ -412,10 +413,27 @@ struct Timer {
     }
 };
 
+// Large slices run each pass as a straight-line specialized kernel (jit.h);
+// the interpreter kernel serves small slices (no compile latency).
+bool useJit(int nLocal) { return qkjit::minQubits() >= 0 && nLocal >= qkjit::minQubits(); }
+
+// Compile (once, cached by content hash) every pass of a compiled program.
+void prepareJit(const Compiled& c, int device) {
+    if (!useJit(c.nLocal)) return;
+    std::vector<const qkdev::PassParams*> passes;
+    for (const CompiledItem& it : c.items)
+        for (const qkeng::Step& s : it.steps)
+            if (s.kind == qkeng::Step::Pass) passes.push_back(s.pass.get());
+    qkjit::prepare(passes, device);
+}
+
 void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_run_stats& rs) {
     for (const qkeng::Step& s : ci.steps) {
         if (s.kind == qkeng::Step::Pass) {
-            cuda(qkdev::launchBlockPass(st->amps, t.gtab, *s.pass, st->nLocal, st->stream), "block pass");
+            if (useJit(st->nLocal))
+                cuda(qkjit::launch(*s.pass, st->amps, t.gtab, st->nLocal, st->stream), "specialized block pass");
+            else
+                cuda(qkdev::launchBlockPass(st->amps, t.gtab, *s.pass, st->nLocal, st->stream), "block pass");
         } else if (s.kind == qkeng::Step::DiagTable) {
             cuda(qkdev::launchDiagTable(st->amps, t.gtab + s.matOff, st->count, s.targets.data() + 1, s.k, st->stream),
                  "diag table");
@@ -750,6 +768,7 @@ int qk_apply_block(qk_state* st, const qk_gate* gates, int ngates, int chunk) {
         DeviceGuard g(st->device);
         auto c = compileFor(&prog, st->nLocal);
         DeviceTables t = tablesFor(&prog, *c, st->device);
+        prepareJit(*c, st->device);
         qk_run_stats rs{};
         runBlock(st, c->items[0], t, rs);
         cuda(cudaStreamSynchronize(st->stream), "apply block");
@@ -761,6 +780,25 @@ int qk_debug_compile_block(const qk_gate* gates, int ngates, int nLocal, char** 
         std::vector<double> gtab;
         const std::vector<qkeng::Step> steps = qkeng::compileBlock(gatesFromC(gates, ngates, nLocal), nLocal, gtab);
         *json = dupText(stepsJson(steps, gtab));
+    });
+}
+
+int qk_set_jit_min_qubits(int v) {
+    return guard([&] { qkjit::setMinQubits(v); });
+}
+
+int qk_debug_jit_compile(const qk_gate* gates, int ngates, int nLocal, char** source) {
+    return guard([&] {
+        std::vector<double> gtab;
+        const std::vector<qkeng::Step> steps = qkeng::compileBlock(gatesFromC(gates, ngates, nLocal), nLocal, gtab);
+        std::string all;
+        for (const qkeng::Step& s : steps)
+            if (s.kind == qkeng::Step::Pass) {
+                const std::string src = qkjit::generatePassSource(*s.pass, "qk_test_pass");
+                qkjit::compileToCubin(src, "qk_test_pass");  // throws with the NVRTC log on failure
+                all += src;
+            }
+        *source = dupText(all);
     });
 }
 
@@ -984,6 +1022,7 @@ int qk_simulate(qk_state* st, const qk_program* cp, const qk_config* cfg, uint64
         DeviceGuard g(st->device);
         auto comp = compileFor(p, st->nLocal);
         const DeviceTables t = tablesFor(p, *comp, st->device);
+        prepareJit(*comp, st->device);
         qk_run_stats rs{};
         Timer timer(st);
         cudaEvent_t e0, e1;
@@ -1036,6 +1075,7 @@ int qk_simulate_local(qk_state** sl, int ns, const qk_program* cp, const qk_conf
             sl[k]->B = c.bufferQubits;
             tabs.push_back(tablesFor(p, *comp, sl[k]->device));
             DeviceGuard g(sl[k]->device);
+            prepareJit(*comp, sl[k]->device);
             setBasis(sl[k], initial);
         }
         if (stats)

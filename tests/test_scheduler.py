@@ -146,3 +146,15 @@ def test_random_programs_lazy(qk, port, ref):
         prog = qk.Program.parse(prog_text, qk.Config.parse(cfg_text))
         got = run_compiled(qk, port, prog, n, 3)
         assert np.max(np.abs(got - want.view(np.complex128))) < 1e-10, i
+
+
+def test_specialized_kernel_sources_compile(qk):
+    # generator output is valid CUDA for sm_100a (NVRTC runs without a GPU)
+    mixed = ["H 0 0", "X 2 1", "U 1 2 0.3 1.1 -0.7", "RX 3 3 0.9", "RY 0 4 -1.3", "RZ 2 5 2.2",
+             "RZZ 1 3 6 0.8", "CP 0 3 7 1.9", "CX 3 1 8", "CX 0 2 9", "SWAP 1 2 10", "CP 3 0 11 -0.6"]
+    src = qk.debug_jit_compile(mixed, 9)
+    assert "__global__" in src and "switch" not in src
+    prog = qk.Program.optimize(qk.generate("qaoa", 12, 1, 3), qk.Config.make(12, 0, chunk=8, fusion_qubits=3))
+    lines = prog.text().splitlines()
+    k = int(lines[0])
+    assert qk.debug_jit_compile(lines[1:1 + k], 14)
