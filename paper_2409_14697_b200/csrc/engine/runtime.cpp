@@ -296,6 +296,87 @@ std::vector<std::vector<std::pair<int, int>>> materializePairs(const std::vector
     return out;
 }
 
+// Free in-tile output permutation of a block's last pass.  A pass may store
+// its tile with any permutation of the tile's own bits (map_out relabel, no
+// extra traffic).  With lazy IMS this is used to (a) move the qubits the next
+// block needs onto the lowest memory bits, so that block's tile stays
+// coalesced (128-B+ rows) even when SQS relabels pushed its qubits to high
+// memory bits, and (b) after the last block, put every bit whose final
+// position lies inside the tile where it belongs, shrinking the closing
+// materialization.  `mem` (program position -> memory bit) is updated.
+void retileOutput(const std::vector<quokka::ProgramItem>& items, size_t idx, std::vector<qkeng::Step>& steps,
+                  std::vector<int>& mem) {
+    if (steps.empty() || steps.back().kind != qkeng::Step::Pass) return;
+    qkdev::PassParams& P = *steps.back().pass;
+    const int n = int(mem.size()), ct = P.ct;
+    std::vector<int> tile(P.tile_phys, P.tile_phys + ct);  // ascending memory bits
+    std::vector<int> where(static_cast<size_t>(n), -1);     // memory bit -> tile index
+    for (int j = 0; j < ct; j++) where[size_t(tile[size_t(j)])] = j;
+    std::vector<int> sigma(static_cast<size_t>(ct));          // tile index -> tile index
+    for (int j = 0; j < ct; j++) sigma[size_t(j)] = j;
+
+    // Look ahead to the next block through the intervening SQS relabels.
+    std::vector<int> after = mem;
+    size_t k = idx + 1;
+    for (; k < items.size() && items[k].type == quokka::ProgramItem::Swap; k++) {
+        if (items[k].swap.kind == quokka::SwapOp::CrossRank) break;
+        for (const auto& [o, i] : items[k].swap.pairs) std::swap(after[size_t(o)], after[size_t(i)]);
+    }
+    if (k < items.size() && items[k].type == quokka::ProgramItem::Block) {
+        std::vector<char> need(static_cast<size_t>(n), 0);  // memory bits the next block touches
+        int count = 0;
+        for (const quokka::Gate& g : items[k].block.gates)
+            for (int q : g.qubits())
+                if (!need[size_t(after[size_t(q)])]) need[size_t(after[size_t(q)])] = 1, count++;
+        const int ctNext = std::min(qkdev::maxTileBits(), n);
+        const int low = std::min({3, ct, std::max(0, count - (ctNext - 3))});  // low bits padding cannot supply
+        // Targets: the `low` lowest tile bits; fill each with a needed bit from the tile.
+        std::vector<int> cand;
+        for (int j = ct - 1; j >= 0; j--)
+            if (need[size_t(tile[size_t(j)])]) cand.push_back(j);
+        size_t ci = 0;
+        for (int t = 0; t < low; t++) {
+            if (tile[size_t(t)] != t) break;               // the tile must own memory bit t
+            if (need[size_t(t)]) continue;                 // already needed and already low
+            while (ci < cand.size() && cand[ci] < low) ci++;
+            if (ci >= cand.size()) break;
+            std::swap(sigma[size_t(t)], sigma[size_t(cand[ci++])]);
+        }
+    } else if (k >= items.size()) {
+        // Last block: place each tile bit whose final position is in the tile.
+        std::vector<int> dest(static_cast<size_t>(n));  // memory bit -> final position (after trailing SQS)
+        for (int q = 0; q < n; q++) dest[size_t(after[size_t(q)])] = q;
+        std::vector<char> taken(static_cast<size_t>(ct), 0);
+        std::vector<int> s2(static_cast<size_t>(ct), -1);
+        for (int j = 0; j < ct; j++) {
+            const int d = where[size_t(dest[size_t(tile[size_t(j)])])];
+            if (d >= 0) s2[size_t(j)] = d, taken[size_t(d)] = 1;
+        }
+        int free = 0;
+        for (int j = 0; j < ct; j++)
+            if (s2[size_t(j)] < 0) {
+                while (taken[size_t(free)]) free++;
+                s2[size_t(j)] = free;
+                taken[size_t(free)] = 1;
+            }
+        sigma = s2;
+    }
+    bool identity = true;
+    for (int j = 0; j < ct; j++) identity &= sigma[size_t(j)] == j;
+    if (identity) return;
+    // Apply: data of tile bit j is stored at tile bit sigma[j].
+    const int last = P.nsegs - 1;
+    for (int s = 0; s < ct; s++) P.map_out[last][s] = uint8_t(sigma[P.map_out[last][s]]);
+    uint32_t xm = 0;
+    for (int j = 0; j < ct; j++)
+        if ((P.xmask_out[last] >> j) & 1) xm |= 1u << sigma[size_t(j)];
+    P.xmask_out[last] = uint16_t(xm);
+    for (int q = 0; q < n; q++) {
+        const int j = where[size_t(mem[size_t(q)])];
+        if (j >= 0) mem[size_t(q)] = tile[size_t(sigma[size_t(j)])];
+    }
+}
+
 std::shared_ptr<Compiled> compileFor(qk_program* p, int nLocal) {
     std::lock_guard<std::mutex> lk(p->mu);
     auto it = p->compiled.find(nLocal);
@@ -322,7 +403,9 @@ std::shared_ptr<Compiled> compileFor(qk_program* p, int nLocal) {
         }
         for (int b = 0; b < nLocal; b++) mem[size_t(b)] = b;
     };
-    for (const quokka::ProgramItem& item : p->prog.items) {
+    const auto& items = p->prog.items;
+    for (size_t idx = 0; idx < items.size(); idx++) {
+        const quokka::ProgramItem& item = items[idx];
         CompiledItem ci;
         if (item.type == quokka::ProgramItem::Block) {
             ci.kind = CompiledItem::Block;
@@ -335,6 +418,7 @@ std::shared_ptr<Compiled> compileFor(qk_program* p, int nLocal) {
                 gates.push_back(std::move(m));
             }
             ci.steps = qkeng::compileBlock(gates, nLocal, c->gtab);
+            if (lazy) retileOutput(items, idx, ci.steps, mem);
             for (qkeng::Step& s : ci.steps) {
                 ci.flopsPerAmp += s.flopsPerAmp;
                 if (s.kind != qkeng::Step::Pass) {
