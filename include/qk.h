@@ -107,6 +107,9 @@ int qk_set_jit_min_qubits(int v);
 int qk_debug_jit_compile(const qk_gate* gates, int ngates, int n_local, char** source);
 /* ... and of a whole program (device item list: blocks, IMS, XRS). */
 int qk_debug_compile_program(const qk_program* p, int n_local, char** json);
+/* ... and the specialized-kernel source of every pass of a program (item/step
+ * order, each preceded by a "//@@PASS <name>" line). */
+int qk_debug_jit_program(const qk_program* p, int n_local, char** sources);
 /* engine.cpp:258-260 applyGate (whole slice, any position < N-R). */
 int qk_apply_gate(qk_state* st, const qk_gate* gate);
 /* engine.cpp:86-101 imsSwap: a[bitswap(i)] <- a[i], in place.  cache_line_qubits

@@ -117,6 +117,7 @@ def lib():
         "qk_debug_compile_block": ([C.POINTER(_Gate), I, I, C.POINTER(P)], I),
         "qk_debug_compile_program": ([P, I, C.POINTER(P)], I),
         "qk_debug_jit_compile": ([C.POINTER(_Gate), I, I, C.POINTER(P)], I),
+        "qk_debug_jit_program": ([P, I, C.POINTER(P)], I),
         "qk_set_jit_min_qubits": ([I], I),
         "qk_ims_swap": ([P, C.POINTER(I), C.POINTER(I), I, I], I),
         "qk_xrs_swap_local": ([C.POINTER(P), I, C.POINTER(I), C.POINTER(I), I, C.POINTER(_XrsStats)], I),
@@ -230,6 +231,15 @@ class Program:
         import json
         n_local = self.cfg.total_qubits - self.cfg.rank_qubits if n_local is None else n_local
         return json.loads(_text(lib().qk_debug_compile_program, self._h, n_local))
+
+    def debug_jit_sources(self, n_local: int | None = None) -> list:
+        """[(name, CUDA source)] of every specialized pass kernel (host only; test hook)."""
+        n_local = self.cfg.total_qubits - self.cfg.rank_qubits if n_local is None else n_local
+        out = []
+        for chunk in _text(lib().qk_debug_jit_program, self._h, n_local).split("//@@PASS ")[1:]:
+            name, src = chunk.split("\n", 1)
+            out.append((name.strip(), src))
+        return out
 
     def counts(self):
         v = [C.c_int64() for _ in range(4)]

@@ -459,6 +459,10 @@ __global__ void __launch_bounds__(1 << (CT - RB), MINB)
         }
     }
 
+    // A single-segment pass may store through a different map than it loaded
+    // with (free in-tile output permutation): wait until every thread of the
+    // CTA has loaded before anyone overwrites the tile.
+    if (P.nsegs == 1) __syncthreads();
     {
         uint64_t off, st[RB];
         globalLayout<CT, RB>(P, P.map_out[P.nsegs - 1], tid, off, st);

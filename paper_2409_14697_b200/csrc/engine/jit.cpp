@@ -102,6 +102,10 @@ public:
         uint64_t gx = 0;
         for (int j = 0; j < ct_; j++)
             if ((P_.xmask_out[last] >> j) & 1) gx |= uint64_t(1) << P_.tile_phys[j];
+        // Single-segment pass whose store map differs from its load map: other
+        // threads may still be loading the addresses this thread stores to.
+        if (P_.nsegs == 1 && (std::memcmp(P_.map_in[0], P_.map_out[0], sizeof P_.map_in[0]) != 0 || P_.xmask_out[0]))
+            o_ << "  __syncthreads();\n";
         o_ << "  { const u64 off = (base | " << threadGlobal(P_.map_out[last]) << ") ^ " << gx << "ull;\n";
         for (int s = 0; s < na_; s++)
             o_ << "  __stcs(st + (off ^ " << regGlobal(P_.map_out[last], s) << "ull), a" << nm_[size_t(s)] << ");\n";
@@ -324,8 +328,11 @@ private:
 
 // ---- compile / load / launch -------------------------------------------------
 
+// Bump when the generated code changes for the same PassParams (on-disk cache key).
+constexpr uint64_t kGeneratorVersion = 2;
+
 uint64_t hashPass(const PassParams& P) {
-    uint64_t h = 1469598103934665603ull;
+    uint64_t h = 1469598103934665603ull ^ (kGeneratorVersion * 0x9E3779B97F4A7C15ull);
     const unsigned char* p = reinterpret_cast<const unsigned char*>(&P);
     for (size_t i = 0; i < sizeof(PassParams); i++) {
         h ^= p[i];

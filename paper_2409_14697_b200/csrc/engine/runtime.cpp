@@ -886,6 +886,25 @@ int qk_debug_jit_compile(const qk_gate* gates, int ngates, int nLocal, char** so
     });
 }
 
+// Specialized-kernel sources of every pass of a compiled program, in item /
+// step order, separated by "//@@PASS <name>" lines (host only; tests replay
+// them on the CPU through tests/jit_host_shim.h).
+int qk_debug_jit_program(const qk_program* cp, int nLocal, char** sources) {
+    return guard([&] {
+        qk_program* p = const_cast<qk_program*>(cp);
+        auto c = compileFor(p, nLocal);
+        std::string all;
+        int k = 0;
+        for (const CompiledItem& it : c->items)
+            for (const qkeng::Step& s : it.steps)
+                if (s.kind == qkeng::Step::Pass) {
+                    const std::string name = "qk_host_pass_" + std::to_string(k++);
+                    all += "//@@PASS " + name + "\n" + qkjit::generatePassSource(*s.pass, name);
+                }
+        *sources = dupText(all);
+    });
+}
+
 int qk_debug_compile_program(const qk_program* cp, int nLocal, char** json) {
     return guard([&] {
         qk_program* p = const_cast<qk_program*>(cp);

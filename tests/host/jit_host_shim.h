@@ -1,0 +1,56 @@
+// TEST INFRASTRUCTURE: lets a generated specialized pass kernel (jit.cpp's
+// CUDA source) compile and run on the CPU with g++.  One std::thread per CUDA
+// thread of a CTA, std::barrier for __syncthreads, one CTA at a time with a
+// static shared-memory array.  Semantics only (no performance meaning).
+#pragma once
+#include <barrier>
+#include <cmath>
+#include <cstdint>
+#include <thread>
+#include <vector>
+
+struct double2 {
+    double x, y;
+};
+static inline double2 make_double2(double x, double y) { return {x, y}; }
+struct QkDim3 {
+    unsigned x;
+};
+inline thread_local unsigned qk_tl_tid = 0, qk_tl_bid = 0;
+#define threadIdx (QkDim3{qk_tl_tid})
+#define blockIdx (QkDim3{qk_tl_bid})
+inline std::barrier<>* qk_bar = nullptr;
+static inline void __syncthreads() { qk_bar->arrive_and_wait(); }
+template <class T>
+static inline T __ldcs(const T* p) { return *p; }
+template <class T>
+static inline T __ldg(const T* p) { return *p; }
+template <class T>
+static inline void __stcs(T* p, T v) { *p = v; }
+#define __global__
+#define __device__
+#define __forceinline__ inline
+#define __launch_bounds__(a, b)
+#define __restrict__
+#define __shared__
+// `extern __shared__ double2 sm[];` in the kernel binds to this array.
+extern "C" double2 sm[1 << 13];
+
+// Launch: every CTA in turn, nt threads each.
+#define QK_HOST_LAUNCHER(KERNEL)                                                              \
+    double2 sm[1 << 13];                                                                      \
+    extern "C" void qk_host_launch(double2* st, const double2* gt, int nLocal, int ct, int rb) { \
+        const unsigned ctas = 1u << (nLocal - ct), nt = 1u << (ct - rb);                     \
+        for (unsigned b = 0; b < ctas; b++) {                                                 \
+            std::barrier<> bar(nt);                                                           \
+            qk_bar = &bar;                                                                    \
+            std::vector<std::thread> ts;                                                      \
+            for (unsigned t = 0; t < nt; t++)                                                 \
+                ts.emplace_back([=] {                                                         \
+                    qk_tl_tid = t;                                                            \
+                    qk_tl_bid = b;                                                            \
+                    KERNEL(st, gt);                                                           \
+                });                                                                           \
+            for (auto& th : ts) th.join();                                                    \
+        }                                                                                     \
+    }

@@ -1,0 +1,55 @@
+"""TEST INFRASTRUCTURE: compile the engine's generated specialized pass
+kernels (jit.cpp) for the CPU with g++ through tests/host/jit_host_shim.h and
+replay a compiled program with them, so the straight-line generator is
+checked against the oracle without a GPU."""
+import ctypes as C
+import hashlib
+import os
+import subprocess
+
+import numpy as np
+
+from emulator import run_steps
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CACHE = os.path.join(HERE, ".jit_host_cache")
+
+
+def host_kernel(name: str, src: str):
+    os.makedirs(CACHE, exist_ok=True)
+    body = src.replace("#include <cuda_runtime.h>", '#include "jit_host_shim.h"')
+    body += f"\nQK_HOST_LAUNCHER({name})\n"
+    h = hashlib.sha1(body.encode()).hexdigest()[:16]
+    so = os.path.join(CACHE, f"{h}.so")
+    if not os.path.exists(so):
+        cpp = os.path.join(CACHE, f"{h}.cpp")
+        open(cpp, "w").write(body)
+        subprocess.run(["g++", "-std=c++20", "-O1", "-fPIC", "-shared", "-w", "-I", os.path.join(HERE, "host"),
+                        cpp, "-o", so + ".tmp", "-lpthread"], check=True)
+        os.replace(so + ".tmp", so)
+    lib = C.CDLL(so)
+    lib.qk_host_launch.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int]
+    return lib.qk_host_launch
+
+
+def run_program_jit(qk, port, prog, n_local, state):
+    """Replay prog's compiled items on `state` (complex128, 2^n_local) with the
+    generated kernels for passes, the emulator for dense/diag-table steps and
+    the oracle for IMS items."""
+    items = prog.debug_compile(n_local)["items"]
+    srcs = iter(prog.debug_jit_sources(n_local))
+    for it in items:
+        if it["kind"] == 0:
+            blk = it["block"]
+            gt = np.array(blk["gtab"] if blk["gtab"] else [0.0, 0.0], dtype=np.float64)
+            for st in blk["steps"]:
+                if st["kind"] == 0:
+                    name, src = next(srcs)
+                    host_kernel(name, src)(state.ctypes.data, gt.ctypes.data, n_local, st["ct"], st["rb"])
+                else:
+                    run_steps(state, n_local, {"gtab": blk["gtab"], "steps": [st]})
+        elif it["kind"] == 1:
+            port.ims_swap(state.view(np.float64), n_local, [tuple(p) for p in it["pairs"]])
+        else:
+            raise AssertionError("cross-rank item")
+    return state
