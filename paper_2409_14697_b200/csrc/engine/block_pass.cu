@@ -311,6 +311,20 @@ __global__ void __launch_bounds__(1 << (CT - RB), MINB)
         for (int s = 0; s < NA; s++) a[s] = __ldcs(state + (off | slotOffset<RB>(s, st)));
     }
 
+    // Per-CTA diagonal factors (functions of the non-tile bits of `base`).
+    double2* F = sm + (1 << CT);
+    if (P.ncta) {
+        for (int f = int(tid); f < P.ncta; f += NT) {
+            double2 acc = make_double2(1.0, 0.0);
+            for (int t = f ? P.cta_end[f - 1] : 0; t < P.cta_end[f]; t++) {
+                const CtaTerm& ct = P.cta_terms[t];
+                if (ct.b1 == 255 || ((base >> ct.b1) & (base >> ct.b2) & 1u)) acc = cmul(acc, coefAt(P, ct.c));
+            }
+            F[f] = acc;
+        }
+        __syncthreads();
+    }
+
     double2 Pt = make_double2(1.0, 0.0);  // pending per-thread scalar
     double2 R[RB];                         // pending per-slot phases (amplitudes with slot bit 1)
 #pragma unroll
@@ -388,6 +402,17 @@ __global__ void __launch_bounds__(1 << (CT - RB), MINB)
                     break;
                 }
                 case OP_SCAL_TAB: Pt = cmul(Pt, __ldg(gtab + o.c + pext8(tid, o.b))); break;
+                case OP_SCAL_CTA: Pt = cmul(Pt, F[o.c]); break;
+                case OP_SCAL_TCTA:
+                    if ((tid >> o.b) & 1u) Pt = cmul(Pt, F[o.c]);
+                    break;
+                case OP_PEND_CTA: {
+                    const double2 e = F[o.c];
+#pragma unroll
+                    for (int k = 0; k < RB; k++)
+                        if (k == o.a) R[k] = cmul(R[k], e);
+                    break;
+                }
                 case OP_PEND_TAB: {
                     const double2 e = __ldg(gtab + o.c + pext8(tid, o.b));
 #pragma unroll
@@ -432,6 +457,8 @@ __global__ void __launch_bounds__(1 << (CT - RB), MINB)
 #pragma unroll
                     for (int j = RB; j < CT; j++)
                         if ((tid >> (j - RB)) & 1u) sub |= cb[j];
+                    for (int j = 0; j < cb[CT]; j++)  // bits outside the tile: constants of the CTA
+                        if ((base >> cb[CT + 1 + 2 * j]) & 1u) sub |= cb[CT + 2 + 2 * j];
                     uint32_t cr[RB];
 #pragma unroll
                     for (int k = 0; k < RB; k++) cr[k] = cb[k];
@@ -517,7 +544,7 @@ static cudaError_t launchCT(double2* state, const double2* gtab, const PassParam
                             cudaStream_t stream) {
     constexpr int NT = 1 << (CT - RB);
     constexpr int MINB = (CT == 12 && RB == 4) ? 2 : 1;
-    const size_t smem = sizeof(double2) << CT;
+    const size_t smem = (sizeof(double2) << CT) + sizeof(double2) * kMaxCtaFactors;
     if (smem > 48 * 1024) {  // per-device attribute; cheap to re-apply
         cudaError_t e = cudaFuncSetAttribute(k_block_pass<CT, RB, MINB>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));

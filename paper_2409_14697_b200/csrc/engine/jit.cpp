@@ -62,7 +62,43 @@ static __device__ __forceinline__ double2 csel(bool c, double2 x, double2 y) {
     return make_double2(c ? x.x : y.x, c ? x.y : y.y);
 }
 static __device__ __forceinline__ u32 swz(u32 u) { return u ^ (((u >> 3) ^ (u >> 6) ^ (u >> 9) ^ (u >> 12)) & 7u); }
+// TMA-engine prefetch of a contiguous row into L2 (no registers, no smem).
+static __device__ __forceinline__ void pf_l2(const void* p, u32 bytes) {
+#ifdef __CUDA_ARCH__
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+#endif
+}
 )";
+
+// Tuning knobs (read once): QK_JIT_PF=0 disables the L2 prefetch of the next
+// tile, QK_JIT_PERSIST=0 launches one CTA per tile instead of a persistent grid.
+int knob(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return v ? std::atoi(v) : dflt;
+}
+bool usePrefetch() {
+    static const bool v = knob("QK_JIT_PF", 1) != 0;
+    return v;
+}
+bool usePersistent() {
+    static const bool v = knob("QK_JIT_PERSIST", 1) != 0;
+    return v;
+}
+
+// Resident CTAs per SM of a pass kernel (register / shared-memory bound).
+int blocksPerSm(int ct, int rb) { return (ct == 12 && rb == 4) ? 2 : ct <= 11 ? 2 : 1; }
+
+int smCount(int dev) {
+    static std::mutex mu;
+    static std::map<int, int> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(dev);
+    if (it != cache.end()) return it->second;
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    cache[dev] = n;
+    return n;
+}
 
 class Gen {
 public:
@@ -70,30 +106,30 @@ public:
         for (int s = 0; s < na_; s++) nm_.push_back(s);
     }
 
+    // Persistent kernel: each CTA walks tiles blockIdx.x, +gridDim.x, ...  While
+    // tile k computes, the rows of the CTA's next tile are prefetched into L2
+    // by the TMA engine, so that tile's register loads hit L2 and the SM's
+    // load phase overlaps its compute phase (one CTA per SM at ct = 13).
     std::string run(const std::string& name) {
-        const int minb = (ct_ == 12 && rb_ == 4) ? 2 : 1;
+        const int minb = blocksPerSm(ct_, rb_);
         o_ << kPrologue;
+        ctaTables();
         o_ << "extern \"C\" __global__ void __launch_bounds__(" << nt_ << "," << minb << ") " << name
-           << "(double2* __restrict__ st, const double2* __restrict__ gt) {\n";
-        o_ << "  extern __shared__ double2 sm[];\n  const u32 tid = threadIdx.x;\n  u64 base = blockIdx.x;\n";
-        for (int j = 0; j < ct_; j++) {
-            const int p = P_.tile_phys[j];
-            o_ << "  base = ((base >> " << p << ") << " << (p + 1) << ") | (base & " << ((uint64_t(1) << p) - 1)
-               << "ull);\n";
-        }
+           << "(double2* __restrict__ st, const double2* __restrict__ gt, const u32 ntiles) {\n";
+        o_ << "  extern __shared__ double2 sm[];\n  double2* const F = sm + " << (1 << ct_)
+           << ";\n  const u32 tid = threadIdx.x;\n";
+        o_ << "  for (u32 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {\n";
+        o_ << "  const u64 base = " << deposit("(u64)tile") << ";\n";
+        std::string decl = "  double2 ";
+        for (int s = 0; s < na_; s++) decl += (s ? ", a" : "a") + std::to_string(s);
+        o_ << decl << ";\n  double2 P = C2(1.0, 0.0);\n" << pendDecl();
         // load (map_in[0], no flips)
         o_ << "  { const u64 off = base | " << threadGlobal(P_.map_in[0]) << ";\n";
         for (int s = 0; s < na_; s++)
             o_ << "  a" << s << " = __ldcs(st + (off | " << regGlobal(P_.map_in[0], s) << "ull));\n";
         o_ << "  }\n";
-        std::string decl = "  double2 ";
-        for (int s = 0; s < na_; s++) decl += (s ? ", a" : "a") + std::to_string(s);
-        // declarations must precede use: splice them in front of the load
-        std::string body = o_.str();
-        const size_t at = body.find("  { const u64 off = base |");
-        body.insert(at, decl + ";\n  double2 P = C2(1.0, 0.0);\n" + pendDecl());
-        o_.str("");
-        o_ << body;
+        prefetchNext();
+        ctaFactors();
 
         for (int i = 0; i < P_.nops; i++) op(P_.ops[i]);
 
@@ -109,11 +145,62 @@ public:
         o_ << "  { const u64 off = (base | " << threadGlobal(P_.map_out[last]) << ") ^ " << gx << "ull;\n";
         for (int s = 0; s < na_; s++)
             o_ << "  __stcs(st + (off ^ " << regGlobal(P_.map_out[last], s) << "ull), a" << nm_[size_t(s)] << ");\n";
-        o_ << "  }\n}\n";
+        o_ << "  }\n";
+        // The next iteration's first shared-memory write must not overtake a
+        // slow thread still reading this tile's last exchange.
+        o_ << "  __syncthreads();\n  }\n}\n";
         return o_.str();
     }
 
 private:
+    // CTA index deposited into the non-tile bits of the slice index.
+    std::string deposit(const std::string& v) const {
+        std::string e = v;
+        for (int j = 0; j < ct_; j++) {
+            const int p = P_.tile_phys[j];
+            e = "(((" + e + ") >> " + std::to_string(p) + ") << " + std::to_string(p + 1) + ") | ((" + e + ") & " +
+                std::to_string((uint64_t(1) << p) - 1) + "ull)";
+        }
+        return e;
+    }
+    // Rows of the tile: the run of tile bits that are the lowest memory bits is
+    // contiguous; the remaining tile bits enumerate rows.
+    void prefetchNext() {
+        int L = 0;
+        while (L < ct_ && P_.tile_phys[L] == L) L++;
+        if (L < 3 || !usePrefetch()) return;  // rows under 128 B: not worth a TMA op each
+        const int rows = 1 << (ct_ - L);
+        const unsigned bytes = 16u << L;
+        o_ << "  if (tile + gridDim.x < ntiles) {\n    u64 nb = (u64)(tile + gridDim.x);\n";
+        for (int j = 0; j < ct_; j++) {
+            const int p = P_.tile_phys[j];
+            o_ << "    nb = ((nb >> " << p << ") << " << (p + 1) << ") | (nb & " << ((uint64_t(1) << p) - 1) << "ull);\n";
+        }
+        o_ << "    for (u32 r = tid; r < " << rows << "u; r += " << nt_ << "u) {\n      u64 o = nb;\n";
+        for (int j = L; j < ct_; j++)
+            o_ << "      o |= (u64)((r >> " << (j - L) << ") & 1u) << " << int(P_.tile_phys[j]) << ";\n";
+        o_ << "      pf_l2(st + o, " << bytes << "u);\n    }\n  }\n";
+    }
+    // Per-CTA factor terms as device tables (one factor per thread at tile start).
+    void ctaTables() {
+        if (!P_.ncta) return;
+        const int nt = P_.cta_end[P_.ncta - 1];
+        o_ << "static __device__ const unsigned char qk_tb[] = {";
+        for (int t = 0; t < nt; t++) o_ << (t ? "," : "") << int(P_.cta_terms[t].b1) << "," << int(P_.cta_terms[t].b2);
+        o_ << "};\nstatic __device__ const double2 qk_tv[] = {";
+        for (int t = 0; t < nt; t++) o_ << (t ? "," : "") << lc(P_.cta_terms[t].c);
+        o_ << "};\nstatic __device__ const unsigned short qk_te[] = {";
+        for (int f = 0; f < P_.ncta; f++) o_ << (f ? "," : "") << P_.cta_end[f];
+        o_ << "};\n";
+    }
+    void ctaFactors() {
+        if (!P_.ncta) return;
+        o_ << "  if (tid < " << P_.ncta << "u) {\n    double2 acc = C2(1.0, 0.0);\n"
+           << "    for (u32 t = tid ? qk_te[tid - 1] : 0u; t < qk_te[tid]; t++) {\n"
+           << "      const u32 b1 = qk_tb[2 * t], b2 = qk_tb[2 * t + 1];\n"
+           << "      if (b1 == 255u || ((base >> b1) & (base >> b2) & 1ull)) acc = cmul(acc, qk_tv[t]);\n"
+           << "    }\n    F[tid] = acc;\n  }\n  __syncthreads();\n";
+    }
     std::string pendDecl() {
         std::string d;
         for (int k = 0; k < rb_; k++) d += "  double2 R" + std::to_string(k) + " = C2(1.0, 0.0);\n";
@@ -231,6 +318,18 @@ private:
                 o_ << "  R" << a << " = cmul(R" << a << ", __ldg(gt + " << d.c << "u + " << pext(d.b) << "));\n";
                 dirtyR_[a] = true;
                 return;
+            case qkdev::OP_SCAL_CTA:
+                o_ << "  P = cmul(P, F[" << d.c << "]);\n";
+                dirtyP_ = true;
+                return;
+            case qkdev::OP_SCAL_TCTA:
+                o_ << "  { const double2 e = F[" << d.c << "]; if (" << tb(b) << ") P = cmul(P, e); }\n";
+                dirtyP_ = true;
+                return;
+            case qkdev::OP_PEND_CTA:
+                o_ << "  R" << a << " = cmul(R" << a << ", F[" << d.c << "]);\n";
+                dirtyR_[a] = true;
+                return;
             case qkdev::OP_FLUSH_SLOT:
                 if (!dirtyR_[a]) return;
                 for (int s = 0; s < na_; s++)
@@ -246,6 +345,9 @@ private:
                 std::string sub = "0u";
                 for (int j = rb_; j < ct_; j++)
                     if (cb[j]) sub += " | (" + tb(j - rb_) + " ? " + std::to_string(cb[j]) + "u : 0u)";
+                for (int j = 0; j < cb[ct_]; j++)  // bits outside the tile: constants of the CTA
+                    sub += " | (((base >> " + std::to_string(cb[ct_ + 1 + 2 * j]) + ") & 1ull) ? " +
+                           std::to_string(cb[ct_ + 2 + 2 * j]) + "u : 0u)";
                 o_ << "  { const u32 sub = " << sub << ";\n";
                 for (int s = 0; s < na_; s++) {
                     uint32_t cs = 0;
@@ -329,10 +431,10 @@ private:
 // ---- compile / load / launch -------------------------------------------------
 
 // Bump when the generated code changes for the same PassParams (on-disk cache key).
-constexpr uint64_t kGeneratorVersion = 2;
+constexpr uint64_t kGeneratorVersion = 4;
 
 uint64_t hashPass(const PassParams& P) {
-    uint64_t h = 1469598103934665603ull ^ (kGeneratorVersion * 0x9E3779B97F4A7C15ull);
+    uint64_t h = 1469598103934665603ull ^ (kGeneratorVersion * 0x9E3779B97F4A7C15ull) ^ (usePrefetch() ? 1u : 0u);
     const unsigned char* p = reinterpret_cast<const unsigned char*>(&P);
     for (size_t i = 0; i < sizeof(PassParams); i++) {
         h ^= p[i];
@@ -415,7 +517,7 @@ void* functionFor(const PassParams& P, uint64_t h, int device) {
     void* fn = nullptr;
     if (d.moduleLoadData(&mod, e.cubin.data()) != 0) throw SimulationError("jit: cuModuleLoadData failed");
     if (d.moduleGetFunction(&fn, mod, kernelName(h).c_str()) != 0) throw SimulationError("jit: cuModuleGetFunction failed");
-    const int smem = int(sizeof(double2) << P.ct);
+    const int smem = int((sizeof(double2) << P.ct) + sizeof(double2) * qkdev::kMaxCtaFactors);
     if (smem > 48 * 1024 && d.funcSetAttribute(fn, 8 /*CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES*/, smem) != 0)
         throw SimulationError("jit: cuFuncSetAttribute failed");
     e.func[device] = fn;
@@ -501,10 +603,12 @@ cudaError_t launch(const PassParams& P, double2* state, const double2* gtab, int
     int dev = 0;
     cudaGetDevice(&dev);
     void* fn = functionFor(P, hashPass(P), dev);
-    const unsigned ctas = unsigned(uint64_t(1) << (nLocal - P.ct));
+    unsigned ntiles = unsigned(uint64_t(1) << (nLocal - P.ct));
+    const unsigned resident = unsigned(smCount(dev) * blocksPerSm(P.ct, P.rb));
+    const unsigned ctas = (ntiles < resident || !usePersistent()) ? ntiles : resident;
     const unsigned nt = 1u << (P.ct - P.rb);
-    const unsigned smem = unsigned(sizeof(double2) << P.ct);
-    void* args[] = {&state, &gtab};
+    const unsigned smem = unsigned((sizeof(double2) << P.ct) + sizeof(double2) * qkdev::kMaxCtaFactors);
+    void* args[] = {&state, &gtab, &ntiles};
     if (driver().launchKernel(fn, ctas, 1, 1, nt, 1, 1, smem, stream, args, nullptr) != 0)
         return cudaErrorLaunchFailure;
     return cudaSuccess;

@@ -36,6 +36,8 @@ constexpr int kMaxOps = 700;
 constexpr int kMaxCoef = 860;               // complex coefficients (double2)
 constexpr int kMaxSegs = 96;
 constexpr int kMaxContrib = 512;            // uint16 words for fused-diagonal index maps
+constexpr int kMaxCtaFactors = 64;          // per-CTA diagonal factors (functions of non-tile bits)
+constexpr int kMaxCtaTerms = 320;
 
 // Register bits used for a tile of ct bits: 16 amplitudes per thread up to
 // ct = 12 (<= 256 threads, no register cap), 32 per thread at ct = 13 (256
@@ -64,6 +66,20 @@ enum OpType : uint8_t {
     OP_EXCHANGE,      // shared-memory exchange: map_out[c-1] -> map_in[c] (segment c starts)
     OP_SCAL_TAB,      // P *= gtab[c + pext(thread, b)]      (b = thread-bit mask)
     OP_PEND_TAB,      // R[a] *= gtab[c + pext(thread, b)]
+    OP_SCAL_CTA,      // P *= F[c]                          (F = this CTA's factors, see cta_terms)
+    OP_PEND_CTA,      // R[a] *= F[c]
+    OP_SCAL_TCTA,     // P *= bit_b(thread) ? F[c] : 1
+};
+
+// Diagonal gates never need their qubits inside the tile: a bit outside the
+// tile is a constant of the CTA (a bit of its base index).  Factors that
+// depend on such bits are computed once per tile: F[f] = product over terms
+// [cta_end[f-1], cta_end[f]) of coef[c] if (base bit b1) & (base bit b2)
+// (b1 = 255: unconditional).  OP_DTABLE indices take CTA bits from the
+// contrib list after the ct tile words: count m, then m (memory bit, value).
+struct CtaTerm {
+    uint8_t b1, b2;
+    uint16_t c;
 };
 
 struct DevOp {
@@ -87,6 +103,9 @@ struct PassParams {
     DevOp ops[kMaxOps];
     double coef[2 * kMaxCoef];        // interleaved complex coefficients
     uint16_t contrib[kMaxContrib];
+    int32_t ncta;                     // CTA factors (0: none)
+    uint16_t cta_end[kMaxCtaFactors];
+    CtaTerm cta_terms[kMaxCtaTerms];
 };
 
 static_assert(sizeof(PassParams) <= 32000, "kernel parameter limit");

@@ -296,71 +296,34 @@ std::vector<std::vector<std::pair<int, int>>> materializePairs(const std::vector
     return out;
 }
 
-// Free in-tile output permutation of a block's last pass.  A pass may store
+// Free in-tile output permutation of a segment's last pass.  A pass may store
 // its tile with any permutation of the tile's own bits (map_out relabel, no
-// extra traffic).  With lazy IMS this is used to (a) move the qubits the next
-// block needs onto the lowest memory bits, so that block's tile stays
-// coalesced (128-B+ rows) even when SQS relabels pushed its qubits to high
-// memory bits, and (b) after the last block, put every bit whose final
-// position lies inside the tile where it belongs, shrinking the closing
-// materialization.  `mem` (program position -> memory bit) is updated.
-void retileOutput(const std::vector<quokka::ProgramItem>& items, size_t idx, std::vector<qkeng::Step>& steps,
-                  std::vector<int>& mem) {
+// extra traffic): before a materialization (end of program, or a cross-rank
+// swap), every tile bit whose destination (memory bit q for program position
+// q) lies inside the tile is stored there, shrinking the IMS that follows.
+// `mem` (program position -> memory bit) is updated.
+void retileFinal(std::vector<qkeng::Step>& steps, std::vector<int>& mem) {
     if (steps.empty() || steps.back().kind != qkeng::Step::Pass) return;
     qkdev::PassParams& P = *steps.back().pass;
     const int n = int(mem.size()), ct = P.ct;
     std::vector<int> tile(P.tile_phys, P.tile_phys + ct);  // ascending memory bits
     std::vector<int> where(static_cast<size_t>(n), -1);     // memory bit -> tile index
     for (int j = 0; j < ct; j++) where[size_t(tile[size_t(j)])] = j;
-    std::vector<int> sigma(static_cast<size_t>(ct));          // tile index -> tile index
-    for (int j = 0; j < ct; j++) sigma[size_t(j)] = j;
-
-    // Look ahead to the next block through the intervening SQS relabels.
-    std::vector<int> after = mem;
-    size_t k = idx + 1;
-    for (; k < items.size() && items[k].type == quokka::ProgramItem::Swap; k++) {
-        if (items[k].swap.kind == quokka::SwapOp::CrossRank) break;
-        for (const auto& [o, i] : items[k].swap.pairs) std::swap(after[size_t(o)], after[size_t(i)]);
+    std::vector<int> dest(static_cast<size_t>(n));  // memory bit -> program position
+    for (int q = 0; q < n; q++) dest[size_t(mem[size_t(q)])] = q;
+    std::vector<char> taken(static_cast<size_t>(ct), 0);
+    std::vector<int> sigma(static_cast<size_t>(ct), -1);  // tile index -> tile index
+    for (int j = 0; j < ct; j++) {
+        const int d = where[size_t(dest[size_t(tile[size_t(j)])])];
+        if (d >= 0) sigma[size_t(j)] = d, taken[size_t(d)] = 1;
     }
-    if (k < items.size() && items[k].type == quokka::ProgramItem::Block) {
-        std::vector<char> need(static_cast<size_t>(n), 0);  // memory bits the next block touches
-        int count = 0;
-        for (const quokka::Gate& g : items[k].block.gates)
-            for (int q : g.qubits())
-                if (!need[size_t(after[size_t(q)])]) need[size_t(after[size_t(q)])] = 1, count++;
-        const int ctNext = std::min(qkdev::maxTileBits(), n);
-        const int low = std::min({3, ct, std::max(0, count - (ctNext - 3))});  // low bits padding cannot supply
-        // Targets: the `low` lowest tile bits; fill each with a needed bit from the tile.
-        std::vector<int> cand;
-        for (int j = ct - 1; j >= 0; j--)
-            if (need[size_t(tile[size_t(j)])]) cand.push_back(j);
-        size_t ci = 0;
-        for (int t = 0; t < low; t++) {
-            if (tile[size_t(t)] != t) break;               // the tile must own memory bit t
-            if (need[size_t(t)]) continue;                 // already needed and already low
-            while (ci < cand.size() && cand[ci] < low) ci++;
-            if (ci >= cand.size()) break;
-            std::swap(sigma[size_t(t)], sigma[size_t(cand[ci++])]);
+    int free = 0;
+    for (int j = 0; j < ct; j++)
+        if (sigma[size_t(j)] < 0) {
+            while (taken[size_t(free)]) free++;
+            sigma[size_t(j)] = free;
+            taken[size_t(free)] = 1;
         }
-    } else if (k >= items.size()) {
-        // Last block: place each tile bit whose final position is in the tile.
-        std::vector<int> dest(static_cast<size_t>(n));  // memory bit -> final position (after trailing SQS)
-        for (int q = 0; q < n; q++) dest[size_t(after[size_t(q)])] = q;
-        std::vector<char> taken(static_cast<size_t>(ct), 0);
-        std::vector<int> s2(static_cast<size_t>(ct), -1);
-        for (int j = 0; j < ct; j++) {
-            const int d = where[size_t(dest[size_t(tile[size_t(j)])])];
-            if (d >= 0) s2[size_t(j)] = d, taken[size_t(d)] = 1;
-        }
-        int free = 0;
-        for (int j = 0; j < ct; j++)
-            if (s2[size_t(j)] < 0) {
-                while (taken[size_t(free)]) free++;
-                s2[size_t(j)] = free;
-                taken[size_t(free)] = 1;
-            }
-        sigma = s2;
-    }
     bool identity = true;
     for (int j = 0; j < ct; j++) identity &= sigma[size_t(j)] == j;
     if (identity) return;
@@ -383,14 +346,35 @@ std::shared_ptr<Compiled> compileFor(qk_program* p, int nLocal) {
     if (it != p->compiled.end()) return it->second;
     auto c = std::make_shared<Compiled>();
     c->nLocal = nLocal;
-    // Lazy in-memory swaps: an SQS only relabels which memory bit holds which
-    // program position (mem[p]); the following blocks address their qubits
-    // through `mem`, so the SQS costs no HBM pass.  The relabeling is
-    // materialized (<= 2 IMS passes) only before a cross-rank swap and at the
-    // end, so the final state is in the program's physical order.
+    // Lazy in-memory swaps: an SQS (and a SWAP gate) only relabels which
+    // memory bit holds which program position (mem[p]); later gates address
+    // their qubits through `mem`, so it costs no HBM pass.  Gates between
+    // materializations form one stream, which the scheduler cuts into passes
+    // (qkeng::compileBlock: diagonal gates ride along with any pass).  The
+    // relabeling is materialized (<= 2 IMS passes) only before a cross-rank
+    // swap and at the end, so the final state is in the program's physical
+    // order.
     std::vector<int> mem(static_cast<size_t>(nLocal));
     for (int b = 0; b < nLocal; b++) mem[size_t(b)] = b;
     const bool lazy = lazyIms();
+    std::vector<quokka::Gate> stream;
+    auto flushStream = [&](bool beforeMaterialize) {
+        if (stream.empty()) return;
+        CompiledItem ci;
+        ci.kind = CompiledItem::Block;
+        ci.steps = qkeng::compileBlock(stream, nLocal, c->gtab);
+        if (lazy && beforeMaterialize) retileFinal(ci.steps, mem);
+        for (qkeng::Step& s : ci.steps) {
+            ci.flopsPerAmp += s.flopsPerAmp;
+            if (s.kind != qkeng::Step::Pass) {
+                const uint64_t off = c->targets.size();
+                c->targets.insert(c->targets.end(), s.targets.begin(), s.targets.end());
+                s.targets.insert(s.targets.begin(), int(off));  // [0] = device offset
+            }
+        }
+        c->items.push_back(std::move(ci));
+        stream.clear();
+    };
     auto materialize = [&] {
         for (const auto& pairs : materializePairs(mem)) {
             CompiledItem ci;
@@ -406,40 +390,36 @@ std::shared_ptr<Compiled> compileFor(qk_program* p, int nLocal) {
     const auto& items = p->prog.items;
     for (size_t idx = 0; idx < items.size(); idx++) {
         const quokka::ProgramItem& item = items[idx];
-        CompiledItem ci;
         if (item.type == quokka::ProgramItem::Block) {
-            ci.kind = CompiledItem::Block;
-            std::vector<quokka::Gate> gates;
             for (const quokka::Gate& g : item.block.gates) {
+                if (lazy && g.kind == quokka::GateKind::SWAP) {  // relabel: no data moves
+                    std::swap(mem[size_t(g.targets[0])], mem[size_t(g.targets[1])]);
+                    continue;
+                }
                 quokka::Gate m = g;
                 m.constituents.clear();
                 for (int& q : m.targets) q = mem[size_t(q)];
                 for (int& q : m.controls) q = mem[size_t(q)];
-                gates.push_back(std::move(m));
+                stream.push_back(std::move(m));
             }
-            ci.steps = qkeng::compileBlock(gates, nLocal, c->gtab);
-            if (lazy) retileOutput(items, idx, ci.steps, mem);
-            for (qkeng::Step& s : ci.steps) {
-                ci.flopsPerAmp += s.flopsPerAmp;
-                if (s.kind != qkeng::Step::Pass) {
-                    const uint64_t off = c->targets.size();
-                    c->targets.insert(c->targets.end(), s.targets.begin(), s.targets.end());
-                    s.targets.insert(s.targets.begin(), int(off));  // [0] = device offset
-                }
-            }
-        } else if (item.swap.kind == quokka::SwapOp::InMemory && lazy) {
+            continue;
+        }
+        if (item.swap.kind == quokka::SwapOp::InMemory && lazy) {
             for (const auto& [o, i] : item.swap.pairs) std::swap(mem[size_t(o)], mem[size_t(i)]);
             continue;
-        } else {
-            if (item.swap.kind == quokka::SwapOp::CrossRank) materialize();
-            ci.kind = item.swap.kind == quokka::SwapOp::InMemory ? CompiledItem::Ims : CompiledItem::Xrs;
-            for (const auto& [o, i] : item.swap.pairs) {
-                ci.outs.push_back(o);
-                ci.ins.push_back(i);
-            }
+        }
+        const bool cross = item.swap.kind == quokka::SwapOp::CrossRank;
+        flushStream(cross);
+        if (cross) materialize();
+        CompiledItem ci;
+        ci.kind = cross ? CompiledItem::Xrs : CompiledItem::Ims;
+        for (const auto& [o, i] : item.swap.pairs) {
+            ci.outs.push_back(o);
+            ci.ins.push_back(i);
         }
         c->items.push_back(std::move(ci));
     }
+    flushStream(true);
     materialize();
     p->compiled[nLocal] = c;
     return c;
@@ -698,6 +678,13 @@ std::string stepsJson(const std::vector<qkeng::Step>& steps, const std::vector<d
             for (int i = 0; i < 2 * qkdev::kMaxCoef; i++) o << (i ? "," : "") << P.coef[i];
             o << "],\"contrib\":[";
             for (int i = 0; i < qkdev::kMaxContrib; i++) o << (i ? "," : "") << P.contrib[i];
+            o << "],\"ncta\":" << P.ncta << ",\"cta_end\":[";
+            for (int f = 0; f < P.ncta; f++) o << (f ? "," : "") << P.cta_end[f];
+            o << "],\"cta_terms\":[";
+            const int nterms = P.ncta ? P.cta_end[P.ncta - 1] : 0;
+            for (int t = 0; t < nterms; t++)
+                o << (t ? "," : "") << "[" << int(P.cta_terms[t].b1) << "," << int(P.cta_terms[t].b2) << ","
+                  << P.cta_terms[t].c << "]";
             o << "]";
         }
         o << "}";

@@ -82,6 +82,11 @@ double referenceFlopsPerAmp(const Gate& g) {
 
 namespace {
 
+// Remapped gate qubits: tile index (< 64) or kCta + memory bit for a bit
+// outside the tile (a constant of the CTA; only diagonal gates may have them).
+constexpr int kCta = 64;
+bool isCtaBit(int q) { return q >= kCta; }
+
 bool denseInRegs(const Gate& g, int rb) {
     return g.kind == GateKind::FusedDense && g.targets.size() >= 2 && int(g.targets.size()) <= std::min(4, rb);
 }
@@ -104,6 +109,28 @@ bool oneQubitDense(const Gate& g, const Gate& orig) {
             return false;
     }
 }
+
+}  // namespace
+
+bool isDiagonalGate(const Gate& g) {
+    switch (g.kind) {
+        case GateKind::RZ:
+        case GateKind::CP:
+        case GateKind::RZZ:
+        case GateKind::FusedDiag:
+            return true;
+        case GateKind::U:
+        case GateKind::RX:
+        case GateKind::RY:
+            return diagonalMatrix(quokka::gateMatrix(g));
+        case GateKind::FusedDense:
+            return g.targets.size() == 1 && diagonalMatrix(g.payload);
+        default:
+            return false;
+    }
+}
+
+namespace {
 
 // Tile bits that must sit in register slots when `g` runs.
 std::vector<int> regNeeds(const Gate& g, const Gate& orig) {
@@ -143,7 +170,7 @@ public:
             P_->tile_phys[j] = int8_t(tilePhys_[size_t(j)]);
             P_->tile_mask |= uint64_t(1) << tilePhys_[size_t(j)];
         }
-        nops_ = ncoef_ = ncontrib_ = 0;
+        nops_ = ncoef_ = ncontrib_ = ncta_ = ncterms_ = 0;
         seg_ = 0;
         hcount_ = 0;
         pendScalar_ = false;
@@ -157,9 +184,9 @@ public:
         double flops = 0;
         while (i < tg_.size()) {
             const int queued = int(regOps_.size());  // ops still held in the diagonal batch
-            if (kMaxOps - nops_ - queued < 16 || kMaxCoef - ncoef_ - 4 * queued < 16 ||
-                kMaxContrib - ncontrib_ < 16 + ct_ ||
-                kMaxSegs - seg_ < 3)
+            if (kMaxOps - nops_ - queued < 16 + ct_ || kMaxCoef - ncoef_ - 4 * queued - pendingCtaTerms() < 24 ||
+                kMaxContrib - ncontrib_ < 48 + ct_ || kMaxSegs - seg_ < 3 || kMaxCtaFactors - ncta_ < ct_ + 2 ||
+                kMaxCtaTerms - ncterms_ - pendingCtaTerms() < 12)
                 break;
             if (!satisfied(tg_[i], orig_[i])) {
                 flushAll();
@@ -177,6 +204,7 @@ public:
         closeSegment();
         P_->nsegs = seg_ + 1;
         P_->nops = nops_;
+        P_->ncta = ncta_;
         step.kind = Step::Pass;
         step.pass = P;
         step.flopsPerAmp = flops;
@@ -366,6 +394,52 @@ private:
             usedR_[s] = false;
         }
         regOps_.clear();
+        ctaP_.clear();
+        for (auto& v : ctaBit_) v.clear();
+    }
+
+    // ---- CTA-dependent factors (bits outside the tile) ---------------------
+    struct Term {
+        int b1, b2;  // memory bits (b1 < 0: unconditional)
+        Amp v;
+    };
+    int pendingCtaTerms() const {
+        size_t n = ctaP_.size();
+        for (const auto& v : ctaBit_) n += v.size();
+        return int(n);
+    }
+    static void addTerm(std::vector<Term>& to, int b1, int b2, Amp v) {
+        if (v != Amp(1.0, 0.0)) to.push_back({b1, b2, v});
+    }
+    // Registers one factor (product of `terms`) for this tile; returns its index.
+    uint32_t ctaFactor(const std::vector<Term>& terms) {
+        const int f = ncta_++;
+        for (const Term& t : terms) {
+            CtaTerm& ct = P_->cta_terms[ncterms_++];
+            ct.b1 = uint8_t(t.b1 < 0 ? 255 : t.b1);
+            ct.b2 = uint8_t(t.b1 < 0 ? 255 : t.b2);
+            ct.c = uint16_t(addCoef({t.v}));
+        }
+        P_->cta_end[f] = uint16_t(ncterms_);
+        return uint32_t(f);
+    }
+    void emitCtaBatch() {
+        if (!ctaP_.empty()) {
+            emit(OP_SCAL_CTA, 0, 0, 0, ctaFactor(ctaP_));
+            pendScalar_ = true;
+        }
+        for (int b = 0; b < ct_; b++) {
+            if (ctaBit_[size_t(b)].empty()) continue;
+            const int s = inv_[b];
+            const uint32_t f = ctaFactor(ctaBit_[size_t(b)]);
+            if (isReg(s)) {
+                emit(OP_PEND_CTA, s, 0, 0, f);
+                pendSlot_[s] = true;
+            } else {
+                emit(OP_SCAL_TCTA, 0, s - rb_, 0, f);
+                pendScalar_ = true;
+            }
+        }
     }
 
     // table over thread index t: t -> f(t)
@@ -403,6 +477,7 @@ private:
 
     void emitBatch() {
         if (!batchAny_) return;
+        emitCtaBatch();
         usedP_ = usedP_ && !allOne(tabP_);
         for (int s = 0; s < rb_; s++) usedR_[s] = usedR_[s] && !allOne(tabR_[s]);
         if (usedP_) {
@@ -421,6 +496,12 @@ private:
     // amplitude *= d[logical bit q].  Slot semantics are physical: a flipped
     // slot holds the logical bit inverted, so the entry pair swaps.
     void diag1(int q, std::vector<Amp> d) {
+        if (isCtaBit(q)) {  // amplitude *= d[c]: d0 now, d1/d0 when the CTA bit is set
+            batchAny_ = true;
+            if (d[0] != Amp(1.0, 0.0)) mulP(0, [&](int) { return d[0]; });
+            addTerm(ctaP_, q - kCta, q - kCta, ratio(d[1], d[0]));
+            return;
+        }
         const int s = inv_[q];
         if (flip(s)) std::swap(d[0], d[1]);
         if (!isReg(s)) {
@@ -434,6 +515,39 @@ private:
 
     // amplitude *= d[2 bit(q0) + bit(q1)] (logical bits).
     void diag2(int q0, int q1, const std::vector<Amp>& dl) {
+        if (isCtaBit(q0) && isCtaBit(q1)) {  // d[2 c0 + c1] = d00 (c0? r0) (c1? r1) (c0 c1? r01)
+            const int c0 = q0 - kCta, c1 = q1 - kCta;
+            batchAny_ = true;
+            if (dl[0] != Amp(1.0, 0.0)) mulP(0, [&](int) { return dl[0]; });
+            const Amp r0 = ratio(dl[2], dl[0]), r1 = ratio(dl[1], dl[0]);
+            addTerm(ctaP_, c0, c0, r0);
+            addTerm(ctaP_, c1, c1, r1);
+            addTerm(ctaP_, c0, c1, ratio(dl[3], dl[0] * r0 * r1));
+            return;
+        }
+        if (isCtaBit(q0) || isCtaBit(q1)) {
+            // e(x, c) with x the tile bit (logical), c the CTA bit:
+            //   e(x, c) = e(0, c) * (x ? e(1, c) / e(0, c) : 1)
+            const bool ctaIsMsb = isCtaBit(q0);
+            const int c = (ctaIsMsb ? q0 : q1) - kCta, q = ctaIsMsb ? q1 : q0;
+            auto e = [&](int x, int cv) { return ctaIsMsb ? dl[size_t(2 * cv + x)] : dl[size_t(2 * x + cv)]; };
+            diag1(q, {e(0, 0), e(1, 0)});                       // the c = 0 values
+            addTerm(ctaP_, c, c, ratio(e(0, 1), e(0, 0)));      // x = 0 part when c = 1
+            const Amp b0 = ratio(e(1, 0), e(0, 0)), b1 = ratio(e(1, 1), e(0, 1));
+            // x = 1 part when c = 1, relative to the c = 0 value already applied
+            const Amp rel = ratio(b1, b0);
+            if (rel != Amp(1.0, 0.0)) {
+                batchAny_ = true;
+                const int s = inv_[q];
+                if (flip(s)) {  // physical bit = logical ^ 1: factor on physical 0 = rel * (phys ? 1/rel : 1)
+                    addTerm(ctaP_, c, c, rel);
+                    addTerm(ctaBit_[size_t(q)], c, c, ratio(Amp(1.0, 0.0), rel));
+                } else {
+                    addTerm(ctaBit_[size_t(q)], c, c, rel);
+                }
+            }
+            return;
+        }
         const int s0 = inv_[q0], s1 = inv_[q1], f0 = flip(s0), f1 = flip(s1);
         std::vector<Amp> d(4);  // physical entries
         for (int b0 = 0; b0 < 2; b0++)
@@ -536,12 +650,23 @@ private:
                 const uint16_t c16 = uint16_t(ncontrib_);
                 uint32_t x = 0;
                 for (int s = 0; s < ct_; s++) P_->contrib[ncontrib_ + s] = 0;
+                std::vector<std::pair<int, int>> cta;  // (memory bit, table-index value)
                 for (int j = 0; j < k; j++) {
-                    const int s = inv_[g.targets[size_t(j)]];
+                    const int q = g.targets[size_t(j)];
+                    if (isCtaBit(q)) {
+                        cta.emplace_back(q - kCta, 1 << (k - 1 - j));
+                        continue;
+                    }
+                    const int s = inv_[q];
                     P_->contrib[ncontrib_ + s] = uint16_t(1u << (k - 1 - j));
                     if (flip(s)) x |= 1u << (k - 1 - j);
                 }
                 ncontrib_ += ct_;
+                P_->contrib[ncontrib_++] = uint16_t(cta.size());
+                for (const auto& [b, v] : cta) {
+                    P_->contrib[ncontrib_++] = uint16_t(b);
+                    P_->contrib[ncontrib_++] = uint16_t(v);
+                }
                 emit(OP_DTABLE, 0, 0, k, addTable(orig.payload), c16);
                 P_->ops[nops_ - 1].x16 = uint16_t(x);
                 return;
@@ -588,6 +713,9 @@ private:
     uint32_t maskR_[kMaxRegBits] = {};
     bool usedR_[kMaxRegBits] = {};
     std::vector<RegOp> regOps_;
+    std::vector<Term> ctaP_;            // CTA-dependent factor of every amplitude (this batch)
+    std::vector<Term> ctaBit_[16];      // ... of the amplitudes whose tile bit b is 1
+    int ncta_ = 0, ncterms_ = 0;
     uint32_t flips_ = 0;  // slots (register and thread) holding an inverted bit
     uint8_t map_[16] = {};
     int inv_[16] = {};
@@ -597,8 +725,8 @@ Gate remapQubits(const Gate& g, const int* tileOf) {
     Gate t;
     t.kind = g.kind;
     t.id = g.id;
-    for (int q : g.targets) t.targets.push_back(tileOf[q]);
-    for (int q : g.controls) t.controls.push_back(tileOf[q]);
+    for (int q : g.targets) t.targets.push_back(tileOf[q] >= 0 ? tileOf[q] : kCta + q);
+    for (int q : g.controls) t.controls.push_back(tileOf[q] >= 0 ? tileOf[q] : kCta + q);
     return t;
 }
 
@@ -628,6 +756,17 @@ void compileGroup(const std::vector<Gate>& gates, uint64_t used, int ct, int nLo
 
 }  // namespace
 
+int lowTileBits() {
+    static const int v = envInt("QK_TILE_LOW", 3, 0, 8);
+    return v;
+}
+
+// Gates (memory-bit positions, program order) -> steps.  Consecutive gates
+// share a pass while the bits their NON-diagonal gates touch, plus the lowest
+// `lowTileBits()` memory bits (coalesced >= 128-B rows), fit in one tile:
+// diagonal gates never constrain the tile (bits outside it are constants of
+// the CTA), so runs of controlled-phase / RZ / RZZ / D_k gates ride along
+// with whichever pass is open.  Gate order is never changed.
 std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::vector<double>& gtab) {
     std::vector<Step> steps;
     for (const Gate& g : gates)
@@ -653,6 +792,7 @@ std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::
     }
     const int ct = std::min(maxTileBits(), nLocal);
     const int rb = regBitsFor(ct);
+    const uint64_t low = (uint64_t(1) << std::min(lowTileBits(), ct)) - 1;
     std::vector<Gate> group;
     uint64_t used = 0;
     auto close = [&] {
@@ -661,21 +801,16 @@ std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::
         used = 0;
     };
     for (const Gate& g : gates) {
-        if (g.kind == GateKind::FusedDense && g.targets.size() > size_t(std::min(4, rb))) {
+        if (g.kind == GateKind::FusedDense && g.targets.size() > size_t(std::min(4, rb)) && !isDiagonalGate(g)) {
             if (g.targets.size() > size_t(kMaxTileBits))
                 throw SimulationError("fused dense gate " + std::to_string(g.id) + " wider than 13 qubits");
             close();
             denseStep(g.payload, g.targets, referenceFlopsPerAmp(g));
             continue;
         }
-        if (g.kind == GateKind::FusedDiag && g.targets.size() > size_t(ct)) {  // wider than a tile
-            close();
-            denseStep(g.payload, g.targets, referenceFlopsPerAmp(g));
-            steps.back().kind = Step::DiagTable;
-            continue;
-        }
-        const uint64_t m = g.depMask();
-        if (__builtin_popcountll(used | m) > ct) close();
+        const uint64_t m = isDiagonalGate(g) ? 0 : g.depMask();
+        const uint64_t u2 = used | m;
+        if (__builtin_popcountll(u2) + __builtin_popcountll(~u2 & low) > ct) close();
         group.push_back(g);
         used |= m;
     }

@@ -6,7 +6,8 @@ against the oracle without a GPU.  Never used by the product."""
 import numpy as np
 
 OPS = ["MAT1", "H", "CX", "DIAG1_R", "DIAG2_RR", "CPHASE_RR", "PEND_R", "PEND_RT", "SCAL", "SCAL_T",
-       "SCAL_TT", "FLUSH_SLOT", "FLUSH", "DTABLE", "DENSE", "EXCHANGE", "SCAL_TAB", "PEND_TAB"]
+       "SCAL_TT", "FLUSH_SLOT", "FLUSH", "DTABLE", "DENSE", "EXCHANGE", "SCAL_TAB", "PEND_TAB", "SCAL_CTA",
+       "PEND_CTA", "SCAL_TCTA"]
 
 
 def pext8(t, m):
@@ -101,6 +102,13 @@ def _run_pass(state, n, P, gt):
             base |= ((cta >> j) & 1) << b
         addr = base | gaddr(P["map_in"][0], 0)
         a = state[addr].copy()  # (nt, na)
+        F = []
+        for f in range(P.get("ncta", 0)):
+            acc = 1 + 0j
+            for (b1, b2, c) in P["cta_terms"][(P["cta_end"][f - 1] if f else 0):P["cta_end"][f]]:
+                if b1 == 255 or ((base >> b1) & (base >> b2) & 1):
+                    acc *= coef[c]
+            F.append(acc)
         Pt = np.ones(nt, dtype=np.complex128)
         R = np.ones((nt, rb), dtype=np.complex128)
         sm = np.zeros(1 << ct, dtype=np.complex128)
@@ -146,6 +154,12 @@ def _run_pass(state, n, P, gt):
                 Pt *= gt[oc + pext8(tid, ob)]
             elif name == "PEND_TAB":
                 R[:, oa] *= gt[oc + pext8(tid, ob)]
+            elif name == "SCAL_CTA":
+                Pt *= F[oc]
+            elif name == "PEND_CTA":
+                R[:, oa] *= F[oc]
+            elif name == "SCAL_TCTA":
+                Pt *= np.where(bit(tid, ob) == 1, F[oc], 1)
             elif name == "SCAL":
                 Pt *= coef[oc]
             elif name == "SCAL_T":
@@ -169,6 +183,9 @@ def _run_pass(state, n, P, gt):
                 sub = np.zeros(nt, dtype=np.int64)
                 for j in range(rb, ct):
                     sub |= np.where(bit(tid, j - rb) == 1, cb[j], 0)
+                for j in range(contrib[oc16 + ct]):
+                    if (base >> contrib[oc16 + ct + 1 + 2 * j]) & 1:
+                        sub |= contrib[oc16 + ct + 2 + 2 * j]
                 sr = np.zeros(na, dtype=np.int64)
                 for kk in range(rb):
                     sr |= np.where(bit(s_idx, kk) == 1, cb[kk], 0)

@@ -19,6 +19,8 @@ struct QkDim3 {
 inline thread_local unsigned qk_tl_tid = 0, qk_tl_bid = 0;
 #define threadIdx (QkDim3{qk_tl_tid})
 #define blockIdx (QkDim3{qk_tl_bid})
+inline unsigned qk_grid = 1;
+#define gridDim (QkDim3{qk_grid})
 inline std::barrier<>* qk_bar = nullptr;
 static inline void __syncthreads() { qk_bar->arrive_and_wait(); }
 template <class T>
@@ -34,14 +36,16 @@ static inline void __stcs(T* p, T v) { *p = v; }
 #define __restrict__
 #define __shared__
 // `extern __shared__ double2 sm[];` in the kernel binds to this array.
-extern "C" double2 sm[1 << 13];
+extern "C" double2 sm[(1 << 13) + 64];
 
-// Launch: every CTA in turn, nt threads each.
+// Launch: a persistent grid of min(ntiles, 3) CTAs run one after another
+// (each walks its tiles), nt threads each.
 #define QK_HOST_LAUNCHER(KERNEL)                                                              \
-    double2 sm[1 << 13];                                                                      \
+    double2 sm[(1 << 13) + 64];                                                               \
     extern "C" void qk_host_launch(double2* st, const double2* gt, int nLocal, int ct, int rb) { \
-        const unsigned ctas = 1u << (nLocal - ct), nt = 1u << (ct - rb);                     \
-        for (unsigned b = 0; b < ctas; b++) {                                                 \
+        const unsigned ntiles = 1u << (nLocal - ct), nt = 1u << (ct - rb);                   \
+        qk_grid = ntiles < 3u ? ntiles : 3u;                                                  \
+        for (unsigned b = 0; b < qk_grid; b++) {                                              \
             std::barrier<> bar(nt);                                                           \
             qk_bar = &bar;                                                                    \
             std::vector<std::thread> ts;                                                      \
@@ -49,7 +53,7 @@ extern "C" double2 sm[1 << 13];
                 ts.emplace_back([=] {                                                         \
                     qk_tl_tid = t;                                                            \
                     qk_tl_bid = b;                                                            \
-                    KERNEL(st, gt);                                                           \
+                    KERNEL(st, gt, ntiles);                                                   \
                 });                                                                           \
             for (auto& th : ts) th.join();                                                    \
         }                                                                                     \

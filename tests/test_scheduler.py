@@ -158,3 +158,22 @@ def test_specialized_kernel_sources_compile(qk):
     lines = prog.text().splitlines()
     k = int(lines[0])
     assert qk.debug_jit_compile(lines[1:1 + k], 14)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_streams_with_out_of_tile_diagonals(qk, port, ref, seed):
+    # n > 13: passes span program blocks and apply diagonal gates whose qubits
+    # lie outside the tile (CTA-constant bits: per-CTA factors, D_k CTA offsets).
+    n = 15
+    rng = np.random.default_rng(seed)
+    kind = ["qft", "qaoa", "random"][seed % 3]
+    circ = ref.gen(kind, n, {"qft": 0, "qaoa": 1, "random": 150}[kind], 40 + seed)
+    cfg_text = config_text(n, 0, int(rng.integers(5, 11)), fusion=seed % 2, diag=(seed // 2) % 2)
+    prog_text = ref.optimize(circ, cfg_text)
+    want, _, _, _ = ref.simulate(prog_text, cfg_text, n, 0, 9, 2)
+    prog = qk.Program.parse(prog_text, qk.Config.parse(cfg_text))
+    compiled = prog.debug_compile()
+    got = run_compiled(qk, port, prog, n, 9)
+    assert np.max(np.abs(got - want.view(np.complex128))) < 1e-10
+    if kind == "qft":
+        assert any(s.get("ncta", 0) > 0 for it in compiled["items"] if it["kind"] == 0 for s in it["block"]["steps"])
