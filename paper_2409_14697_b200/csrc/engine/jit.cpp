@@ -188,7 +188,10 @@ private:
         o_ << "static __device__ const unsigned char qk_tb[] = {";
         for (int t = 0; t < nt; t++) o_ << (t ? "," : "") << int(P_.cta_terms[t].b1) << "," << int(P_.cta_terms[t].b2);
         o_ << "};\nstatic __device__ const double2 qk_tv[] = {";
-        for (int t = 0; t < nt; t++) o_ << (t ? "," : "") << lc(P_.cta_terms[t].c);
+        for (int t = 0; t < nt; t++) {
+            const uint32_t c = P_.cta_terms[t].c;
+            o_ << (t ? ",{" : "{") << lit(P_.coef[2 * c]) << "," << lit(P_.coef[2 * c + 1]) << "}";
+        }
         o_ << "};\nstatic __device__ const unsigned short qk_te[] = {";
         for (int f = 0; f < P_.ncta; f++) o_ << (f ? "," : "") << P_.cta_end[f];
         o_ << "};\n";

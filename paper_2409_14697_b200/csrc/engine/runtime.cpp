@@ -874,8 +874,9 @@ int qk_debug_jit_compile(const qk_gate* gates, int ngates, int nLocal, char** so
 }
 
 // Specialized-kernel sources of every pass of a compiled program, in item /
-// step order, separated by "//@@PASS <name>" lines (host only; tests replay
-// them on the CPU through tests/jit_host_shim.h).
+// step order, separated by "//@@PASS <name>" lines, each also compiled by
+// NVRTC for sm_100a (host only; tests replay them on the CPU through
+// tests/host/jit_host_shim.h).
 int qk_debug_jit_program(const qk_program* cp, int nLocal, char** sources) {
     return guard([&] {
         qk_program* p = const_cast<qk_program*>(cp);
@@ -886,7 +887,9 @@ int qk_debug_jit_program(const qk_program* cp, int nLocal, char** sources) {
             for (const qkeng::Step& s : it.steps)
                 if (s.kind == qkeng::Step::Pass) {
                     const std::string name = "qk_host_pass_" + std::to_string(k++);
-                    all += "//@@PASS " + name + "\n" + qkjit::generatePassSource(*s.pass, name);
+                    const std::string src = qkjit::generatePassSource(*s.pass, name);
+                    qkjit::compileToCubin(src, name);  // NVRTC (no GPU needed): throws with the log
+                    all += "//@@PASS " + name + "\n" + src;
                 }
         *sources = dupText(all);
     });
