@@ -841,7 +841,10 @@ int qk_apply_block(qk_state* st, const qk_gate* gates, int ngates, int chunk) {
         DeviceTables t = tablesFor(&prog, *c, st->device);
         prepareJit(*c, st->device);
         qk_run_stats rs{};
-        runBlock(st, c->items[0], t, rs);
+        for (const CompiledItem& it : c->items) {  // passes, then the materialization of SWAP relabels
+            if (it.kind == CompiledItem::Block) runBlock(st, it, t, rs);
+            else runIms(st, it.outs, it.ins, rs);
+        }
         cuda(cudaStreamSynchronize(st->stream), "apply block");
     });
 }

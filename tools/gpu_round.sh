@@ -4,7 +4,7 @@
 TAG=${1:-r1}
 O=gpurun_out/$TAG
 mkdir -p $O
-export QK_JIT_CACHE=$PWD/gpurun_out/jitcache
+export QK_JIT_CACHE=/tmp/qk_jit_cache
 nvidia-smi > $O/nvsmi.txt 2>&1
 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc $?"; tail -3 $O/smoke.log
 timeout 1200 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "pytest rc $?"; tail -3 $O/pytest_gpu.log
