@@ -254,7 +254,8 @@ def main():
     blk_launch_ms = s0["block_ms"] / max(1, s0["block_launches"])
     blk_gbs = 32.0 * amps / (blk_launch_ms * 1e-3) / 1e9
     ims_launch_ms = s0["ims_ms"] / max(1, s0["ims_launches"]) if s0["ims_launches"] else 0.0
-    traffic = ncu_traffic()
+    tr = ncu_traffic()
+    traffic = round(tr["dram_bytes_per_amp"] * amps) if tr else None
     # program-level roofline: T_roof = sum over items, HBM-bound
     t_roof = (s0["block_bytes"] + s0["ims_bytes"]) / (peak * 1e9) + s0["xrs_bytes"] / 770e9
 
@@ -282,6 +283,7 @@ def main():
         "roofline": {"bound": "hbm", "kernel": "k_block_pass", "achieved": round(blk_gbs, 1),
                      "peak": peak, "unit": "GB/s", "frac": round(blk_gbs / peak, 4),
                      "peak_source": peak_src, "traffic": traffic,
+                     "traffic_source": (tr["source"] + ", DRAM bytes/amp x this slice") if tr else None,
                      "algorithmic_bytes_per_launch": 32 * amps, "avg_launch_ms": round(blk_launch_ms, 3)},
         "breakdown": {"block_ms": round(s0["block_ms"], 2), "ims_ms": round(s0["ims_ms"], 2),
                       "xrs_ms": round(s0["xrs_ms"], 2), "block_launches": s0["block_launches"],
