@@ -762,11 +762,12 @@ int lowTileBits() {
 }
 
 // Gates (memory-bit positions, program order) -> steps.  Consecutive gates
-// share a pass while the bits their NON-diagonal gates touch, plus the lowest
-// `lowTileBits()` memory bits (coalesced >= 128-B rows), fit in one tile:
-// diagonal gates never constrain the tile (bits outside it are constants of
-// the CTA), so runs of controlled-phase / RZ / RZZ / D_k gates ride along
-// with whichever pass is open.  Gate order is never changed.
+// share a pass while the bits their NON-diagonal gates touch fit in one tile
+// (padded with the lowest memory bits for coalesced rows): diagonal gates
+// never constrain the tile (bits outside it are constants of the CTA), so
+// runs of controlled-phase / RZ / RZZ / D_k gates ride along with whichever
+// pass is open.  Gate order is never changed; the cut points minimize the
+// estimated HBM cost.
 std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::vector<double>& gtab) {
     std::vector<Step> steps;
     for (const Gate& g : gates)
@@ -792,29 +793,62 @@ std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::
     }
     const int ct = std::min(maxTileBits(), nLocal);
     const int rb = regBitsFor(ct);
-    const uint64_t low = (uint64_t(1) << std::min(lowTileBits(), ct)) - 1;
-    std::vector<Gate> group;
-    uint64_t used = 0;
-    auto close = [&] {
-        if (!group.empty()) compileGroup(group, used, ct, nLocal, gtab, steps);
-        group.clear();
-        used = 0;
+    // Cut each run of gates (between wide dense steps) into passes by dynamic
+    // programming over cut points.  A pass costs one HBM round trip, more when
+    // its tile cannot start with >= 3 contiguous low memory bits (rows under
+    // 128 B; measured ~1.7x slower at 16-32 B rows).
+    auto passCost = [&](uint64_t used) {
+        uint64_t tile = used;
+        for (int b = 0; b < nLocal && __builtin_popcountll(tile) < ct; b++) tile |= uint64_t(1) << b;
+        int L = 0;
+        while (L < ct && ((tile >> L) & 1)) L++;
+        static const double pen[4] = {1.0, 0.6, 0.3, 0.0};
+        return 1.0 + pen[std::min(L, lowTileBits())];
+    };
+    std::vector<Gate> run;
+    auto cutRun = [&] {
+        const size_t m = run.size();
+        if (!m) return;
+        std::vector<uint64_t> mask(m);
+        for (size_t k = 0; k < m; k++) mask[k] = isDiagonalGate(run[k]) ? 0 : run[k].depMask();
+        std::vector<double> best(m + 1, 1e300);
+        std::vector<size_t> from(m + 1, 0);
+        best[0] = 0;
+        for (size_t i = 1; i <= m; i++) {
+            uint64_t used = 0;
+            for (size_t j = i; j-- > 0;) {
+                used |= mask[j];
+                if (__builtin_popcountll(used) > ct) break;
+                const double c = best[j] + passCost(used);
+                if (c < best[i] - 1e-9) {
+                    best[i] = c;
+                    from[i] = j;
+                }
+            }
+        }
+        std::vector<size_t> cuts;
+        for (size_t i = m; i > 0; i = from[i]) cuts.push_back(from[i]);
+        std::reverse(cuts.begin(), cuts.end());
+        cuts.push_back(m);
+        for (size_t c = 0; c + 1 < cuts.size(); c++) {
+            std::vector<Gate> group(run.begin() + long(cuts[c]), run.begin() + long(cuts[c + 1]));
+            uint64_t used = 0;
+            for (size_t k = cuts[c]; k < cuts[c + 1]; k++) used |= mask[k];
+            compileGroup(group, used, ct, nLocal, gtab, steps);
+        }
+        run.clear();
     };
     for (const Gate& g : gates) {
         if (g.kind == GateKind::FusedDense && g.targets.size() > size_t(std::min(4, rb)) && !isDiagonalGate(g)) {
             if (g.targets.size() > size_t(kMaxTileBits))
                 throw SimulationError("fused dense gate " + std::to_string(g.id) + " wider than 13 qubits");
-            close();
+            cutRun();
             denseStep(g.payload, g.targets, referenceFlopsPerAmp(g));
             continue;
         }
-        const uint64_t m = isDiagonalGate(g) ? 0 : g.depMask();
-        const uint64_t u2 = used | m;
-        if (__builtin_popcountll(u2) + __builtin_popcountll(~u2 & low) > ct) close();
-        group.push_back(g);
-        used |= m;
+        run.push_back(g);
     }
-    close();
+    cutRun();
     return steps;
 }
 
