@@ -288,7 +288,8 @@ __device__ __forceinline__ void flushAll(double2 (&a)[1 << RB], double2 P, doubl
 
 template <int CT, int RB, int MINB>
 __global__ void __launch_bounds__(1 << (CT - RB), MINB)
-    k_block_pass(double2* __restrict__ state, const double2* __restrict__ gtab, const __grid_constant__ PassParams P) {
+    k_block_pass(double2* __restrict__ state, const double2* __restrict__ gtab, const __grid_constant__ PassParams P,
+                 const uint64_t basis) {
     constexpr int NT = 1 << (CT - RB);
     constexpr int NA = 1 << RB;
     extern __shared__ double2 sm[];
@@ -307,8 +308,14 @@ __global__ void __launch_bounds__(1 << (CT - RB), MINB)
         uint64_t off, st[RB];
         globalLayout<CT, RB>(P, P.map_in[0], tid, off, st);
         off |= base;
+        if (basis == ~uint64_t(0)) {
 #pragma unroll
-        for (int s = 0; s < NA; s++) a[s] = __ldcs(state + (off | slotOffset<RB>(s, st)));
+            for (int s = 0; s < NA; s++) a[s] = __ldcs(state + (off | slotOffset<RB>(s, st)));
+        } else {  // first pass of a run: synthesize the basis state |basis> instead of reading it
+#pragma unroll
+            for (int s = 0; s < NA; s++)
+                a[s] = make_double2((off | slotOffset<RB>(s, st)) == basis ? 1.0 : 0.0, 0.0);
+        }
     }
 
     // Per-CTA diagonal factors (functions of the non-tile bits of `base`).
@@ -541,7 +548,7 @@ __global__ void k_dense_group(double2* __restrict__ state, const double2* __rest
 // per SM) or RB = 4 (512 threads x 128 registers).
 template <int CT, int RB = (CT < 4 ? CT : 4)>
 static cudaError_t launchCT(double2* state, const double2* gtab, const PassParams& P, uint64_t ctas,
-                            cudaStream_t stream) {
+                            uint64_t basis, cudaStream_t stream) {
     constexpr int NT = 1 << (CT - RB);
     constexpr int MINB = (CT == 12 && RB == 4) ? 2 : 1;
     const size_t smem = (sizeof(double2) << CT) + sizeof(double2) * kMaxCtaFactors;
@@ -550,26 +557,26 @@ static cudaError_t launchCT(double2* state, const double2* gtab, const PassParam
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         if (e != cudaSuccess) return e;
     }
-    k_block_pass<CT, RB, MINB><<<dim3(unsigned(ctas)), NT, smem, stream>>>(state, gtab, P);
+    k_block_pass<CT, RB, MINB><<<dim3(unsigned(ctas)), NT, smem, stream>>>(state, gtab, P, basis);
     return cudaGetLastError();
 }
 
-cudaError_t launchBlockPass(double2* state, const double2* gtab, const PassParams& P, int nLocal,
+cudaError_t launchBlockPass(double2* state, const double2* gtab, const PassParams& P, int nLocal, uint64_t basis,
                             cudaStream_t stream) {
     if (P.rb != regBitsFor(P.ct)) return cudaErrorInvalidValue;
     const uint64_t ctas = uint64_t(1) << (nLocal - P.ct);
-    if (P.ct == 13) return P.rb == 5 ? launchCT<13, 5>(state, gtab, P, ctas, stream)
-                                     : launchCT<13, 4>(state, gtab, P, ctas, stream);
+    if (P.ct == 13) return P.rb == 5 ? launchCT<13, 5>(state, gtab, P, ctas, basis, stream)
+                                     : launchCT<13, 4>(state, gtab, P, ctas, basis, stream);
     switch (P.ct) {
-        case 4: return launchCT<4>(state, gtab, P, ctas, stream);
-        case 5: return launchCT<5>(state, gtab, P, ctas, stream);
-        case 6: return launchCT<6>(state, gtab, P, ctas, stream);
-        case 7: return launchCT<7>(state, gtab, P, ctas, stream);
-        case 8: return launchCT<8>(state, gtab, P, ctas, stream);
-        case 9: return launchCT<9>(state, gtab, P, ctas, stream);
-        case 10: return launchCT<10>(state, gtab, P, ctas, stream);
-        case 11: return launchCT<11>(state, gtab, P, ctas, stream);
-        case 12: return launchCT<12>(state, gtab, P, ctas, stream);
+        case 4: return launchCT<4>(state, gtab, P, ctas, basis, stream);
+        case 5: return launchCT<5>(state, gtab, P, ctas, basis, stream);
+        case 6: return launchCT<6>(state, gtab, P, ctas, basis, stream);
+        case 7: return launchCT<7>(state, gtab, P, ctas, basis, stream);
+        case 8: return launchCT<8>(state, gtab, P, ctas, basis, stream);
+        case 9: return launchCT<9>(state, gtab, P, ctas, basis, stream);
+        case 10: return launchCT<10>(state, gtab, P, ctas, basis, stream);
+        case 11: return launchCT<11>(state, gtab, P, ctas, basis, stream);
+        case 12: return launchCT<12>(state, gtab, P, ctas, basis, stream);
         default: return cudaErrorInvalidValue;
     }
 }

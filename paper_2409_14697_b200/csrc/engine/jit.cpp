@@ -117,7 +117,7 @@ public:
         o_ << kPrologue;
         ctaTables();
         o_ << "extern \"C\" __global__ void __launch_bounds__(" << nt_ << "," << minb << ") " << name
-           << "(double2* __restrict__ st, const double2* __restrict__ gt, const u32 ntiles) {\n";
+           << "(double2* __restrict__ st, const double2* __restrict__ gt, const u32 ntiles, const u64 basis) {\n";
         o_ << "  extern __shared__ double2 sm[];\n  double2* const F = sm + " << (1 << ct_)
            << ";\n  const u32 tid = threadIdx.x;\n";
         o_ << "  for (u32 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {\n";
@@ -126,10 +126,13 @@ public:
         for (int s = 0; s < na_; s++) decl += (s ? ", a" : "a") + std::to_string(s);
         o_ << decl << ";\n  double2 P = C2(1.0, 0.0);\n" << pendDecl();
         // load (map_in[0], no flips)
-        o_ << "  { const u64 off = base | " << threadGlobal(P_.map_in[0]) << ";\n";
+        o_ << "  { const u64 off = base | " << threadGlobal(P_.map_in[0]) << ";\n  if (basis == ~0ull) {\n";
         for (int s = 0; s < na_; s++)
             o_ << "  a" << s << " = __ldcs(st + (off | " << regGlobal(P_.map_in[0], s) << "ull));\n";
-        o_ << "  }\n";
+        o_ << "  } else {  // first pass of a run: synthesize |basis> instead of reading it\n";
+        for (int s = 0; s < na_; s++)
+            o_ << "  a" << s << " = C2((off | " << regGlobal(P_.map_in[0], s) << "ull) == basis ? 1.0 : 0.0, 0.0);\n";
+        o_ << "  }\n  }\n";
         prefetchNext();
         ctaFactors();
 
@@ -436,7 +439,7 @@ private:
 // ---- compile / load / launch -------------------------------------------------
 
 // Bump when the generated code changes for the same PassParams (on-disk cache key).
-constexpr uint64_t kGeneratorVersion = 4;
+constexpr uint64_t kGeneratorVersion = 5;
 
 uint64_t hashPass(const PassParams& P) {
     uint64_t h = 1469598103934665603ull ^ (kGeneratorVersion * 0x9E3779B97F4A7C15ull) ^ (usePrefetch() ? 1u : 0u) ^ (usePersistent() ? 2u : 0u);
@@ -604,7 +607,8 @@ void prepare(const std::vector<const PassParams*>& passes, int device) {
     for (const PassParams* P : passes) functionFor(*P, hashPass(*P), device);
 }
 
-cudaError_t launch(const PassParams& P, double2* state, const double2* gtab, int nLocal, cudaStream_t stream) {
+cudaError_t launch(const PassParams& P, double2* state, const double2* gtab, int nLocal, uint64_t basis,
+                   cudaStream_t stream) {
     int dev = 0;
     cudaGetDevice(&dev);
     void* fn = functionFor(P, hashPass(P), dev);
@@ -613,7 +617,7 @@ cudaError_t launch(const PassParams& P, double2* state, const double2* gtab, int
     const unsigned ctas = (ntiles < resident || !usePersistent()) ? ntiles : resident;
     const unsigned nt = 1u << (P.ct - P.rb);
     const unsigned smem = unsigned((sizeof(double2) << P.ct) + sizeof(double2) * qkdev::kMaxCtaFactors);
-    void* args[] = {&state, &gtab, &ntiles};
+    void* args[] = {&state, &gtab, &ntiles, &basis};
     if (driver().launchKernel(fn, ctas, 1, 1, nt, 1, 1, smem, stream, args, nullptr) != 0)
         return cudaErrorLaunchFailure;
     return cudaSuccess;

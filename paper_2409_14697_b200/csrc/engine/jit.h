@@ -24,7 +24,9 @@ std::string generatePassSource(const qkdev::PassParams& P, const std::string& na
 void prepare(const std::vector<const qkdev::PassParams*>& passes, int device);
 
 // Launch the specialized kernel of P (prepare()d for the current device).
-cudaError_t launch(const qkdev::PassParams& P, double2* state, const double2* gtab, int nLocal,
+// basis != ~0: synthesize the basis state |basis> (slice index) instead of
+// loading the slice (the first pass of a simulation needs no initState).
+cudaError_t launch(const qkdev::PassParams& P, double2* state, const double2* gtab, int nLocal, uint64_t basis,
                    cudaStream_t stream);
 
 // Slices with at least this many local qubits use specialized kernels

@@ -78,6 +78,72 @@ __global__ void __launch_bounds__(256) k_ims(double2* __restrict__ a, int logN, 
     }
 }
 
+// Tiled IMS.  T = a P-closed set of k <= 6 bits containing memory bits 0..2
+// (128-B rows) and their pair partners; a "tile" is the 2^k indices varying
+// over T.  P maps tile(h) onto tile(P(h)) (h = the non-T bits), permuting the
+// tile coordinates by pi.  One warp per orbit {h, P(h)}: both tiles are read
+// with coalesced 128-B rows, staged in warp-private shared memory, and written
+// back permuted, so pairs with a low "out" bit cost no sector waste (k_ims
+// reads 1.4x the bytes for those).
+struct ImsTileSpec {
+    int k;                 // tile bits
+    int n;                 // slice bits
+    int tbit[6];           // tile coordinate r -> memory bit (ascending)
+    int pi[6];             // tile coordinate r -> coordinate of P(bit)
+    int nfree;             // non-tile bits, ascending
+    int fbit[58];
+    int nhp;               // pairs among non-tile bits (memory bits)
+    int ho[29], hi[29];
+};
+
+__global__ void __launch_bounds__(256) k_ims_tiled(double2* __restrict__ a, const __grid_constant__ ImsTileSpec sp) {
+    __shared__ double2 buf[8][2][64];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int per = (1 << sp.k) >> 5;  // amplitudes per lane per tile (1 or 2)
+    // tile coordinates handled by this lane, their memory offsets, and the
+    // memory offsets of the permuted coordinates
+    uint64_t off[2];
+    int tpi[2];
+    _Pragma("unroll") for (int e = 0; e < 2; e++) if (e < per) {
+        const int t = lane + 32 * e;
+        uint64_t o = 0;
+        int u = 0;
+        for (int r = 0; r < sp.k; r++)
+            if ((t >> r) & 1) {
+                o |= uint64_t(1) << sp.tbit[r];
+                u |= 1 << sp.pi[r];
+            }
+        off[e] = o;
+        tpi[e] = u;  // pi(t): source coordinate for output coordinate t (pi is an involution)
+    }
+    const uint64_t groups = uint64_t(1) << sp.nfree;
+    const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x >> 5);
+    for (uint64_t g = uint64_t(blockIdx.x) * (blockDim.x >> 5) + w; g < groups; g += warps) {
+        uint64_t h = 0;
+        for (int j = 0; j < sp.nfree; j++) h |= ((g >> j) & 1) << sp.fbit[j];
+        uint64_t ph = h;
+        for (int j = 0; j < sp.nhp; j++) {
+            const uint64_t d = ((ph >> sp.ho[j]) ^ (ph >> sp.hi[j])) & 1u;
+            ph ^= (d << sp.ho[j]) | (d << sp.hi[j]);
+        }
+        if (ph < h) continue;  // the orbit's smaller member does the work
+        double2 va[2], vb[2];
+        _Pragma("unroll") for (int e = 0; e < 2; e++) if (e < per) va[e] = __ldcs(a + (h | off[e]));
+        if (ph != h)
+            _Pragma("unroll") for (int e = 0; e < 2; e++) if (e < per) vb[e] = __ldcs(a + (ph | off[e]));
+        _Pragma("unroll") for (int e = 0; e < 2; e++) if (e < per) {
+            buf[w][0][lane + 32 * e] = va[e];
+            if (ph != h) buf[w][1][lane + 32 * e] = vb[e];
+        }
+        __syncwarp();
+        // tile(ph)[t] <- tile(h)[pi(t)];  tile(h)[t] <- tile(ph)[pi(t)]
+        _Pragma("unroll") for (int e = 0; e < 2; e++) if (e < per) __stcs(a + (ph | off[e]), buf[w][0][tpi[e]]);
+        if (ph != h)
+            _Pragma("unroll") for (int e = 0; e < 2; e++) if (e < per) __stcs(a + (h | off[e]), buf[w][1][tpi[e]]);
+        __syncwarp();
+    }
+}
+
 // Offsets of a slab element: o deposited around the (ascending) out positions.
 struct SlabSpec {
     int s;
@@ -193,7 +259,7 @@ static unsigned gridFor(uint64_t work, unsigned threads, unsigned cap) {
     return unsigned(g ? g : 1);
 }
 
-cudaError_t launchIms(double2* a, int logN, const int* outs, const int* ins, int s, cudaStream_t st) {
+cudaError_t launchImsGeneric(double2* a, int logN, const int* outs, const int* ins, int s, cudaStream_t st) {
     PairSpec p{};
     p.s = s;
     for (int j = 0; j < s; j++) {
@@ -206,6 +272,57 @@ cudaError_t launchIms(double2* a, int logN, const int* outs, const int* ins, int
     const uint64_t T = uint64_t(1) << logT;
     const unsigned threads = T < 256 ? unsigned(T) : 256u;
     k_ims<<<unsigned(T / threads), threads, 0, st>>>(a, logN, logT, p);
+    return cudaGetLastError();
+}
+
+// Tiled IMS when the slice has >= 6 bits and a P-closed 5..6-bit tile exists.
+static bool imsTileSpec(int logN, const int* outs, const int* ins, int s, ImsTileSpec& sp) {
+    if (logN < 6) return false;
+    int partner[64];
+    for (int b = 0; b < 64; b++) partner[b] = b;
+    for (int j = 0; j < s; j++) {
+        partner[outs[j]] = ins[j];
+        partner[ins[j]] = outs[j];
+    }
+    uint64_t T = 0;
+    for (int b = 0; b < 3; b++) T |= (uint64_t(1) << b) | (uint64_t(1) << partner[b]);
+    if (__builtin_popcountll(T) > 6) return false;
+    for (int b = 0; b < logN && __builtin_popcountll(T) < 6; b++) {
+        if ((T >> b) & 1) continue;
+        const uint64_t add = (uint64_t(1) << b) | (uint64_t(1) << partner[b]);
+        if (__builtin_popcountll(T | add) <= 6) T |= add;
+    }
+    const int k = __builtin_popcountll(T);
+    if (k < 5) return false;
+    sp = ImsTileSpec{};
+    sp.k = k;
+    sp.n = logN;
+    int coord[64];
+    int r = 0;
+    for (int b = 0; b < logN; b++)
+        if ((T >> b) & 1) {
+            coord[b] = r;
+            sp.tbit[r++] = b;
+        }
+    for (int q = 0; q < k; q++) sp.pi[q] = coord[partner[sp.tbit[q]]];
+    for (int b = 0; b < logN; b++)
+        if (!((T >> b) & 1)) sp.fbit[sp.nfree++] = b;
+    for (int j = 0; j < s; j++)
+        if (!((T >> outs[j]) & 1)) {
+            sp.ho[sp.nhp] = outs[j];
+            sp.hi[sp.nhp] = ins[j];
+            sp.nhp++;
+        }
+    return true;
+}
+
+cudaError_t launchIms(double2* a, int logN, const int* outs, const int* ins, int s, cudaStream_t st) {
+    ImsTileSpec sp;
+    if (!imsTileSpec(logN, outs, ins, s, sp)) return launchImsGeneric(a, logN, outs, ins, s, st);
+    const uint64_t groups = uint64_t(1) << sp.nfree;
+    uint64_t ctas = (groups + 7) / 8;
+    if (ctas > 148u * 32u) ctas = 148u * 32u;
+    k_ims_tiled<<<unsigned(ctas), 256, 0, st>>>(a, sp);
     return cudaGetLastError();
 }
 

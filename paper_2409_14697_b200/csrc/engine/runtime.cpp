@@ -27,7 +27,7 @@
 #include "schedule.h"
 
 namespace qkdev {
-cudaError_t launchBlockPass(double2*, const double2*, const PassParams&, int, cudaStream_t);
+cudaError_t launchBlockPass(double2*, const double2*, const PassParams&, int, uint64_t, cudaStream_t);
 cudaError_t launchDenseGroup(double2*, const double2*, int, const int*, uint64_t, int, cudaStream_t);
 cudaError_t launchIms(double2*, int, const int*, const int*, int, cudaStream_t);
 cudaError_t launchSlabSwap(double2*, double2*, uint64_t, const int*, int, cudaStream_t);
@@ -491,13 +491,19 @@ void prepareJit(const Compiled& c, int device) {
     qkjit::prepare(passes, device);
 }
 
-void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_run_stats& rs) {
+constexpr uint64_t kNoBasis = ~uint64_t(0);
+
+// basis != kNoBasis: the first step is a pass that synthesizes |basis> (slice
+// index) instead of reading the slice (replaces initState's memset + store).
+void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_run_stats& rs,
+              uint64_t basis = kNoBasis) {
     for (const qkeng::Step& s : ci.steps) {
         if (s.kind == qkeng::Step::Pass) {
             if (useJit(st->nLocal))
-                cuda(qkjit::launch(*s.pass, st->amps, t.gtab, st->nLocal, st->stream), "specialized block pass");
+                cuda(qkjit::launch(*s.pass, st->amps, t.gtab, st->nLocal, basis, st->stream), "specialized block pass");
             else
-                cuda(qkdev::launchBlockPass(st->amps, t.gtab, *s.pass, st->nLocal, st->stream), "block pass");
+                cuda(qkdev::launchBlockPass(st->amps, t.gtab, *s.pass, st->nLocal, basis, st->stream), "block pass");
+            basis = kNoBasis;
         } else if (s.kind == qkeng::Step::DiagTable) {
             cuda(qkdev::launchDiagTable(st->amps, t.gtab + s.matOff, st->count, s.targets.data() + 1, s.k, st->stream),
                  "diag table");
@@ -1119,15 +1125,25 @@ int qk_simulate(qk_state* st, const qk_program* cp, const qk_config* cfg, uint64
         auto comp = compileFor(p, st->nLocal);
         const DeviceTables t = tablesFor(p, *comp, st->device);
         prepareJit(*comp, st->device);
+        if (initial >= (Index(1) << st->n)) throw SimulationError("initial basis state out of range");
         qk_run_stats rs{};
         Timer timer(st);
         cudaEvent_t e0, e1;
         cuda(cudaEventCreate(&e0), "event");
         cuda(cudaEventCreate(&e1), "event");
         cuda(cudaEventRecord(e0, st->stream), "event");
-        setBasis(st, initial);
+        // initState (engine.cpp:18-28): folded into the first pass when the
+        // program starts with one, else memset + one store.
+        const bool synth = !comp->items.empty() && comp->items[0].kind == CompiledItem::Block &&
+                           !comp->items[0].steps.empty() && comp->items[0].steps[0].kind == qkeng::Step::Pass;
+        uint64_t basis = kNoBasis;
+        if (synth) basis = (initial >> st->nLocal) == Index(st->rank) ? (initial & (st->count - 1)) : st->count;
+        else setBasis(st, initial);
         for (const CompiledItem& it : comp->items) {
-            if (it.kind == CompiledItem::Block) timer.time(0, [&] { runBlock(st, it, t, rs); });
+            if (it.kind == CompiledItem::Block) {
+                timer.time(0, [&] { runBlock(st, it, t, rs, basis); });
+                basis = kNoBasis;
+            }
             else if (it.kind == CompiledItem::Ims) timer.time(1, [&] { runIms(st, it.outs, it.ins, rs); });
             else {
                 quokka::SwapOp op;

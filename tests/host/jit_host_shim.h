@@ -42,7 +42,8 @@ extern "C" double2 sm[(1 << 13) + 64];
 // (each walks its tiles), nt threads each.
 #define QK_HOST_LAUNCHER(KERNEL)                                                              \
     double2 sm[(1 << 13) + 64];                                                               \
-    extern "C" void qk_host_launch(double2* st, const double2* gt, int nLocal, int ct, int rb) { \
+    extern "C" void qk_host_launch(double2* st, const double2* gt, int nLocal, int ct, int rb,    \
+                                   unsigned long long basis) {                              \
         const unsigned ntiles = 1u << (nLocal - ct), nt = 1u << (ct - rb);                   \
         qk_grid = ntiles < 3u ? ntiles : 3u;                                                  \
         for (unsigned b = 0; b < qk_grid; b++) {                                              \
@@ -53,7 +54,7 @@ extern "C" double2 sm[(1 << 13) + 64];
                 ts.emplace_back([=] {                                                         \
                     qk_tl_tid = t;                                                            \
                     qk_tl_bid = b;                                                            \
-                    KERNEL(st, gt, ntiles);                                                   \
+                    KERNEL(st, gt, ntiles, basis);                                            \
                 });                                                                           \
             for (auto& th : ts) th.join();                                                    \
         }                                                                                     \

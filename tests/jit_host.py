@@ -28,15 +28,24 @@ def host_kernel(name: str, src: str):
                         cpp, "-o", so + ".tmp", "-lpthread"], check=True)
         os.replace(so + ".tmp", so)
     lib = C.CDLL(so)
-    lib.qk_host_launch.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int]
+    lib.qk_host_launch.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_uint64]
     return lib.qk_host_launch
 
 
-def run_program_jit(qk, port, prog, n_local, state):
+NO_BASIS = (1 << 64) - 1
+
+
+def run_program_jit(qk, port, prog, n_local, state, basis=None):
     """Replay prog's compiled items on `state` (complex128, 2^n_local) with the
     generated kernels for passes, the emulator for dense/diag-table steps and
-    the oracle for IMS items."""
+    the oracle for IMS items.  basis: the first pass synthesizes |basis>
+    instead of reading `state` (the engine's folded initState)."""
+    first = NO_BASIS if basis is None else basis
     items = prog.debug_compile(n_local)["items"]
+    if basis is not None and not (items and items[0]["kind"] == 0 and items[0]["block"]["steps"][0]["kind"] == 0):
+        state[:] = 0  # the engine folds initState only into a leading pass
+        state[basis] = 1
+        first = NO_BASIS
     srcs = iter(prog.debug_jit_sources(n_local))
     for it in items:
         if it["kind"] == 0:
@@ -45,7 +54,8 @@ def run_program_jit(qk, port, prog, n_local, state):
             for st in blk["steps"]:
                 if st["kind"] == 0:
                     name, src = next(srcs)
-                    host_kernel(name, src)(state.ctypes.data, gt.ctypes.data, n_local, st["ct"], st["rb"])
+                    host_kernel(name, src)(state.ctypes.data, gt.ctypes.data, n_local, st["ct"], st["rb"], first)
+                    first = NO_BASIS
                 else:
                     run_steps(state, n_local, {"gtab": blk["gtab"], "steps": [st]})
         elif it["kind"] == 1:

@@ -26,3 +26,7 @@ def test_specialized_kernels_on_host(ref, qk, port, kind, n, chunk, fusion, diag
     st[5] = 1
     run_program_jit(qk, port, prog, n, st)
     assert np.max(np.abs(st - want.view(np.complex128))) < 1e-10
+    # folded initState: the first pass synthesizes |5> and never reads the slice
+    st = np.full(1 << n, np.nan, dtype=np.complex128)
+    run_program_jit(qk, port, prog, n, st, basis=5)
+    assert np.max(np.abs(st - want.view(np.complex128))) < 1e-10
