@@ -13,6 +13,7 @@
 #include <dlfcn.h>
 #include <nvrtc.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
@@ -62,6 +63,47 @@ static __device__ __forceinline__ double2 csel(bool c, double2 x, double2 y) {
     return make_double2(c ? x.x : y.x, c ? x.y : y.y);
 }
 static __device__ __forceinline__ u32 swz(u32 u) { return u ^ (((u >> 3) ^ (u >> 6) ^ (u >> 9) ^ (u >> 12)) & 7u); }
+// TMA bulk copies into shared memory, tracked by an mbarrier (host builds of
+// the generated source, tests/host/jit_host_shim.h, copy synchronously).
+static __device__ __forceinline__ u32 smem_u32(const void* p) {
+#ifdef __CUDA_ARCH__
+    return (u32)__cvta_generic_to_shared(p);
+#else
+    return 0u;
+#endif
+}
+static __device__ __forceinline__ void mbar_init(u64* m) {
+#ifdef __CUDA_ARCH__
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(m)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+#endif
+}
+static __device__ __forceinline__ void mbar_expect_tx(u64* m, u32 bytes) {
+#ifdef __CUDA_ARCH__
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes) : "memory");
+#endif
+}
+static __device__ __forceinline__ void mbar_wait(u64* m, u32 phase) {
+#ifdef __CUDA_ARCH__
+    asm volatile("{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}"
+                 ::"r"(smem_u32(m)), "r"(phase) : "memory");
+#else
+    __syncthreads();  // host replay: the synchronous copies are done once every thread is here
+#endif
+}
+static __device__ __forceinline__ void fence_async() {
+#ifdef __CUDA_ARCH__
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
+}
+static __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, u32 bytes, u64* m) {
+#ifdef __CUDA_ARCH__
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(m)) : "memory");
+#else
+    memcpy(dst, src, bytes);
+#endif
+}
 // TMA-engine prefetch of a contiguous row into L2 (no registers, no smem).
 static __device__ __forceinline__ void pf_l2(const void* p, u32 bytes) {
 #ifdef __CUDA_ARCH__
@@ -102,9 +144,34 @@ int smCount(int dev) {
     return n;
 }
 
+// Contiguous low tile bits (tile bit j == memory bit j): the tile's row length.
+int lowRun(const PassParams& P) {
+    int L = 0;
+    while (L < P.ct && P.tile_phys[L] == L) L++;
+    return L;
+}
+
+// TMA-pipelined form (QK_JIT_TMA, default on): a persistent CTA per SM keeps
+// the NEXT tile streaming into a 128 KB shared-memory buffer (cp.async.bulk
+// rows, mbarrier) while the current tile computes in registers; exchanges
+// run in two halves through a 64 KB buffer, split on a tile bit that stays in
+// the same register slot (schedule.cpp guarantees one).  Needs 2^13 tiles, 32
+// amplitudes per thread and >= 128-B rows.
+bool pipelined(const PassParams& P) {
+    static const bool on = knob("QK_JIT_TMA", 1) != 0;
+    if (!on || P.ct != 13 || P.rb != 5 || lowRun(P) < 3) return false;
+    for (int c = 1; c < P.nsegs; c++) {
+        const int k = P.xsplit[c];
+        if (k >= P.rb || P.map_out[c - 1][k] != P.map_in[c][k] || P.map_out[c - 1][k] < 3) return false;
+    }
+    return true;
+}
+constexpr int kPipeSmemAmps = (1 << 13) + (1 << 12) + qkdev::kMaxCtaFactors + 1;  // PB | XS | F | mbarrier
+
 class Gen {
 public:
-    explicit Gen(const PassParams& P) : P_(P), ct_(P.ct), rb_(P.rb), na_(1 << P.rb), nt_(1 << (P.ct - P.rb)) {
+    explicit Gen(const PassParams& P)
+        : P_(P), ct_(P.ct), rb_(P.rb), na_(1 << P.rb), nt_(1 << (P.ct - P.rb)), pipe_(pipelined(P)) {
         for (int s = 0; s < na_; s++) nm_.push_back(s);
     }
 
@@ -113,6 +180,7 @@ public:
     // by the TMA engine, so that tile's register loads hit L2 and the SM's
     // load phase overlaps its compute phase (one CTA per SM at ct = 13).
     std::string run(const std::string& name) {
+        if (pipe_) return runPipelined(name);
         const int minb = blocksPerSm(ct_, rb_);
         o_ << kPrologue;
         ctaTables();
@@ -121,7 +189,7 @@ public:
         o_ << "  extern __shared__ double2 sm[];\n  double2* const F = sm + " << (1 << ct_)
            << ";\n  const u32 tid = threadIdx.x;\n";
         o_ << "  for (u32 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {\n";
-        o_ << "  const u64 base = " << deposit("(u64)tile") << ";\n";
+        o_ << "  " << deposit("base", "(u64)tile") << "\n";
         std::string decl = "  double2 ";
         for (int s = 0; s < na_; s++) decl += (s ? ", a" : "a") + std::to_string(s);
         o_ << decl << ";\n  double2 P = C2(1.0, 0.0);\n" << pendDecl();
@@ -157,14 +225,76 @@ public:
         return o_.str();
     }
 
+    std::string runPipelined(const std::string& name) {
+        const int L = lowRun(P_);
+        o_ << kPrologue;
+        ctaTables();
+        o_ << "extern \"C\" __global__ void __launch_bounds__(" << nt_ << ",1) " << name
+           << "(double2* __restrict__ st, const double2* __restrict__ gt, const u32 ntiles, const u64 basis) {\n"
+           << "  extern __shared__ double2 sm[];  // PB: next tile (linear tile coordinates) | XS | F | mbarrier\n"
+           << "  double2* const XS = sm + 8192;\n  double2* const F = sm + 12288;\n"
+           << "  u64* const mbar = (u64*)(sm + 12352);\n  const u32 tid = threadIdx.x;\n"
+           << "  const bool tma = basis == ~0ull;\n  u32 phase = 0u;\n"
+           << "  if (tid == 0) mbar_init(mbar);\n  __syncthreads();\n"
+           << "  if (tma && blockIdx.x < ntiles) {\n";
+        issueTile("blockIdx.x", L);
+        o_ << "  }\n  for (u32 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {\n"
+           << "  " << deposit("base", "(u64)tile") << "\n";
+        std::string decl = "  double2 ";
+        for (int s = 0; s < na_; s++) decl += (s ? ", a" : "a") + std::to_string(s);
+        o_ << decl << ";\n  double2 P = C2(1.0, 0.0);\n" << pendDecl();
+        o_ << "  if (tma) {\n    mbar_wait(mbar, phase);\n    phase ^= 1u;\n    { const u32 u = "
+           << threadSmem(P_.map_in[0]) << ";\n";
+        for (int s = 0; s < na_; s++) o_ << "    a" << s << " = sm[u | " << regCoord(P_.map_in[0], s) << "u];\n";
+        o_ << "    }\n    __syncthreads();  // PB drained: stream the next tile into it\n"
+           << "    if (tile + gridDim.x < ntiles) {\n";
+        issueTile("tile + gridDim.x", L);
+        o_ << "    }\n  } else {  // first pass of a run: synthesize |basis>\n"
+           << "    const u64 off = base | " << threadGlobal(P_.map_in[0]) << ";\n";
+        for (int s = 0; s < na_; s++)
+            o_ << "    a" << s << " = C2((off | " << regGlobal(P_.map_in[0], s) << "ull) == basis ? 1.0 : 0.0, 0.0);\n";
+        o_ << "  }\n";
+        ctaFactors();
+        for (int i = 0; i < P_.nops; i++) op(P_.ops[i]);
+        const int last = P_.nsegs - 1;
+        uint64_t gx = 0;
+        for (int j = 0; j < ct_; j++)
+            if ((P_.xmask_out[last] >> j) & 1) gx |= uint64_t(1) << P_.tile_phys[j];
+        o_ << "  { const u64 off = (base | " << threadGlobal(P_.map_out[last]) << ") ^ " << gx << "ull;\n";
+        for (int s = 0; s < na_; s++)
+            o_ << "  __stcs(st + (off ^ " << regGlobal(P_.map_out[last], s) << "ull), a" << nm_[size_t(s)] << ");\n";
+        // (TMA tiles re-synchronize after draining PB; synthesized tiles must
+        // not start writing F / XS while a slow thread still reads them.)
+        o_ << "  }\n  if (!tma && tile + gridDim.x < ntiles) __syncthreads();\n  }\n}\n";
+        return o_.str();
+    }
+
 private:
+    // Warp 0 streams tile `t` into PB: one cp.async.bulk per contiguous row.
+    void issueTile(const std::string& t, int Lrun) {
+        const int L = std::min(Lrun, 8);  // rows of <= 4 KB, spread over warp 0's lanes
+        const int rows = 1 << (ct_ - L);
+        o_ << "    if (tid < 32u) {\n      " << deposit("nb", "(u64)(" + t + ")") << "\n"
+           << "      fence_async();\n      if (tid == 0u) mbar_expect_tx(mbar, " << (16u << ct_) << "u);\n"
+           << "      __syncwarp();\n      for (u32 r = tid; r < " << rows << "u; r += 32u) {\n        u64 o = nb;\n";
+        for (int j = L; j < ct_; j++)
+            o_ << "        o |= (u64)((r >> " << (j - L) << ") & 1u) << " << int(P_.tile_phys[j]) << ";\n";
+        o_ << "        bulk_g2s(sm + (r << " << L << "), st + o, " << (16u << L) << "u, mbar);\n      }\n    }\n";
+    }
+    uint32_t regCoord(const uint8_t* m, int s) const {
+        uint32_t u = 0;
+        for (int k = 0; k < rb_; k++)
+            if ((s >> k) & 1) u |= 1u << m[k];
+        return u;
+    }
     // CTA index deposited into the non-tile bits of the slice index.
-    std::string deposit(const std::string& v) const {
-        std::string e = v;
+    // Statement block declaring `u64 var` = v deposited into the non-tile bits.
+    std::string deposit(const std::string& var, const std::string& v) const {
+        std::string e = "u64 " + var + " = " + v + ";";
         for (int j = 0; j < ct_; j++) {
             const int p = P_.tile_phys[j];
-            e = "(((" + e + ") >> " + std::to_string(p) + ") << " + std::to_string(p + 1) + ") | ((" + e + ") & " +
-                std::to_string((uint64_t(1) << p) - 1) + "ull)";
+            e += " " + var + " = ((" + var + " >> " + std::to_string(p) + ") << " + std::to_string(p + 1) + ") | (" +
+                 var + " & " + std::to_string((uint64_t(1) << p) - 1) + "ull);";
         }
         return e;
     }
@@ -385,6 +515,7 @@ private:
             case qkdev::OP_EXCHANGE: {
                 const uint8_t* mo = P_.map_out[d.c - 1];
                 const uint8_t* mi = P_.map_in[d.c];
+                if (pipe_) return halfExchange(d.c, mo, mi);
                 o_ << "  __syncthreads();\n  { const u32 u = swz(" << threadSmem(mo) << ") ^ "
                    << swzHost(P_.xmask_out[d.c - 1]) << "u;\n";
                 for (int s = 0; s < na_; s++) o_ << "  sm[u ^ " << regSmem(mo, s) << "u] = " << A(s) << ";\n";
@@ -397,6 +528,45 @@ private:
             default:
                 throw SimulationError("jit: unknown op");
         }
+    }
+
+    // Exchange in two phases through the 2^12-amplitude XS buffer, split on
+    // tile bit x held by register slot k before and after.  Phase h moves the
+    // amplitudes whose (true) bit x is h; they are read back into exactly the
+    // registers that phase freed, so no value is overwritten before it is
+    // written out.  XS index = swizzled tile coordinate with bit x removed
+    // (x >= 3: the swizzle only touches bits 0..2, so banks are unchanged).
+    void halfExchange(int c, const uint8_t* mo, const uint8_t* mi) {
+        const int k = P_.xsplit[c], x = mo[k];
+        const int fx = (P_.xmask_out[c - 1] >> x) & 1;
+        const uint32_t lo = (1u << x) - 1;
+        auto cmp = [&](uint32_t v) { return (v & lo) | ((v >> (x + 1)) << x); };
+        const std::string cmpE = [&](const std::string& v) {
+            return "((" + v + ") & " + std::to_string(lo) + "u) | (((" + v + ") >> " + std::to_string(x + 1) + ") << " +
+                   std::to_string(x) + ")";
+        }("v");
+        std::vector<int> nm(nm_);
+        for (int h = 0; h < 2; h++) {
+            std::vector<int> freed;
+            o_ << "  __syncthreads();\n  { const u32 v = swz(" << threadSmem(mo) << ") ^ " << swzHost(P_.xmask_out[c - 1])
+               << "u; const u32 u = " << cmpE << ";\n";
+            for (int s = 0; s < na_; s++)
+                if ((((s >> k) & 1) ^ fx) == h) {
+                    o_ << "  XS[u ^ " << cmp(regSmem(mo, s)) << "u] = a" << nm_[size_t(s)] << ";\n";
+                    freed.push_back(nm_[size_t(s)]);
+                }
+            std::sort(freed.begin(), freed.end());
+            o_ << "  }\n  __syncthreads();\n  { const u32 v = swz(" << threadSmem(mi) << "); const u32 u = " << cmpE
+               << ";\n";
+            size_t f = 0;
+            for (int s = 0; s < na_; s++)
+                if (((s >> k) & 1) == h) {
+                    nm[size_t(s)] = freed[f++];
+                    o_ << "  a" << nm[size_t(s)] << " = XS[u ^ " << cmp(regSmem(mi, s)) << "u];\n";
+                }
+            o_ << "  }\n";
+        }
+        nm_ = nm;
     }
 
     // a[s] *= scale * P * prod_{k: bit k of s} R[k], touching only dirty factors.
@@ -430,6 +600,7 @@ private:
 
     const PassParams& P_;
     int ct_, rb_, na_, nt_;
+    bool pipe_;
     std::vector<int> nm_;
     bool dirtyP_ = false;
     bool dirtyR_[qkdev::kMaxRegBits] = {};
@@ -439,10 +610,11 @@ private:
 // ---- compile / load / launch -------------------------------------------------
 
 // Bump when the generated code changes for the same PassParams (on-disk cache key).
-constexpr uint64_t kGeneratorVersion = 5;
+constexpr uint64_t kGeneratorVersion = 6;
 
 uint64_t hashPass(const PassParams& P) {
-    uint64_t h = 1469598103934665603ull ^ (kGeneratorVersion * 0x9E3779B97F4A7C15ull) ^ (usePrefetch() ? 1u : 0u) ^ (usePersistent() ? 2u : 0u);
+    uint64_t h = 1469598103934665603ull ^ (kGeneratorVersion * 0x9E3779B97F4A7C15ull) ^ (usePrefetch() ? 1u : 0u) ^ (usePersistent() ? 2u : 0u) ^
+                 (knob("QK_JIT_TMA", 1) ? 4u : 0u);
     const unsigned char* p = reinterpret_cast<const unsigned char*>(&P);
     for (size_t i = 0; i < sizeof(PassParams); i++) {
         h ^= p[i];
@@ -525,7 +697,8 @@ void* functionFor(const PassParams& P, uint64_t h, int device) {
     void* fn = nullptr;
     if (d.moduleLoadData(&mod, e.cubin.data()) != 0) throw SimulationError("jit: cuModuleLoadData failed");
     if (d.moduleGetFunction(&fn, mod, kernelName(h).c_str()) != 0) throw SimulationError("jit: cuModuleGetFunction failed");
-    const int smem = int((sizeof(double2) << P.ct) + sizeof(double2) * qkdev::kMaxCtaFactors);
+    const int smem = pipelined(P) ? int(sizeof(double2) * kPipeSmemAmps)
+                                  : int((sizeof(double2) << P.ct) + sizeof(double2) * qkdev::kMaxCtaFactors);
     if (smem > 48 * 1024 && d.funcSetAttribute(fn, 8 /*CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES*/, smem) != 0)
         throw SimulationError("jit: cuFuncSetAttribute failed");
     e.func[device] = fn;
@@ -614,9 +787,11 @@ cudaError_t launch(const PassParams& P, double2* state, const double2* gtab, int
     void* fn = functionFor(P, hashPass(P), dev);
     unsigned ntiles = unsigned(uint64_t(1) << (nLocal - P.ct));
     const unsigned resident = unsigned(smCount(dev) * blocksPerSm(P.ct, P.rb));
-    const unsigned ctas = (ntiles < resident || !usePersistent()) ? ntiles : resident;
+    const bool pipe = pipelined(P);
+    const unsigned ctas = (ntiles < resident || !(usePersistent() || pipe)) ? ntiles : resident;
     const unsigned nt = 1u << (P.ct - P.rb);
-    const unsigned smem = unsigned((sizeof(double2) << P.ct) + sizeof(double2) * qkdev::kMaxCtaFactors);
+    const unsigned smem = pipe ? unsigned(sizeof(double2) * kPipeSmemAmps)
+                               : unsigned((sizeof(double2) << P.ct) + sizeof(double2) * qkdev::kMaxCtaFactors);
     void* args[] = {&state, &gtab, &ntiles, &basis};
     if (driver().launchKernel(fn, ctas, 1, 1, nt, 1, 1, smem, stream, args, nullptr) != 0)
         return cudaErrorLaunchFailure;

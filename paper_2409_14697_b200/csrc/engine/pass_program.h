@@ -98,6 +98,8 @@ struct PassParams {
     int8_t tile_phys[16];             // physical bit of tile bit j (ascending)
     uint16_t seg_end[kMaxSegs];       // ops [seg_end[s-1], seg_end[s]) run in segment s
     uint16_t xmask_out[kMaxSegs];     // tile-index XOR of the data at segment end (X gates are relabels)
+    uint8_t xsplit[kMaxSegs];         // exchange into segment c: register slot holding the same tile bit (>= 3)
+                                      // before and after (255: none) -> two half-tile exchange phases
     uint8_t map_in[kMaxSegs][16];     // mapping at segment start (load / exchange-read)
     uint8_t map_out[kMaxSegs][16];    // mapping at segment end (exchange-write / store)
     DevOp ops[kMaxOps];

@@ -10,6 +10,7 @@
 //   k_set_basis    initState (engine.cpp:18-28) after a memset
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 namespace qkdev {
 
@@ -316,9 +317,24 @@ static bool imsTileSpec(int logN, const int* outs, const int* ins, int s, ImsTil
     return true;
 }
 
+// QK_IMS_TILED: 0 = always the per-element kernel, 1 = tiled whenever
+// possible, 2 (default) = tiled only when a pair has an out bit < 3 (the case
+// where per-element access wastes sectors).
+static int imsMode() {
+    static const int v = [] {
+        const char* e = std::getenv("QK_IMS_TILED");
+        return e ? std::atoi(e) : 2;
+    }();
+    return v;
+}
+
 cudaError_t launchIms(double2* a, int logN, const int* outs, const int* ins, int s, cudaStream_t st) {
     ImsTileSpec sp;
-    if (!imsTileSpec(logN, outs, ins, s, sp)) return launchImsGeneric(a, logN, outs, ins, s, st);
+    bool lowPair = false;
+    for (int j = 0; j < s; j++) lowPair |= outs[j] < 3 || ins[j] < 3;
+    const int mode = imsMode();
+    if (mode == 0 || (mode == 2 && !lowPair) || !imsTileSpec(logN, outs, ins, s, sp))
+        return launchImsGeneric(a, logN, outs, ins, s, st);
     const uint64_t groups = uint64_t(1) << sp.nfree;
     uint64_t ctas = (groups + 7) / 8;
     if (ctas > 148u * 32u) ctas = 148u * 32u;

@@ -192,7 +192,7 @@ public:
                 flushAll();
                 closeSegment();
                 seg_++;
-                chooseMap(i);
+                chooseMap(i, &P_->xsplit[seg_]);
                 std::memcpy(P_->map_in[seg_], map_, sizeof map_);
                 emit(OP_EXCHANGE, 0, 0, 0, uint32_t(seg_));
             }
@@ -240,14 +240,21 @@ private:
     }
 
     // Choose which tile bits occupy the register slots from gate i onward.
-    void chooseMap(size_t i) {
+    // For an exchange (`split` != nullptr) one register slot keeps its tile
+    // bit (tile index >= 3) across it: the exchange can then run in two
+    // halves split on that bit, through a half-tile shared-memory buffer.
+    void chooseMap(size_t i, uint8_t* split = nullptr) {
+        int prev[kMaxRegBits];
+        for (int s = 0; s < rb_; s++) prev[s] = map_[s];
         int slotBit[kMaxRegBits];
+        bool fixedSlot[kMaxRegBits] = {};
         std::fill(slotBit, slotBit + kMaxRegBits, -1);
         std::vector<int> regs;  // tile bits at time i
         if (i < tg_.size() && denseInRegs(tg_[i], rb_)) {
             const Gate& g = tg_[i];
             const int k = int(g.targets.size());
             for (int j = 0; j < k; j++) slotBit[k - 1 - j] = g.targets[size_t(j)];
+            for (int j = 0; j < k; j++) fixedSlot[k - 1 - j] = true;
             for (int j = 0; j < k; j++) regs.push_back(g.targets[size_t(j)]);
         }
         // Look ahead: add needed bits in order of first use while they fit.
@@ -289,6 +296,29 @@ private:
             if (slotBit[s] >= 0) continue;
             while (r < regs.size() && taken(regs[r])) r++;
             slotBit[s] = regs[r++];
+        }
+        if (split) {
+            std::vector<char> must(static_cast<size_t>(ct_), 0);  // needed by gate i itself
+            if (i < tg_.size())
+                for (int b : regNeeds(tg_[i], orig_[i])) must[size_t(b)] = 1;
+            int common = -1;
+            for (int s = 0; s < rb_ && common < 0; s++)
+                if (slotBit[s] == prev[s] && prev[s] >= 3) common = s;
+            for (int s = 0; s < rb_ && common < 0; s++) {  // an old register bit moved slots: move it back
+                if (prev[s] < 3 || fixedSlot[s]) continue;
+                for (int s2 = 0; s2 < rb_; s2++)
+                    if (slotBit[s2] == prev[s] && !fixedSlot[s2]) {
+                        std::swap(slotBit[s], slotBit[s2]);
+                        common = s;
+                        break;
+                    }
+            }
+            for (int s = 0; s < rb_ && common < 0; s++)  // keep an old register bit instead of a spare new one
+                if (!fixedSlot[s] && prev[s] >= 3 && !taken(prev[s]) && !must[size_t(slotBit[s])]) {
+                    slotBit[s] = prev[s];
+                    common = s;
+                }
+            *split = uint8_t(common < 0 ? 255 : common);
         }
         // Thread bits ascending; lane bits 0..2 with distinct residues mod 3
         // (conflict-free swizzled exchange).

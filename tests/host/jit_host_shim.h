@@ -5,6 +5,7 @@
 #pragma once
 #include <barrier>
 #include <cmath>
+#include <cstring>
 #include <cstdint>
 #include <thread>
 #include <vector>
@@ -23,6 +24,7 @@ inline unsigned qk_grid = 1;
 #define gridDim (QkDim3{qk_grid})
 inline std::barrier<>* qk_bar = nullptr;
 static inline void __syncthreads() { qk_bar->arrive_and_wait(); }
+static inline void __syncwarp() {}
 template <class T>
 static inline T __ldcs(const T* p) { return *p; }
 template <class T>
@@ -36,12 +38,12 @@ static inline void __stcs(T* p, T v) { *p = v; }
 #define __restrict__
 #define __shared__
 // `extern __shared__ double2 sm[];` in the kernel binds to this array.
-extern "C" double2 sm[(1 << 13) + 64];
+extern "C" double2 sm[1 << 14];
 
 // Launch: a persistent grid of min(ntiles, 3) CTAs run one after another
 // (each walks its tiles), nt threads each.
 #define QK_HOST_LAUNCHER(KERNEL)                                                              \
-    double2 sm[(1 << 13) + 64];                                                               \
+    double2 sm[1 << 14];                                                                      \
     extern "C" void qk_host_launch(double2* st, const double2* gt, int nLocal, int ct, int rb,    \
                                    unsigned long long basis) {                              \
         const unsigned ntiles = 1u << (nLocal - ct), nt = 1u << (ct - rb);                   \

@@ -30,3 +30,13 @@ def test_specialized_kernels_on_host(ref, qk, port, kind, n, chunk, fusion, diag
     st = np.full(1 << n, np.nan, dtype=np.complex128)
     run_program_jit(qk, port, prog, n, st, basis=5)
     assert np.max(np.abs(st - want.view(np.complex128))) < 1e-10
+
+
+def test_qft_passes_use_the_tma_pipeline(qk):
+    # 2^13 tiles with >= 128-B rows run as persistent TMA-pipelined kernels
+    # (next tile streamed into shared memory, half-buffer exchanges).
+    n = 18
+    prog = qk.Program.optimize(qk.generate("qft", n), qk.Config.make(n, 0, chunk=13, fusion=0, diag=0))
+    srcs = prog.debug_jit_sources()
+    assert srcs and all("mbar_wait(mbar, phase)" in src for _, src in srcs)
+    assert all(len(src) < 200_000 for _, src in srcs)  # linear-size code generation
