@@ -320,14 +320,18 @@ __global__ void __launch_bounds__(1 << (CT - RB), MINB)
 
     // Per-CTA diagonal factors (functions of the non-tile bits of `base`).
     double2* F = sm + (1 << CT);
-    if (P.ncta) {
-        for (int f = int(tid); f < P.ncta; f += NT) {
+    if (P.ncta) {  // warp per factor, lanes over its terms, shuffle-tree product
+        const int w = int(tid >> 5), l = int(tid & 31u);
+        for (int f = w; f < P.ncta; f += (NT + 31) / 32) {
             double2 acc = make_double2(1.0, 0.0);
-            for (int t = f ? P.cta_end[f - 1] : 0; t < P.cta_end[f]; t++) {
+            for (int t = (f ? P.cta_end[f - 1] : 0) + l; t < P.cta_end[f]; t += 32) {
                 const CtaTerm& ct = P.cta_terms[t];
                 if (ct.b1 == 255 || ((base >> ct.b1) & (base >> ct.b2) & 1u)) acc = cmul(acc, coefAt(P, ct.c));
             }
-            F[f] = acc;
+            const unsigned mask = NT >= 32 ? 0xffffffffu : ((1u << NT) - 1u);
+            for (int o = (NT >= 32 ? 16 : NT / 2); o > 0; o >>= 1)
+                acc = cmul(acc, make_double2(__shfl_xor_sync(mask, acc.x, o), __shfl_xor_sync(mask, acc.y, o)));
+            if (l == 0) F[f] = acc;
         }
         __syncthreads();
     }

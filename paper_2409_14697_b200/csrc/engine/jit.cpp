@@ -151,14 +151,15 @@ int lowRun(const PassParams& P) {
     return L;
 }
 
-// TMA-pipelined form (QK_JIT_TMA, default on): a persistent CTA per SM keeps
+// TMA-pipelined form (QK_JIT_TMA=1; off by default: issuing one bulk copy per
+// <= 4 KB row costs more than the overlap gains on B200): a persistent CTA per SM keeps
 // the NEXT tile streaming into a 128 KB shared-memory buffer (cp.async.bulk
 // rows, mbarrier) while the current tile computes in registers; exchanges
 // run in two halves through a 64 KB buffer, split on a tile bit that stays in
 // the same register slot (schedule.cpp guarantees one).  Needs 2^13 tiles, 32
 // amplitudes per thread and >= 128-B rows.
 bool pipelined(const PassParams& P) {
-    static const bool on = knob("QK_JIT_TMA", 1) != 0;
+    static const bool on = qkdev::halfExchanges();
     if (!on || P.ct != 13 || P.rb != 5 || lowRun(P) < 3) return false;
     for (int c = 1; c < P.nsegs; c++) {
         const int k = P.xsplit[c];
@@ -331,13 +332,21 @@ private:
         for (int f = 0; f < P_.ncta; f++) o_ << (f ? "," : "") << P_.cta_end[f];
         o_ << "};\n";
     }
+    // Warp w computes factors w, w + #warps, ...: its lanes take the terms in
+    // turn and the partial products meet in a shuffle tree.
     void ctaFactors() {
         if (!P_.ncta) return;
-        o_ << "  if (tid < " << P_.ncta << "u) {\n    double2 acc = C2(1.0, 0.0);\n"
-           << "    for (u32 t = tid ? qk_te[tid - 1] : 0u; t < qk_te[tid]; t++) {\n"
-           << "      const u32 b1 = qk_tb[2 * t], b2 = qk_tb[2 * t + 1];\n"
-           << "      if (b1 == 255u || ((base >> b1) & (base >> b2) & 1ull)) acc = cmul(acc, qk_tv[t]);\n"
-           << "    }\n    F[tid] = acc;\n  }\n  __syncthreads();\n";
+        o_ << "  { const u32 w = tid >> 5, l = tid & 31u;\n"
+           << "    for (u32 f = w; f < " << P_.ncta << "u; f += " << (nt_ / 32) << "u) {\n"
+           << "      double2 acc = C2(1.0, 0.0);\n"
+           << "      for (u32 t = (f ? qk_te[f - 1] : 0u) + l; t < qk_te[f]; t += 32u) {\n"
+           << "        const u32 b1 = qk_tb[2 * t], b2 = qk_tb[2 * t + 1];\n"
+           << "        if (b1 == 255u || ((base >> b1) & (base >> b2) & 1ull)) acc = cmul(acc, qk_tv[t]);\n"
+           << "      }\n"
+           << "      for (int o = 16; o > 0; o >>= 1)\n"
+           << "        acc = cmul(acc, make_double2(__shfl_xor_sync(0xffffffffu, acc.x, o), "
+              "__shfl_xor_sync(0xffffffffu, acc.y, o)));\n"
+           << "      if (l == 0u) F[f] = acc;\n    }\n  }\n  __syncthreads();\n";
     }
     std::string pendDecl() {
         std::string d;
@@ -610,11 +619,11 @@ private:
 // ---- compile / load / launch -------------------------------------------------
 
 // Bump when the generated code changes for the same PassParams (on-disk cache key).
-constexpr uint64_t kGeneratorVersion = 6;
+constexpr uint64_t kGeneratorVersion = 7;
 
 uint64_t hashPass(const PassParams& P) {
     uint64_t h = 1469598103934665603ull ^ (kGeneratorVersion * 0x9E3779B97F4A7C15ull) ^ (usePrefetch() ? 1u : 0u) ^ (usePersistent() ? 2u : 0u) ^
-                 (knob("QK_JIT_TMA", 1) ? 4u : 0u);
+                 (qkdev::halfExchanges() ? 4u : 0u);
     const unsigned char* p = reinterpret_cast<const unsigned char*>(&P);
     for (size_t i = 0; i < sizeof(PassParams); i++) {
         h ^= p[i];

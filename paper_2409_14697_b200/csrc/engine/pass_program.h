@@ -46,6 +46,7 @@ constexpr int kMaxCtaTerms = 320;
 // QK_RB13 = 4|5 register bits at ct = 13 (default 5).
 int maxTileBits();
 int regBitsFor(int ct);
+bool halfExchanges();
 
 enum OpType : uint8_t {
     OP_MAT1 = 0,      // a = slot; coef[c..c+3] = 2x2 row-major

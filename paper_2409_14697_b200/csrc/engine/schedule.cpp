@@ -43,6 +43,13 @@ int maxTileBits() {
     return v;
 }
 
+// QK_JIT_TMA=1: specialized kernels stream the next tile through shared
+// memory, so exchanges must be splittable into halves (see chooseMap).
+bool halfExchanges() {
+    static const bool v = envInt("QK_JIT_TMA", 0, 0, 1) != 0;
+    return v;
+}
+
 int regBitsFor(int ct) {
     static const int rb13 = envInt("QK_RB13", 5, 4, 5);
     return ct >= 13 ? rb13 : (ct < 4 ? ct : 4);
@@ -192,7 +199,8 @@ public:
                 flushAll();
                 closeSegment();
                 seg_++;
-                chooseMap(i, &P_->xsplit[seg_]);
+                chooseMap(i, halfExchanges() ? &P_->xsplit[seg_] : nullptr);
+                if (!halfExchanges()) P_->xsplit[seg_] = 255;
                 std::memcpy(P_->map_in[seg_], map_, sizeof map_);
                 emit(OP_EXCHANGE, 0, 0, 0, uint32_t(seg_));
             }

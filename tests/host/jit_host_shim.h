@@ -6,6 +6,7 @@
 #include <barrier>
 #include <cmath>
 #include <cstring>
+#include <memory>
 #include <cstdint>
 #include <thread>
 #include <vector>
@@ -25,6 +26,21 @@ inline unsigned qk_grid = 1;
 inline std::barrier<>* qk_bar = nullptr;
 static inline void __syncthreads() { qk_bar->arrive_and_wait(); }
 static inline void __syncwarp() {}
+// Warp shuffles: per-warp exchange slots + a 32-thread barrier.
+struct QkWarp {
+    std::barrier<>* bar;
+    double buf[32];
+};
+inline QkWarp* qk_warps = nullptr;
+static inline double __shfl_xor_sync(unsigned, double v, int o) {
+    QkWarp& w = qk_warps[qk_tl_tid >> 5];
+    const unsigned l = qk_tl_tid & 31u;
+    w.buf[l] = v;
+    w.bar->arrive_and_wait();
+    const double r = w.buf[l ^ unsigned(o)];
+    w.bar->arrive_and_wait();
+    return r;
+}
 template <class T>
 static inline T __ldcs(const T* p) { return *p; }
 template <class T>
@@ -51,6 +67,13 @@ extern "C" double2 sm[1 << 14];
         for (unsigned b = 0; b < qk_grid; b++) {                                              \
             std::barrier<> bar(nt);                                                           \
             qk_bar = &bar;                                                                    \
+            std::vector<std::unique_ptr<std::barrier<>>> wbars;                               \
+            std::vector<QkWarp> warps(nt / 32 + 1);                                           \
+            for (unsigned w = 0; w < nt / 32 + 1; w++) {                                      \
+                wbars.push_back(std::make_unique<std::barrier<>>(nt >= 32 ? 32 : nt));        \
+                warps[w].bar = wbars.back().get();                                            \
+            }                                                                                 \
+            qk_warps = warps.data();                                                          \
             std::vector<std::thread> ts;                                                      \
             for (unsigned t = 0; t < nt; t++)                                                 \
                 ts.emplace_back([=] {                                                         \
