@@ -63,6 +63,21 @@ static __device__ __forceinline__ double2 csel(bool c, double2 x, double2 y) {
     return make_double2(c ? x.x : y.x, c ? x.y : y.y);
 }
 static __device__ __forceinline__ u32 swz(u32 u) { return u ^ (((u >> 3) ^ (u >> 6) ^ (u >> 9) ^ (u >> 12)) & 7u); }
+// 256-bit global accesses (two neighbouring amplitudes), sm_100.
+static __device__ __forceinline__ void ld256(const double2* p, double2& lo, double2& hi) {
+#ifdef __CUDA_ARCH__
+    asm volatile("ld.global.cs.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(lo.x), "=d"(lo.y), "=d"(hi.x), "=d"(hi.y) : "l"(p));
+#else
+    lo = p[0]; hi = p[1];
+#endif
+}
+static __device__ __forceinline__ void st256(double2* p, const double2& lo, const double2& hi) {
+#ifdef __CUDA_ARCH__
+    asm volatile("st.global.cs.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(lo.x), "d"(lo.y), "d"(hi.x), "d"(hi.y) : "memory");
+#else
+    p[0] = lo; p[1] = hi;
+#endif
+}
 // TMA bulk copies into shared memory, tracked by an mbarrier (host builds of
 // the generated source, tests/host/jit_host_shim.h, copy synchronously).
 static __device__ __forceinline__ u32 smem_u32(const void* p) {
@@ -196,8 +211,16 @@ public:
         o_ << decl << ";\n  double2 P = C2(1.0, 0.0);\n" << pendDecl();
         // load (map_in[0], no flips)
         o_ << "  { const u64 off = base | " << threadGlobal(P_.map_in[0]) << ";\n  if (basis == ~0ull) {\n";
-        for (int s = 0; s < na_; s++)
+        const int kl = slotOfMem0(P_.map_in[0]);
+        for (int s = 0; s < na_; s++) {
+            if (kl >= 0) {  // neighbours (slot kl = 0 / 1) in one 256-bit load
+                if (!((s >> kl) & 1))
+                    o_ << "  ld256(st + (off | " << regGlobal(P_.map_in[0], s) << "ull), a" << s << ", a" << (s | (1 << kl))
+                       << ");\n";
+                continue;
+            }
             o_ << "  a" << s << " = __ldcs(st + (off | " << regGlobal(P_.map_in[0], s) << "ull));\n";
+        }
         o_ << "  } else {  // first pass of a run: synthesize |basis> instead of reading it\n";
         for (int s = 0; s < na_; s++)
             o_ << "  a" << s << " = C2((off | " << regGlobal(P_.map_in[0], s) << "ull) == basis ? 1.0 : 0.0, 0.0);\n";
@@ -217,8 +240,18 @@ public:
         if (P_.nsegs == 1 && (std::memcmp(P_.map_in[0], P_.map_out[0], sizeof P_.map_in[0]) != 0 || P_.xmask_out[0]))
             o_ << "  __syncthreads();\n";
         o_ << "  { const u64 off = (base | " << threadGlobal(P_.map_out[last]) << ") ^ " << gx << "ull;\n";
-        for (int s = 0; s < na_; s++)
+        const int ks = slotOfMem0(P_.map_out[last]);
+        for (int s = 0; s < na_; s++) {
+            if (ks >= 0) {  // slot ks stores memory bit 0: neighbours in one 256-bit store
+                if ((s >> ks) & 1) continue;
+                const int s1 = s | (1 << ks);
+                const bool swap = gx & 1;  // memory bit 0 flipped: slot value 0 lands on the odd address
+                o_ << "  st256(st + ((off ^ " << regGlobal(P_.map_out[last], s) << "ull) & ~1ull), a"
+                   << nm_[size_t(swap ? s1 : s)] << ", a" << nm_[size_t(swap ? s : s1)] << ");\n";
+                continue;
+            }
             o_ << "  __stcs(st + (off ^ " << regGlobal(P_.map_out[last], s) << "ull), a" << nm_[size_t(s)] << ");\n";
+        }
         o_ << "  }\n";
         // The next iteration's first shared-memory write must not overtake a
         // slow thread still reading this tile's last exchange.
@@ -281,6 +314,13 @@ private:
         for (int j = L; j < ct_; j++)
             o_ << "        o |= (u64)((r >> " << (j - L) << ") & 1u) << " << int(P_.tile_phys[j]) << ";\n";
         o_ << "        bulk_g2s(sm + (r << " << L << "), st + o, " << (16u << L) << "u, mbar);\n      }\n    }\n";
+    }
+    // Register slot whose tile bit is memory bit 0 (-1: none / wide access off).
+    int slotOfMem0(const uint8_t* m) const {
+        if (!qkdev::wideAccess() || P_.tile_phys[0] != 0) return -1;
+        for (int k = 0; k < rb_; k++)
+            if (m[k] == 0) return k;
+        return -1;
     }
     uint32_t regCoord(const uint8_t* m, int s) const {
         uint32_t u = 0;
@@ -619,7 +659,7 @@ private:
 // ---- compile / load / launch -------------------------------------------------
 
 // Bump when the generated code changes for the same PassParams (on-disk cache key).
-constexpr uint64_t kGeneratorVersion = 7;
+constexpr uint64_t kGeneratorVersion = 8;
 
 uint64_t hashPass(const PassParams& P) {
     uint64_t h = 1469598103934665603ull ^ (kGeneratorVersion * 0x9E3779B97F4A7C15ull) ^ (usePrefetch() ? 1u : 0u) ^ (usePersistent() ? 2u : 0u) ^

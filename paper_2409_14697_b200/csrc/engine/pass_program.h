@@ -47,6 +47,7 @@ constexpr int kMaxCtaTerms = 320;
 int maxTileBits();
 int regBitsFor(int ct);
 bool halfExchanges();
+bool wideAccess();
 
 enum OpType : uint8_t {
     OP_MAT1 = 0,      // a = slot; coef[c..c+3] = 2x2 row-major

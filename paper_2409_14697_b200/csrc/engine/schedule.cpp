@@ -45,6 +45,13 @@ int maxTileBits() {
 
 // QK_JIT_TMA=1: specialized kernels stream the next tile through shared
 // memory, so exchanges must be splittable into halves (see chooseMap).
+// QK_WIDE_ACCESS (default 1): first segments hold memory bit 0 in a register
+// slot so tile loads / stores are 256-bit (LDG.256 / STG.256, sm_100).
+bool wideAccess() {
+    static const bool v = envInt("QK_WIDE_ACCESS", 1, 0, 1) != 0;
+    return v;
+}
+
 bool halfExchanges() {
     static const bool v = envInt("QK_JIT_TMA", 0, 0, 1) != 0;
     return v;
@@ -184,7 +191,7 @@ public:
         std::fill(pendSlot_, pendSlot_ + kMaxRegBits, false);
         flips_ = 0;
         batchReset();
-        chooseMap(i);
+        chooseMap(i, nullptr, wideAccess() && tilePhys_[0] == 0);
         std::memcpy(P_->map_in[0], map_, sizeof map_);
 
         const size_t first = i;
@@ -251,7 +258,9 @@ private:
     // For an exchange (`split` != nullptr) one register slot keeps its tile
     // bit (tile index >= 3) across it: the exchange can then run in two
     // halves split on that bit, through a half-tile shared-memory buffer.
-    void chooseMap(size_t i, uint8_t* split = nullptr) {
+    // wantBit0: hold tile bit 0 (= memory bit 0) in a register slot, so each
+    // thread's amplitudes pair up into 32-B neighbours (one 256-bit load each).
+    void chooseMap(size_t i, uint8_t* split = nullptr, bool wantBit0 = false) {
         int prev[kMaxRegBits];
         for (int s = 0; s < rb_; s++) prev[s] = map_[s];
         int slotBit[kMaxRegBits];
@@ -287,6 +296,20 @@ private:
             for (int b : need) {
                 inSet[size_t(b)] = 1;
                 regs.push_back(origin[size_t(b)]);
+            }
+        }
+        if (wantBit0 && std::find(regs.begin(), regs.end(), 0) == regs.end()) {
+            if (int(regs.size()) < rb_) {
+                regs.push_back(0);
+            } else {
+                std::vector<char> must(static_cast<size_t>(ct_), 0);
+                if (i < tg_.size())
+                    for (int b : regNeeds(tg_[i], orig_[i])) must[size_t(b)] = 1;
+                for (size_t j = regs.size(); j-- > 0;)
+                    if (!must[size_t(regs[j])] && std::find(slotBit, slotBit + rb_, regs[j]) == slotBit + rb_) {
+                        regs[j] = 0;
+                        break;
+                    }
             }
         }
         // Fill with the highest remaining tile bits (keeps low bits in lanes).
