@@ -32,6 +32,8 @@ using qkdev::DevOp;
 using qkdev::PassParams;
 using quokka::SimulationError;
 
+bool nvrtcSupportsWideAccess();  // NVRTC >= 12.9 (sm_100 256-bit accesses)
+
 namespace {
 
 std::string lit(double v) {
@@ -317,7 +319,7 @@ private:
     }
     // Register slot whose tile bit is memory bit 0 (-1: none / wide access off).
     int slotOfMem0(const uint8_t* m) const {
-        if (!qkdev::wideAccess() || P_.tile_phys[0] != 0) return -1;
+        if (!qkdev::wideAccess() || !nvrtcSupportsWideAccess() || P_.tile_phys[0] != 0) return -1;
         for (int k = 0; k < rb_; k++)
             if (m[k] == 0) return k;
         return -1;
@@ -659,7 +661,7 @@ private:
 // ---- compile / load / launch -------------------------------------------------
 
 // Bump when the generated code changes for the same PassParams (on-disk cache key).
-constexpr uint64_t kGeneratorVersion = 8;
+constexpr uint64_t kGeneratorVersion = 9;
 
 uint64_t hashPass(const PassParams& P) {
     uint64_t h = 1469598103934665603ull ^ (kGeneratorVersion * 0x9E3779B97F4A7C15ull) ^ (usePrefetch() ? 1u : 0u) ^ (usePersistent() ? 2u : 0u) ^
@@ -758,26 +760,81 @@ void* functionFor(const PassParams& P, uint64_t h, int device) {
 
 std::string generatePassSource(const PassParams& P, const std::string& name) { return Gen(P).run(name); }
 
+namespace {
+// NVRTC, loaded by absolute path with RTLD_LOCAL: a process that imported
+// torch first already has torch's own libnvrtc.so.12 (an older 12.x) under the
+// same soname, whose ptxas rejects sm_100 256-bit accesses.  QK_NVRTC_PATH
+// overrides the path.
+struct Nvrtc {
+    nvrtcResult (*create)(nvrtcProgram*, const char*, const char*, int, const char* const*, const char* const*) = nullptr;
+    nvrtcResult (*compile)(nvrtcProgram, int, const char* const*) = nullptr;
+    nvrtcResult (*logSize)(nvrtcProgram, size_t*) = nullptr;
+    nvrtcResult (*getLog)(nvrtcProgram, char*) = nullptr;
+    nvrtcResult (*cubinSize)(nvrtcProgram, size_t*) = nullptr;
+    nvrtcResult (*getCubin)(nvrtcProgram, char*) = nullptr;
+    nvrtcResult (*destroy)(nvrtcProgram*) = nullptr;
+    nvrtcResult (*version)(int*, int*) = nullptr;
+    int major = 0, minor = 0;
+    Nvrtc() {
+        const char* env = std::getenv("QK_NVRTC_PATH");
+        const char* paths[] = {env, "/usr/local/cuda/lib64/libnvrtc.so.12", "libnvrtc.so.12"};
+        for (const char* path : paths) {
+            if (!path) continue;
+            void* h = dlopen(path, RTLD_NOW | RTLD_LOCAL);
+            if (!h) continue;
+            create = reinterpret_cast<decltype(create)>(dlsym(h, "nvrtcCreateProgram"));
+            compile = reinterpret_cast<decltype(compile)>(dlsym(h, "nvrtcCompileProgram"));
+            logSize = reinterpret_cast<decltype(logSize)>(dlsym(h, "nvrtcGetProgramLogSize"));
+            getLog = reinterpret_cast<decltype(getLog)>(dlsym(h, "nvrtcGetProgramLog"));
+            cubinSize = reinterpret_cast<decltype(cubinSize)>(dlsym(h, "nvrtcGetCUBINSize"));
+            getCubin = reinterpret_cast<decltype(getCubin)>(dlsym(h, "nvrtcGetCUBIN"));
+            destroy = reinterpret_cast<decltype(destroy)>(dlsym(h, "nvrtcDestroyProgram"));
+            version = reinterpret_cast<decltype(version)>(dlsym(h, "nvrtcVersion"));
+            if (create && compile && logSize && getLog && cubinSize && getCubin && destroy && version) {
+                version(&major, &minor);
+                return;
+            }
+        }
+        create = nullptr;
+    }
+};
+Nvrtc& nvrtc() {
+    static Nvrtc n;
+    return n;
+}
+}  // namespace
+
+bool nvrtcSupportsWideAccess() {
+    const Nvrtc& n = nvrtc();
+    return n.create && (n.major > 12 || (n.major == 12 && n.minor >= 9));
+}
+
 std::vector<char> compileToCubin(const std::string& src, const std::string& name) {
+    Nvrtc& N = nvrtc();
+    if (!N.create) throw SimulationError("jit: libnvrtc.so.12 not found (set QK_NVRTC_PATH)");
     nvrtcProgram prog;
-    if (nvrtcCreateProgram(&prog, src.c_str(), (name + ".cu").c_str(), 0, nullptr, nullptr) != NVRTC_SUCCESS)
+    if (N.create(&prog, src.c_str(), (name + ".cu").c_str(), 0, nullptr, nullptr) != NVRTC_SUCCESS)
         throw SimulationError("jit: nvrtcCreateProgram failed");
     const char* opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-default-device", "-lineinfo",
-                          "-I/usr/local/cuda/include"};
-    const nvrtcResult r = nvrtcCompileProgram(prog, 5, opts);
+                          "-I/usr/local/cuda/include", "-diag-suppress=177"};
+    const nvrtcResult r = N.compile(prog, 6, opts);
     if (r != NVRTC_SUCCESS) {
         size_t n = 0;
-        nvrtcGetProgramLogSize(prog, &n);
+        N.logSize(prog, &n);
         std::string log(n, '\0');
-        nvrtcGetProgramLog(prog, &log[0]);
-        nvrtcDestroyProgram(&prog);
-        throw SimulationError("jit: NVRTC failed: " + log.substr(0, 2000));
+        N.getLog(prog, &log[0]);
+        N.destroy(&prog);
+        std::string errs;  // error lines first (warnings can be long)
+        std::istringstream ls(log);
+        for (std::string line; std::getline(ls, line);)
+            if (line.find("error") != std::string::npos) errs += line + "\n";
+        throw SimulationError("jit: NVRTC failed: " + (errs + log).substr(0, 3000));
     }
     size_t n = 0;
-    nvrtcGetCUBINSize(prog, &n);
+    N.cubinSize(prog, &n);
     std::vector<char> bin(n);
-    nvrtcGetCUBIN(prog, bin.data());
-    nvrtcDestroyProgram(&prog);
+    N.getCubin(prog, bin.data());
+    N.destroy(&prog);
     return bin;
 }
 

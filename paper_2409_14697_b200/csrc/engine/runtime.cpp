@@ -897,7 +897,8 @@ int qk_debug_jit_program(const qk_program* cp, int nLocal, char** sources) {
                 if (s.kind == qkeng::Step::Pass) {
                     const std::string name = "qk_host_pass_" + std::to_string(k++);
                     const std::string src = qkjit::generatePassSource(*s.pass, name);
-                    qkjit::compileToCubin(src, name);  // NVRTC (no GPU needed): throws with the log
+                    if (!std::getenv("QK_JIT_DEBUG_NOCOMPILE"))
+                        qkjit::compileToCubin(src, name);  // NVRTC (no GPU needed): throws with the log
                     all += "//@@PASS " + name + "\n" + src;
                 }
         *sources = dupText(all);
