@@ -49,11 +49,11 @@ __global__ void __launch_bounds__(256) k_ims(double2* __restrict__ a, int logN, 
     const uint64_t K = uint64_t(1) << hiBits;
     uint64_t k = 0;
     while (k < K) {
-        // 4 independent elements per trip for memory-level parallelism.
-        uint64_t xs[4], ys[4];
+        // 8 independent elements per trip for memory-level parallelism.
+        uint64_t xs[8], ys[8];
         int n = 0;
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
+        for (int u = 0; u < 8; u++) {
             if (k < K) {
                 xs[u] = t | (k << logT);
                 ys[u] = px;
@@ -63,18 +63,18 @@ __global__ void __launch_bounds__(256) k_ims(double2* __restrict__ a, int logN, 
                 k++;
             }
         }
-        double2 vx[4], vy[4];
+        double2 vx[8], vy[8];
 #pragma unroll
-        for (int u = 0; u < 4; u++)
+        for (int u = 0; u < 8; u++)
             if (u < n && xs[u] < ys[u]) {
-                vx[u] = a[xs[u]];
-                vy[u] = a[ys[u]];
+                vx[u] = __ldcs(a + xs[u]);
+                vy[u] = __ldcs(a + ys[u]);
             }
 #pragma unroll
-        for (int u = 0; u < 4; u++)
+        for (int u = 0; u < 8; u++)
             if (u < n && xs[u] < ys[u]) {
-                a[xs[u]] = vy[u];
-                a[ys[u]] = vx[u];
+                __stcs(a + xs[u], vy[u]);
+                __stcs(a + ys[u], vx[u]);
             }
     }
 }
@@ -318,8 +318,9 @@ static bool imsTileSpec(int logN, const int* outs, const int* ins, int s, ImsTil
 }
 
 // QK_IMS_TILED: 0 = always the per-element kernel, 1 = tiled whenever
-// possible, 2 (default) = tiled only when a pair has an out bit < 3 (the case
-// where per-element access wastes sectors).
+// possible, 2 (default) = tiled only when a pair moves memory bit 0 or 1 (the
+// case where per-element access wastes sectors; measured on B200 the tiled
+// kernel loses otherwise).
 static int imsMode() {
     static const int v = [] {
         const char* e = std::getenv("QK_IMS_TILED");
@@ -331,7 +332,7 @@ static int imsMode() {
 cudaError_t launchIms(double2* a, int logN, const int* outs, const int* ins, int s, cudaStream_t st) {
     ImsTileSpec sp;
     bool lowPair = false;
-    for (int j = 0; j < s; j++) lowPair |= outs[j] < 3 || ins[j] < 3;
+    for (int j = 0; j < s; j++) lowPair |= outs[j] < 2 || ins[j] < 2;  // sub-64-B neighbours move apart
     const int mode = imsMode();
     if (mode == 0 || (mode == 2 && !lowPair) || !imsTileSpec(logN, outs, ins, s, sp))
         return launchImsGeneric(a, logN, outs, ins, s, st);

@@ -296,50 +296,6 @@ std::vector<std::vector<std::pair<int, int>>> materializePairs(const std::vector
     return out;
 }
 
-// Free in-tile output permutation of a segment's last pass.  A pass may store
-// its tile with any permutation of the tile's own bits (map_out relabel, no
-// extra traffic): before a materialization (end of program, or a cross-rank
-// swap), every tile bit whose destination (memory bit q for program position
-// q) lies inside the tile is stored there, shrinking the IMS that follows.
-// `mem` (program position -> memory bit) is updated.
-void retileFinal(std::vector<qkeng::Step>& steps, std::vector<int>& mem) {
-    if (steps.empty() || steps.back().kind != qkeng::Step::Pass) return;
-    qkdev::PassParams& P = *steps.back().pass;
-    const int n = int(mem.size()), ct = P.ct;
-    std::vector<int> tile(P.tile_phys, P.tile_phys + ct);  // ascending memory bits
-    std::vector<int> where(static_cast<size_t>(n), -1);     // memory bit -> tile index
-    for (int j = 0; j < ct; j++) where[size_t(tile[size_t(j)])] = j;
-    std::vector<int> dest(static_cast<size_t>(n));  // memory bit -> program position
-    for (int q = 0; q < n; q++) dest[size_t(mem[size_t(q)])] = q;
-    std::vector<char> taken(static_cast<size_t>(ct), 0);
-    std::vector<int> sigma(static_cast<size_t>(ct), -1);  // tile index -> tile index
-    for (int j = 0; j < ct; j++) {
-        const int d = where[size_t(dest[size_t(tile[size_t(j)])])];
-        if (d >= 0) sigma[size_t(j)] = d, taken[size_t(d)] = 1;
-    }
-    int free = 0;
-    for (int j = 0; j < ct; j++)
-        if (sigma[size_t(j)] < 0) {
-            while (taken[size_t(free)]) free++;
-            sigma[size_t(j)] = free;
-            taken[size_t(free)] = 1;
-        }
-    bool identity = true;
-    for (int j = 0; j < ct; j++) identity &= sigma[size_t(j)] == j;
-    if (identity) return;
-    // Apply: data of tile bit j is stored at tile bit sigma[j].
-    const int last = P.nsegs - 1;
-    for (int s = 0; s < ct; s++) P.map_out[last][s] = uint8_t(sigma[P.map_out[last][s]]);
-    uint32_t xm = 0;
-    for (int j = 0; j < ct; j++)
-        if ((P.xmask_out[last] >> j) & 1) xm |= 1u << sigma[size_t(j)];
-    P.xmask_out[last] = uint16_t(xm);
-    for (int q = 0; q < n; q++) {
-        const int j = where[size_t(mem[size_t(q)])];
-        if (j >= 0) mem[size_t(q)] = tile[size_t(sigma[size_t(j)])];
-    }
-}
-
 std::shared_ptr<Compiled> compileFor(qk_program* p, int nLocal) {
     std::lock_guard<std::mutex> lk(p->mu);
     auto it = p->compiled.find(nLocal);
@@ -362,8 +318,15 @@ std::shared_ptr<Compiled> compileFor(qk_program* p, int nLocal) {
         if (stream.empty()) return;
         CompiledItem ci;
         ci.kind = CompiledItem::Block;
-        ci.steps = qkeng::compileBlock(stream, nLocal, c->gtab);
-        if (lazy && beforeMaterialize) retileFinal(ci.steps, mem);
+        if (lazy && beforeMaterialize) {
+            // route the data toward the program's physical order (mem = identity)
+            std::vector<int> dest(static_cast<size_t>(nLocal)), moved;
+            for (int q = 0; q < nLocal; q++) dest[size_t(mem[size_t(q)])] = q;
+            ci.steps = qkeng::compileBlock(stream, nLocal, c->gtab, &dest, &moved);
+            for (int q = 0; q < nLocal; q++) mem[size_t(q)] = moved[size_t(mem[size_t(q)])];
+        } else {
+            ci.steps = qkeng::compileBlock(stream, nLocal, c->gtab);
+        }
         for (qkeng::Step& s : ci.steps) {
             ci.flopsPerAmp += s.flopsPerAmp;
             if (s.kind != qkeng::Step::Pass) {

@@ -829,8 +829,65 @@ int lowTileBits() {
 // runs of controlled-phase / RZ / RZZ / D_k gates ride along with whichever
 // pass is open.  Gate order is never changed; the cut points minimize the
 // estimated HBM cost.
-std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::vector<double>& gtab) {
+// Store permutation of a pass: the data of tile bit j is written to tile bit
+// sigma[j] (map_out of the last segment relabelled; no extra traffic).
+void applyStorePermutation(PassParams& P, const std::vector<int>& sigma) {
+    const int last = P.nsegs - 1;
+    for (int s = 0; s < P.ct; s++) P.map_out[last][s] = uint8_t(sigma[P.map_out[last][s]]);
+    uint32_t xm = 0;
+    for (int j = 0; j < P.ct; j++)
+        if ((P.xmask_out[last] >> j) & 1) xm |= 1u << sigma[size_t(j)];
+    P.xmask_out[last] = uint16_t(xm);
+}
+
+std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::vector<double>& gtab,
+                               const std::vector<int>* dest, std::vector<int>* relabel) {
     std::vector<Step> steps;
+    // Routing (dest given): memory bit b's data should end at memory bit
+    // dest[b].  Each pass stores its tile with the permutation that puts every
+    // tile bit whose destination lies in the tile where it belongs, so the
+    // materialization after the stream shrinks or vanishes.  R[b] = memory bit
+    // that now holds the data that started at b; later gates are relabelled.
+    std::vector<int> R(static_cast<size_t>(nLocal)), Rinv(static_cast<size_t>(nLocal));
+    for (int b = 0; b < nLocal; b++) R[size_t(b)] = Rinv[size_t(b)] = b;
+    auto relabelGate = [&](const Gate& g) {
+        Gate m = g;
+        for (int& q : m.targets) q = R[size_t(q)];
+        for (int& q : m.controls) q = R[size_t(q)];
+        return m;
+    };
+    auto route = [&](size_t firstStep) {
+        if (!dest) return;
+        for (size_t k = steps.size(); k-- > firstStep;) {
+            if (steps[k].kind != Step::Pass) continue;
+            PassParams& P = *steps[k].pass;
+            const int ct = P.ct;
+            std::vector<int> where(static_cast<size_t>(nLocal), -1);  // memory bit -> tile index
+            for (int j = 0; j < ct; j++) where[size_t(P.tile_phys[j])] = j;
+            std::vector<int> sigma(static_cast<size_t>(ct), -1);
+            std::vector<char> taken(static_cast<size_t>(ct), 0);
+            for (int j = 0; j < ct; j++) {
+                const int d = where[size_t((*dest)[size_t(Rinv[size_t(P.tile_phys[j])])])];
+                if (d >= 0) sigma[size_t(j)] = d, taken[size_t(d)] = 1;
+            }
+            for (int j = 0; j < ct; j++)  // the rest: stay put where free, else any free slot
+                if (sigma[size_t(j)] < 0 && !taken[size_t(j)]) sigma[size_t(j)] = j, taken[size_t(j)] = 1;
+            int free = 0;
+            for (int j = 0; j < ct; j++)
+                if (sigma[size_t(j)] < 0) {
+                    while (taken[size_t(free)]) free++;
+                    sigma[size_t(j)] = free;
+                    taken[size_t(free)] = 1;
+                }
+            applyStorePermutation(P, sigma);
+            std::vector<int> moved(static_cast<size_t>(nLocal));
+            for (int b = 0; b < nLocal; b++) moved[size_t(b)] = b;
+            for (int j = 0; j < ct; j++) moved[size_t(P.tile_phys[j])] = P.tile_phys[sigma[size_t(j)]];
+            for (int b = 0; b < nLocal; b++) R[size_t(b)] = moved[size_t(R[size_t(b)])];
+            for (int b = 0; b < nLocal; b++) Rinv[size_t(R[size_t(b)])] = b;
+            return;  // the group's last pass only
+        }
+    };
     for (const Gate& g : gates)
         for (int q : g.qubits())
             if (q < 0 || q >= nLocal)
@@ -892,10 +949,15 @@ std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::
         std::reverse(cuts.begin(), cuts.end());
         cuts.push_back(m);
         for (size_t c = 0; c + 1 < cuts.size(); c++) {
-            std::vector<Gate> group(run.begin() + long(cuts[c]), run.begin() + long(cuts[c + 1]));
+            std::vector<Gate> group;
             uint64_t used = 0;
-            for (size_t k = cuts[c]; k < cuts[c + 1]; k++) used |= mask[k];
+            for (size_t k = cuts[c]; k < cuts[c + 1]; k++) {
+                group.push_back(relabelGate(run[k]));
+                if (mask[k]) used |= group.back().depMask();
+            }
+            const size_t first = steps.size();
             compileGroup(group, used, ct, nLocal, gtab, steps);
+            route(first);
         }
         run.clear();
     };
@@ -904,12 +966,14 @@ std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::
             if (g.targets.size() > size_t(kMaxTileBits))
                 throw SimulationError("fused dense gate " + std::to_string(g.id) + " wider than 13 qubits");
             cutRun();
-            denseStep(g.payload, g.targets, referenceFlopsPerAmp(g));
+            const Gate m = relabelGate(g);
+            denseStep(m.payload, m.targets, referenceFlopsPerAmp(m));
             continue;
         }
         run.push_back(g);
     }
     cutRun();
+    if (relabel) *relabel = R;
     return steps;
 }
 

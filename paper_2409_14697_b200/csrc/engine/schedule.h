@@ -27,7 +27,12 @@ struct Step {
 // (interleaved complex) and returns the steps that apply `gates` in order to a
 // slice of 2^nLocal amplitudes.  Throws SimulationError if a gate reaches a
 // position >= nLocal.
-std::vector<Step> compileBlock(const std::vector<quokka::Gate>& gates, int nLocal, std::vector<double>& gtab);
+// With `dest` (memory bit -> memory bit where its data should end up), the
+// passes also route data toward dest with free in-tile store permutations;
+// `relabel` receives the resulting move (data that started at memory bit b is
+// now at relabel[b]).
+std::vector<Step> compileBlock(const std::vector<quokka::Gate>& gates, int nLocal, std::vector<double>& gtab,
+                               const std::vector<int>* dest = nullptr, std::vector<int>* relabel = nullptr);
 
 // Reference-formula flops per amplitude for one gate.
 double referenceFlopsPerAmp(const quokka::Gate& g);
