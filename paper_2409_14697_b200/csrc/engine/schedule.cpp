@@ -866,9 +866,15 @@ std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::
             for (int j = 0; j < ct; j++) where[size_t(P.tile_phys[j])] = j;
             std::vector<int> sigma(static_cast<size_t>(ct), -1);
             std::vector<char> taken(static_cast<size_t>(ct), 0);
+            // Memory bits 0..2 keep their data: the store's lane bits write
+            // them (128-B coalesced rows), whatever the routing would like.
+            auto pinned = [&](int j) { return P.tile_phys[j] < 3; };
+            for (int j = 0; j < ct; j++)
+                if (pinned(j)) sigma[size_t(j)] = j, taken[size_t(j)] = 1;
             for (int j = 0; j < ct; j++) {
+                if (pinned(j)) continue;
                 const int d = where[size_t((*dest)[size_t(Rinv[size_t(P.tile_phys[j])])])];
-                if (d >= 0) sigma[size_t(j)] = d, taken[size_t(d)] = 1;
+                if (d >= 0 && !taken[size_t(d)]) sigma[size_t(j)] = d, taken[size_t(d)] = 1;
             }
             for (int j = 0; j < ct; j++)  // the rest: stay put where free, else any free slot
                 if (sigma[size_t(j)] < 0 && !taken[size_t(j)]) sigma[size_t(j)] = j, taken[size_t(j)] = 1;
