@@ -95,7 +95,19 @@ struct ImsTileSpec {
     int fbit[58];
     int nhp;               // pairs among non-tile bits (memory bits)
     int ho[29], hi[29];
+    int swz[3];            // staging swizzle: coordinate bit 3+i XORs swz[i] into bits 0..2
 };
+
+// Staging index: coordinate u with bits 0..2 XORed by a linear function of
+// bits 3..5, chosen on the host so both the write pattern (lanes 0..7 vary
+// coordinate bits 0..2) and the permuted read pattern are bank-conflict free.
+__device__ __forceinline__ int stageIdx(int u, const ImsTileSpec& sp) {
+    int x = u;
+#pragma unroll
+    for (int i = 0; i < 3; i++)
+        if ((u >> (3 + i)) & 1) x ^= sp.swz[i];
+    return x;
+}
 
 __global__ void __launch_bounds__(256) k_ims_tiled(double2* __restrict__ a, const __grid_constant__ ImsTileSpec sp) {
     __shared__ double2 buf[8][2][64];
@@ -104,7 +116,7 @@ __global__ void __launch_bounds__(256) k_ims_tiled(double2* __restrict__ a, cons
     // tile coordinates handled by this lane, their memory offsets, and the
     // memory offsets of the permuted coordinates
     uint64_t off[2];
-    int tpi[2];
+    int tpi[2], sidx[2];
     _Pragma("unroll") for (int e = 0; e < 2; e++) if (e < per) {
         const int t = lane + 32 * e;
         uint64_t o = 0;
@@ -115,7 +127,8 @@ __global__ void __launch_bounds__(256) k_ims_tiled(double2* __restrict__ a, cons
                 u |= 1 << sp.pi[r];
             }
         off[e] = o;
-        tpi[e] = u;  // pi(t): source coordinate for output coordinate t (pi is an involution)
+        tpi[e] = stageIdx(u, sp);  // pi(t): source coordinate for output coordinate t (pi is an involution)
+        sidx[e] = stageIdx(t, sp);
     }
     const uint64_t groups = uint64_t(1) << sp.nfree;
     const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x >> 5);
@@ -133,8 +146,8 @@ __global__ void __launch_bounds__(256) k_ims_tiled(double2* __restrict__ a, cons
         if (ph != h)
             _Pragma("unroll") for (int e = 0; e < 2; e++) if (e < per) vb[e] = __ldcs(a + (ph | off[e]));
         _Pragma("unroll") for (int e = 0; e < 2; e++) if (e < per) {
-            buf[w][0][lane + 32 * e] = va[e];
-            if (ph != h) buf[w][1][lane + 32 * e] = vb[e];
+            buf[w][0][sidx[e]] = va[e];
+            if (ph != h) buf[w][1][sidx[e]] = vb[e];
         }
         __syncwarp();
         // tile(ph)[t] <- tile(h)[pi(t)];  tile(h)[t] <- tile(ph)[pi(t)]
@@ -314,6 +327,31 @@ static bool imsTileSpec(int logN, const int* outs, const int* ins, int s, ImsTil
             sp.hi[sp.nhp] = ins[j];
             sp.nhp++;
         }
+    // Swizzle: bank(u) = (u & 7) ^ sum_i bit_{3+i}(u) * swz[i] must be
+    // injective on the lane patterns of the writes (span of coordinate bits
+    // 0..2, always) and of the permuted reads (span of pi(0..2)).
+    int img[3];
+    for (int i = 0; i < 3; i++) img[i] = 1 << sp.pi[i];
+    for (int m = 0; m < 512; m++) {
+        const int z[3] = {m & 7, (m >> 3) & 7, (m >> 6) & 7};
+        auto bank = [&](int u) {
+            int x = u & 7;
+            for (int i = 0; i < 3; i++)
+                if ((u >> (3 + i)) & 1) x ^= z[i];
+            return x;
+        };
+        bool ok = true;
+        for (int c = 1; c < 8 && ok; c++) {
+            int u = 0;
+            for (int i = 0; i < 3; i++)
+                if ((c >> i) & 1) u ^= img[i];
+            ok = bank(u) != 0;
+        }
+        if (ok) {
+            for (int i = 0; i < 3; i++) sp.swz[i] = z[i];
+            break;
+        }
+    }
     return true;
 }
 
