@@ -96,6 +96,9 @@ struct ImsTileSpec {
     int nhp;               // pairs among non-tile bits (memory bits)
     int ho[29], hi[29];
     int swz[3];            // staging swizzle: coordinate bit 3+i XORs swz[i] into bits 0..2
+    int a;                 // 2^a warps; warp w walks g = w | (k << a)
+    uint64_t hstep[58];    // dep(trailing-ones mask j+1, shifted by a): h(k+1) = h(k) ^ hstep[tz(~k)]
+    uint64_t pstep[58];    // P(hstep[j])
 };
 
 // Staging index: coordinate u with bits 0..2 XORed by a linear function of
@@ -130,15 +133,22 @@ __global__ void __launch_bounds__(256) k_ims_tiled(double2* __restrict__ a, cons
         tpi[e] = stageIdx(u, sp);  // pi(t): source coordinate for output coordinate t (pi is an involution)
         sidx[e] = stageIdx(t, sp);
     }
-    const uint64_t groups = uint64_t(1) << sp.nfree;
-    const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x >> 5);
-    for (uint64_t g = uint64_t(blockIdx.x) * (blockDim.x >> 5) + w; g < groups; g += warps) {
-        uint64_t h = 0;
-        for (int j = 0; j < sp.nfree; j++) h |= ((g >> j) & 1) << sp.fbit[j];
-        uint64_t ph = h;
-        for (int j = 0; j < sp.nhp; j++) {
-            const uint64_t d = ((ph >> sp.ho[j]) ^ (ph >> sp.hi[j])) & 1u;
-            ph ^= (d << sp.ho[j]) | (d << sp.hi[j]);
+    // Warp w walks h = dep(w | k << a) for k = 0.. with incremental XOR steps
+    // (deposit and P are GF(2)-linear), a handful of integer ops per orbit.
+    const uint64_t wid = uint64_t(blockIdx.x) * (blockDim.x >> 5) + w;
+    uint64_t h = 0;
+    for (int j = 0; j < sp.a; j++) h |= ((wid >> j) & 1) << sp.fbit[j];
+    uint64_t ph = h;
+    for (int j = 0; j < sp.nhp; j++) {
+        const uint64_t d = ((ph >> sp.ho[j]) ^ (ph >> sp.hi[j])) & 1u;
+        ph ^= (d << sp.ho[j]) | (d << sp.hi[j]);
+    }
+    const uint64_t K = uint64_t(1) << (sp.nfree - sp.a);
+    for (uint64_t k = 0; k < K; k++) {
+        if (k) {
+            const int tz = __ffsll((long long)(~(k - 1))) - 1;
+            h ^= sp.hstep[tz];
+            ph ^= sp.pstep[tz];
         }
         if (ph < h) continue;  // the orbit's smaller member does the work
         double2 va[2], vb[2];
@@ -327,6 +337,24 @@ static bool imsTileSpec(int logN, const int* outs, const int* ins, int s, ImsTil
             sp.hi[sp.nhp] = ins[j];
             sp.nhp++;
         }
+    sp.a = sp.nfree < 13 ? sp.nfree : 13;  // 8192 warps
+    auto depFree = [&](uint64_t g) {
+        uint64_t h = 0;
+        for (int j = 0; j < sp.nfree; j++) h |= ((g >> j) & 1) << sp.fbit[j];
+        return h;
+    };
+    auto Ph = [&](uint64_t h) {
+        for (int j = 0; j < sp.nhp; j++) {
+            const uint64_t d = ((h >> sp.ho[j]) ^ (h >> sp.hi[j])) & 1u;
+            h ^= (d << sp.ho[j]) | (d << sp.hi[j]);
+        }
+        return h;
+    };
+    for (int j = 0; j + sp.a < sp.nfree && j < 58; j++) {
+        const uint64_t m = ((uint64_t(2) << j) - 1) << sp.a;
+        sp.hstep[j] = depFree(m);
+        sp.pstep[j] = Ph(sp.hstep[j]);
+    }
     // Swizzle: bank(u) = (u & 7) ^ sum_i bit_{3+i}(u) * swz[i] must be
     // injective on the lane patterns of the writes (span of coordinate bits
     // 0..2, always) and of the permuted reads (span of pi(0..2)).
@@ -374,10 +402,8 @@ cudaError_t launchIms(double2* a, int logN, const int* outs, const int* ins, int
     const int mode = imsMode();
     if (mode == 0 || (mode == 2 && !lowPair) || !imsTileSpec(logN, outs, ins, s, sp))
         return launchImsGeneric(a, logN, outs, ins, s, st);
-    const uint64_t groups = uint64_t(1) << sp.nfree;
-    uint64_t ctas = (groups + 7) / 8;
-    if (ctas > 148u * 32u) ctas = 148u * 32u;
-    k_ims_tiled<<<unsigned(ctas), 256, 0, st>>>(a, sp);
+    const uint64_t ctas = ((uint64_t(1) << sp.a) + 7) / 8;  // 8 warps per CTA
+    k_ims_tiled<<<unsigned(ctas), sp.a >= 3 ? 256 : (32 << sp.a), 0, st>>>(a, sp);
     return cudaGetLastError();
 }
 
