@@ -113,7 +113,7 @@ __device__ __forceinline__ int stageIdx(int u, const ImsTileSpec& sp) {
 }
 
 __global__ void __launch_bounds__(256) k_ims_tiled(double2* __restrict__ a, const __grid_constant__ ImsTileSpec sp) {
-    __shared__ double2 buf[8][2][64];
+    __shared__ double2 buf[8][4][64];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int per = (1 << sp.k) >> 5;  // amplitudes per lane per tile (1 or 2)
     // tile coordinates handled by this lane, their memory offsets, and the
@@ -143,27 +143,41 @@ __global__ void __launch_bounds__(256) k_ims_tiled(double2* __restrict__ a, cons
         const uint64_t d = ((ph >> sp.ho[j]) ^ (ph >> sp.hi[j])) & 1u;
         ph ^= (d << sp.ho[j]) | (d << sp.hi[j]);
     }
+    // Two orbits per trip (k, k+1): 8 independent 16-B loads per lane in flight.
     const uint64_t K = uint64_t(1) << (sp.nfree - sp.a);
-    for (uint64_t k = 0; k < K; k++) {
-        if (k) {
-            const int tz = __ffsll((long long)(~(k - 1))) - 1;
-            h ^= sp.hstep[tz];
-            ph ^= sp.pstep[tz];
+    for (uint64_t k = 0; k < K; k += 2) {
+        uint64_t hs[2], ps[2];
+        _Pragma("unroll") for (int q = 0; q < 2; q++) {
+            const uint64_t kk = k + q;
+            if (kk) {
+                const int tz = __ffsll((long long)(~(kk - 1))) - 1;
+                h ^= sp.hstep[tz];
+                ph ^= sp.pstep[tz];
+            }
+            hs[q] = h;
+            ps[q] = ph;
         }
-        if (ph < h) continue;  // the orbit's smaller member does the work
-        double2 va[2], vb[2];
-        _Pragma("unroll") for (int e = 0; e < 2; e++) if (e < per) va[e] = __ldcs(a + (h | off[e]));
-        if (ph != h)
-            _Pragma("unroll") for (int e = 0; e < 2; e++) if (e < per) vb[e] = __ldcs(a + (ph | off[e]));
-        _Pragma("unroll") for (int e = 0; e < 2; e++) if (e < per) {
-            buf[w][0][sidx[e]] = va[e];
-            if (ph != h) buf[w][1][sidx[e]] = vb[e];
+        const bool lead[2] = {ps[0] >= hs[0], K > 1 && ps[1] >= hs[1]};  // smaller member does the work
+        double2 va[2][2], vb[2][2];
+        _Pragma("unroll") for (int q = 0; q < 2; q++) if (lead[q]) {
+            _Pragma("unroll") for (int e = 0; e < 2; e++) if (e < per) va[q][e] = __ldcs(a + (hs[q] | off[e]));
+            if (ps[q] != hs[q])
+                _Pragma("unroll") for (int e = 0; e < 2; e++) if (e < per) vb[q][e] = __ldcs(a + (ps[q] | off[e]));
+        }
+        _Pragma("unroll") for (int q = 0; q < 2; q++) if (lead[q]) {
+            _Pragma("unroll") for (int e = 0; e < 2; e++) if (e < per) {
+                buf[w][2 * q][sidx[e]] = va[q][e];
+                if (ps[q] != hs[q]) buf[w][2 * q + 1][sidx[e]] = vb[q][e];
+            }
         }
         __syncwarp();
         // tile(ph)[t] <- tile(h)[pi(t)];  tile(h)[t] <- tile(ph)[pi(t)]
-        _Pragma("unroll") for (int e = 0; e < 2; e++) if (e < per) __stcs(a + (ph | off[e]), buf[w][0][tpi[e]]);
-        if (ph != h)
-            _Pragma("unroll") for (int e = 0; e < 2; e++) if (e < per) __stcs(a + (h | off[e]), buf[w][1][tpi[e]]);
+        _Pragma("unroll") for (int q = 0; q < 2; q++) if (lead[q]) {
+            _Pragma("unroll") for (int e = 0; e < 2; e++) if (e < per) __stcs(a + (ps[q] | off[e]), buf[w][2 * q][tpi[e]]);
+            if (ps[q] != hs[q])
+                _Pragma("unroll") for (int e = 0; e < 2; e++) if (e < per)
+                    __stcs(a + (hs[q] | off[e]), buf[w][2 * q + 1][tpi[e]]);
+        }
         __syncwarp();
     }
 }
