@@ -911,6 +911,7 @@ std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::
         steps.push_back(std::move(s));
     };
 
+    if (relabel) *relabel = R;  // identity unless passes route data (below)
     if (nLocal < 4) {  // too small for a register tile: every gate as a dense group
         for (const Gate& g : gates) denseStep(quokka::gateMatrix(g), g.qubits(), referenceFlopsPerAmp(g));
         return steps;

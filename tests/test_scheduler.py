@@ -177,3 +177,14 @@ def test_streams_with_out_of_tile_diagonals(qk, port, ref, seed):
     assert np.max(np.abs(got - want.view(np.complex128))) < 1e-10
     if kind == "qft":
         assert any(s.get("ncta", 0) > 0 for it in compiled["items"] if it["kind"] == 0 for s in it["block"]["steps"])
+
+
+@pytest.mark.parametrize("n", [1, 2, 3])
+def test_tiny_programs_compile(qk, port, ref, n):
+    # slices under 4 qubits run every gate as a dense group (no routing)
+    cfg_text = config_text(n, 0, n, fusion=0, diag=0)
+    prog_text = ref.optimize(ref.gen("random", n, 25, 40 + n), cfg_text)
+    prog = qk.Program.parse(prog_text, qk.Config.parse(cfg_text))
+    want, _, _, _ = ref.simulate(prog_text, cfg_text, n, 0, 1, 1)
+    got = run_compiled(qk, port, prog, n, 1)
+    assert np.max(np.abs(got - want.view(np.complex128))) < 1e-12
