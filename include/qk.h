@@ -141,6 +141,11 @@ int qk_xrs_slab_index(int n_qubits, int rank_qubits, const int* outs, int s, int
 int qk_comm_unique_id(unsigned char id[128]);
 int qk_comm_init(qk_state* st, const unsigned char id[128], int nranks, int rank);
 int qk_xrs_swap(qk_state* st, const int* outs, const int* ins, int s, qk_xrs_stats* stats);
+/* Test hook: every rank's qk_xrs_swap schedule (plan, pack, single receive
+ * buffer, copy-back kernels) for slices owned by this process, with the NCCL
+ * transfers replaced by device copies matched peer-to-peer per round. */
+int qk_xrs_swap_loopback(qk_state** slices, int nslices, const int* outs, const int* ins, int s,
+                         qk_xrs_stats* stats);
 
 /* ---- programs: circuit.cpp:394-485, optimizer.cpp:478-485 ------------------ */
 int qk_config_parse(const char* ini_text, qk_config* out);    /* parseConfig + finalize */

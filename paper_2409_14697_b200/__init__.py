@@ -127,6 +127,7 @@ def lib():
         "qk_comm_unique_id": ([C.c_char_p], I),
         "qk_comm_init": ([P, C.c_char_p, I, I], I),
         "qk_xrs_swap": ([P, C.POINTER(I), C.POINTER(I), I, C.POINTER(_XrsStats)], I),
+        "qk_xrs_swap_loopback": ([C.POINTER(P), I, C.POINTER(I), C.POINTER(I), I, C.POINTER(_XrsStats)], I),
         "qk_config_parse": ([C.c_char_p, C.POINTER(_Config)], I),
         "qk_config_finalize": ([C.POINTER(_Config)], I),
         "qk_config_serialize": ([C.POINTER(_Config), C.POINTER(P)], I),
@@ -451,6 +452,16 @@ def xrs_swap(slices, pairs):
     arr = (C.c_void_p * len(slices))(*[x._h.value for x in slices])
     stats = (_XrsStats * len(slices))()
     _check(lib().qk_xrs_swap_local(arr, len(slices), outs, ins, s, stats))
+    return [(x.bytes_sent, x.bytes_received, x.peak_buffer_bytes, x.rounds) for x in stats]
+
+
+def xrs_swap_loopback(slices, pairs):
+    """The NCCL path's per-rank XRS schedule (pack / single receive buffer /
+    copy-back) for slices in this process, transfers as device copies."""
+    outs, ins, s = _pairs(pairs)
+    arr = (C.c_void_p * len(slices))(*[x._h.value for x in slices])
+    stats = (_XrsStats * len(slices))()
+    _check(lib().qk_xrs_swap_loopback(arr, len(slices), outs, ins, s, stats))
     return [(x.bytes_sent, x.bytes_received, x.peak_buffer_bytes, x.rounds) for x in stats]
 
 

@@ -506,48 +506,116 @@ void ensureXrsBuffers(qk_state* st, uint64_t amps, bool pack) {
 
 // NCCL XRS for this rank (one process per GPU): per window round, one grouped
 // ncclSend/ncclRecv per partner into a single receive buffer, then copy-back.
-void runXrsNccl(qk_state* st, const XrsPlan& p, qk_run_stats& rs) {
-    if (!st->comm) throw SimulationError("cross-rank swap needs a communicator (qk_comm_init) or qk_simulate_local");
-    if (p.s == 0) return;
-    const int region = st->nLocal, slabs = 1 << p.s, own = ownSlab(st->rank, p);
-    bool contiguous = true;  // AIO staging: outs are the top S in-rank positions
-    for (int j = 0; j < p.s; j++) contiguous &= p.outs[size_t(j)] == region - p.s + j;
-    (void)own;
-    ensureXrsBuffers(st, uint64_t(slabs - 1) * p.window, !contiguous);
-    const std::vector<qk_xrs_msg> msgs = xrsMessages(p, st->rank);
-    for (size_t a = 0; a < msgs.size();) {
-        size_t b = a;
-        while (b < msgs.size() && msgs[b].round == msgs[a].round) b++;  // one window round
-        if (!contiguous)
-            for (size_t m = a; m < b; m++) {
-                cuda(qkdev::launchWindowPack(st->packBuf + uint64_t(msgs[m].section) * msgs[m].count,
-                                             st->amps + slabBits(msgs[m].slab, p), msgs[m].w0, msgs[m].count,
-                                             p.outs.data(), p.s, st->stream),
-                     "xrs pack");
-                rs.kernel_launches++;
-            }
-        nccl(ncclGroupStart(), "ncclGroupStart");
+// One rank's side of an XRS (distributed.cpp:76-120) as the NCCL path runs
+// it: per window round, pack (only if the outs are not the AIO-staged top S
+// in-rank positions), exchange, copy back from the single receive buffer.
+struct XrsRank {
+    qk_state* st;
+    const XrsPlan& p;
+    bool contiguous = true;
+    std::vector<qk_xrs_msg> msgs;
+    XrsRank(qk_state* s, const XrsPlan& plan) : st(s), p(plan) {
+        for (int j = 0; j < p.s; j++) contiguous &= p.outs[size_t(j)] == st->nLocal - p.s + j;
+        ensureXrsBuffers(st, uint64_t((1 << p.s) - 1) * p.window, !contiguous);
+        msgs = xrsMessages(p, st->rank);
+    }
+    const double2* sendSrc(const qk_xrs_msg& x) const {
+        return contiguous ? st->amps + slabBits(x.slab, p) + x.w0 : st->packBuf + uint64_t(x.section) * x.count;
+    }
+    double2* recvDst(const qk_xrs_msg& x) const { return st->recvBuf + uint64_t(x.section) * x.count; }
+    void pack(size_t a, size_t b, qk_run_stats& rs) {
+        if (contiguous) return;
         for (size_t m = a; m < b; m++) {
-            const qk_xrs_msg& x = msgs[m];
-            const double2* src = contiguous ? st->amps + slabBits(x.slab, p) + x.w0
-                                            : st->packBuf + uint64_t(x.section) * x.count;
-            nccl(ncclSend(src, 2 * x.count, ncclDouble, x.peer, st->comm, st->stream), "ncclSend");
-            nccl(ncclRecv(st->recvBuf + uint64_t(x.section) * x.count, 2 * x.count, ncclDouble, x.peer, st->comm,
-                          st->stream),
-                 "ncclRecv");
+            cuda(qkdev::launchWindowPack(st->packBuf + uint64_t(msgs[m].section) * msgs[m].count,
+                                         st->amps + slabBits(msgs[m].slab, p), msgs[m].w0, msgs[m].count,
+                                         p.outs.data(), p.s, st->stream),
+                 "xrs pack");
+            rs.kernel_launches++;
         }
-        nccl(ncclGroupEnd(), "ncclGroupEnd");
+    }
+    void unpack(size_t a, size_t b, qk_run_stats& rs) {
         for (size_t m = a; m < b; m++) {
             const qk_xrs_msg& x = msgs[m];
-            cuda(qkdev::launchWindowUnpack(st->amps + slabBits(x.slab, p), st->recvBuf + uint64_t(x.section) * x.count,
-                                           x.w0, x.count, p.outs.data(), p.s, st->stream),
+            cuda(qkdev::launchWindowUnpack(st->amps + slabBits(x.slab, p), recvDst(x), x.w0, x.count, p.outs.data(), p.s,
+                                           st->stream),
                  "xrs copy-back");
             rs.kernel_launches++;
         }
+    }
+    size_t roundEnd(size_t a) const {
+        size_t b = a;
+        while (b < msgs.size() && msgs[b].round == msgs[a].round) b++;
+        return b;
+    }
+};
+
+// NCCL XRS for this rank (one process per GPU): per window round, one grouped
+// ncclSend/ncclRecv per partner into a single receive buffer, then copy-back.
+void runXrsNccl(qk_state* st, const XrsPlan& p, qk_run_stats& rs) {
+    if (!st->comm) throw SimulationError("cross-rank swap needs a communicator (qk_comm_init) or qk_simulate_local");
+    if (p.s == 0) return;
+    XrsRank x(st, p);
+    for (size_t a = 0; a < x.msgs.size();) {
+        const size_t b = x.roundEnd(a);
+        x.pack(a, b, rs);
+        nccl(ncclGroupStart(), "ncclGroupStart");
+        for (size_t m = a; m < b; m++) {
+            const qk_xrs_msg& msg = x.msgs[m];
+            nccl(ncclSend(x.sendSrc(msg), 2 * msg.count, ncclDouble, msg.peer, st->comm, st->stream), "ncclSend");
+            nccl(ncclRecv(x.recvDst(msg), 2 * msg.count, ncclDouble, msg.peer, st->comm, st->stream), "ncclRecv");
+        }
+        nccl(ncclGroupEnd(), "ncclGroupEnd");
+        x.unpack(a, b, rs);
         rs.xrs_rounds++;
         a = b;
     }
     rs.xrs_bytes += 16.0 * double(st->count) * (1.0 - std::ldexp(1.0, -p.s));
+}
+
+// The same per-rank schedule with every rank in this process and the NCCL
+// transfer replaced by device copies (send matched to receive by peer and
+// round, as NCCL's grouped point-to-point does).  Test hook for the NCCL
+// path's plan, pack and copy-back kernels on a single GPU.
+void runXrsLoopback(qk_state** sl, int ns, const XrsPlan& p) {
+    if (p.s == 0) return;
+    std::vector<std::unique_ptr<XrsRank>> rk;
+    for (int r = 0; r < ns; r++) rk.push_back(std::make_unique<XrsRank>(sl[r], p));
+    qk_run_stats rs{};
+    std::vector<size_t> pos(static_cast<size_t>(ns), 0);
+    for (;;) {
+        bool any = false;
+        std::vector<size_t> end(static_cast<size_t>(ns));
+        for (int r = 0; r < ns; r++) {
+            end[size_t(r)] = pos[size_t(r)] < rk[size_t(r)]->msgs.size() ? rk[size_t(r)]->roundEnd(pos[size_t(r)])
+                                                                        : pos[size_t(r)];
+            any |= end[size_t(r)] > pos[size_t(r)];
+        }
+        if (!any) break;
+        for (int r = 0; r < ns; r++) {
+            DeviceGuard g(sl[r]->device);
+            rk[size_t(r)]->pack(pos[size_t(r)], end[size_t(r)], rs);
+        }
+        for (int r = 0; r < ns; r++) cuda(cudaStreamSynchronize(sl[r]->stream), "loopback pack");
+        for (int r = 0; r < ns; r++)
+            for (size_t m = pos[size_t(r)]; m < end[size_t(r)]; m++) {
+                const qk_xrs_msg& in = rk[size_t(r)]->msgs[m];  // r receives from in.peer
+                const XrsRank& q = *rk[size_t(in.peer)];
+                const qk_xrs_msg* out = nullptr;
+                for (size_t k = pos[size_t(in.peer)]; k < end[size_t(in.peer)]; k++)
+                    if (q.msgs[k].peer == r) out = &q.msgs[k];
+                if (!out || out->count != in.count) throw SimulationError("xrs loopback: unmatched message");
+                cuda(cudaMemcpyAsync(rk[size_t(r)]->recvDst(in), q.sendSrc(*out), in.count * sizeof(double2),
+                                     cudaMemcpyDeviceToDevice, sl[r]->stream),
+                     "loopback copy");
+            }
+        for (int r = 0; r < ns; r++) cuda(cudaStreamSynchronize(sl[r]->stream), "loopback copy");
+        for (int r = 0; r < ns; r++) {
+            DeviceGuard g(sl[r]->device);
+            rk[size_t(r)]->unpack(pos[size_t(r)], end[size_t(r)], rs);
+        }
+        for (int r = 0; r < ns; r++) cuda(cudaStreamSynchronize(sl[r]->stream), "loopback unpack");
+        pos = end;
+    }
 }
 
 // In-process XRS: every slab pair swapped in place by one kernel reading and
@@ -955,6 +1023,20 @@ int qk_xrs_swap(qk_state* st, const int* outs, const int* ins, int s, qk_xrs_sta
         qk_run_stats rs{};
         runXrsNccl(st, p, rs);
         cuda(cudaStreamSynchronize(st->stream), "xrs");
+    });
+}
+
+int qk_xrs_swap_loopback(qk_state** sl, int ns, const int* outs, const int* ins, int s, qk_xrs_stats* stats) {
+    return guard([&] {
+        if (ns < 1 || (ns & (ns - 1))) throw SimulationError("slice count must be a power of two");
+        for (int r = 0; r < ns; r++)
+            if (sl[r]->rank != r || (1 << sl[r]->R) != ns) throw SimulationError("slices must be ranks 0..2^R-1");
+        quokka::SwapOp op;
+        op.kind = quokka::SwapOp::CrossRank;
+        for (int j = 0; j < s; j++) op.pairs.emplace_back(outs[j], ins[j]);
+        const XrsPlan p = planXrs(op, sl[0]->n, sl[0]->R, sl[0]->B);
+        for (int r = 0; r < ns; r++) accountXrs(p, stats ? stats + r : nullptr);
+        runXrsLoopback(sl, ns, p);
     });
 }
 

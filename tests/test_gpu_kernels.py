@@ -185,6 +185,31 @@ def test_xrs_sweep_bitexact(ref, qk):
                     assert np.array_equal(np.array(stats, dtype=np.uint64), wstats)
 
 
+def test_xrs_nccl_schedule_loopback_bitexact(ref, qk):
+    # The one-process-per-GPU path (runXrsNccl): per-rank message plan, pack
+    # kernel for arbitrary outs, one 2^B receive buffer, copy-back kernel --
+    # with the NCCL transfers replaced by device copies (single GPU here).
+    rng = np.random.default_rng(777)
+    for n in range(4, 12):
+        for r in range(1, min(3, n - 1) + 1):
+            region = n - r
+            for s in range(1, min(r, region) + 1):
+                for b in sorted({s, (s + region) // 2, region}):
+                    for staged in (False, True):  # AIO-staged outs = top S in-rank positions (zero-copy send)
+                        outs = list(range(region - s, region)) if staged else \
+                            sorted(int(x) for x in rng.choice(region, s, replace=False))
+                        ins = sorted(int(x) for x in rng.choice(np.arange(region, n), s, replace=False))
+                        pairs = list(zip(outs, ins))
+                        st = rng.standard_normal(2 << n)
+                        want = st.copy()
+                        wstats = ref.xrs_swap(want, n, r, b, pairs)
+                        sl = _slices(qk, st, n, r, b)
+                        stats = qk.xrs_swap_loopback(sl, pairs)
+                        got = np.concatenate([x.download() for x in sl]).view(np.float64)
+                        assert np.array_equal(got, want), (n, r, s, b, staged)
+                        assert np.array_equal(np.array(stats, dtype=np.uint64), wstats)
+
+
 def test_xrs_validation(qk):
     sl = _slices(qk, np.zeros(2 << 6), 6, 2, 4)
     for pairs in ([(4, 5)], [(0, 3)], [(0, 6)]):
