@@ -129,7 +129,9 @@ def cpu_reference_sample(kind, n_target, chunk, n_sample, threads):
     ref = Ref()
     a, seed = circuit_args(kind, n_sample)
     cfg_s = config_text(n_sample, 0, min(chunk, n_sample), fusion=0, diag=0)
-    prog_s = ref.optimize(ref.gen(kind, n_sample, a, seed), cfg_s)
+    # circuit text from this repo's generators: byte-identical to the
+    # reference's for its kinds (tests/test_host_formats.py), plus grover
+    prog_s = ref.optimize(qk.generate(kind, n_sample, a, seed), cfg_s)
     t0 = time.perf_counter()
     _, _, _, sec = ref.simulate(prog_s, cfg_s, n_sample, 0, 0, threads)
     wall = time.perf_counter() - t0
@@ -252,10 +254,11 @@ def main():
     amps = 1 << (n - R)
     peak, peak_src = measured_peaks()
     blk_launch_ms = s0["block_ms"] / max(1, s0["block_launches"])
-    blk_gbs = 32.0 * amps / (blk_launch_ms * 1e-3) / 1e9
+    blk_bytes_per_launch = s0["block_bytes"] / max(1, s0["block_launches"])  # 32 B/amp; 16 for the pass that
+    blk_gbs = blk_bytes_per_launch / (blk_launch_ms * 1e-3) / 1e9            # synthesizes |initial> (write only)
     ims_launch_ms = s0["ims_ms"] / max(1, s0["ims_launches"]) if s0["ims_launches"] else 0.0
     tr = ncu_traffic()
-    traffic = round(tr["dram_bytes_per_amp"] * amps) if tr else None
+    traffic = round(tr["dram_bytes_per_amp"] / 32.0 * blk_bytes_per_launch) if tr else None
     # program-level roofline: T_roof = sum over items, HBM-bound
     t_roof = (s0["block_bytes"] + s0["ims_bytes"]) / (peak * 1e9) + s0["xrs_bytes"] / 770e9
 
@@ -284,7 +287,8 @@ def main():
                      "peak": peak, "unit": "GB/s", "frac": round(blk_gbs / peak, 4),
                      "peak_source": peak_src, "traffic": traffic,
                      "traffic_source": (tr["source"] + ", DRAM bytes/amp x this slice") if tr else None,
-                     "algorithmic_bytes_per_launch": 32 * amps, "avg_launch_ms": round(blk_launch_ms, 3)},
+                     "algorithmic_bytes_per_launch": round(blk_bytes_per_launch),
+                     "avg_launch_ms": round(blk_launch_ms, 3)},
         "breakdown": {"block_ms": round(s0["block_ms"], 2), "ims_ms": round(s0["ims_ms"], 2),
                       "xrs_ms": round(s0["xrs_ms"], 2), "block_launches": s0["block_launches"],
                       "ims_launches": s0["ims_launches"], "xrs_rounds": s0["xrs_rounds"],

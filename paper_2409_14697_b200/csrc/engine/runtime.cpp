@@ -460,6 +460,7 @@ constexpr uint64_t kNoBasis = ~uint64_t(0);
 // index) instead of reading the slice (replaces initState's memset + store).
 void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_run_stats& rs,
               uint64_t basis = kNoBasis) {
+    const bool synthesized = basis != kNoBasis;
     for (const qkeng::Step& s : ci.steps) {
         if (s.kind == qkeng::Step::Pass) {
             if (useJit(st->nLocal))
@@ -480,7 +481,9 @@ void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_ru
         rs.kernel_launches++;
         rs.block_launches++;
     }
-    rs.block_bytes += 32.0 * double(st->count) * double(ci.steps.size());
+    // algorithmic bytes: read + write every amplitude per step; a pass that
+    // synthesizes its input (folded initState) only writes
+    rs.block_bytes += 32.0 * double(st->count) * double(ci.steps.size()) - (synthesized ? 16.0 * double(st->count) : 0.0);
     rs.block_flops += ci.flopsPerAmp * double(st->count);
 }
 
