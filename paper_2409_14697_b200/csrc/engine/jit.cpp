@@ -201,7 +201,6 @@ public:
         if (pipe_) return runPipelined(name);
         const int minb = blocksPerSm(ct_, rb_);
         o_ << kPrologue;
-        ctaTables();
         o_ << "extern \"C\" __global__ void __launch_bounds__(" << nt_ << "," << minb << ") " << name
            << "(double2* __restrict__ st, const double2* __restrict__ gt, const u32 ntiles, const u64 basis) {\n";
         o_ << "  extern __shared__ double2 sm[];\n  double2* const F = sm + " << (1 << ct_)
@@ -264,7 +263,6 @@ public:
     std::string runPipelined(const std::string& name) {
         const int L = lowRun(P_);
         o_ << kPrologue;
-        ctaTables();
         o_ << "extern \"C\" __global__ void __launch_bounds__(" << nt_ << ",1) " << name
            << "(double2* __restrict__ st, const double2* __restrict__ gt, const u32 ntiles, const u64 basis) {\n"
            << "  extern __shared__ double2 sm[];  // PB: next tile (linear tile coordinates) | XS | F | mbarrier\n"
@@ -359,36 +357,37 @@ private:
             o_ << "      o |= (u64)((r >> " << (j - L) << ") & 1u) << " << int(P_.tile_phys[j]) << ";\n";
         o_ << "      pf_l2(st + o, " << bytes << "u);\n    }\n  }\n";
     }
-    // Per-CTA factor terms as device tables (one factor per thread at tile start).
-    void ctaTables() {
-        if (!P_.ncta) return;
-        const int nt = P_.cta_end[P_.ncta - 1];
-        o_ << "static __device__ const unsigned char qk_tb[] = {";
-        for (int t = 0; t < nt; t++) o_ << (t ? "," : "") << int(P_.cta_terms[t].b1) << "," << int(P_.cta_terms[t].b2);
-        o_ << "};\nstatic __device__ const double2 qk_tv[] = {";
-        for (int t = 0; t < nt; t++) {
-            const uint32_t c = P_.cta_terms[t].c;
-            o_ << (t ? ",{" : "{") << lit(P_.coef[2 * c]) << "," << lit(P_.coef[2 * c + 1]) << "}";
-        }
-        o_ << "};\nstatic __device__ const unsigned short qk_te[] = {";
-        for (int f = 0; f < P_.ncta; f++) o_ << (f ? "," : "") << P_.cta_end[f];
-        o_ << "};\n";
-    }
-    // Warp w computes factors w, w + #warps, ...: its lanes take the terms in
-    // turn and the partial products meet in a shuffle tree.
+    // Factor f is computed by warp f mod #warps: lane j takes term j (mod 32)
+    // with its condition and value as literals (no table loads), then the
+    // partial products meet in a shuffle tree.
     void ctaFactors() {
         if (!P_.ncta) return;
-        o_ << "  { const u32 w = tid >> 5, l = tid & 31u;\n"
-           << "    for (u32 f = w; f < " << P_.ncta << "u; f += " << (nt_ / 32) << "u) {\n"
-           << "      double2 acc = C2(1.0, 0.0);\n"
-           << "      for (u32 t = (f ? qk_te[f - 1] : 0u) + l; t < qk_te[f]; t += 32u) {\n"
-           << "        const u32 b1 = qk_tb[2 * t], b2 = qk_tb[2 * t + 1];\n"
-           << "        if (b1 == 255u || ((base >> b1) & (base >> b2) & 1ull)) acc = cmul(acc, qk_tv[t]);\n"
-           << "      }\n"
-           << "      for (int o = 16; o > 0; o >>= 1)\n"
-           << "        acc = cmul(acc, make_double2(__shfl_xor_sync(0xffffffffu, acc.x, o), "
-              "__shfl_xor_sync(0xffffffffu, acc.y, o)));\n"
-           << "      if (l == 0u) F[f] = acc;\n    }\n  }\n  __syncthreads();\n";
+        const int nw = std::max(1, nt_ / 32);
+        o_ << "  { const u32 w = tid >> 5, l = tid & 31u;\n";
+        for (int f = 0; f < P_.ncta; f++) {
+            const int t0 = f ? P_.cta_end[f - 1] : 0, t1 = P_.cta_end[f], nterm = t1 - t0;
+            o_ << "    if (w == " << (f % nw) << "u) {\n      double2 acc = C2(1.0, 0.0);\n";
+            for (int t = t0; t < t1; t++) {
+                const qkdev::CtaTerm& ct = P_.cta_terms[t];
+                const std::string cond =
+                    ct.b1 == 255 ? std::string("true")
+                                 : "((base >> " + std::to_string(int(ct.b1)) + ") & (base >> " + std::to_string(int(ct.b2)) +
+                                       ") & 1ull)";
+                const std::string v = c2(P_.coef[2 * ct.c], P_.coef[2 * ct.c + 1]);
+                if (t - t0 < 32)
+                    o_ << "      if (l == " << (t - t0) << "u && " << cond << ") acc = " << v << ";\n";
+                else
+                    o_ << "      if (l == " << ((t - t0) % 32) << "u && " << cond << ") acc = cmul(acc, " << v << ");\n";
+            }
+            const int width = std::min(nterm, 32);
+            int span = 1;
+            while (span < width) span <<= 1;
+            for (int off = span / 2; off > 0; off >>= 1)
+                o_ << "      acc = cmul(acc, make_double2(__shfl_xor_sync(0xffffffffu, acc.x, " << off
+                   << "), __shfl_xor_sync(0xffffffffu, acc.y, " << off << ")));\n";
+            o_ << "      if (l == 0u) F[" << f << "] = acc;\n    }\n";
+        }
+        o_ << "  }\n  __syncthreads();\n";
     }
     std::string pendDecl() {
         std::string d;
@@ -661,7 +660,7 @@ private:
 // ---- compile / load / launch -------------------------------------------------
 
 // Bump when the generated code changes for the same PassParams (on-disk cache key).
-constexpr uint64_t kGeneratorVersion = 9;
+constexpr uint64_t kGeneratorVersion = 10;
 
 uint64_t hashPass(const PassParams& P) {
     uint64_t h = 1469598103934665603ull ^ (kGeneratorVersion * 0x9E3779B97F4A7C15ull) ^ (usePrefetch() ? 1u : 0u) ^ (usePersistent() ? 2u : 0u) ^
