@@ -146,6 +146,13 @@ bool usePrefetch() {
     return v;
 }
 
+// QK_CTA_LITERAL (default 1): per-CTA factors as straight-line code with
+// literal terms; 0: a loop over device term tables.
+bool literalFactors() {
+    static const bool v = knob("QK_CTA_LITERAL", 1) != 0;
+    return v;
+}
+
 // Resident CTAs per SM of a pass kernel (register / shared-memory bound).
 int blocksPerSm(int ct, int rb) { return (ct == 12 && rb == 4) ? 2 : ct <= 11 ? 2 : 1; }
 
@@ -201,6 +208,7 @@ public:
         if (pipe_) return runPipelined(name);
         const int minb = blocksPerSm(ct_, rb_);
         o_ << kPrologue;
+        ctaTables();
         o_ << "extern \"C\" __global__ void __launch_bounds__(" << nt_ << "," << minb << ") " << name
            << "(double2* __restrict__ st, const double2* __restrict__ gt, const u32 ntiles, const u64 basis) {\n";
         o_ << "  extern __shared__ double2 sm[];\n  double2* const F = sm + " << (1 << ct_)
@@ -263,6 +271,7 @@ public:
     std::string runPipelined(const std::string& name) {
         const int L = lowRun(P_);
         o_ << kPrologue;
+        ctaTables();
         o_ << "extern \"C\" __global__ void __launch_bounds__(" << nt_ << ",1) " << name
            << "(double2* __restrict__ st, const double2* __restrict__ gt, const u32 ntiles, const u64 basis) {\n"
            << "  extern __shared__ double2 sm[];  // PB: next tile (linear tile coordinates) | XS | F | mbarrier\n"
@@ -360,8 +369,37 @@ private:
     // Factor f is computed by warp f mod #warps: lane j takes term j (mod 32)
     // with its condition and value as literals (no table loads), then the
     // partial products meet in a shuffle tree.
+    // Per-CTA factor terms as device tables (QK_CTA_LITERAL=0 form).
+    void ctaTables() {
+        if (!P_.ncta || literalFactors()) return;
+        const int nt = P_.cta_end[P_.ncta - 1];
+        o_ << "static __device__ const unsigned char qk_tb[] = {";
+        for (int t = 0; t < nt; t++) o_ << (t ? "," : "") << int(P_.cta_terms[t].b1) << "," << int(P_.cta_terms[t].b2);
+        o_ << "};\nstatic __device__ const double2 qk_tv[] = {";
+        for (int t = 0; t < nt; t++) {
+            const uint32_t c = P_.cta_terms[t].c;
+            o_ << (t ? ",{" : "{") << lit(P_.coef[2 * c]) << "," << lit(P_.coef[2 * c + 1]) << "}";
+        }
+        o_ << "};\nstatic __device__ const unsigned short qk_te[] = {";
+        for (int f = 0; f < P_.ncta; f++) o_ << (f ? "," : "") << P_.cta_end[f];
+        o_ << "};\n";
+    }
+    void ctaFactorsTable() {
+        o_ << "  { const u32 w = tid >> 5, l = tid & 31u;\n"
+           << "    for (u32 f = w; f < " << P_.ncta << "u; f += " << std::max(1, nt_ / 32) << "u) {\n"
+           << "      double2 acc = C2(1.0, 0.0);\n"
+           << "      for (u32 t = (f ? qk_te[f - 1] : 0u) + l; t < qk_te[f]; t += 32u) {\n"
+           << "        const u32 b1 = qk_tb[2 * t], b2 = qk_tb[2 * t + 1];\n"
+           << "        if (b1 == 255u || ((base >> b1) & (base >> b2) & 1ull)) acc = cmul(acc, qk_tv[t]);\n"
+           << "      }\n"
+           << "      for (int o = 16; o > 0; o >>= 1)\n"
+           << "        acc = cmul(acc, make_double2(__shfl_xor_sync(0xffffffffu, acc.x, o), "
+              "__shfl_xor_sync(0xffffffffu, acc.y, o)));\n"
+           << "      if (l == 0u) F[f] = acc;\n    }\n  }\n  __syncthreads();\n";
+    }
     void ctaFactors() {
         if (!P_.ncta) return;
+        if (!literalFactors()) return ctaFactorsTable();
         const int nw = std::max(1, nt_ / 32);
         o_ << "  { const u32 w = tid >> 5, l = tid & 31u;\n";
         for (int f = 0; f < P_.ncta; f++) {
