@@ -10,6 +10,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -432,6 +433,8 @@ struct Timer {
                 cudaEventSynchronize(b);
                 cudaEventElapsedTime(&ms, a, b);
                 out[c] += ms;
+                static const bool perItem = std::getenv("QK_PROFILE_ITEMS") != nullptr;
+                if (perItem) std::fprintf(stderr, "qk item %s %.3f ms\n", c == 0 ? "pass" : c == 1 ? "ims" : "xrs", ms);
                 cudaEventDestroy(a);
                 cudaEventDestroy(b);
             }

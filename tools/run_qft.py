@@ -8,6 +8,7 @@ kind = sys.argv[4] if len(sys.argv) > 4 else "qft"
 cfg = qk.Config.make(n, 0, chunk=chunk, fusion=0, diag=0)
 prog = qk.Program.optimize(qk.generate(kind, n, {"qaoa": 1, "random": 400}.get(kind, 0), 7), cfg)
 st = qk.State(n)
+st.set_profiling(bool(os.environ.get("QK_PROFILE_ITEMS")))
 for _ in range(reps):
     s = st.simulate(prog, 0)
 print(prog.counts(), s["total_ms"], st.norm())
