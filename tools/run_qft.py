@@ -6,7 +6,7 @@ n = int(sys.argv[1]); chunk = int(sys.argv[2]) if len(sys.argv) > 2 else 13
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 1
 kind = sys.argv[4] if len(sys.argv) > 4 else "qft"
 cfg = qk.Config.make(n, 0, chunk=chunk, fusion=0, diag=0)
-prog = qk.Program.optimize(qk.generate(kind, n, {"qaoa": 1, "random": 400}.get(kind, 0), 7), cfg)
+prog = qk.Program.optimize(qk.generate(kind, n, *{"qaoa": (1, 1), "random": (400, 7), "grover": (1, 5)}.get(kind, (0, 0))), cfg)
 st = qk.State(n)
 st.set_profiling(bool(os.environ.get("QK_PROFILE_ITEMS")))
 for _ in range(reps):
