@@ -351,7 +351,7 @@ static bool imsTileSpec(int logN, const int* outs, const int* ins, int s, ImsTil
             sp.hi[sp.nhp] = ins[j];
             sp.nhp++;
         }
-    sp.a = sp.nfree < 13 ? sp.nfree : 13;  // 8192 warps
+    sp.a = sp.nfree < 16 ? sp.nfree : 16;  // 65536 warps: ~9 waves of resident CTAs (small tail)
     auto depFree = [&](uint64_t g) {
         uint64_t h = 0;
         for (int j = 0; j < sp.nfree; j++) h |= ((g >> j) & 1) << sp.fbit[j];
