@@ -24,6 +24,10 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
     return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
 }
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 cinv(double2 a) {
+    const double d = 1.0 / fma(a.x, a.x, a.y * a.y);
+    return make_double2(a.x * d, -a.y * d);
+}
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
 // acc + m * x
 __device__ __forceinline__ double2 cmac(double2 acc, double2 m, double2 x) {
@@ -414,6 +418,16 @@ __global__ void __launch_bounds__(1 << (CT - RB), MINB)
                 }
                 case OP_SCAL_TAB: Pt = cmul(Pt, __ldg(gtab + o.c + pext8(tid, o.b))); break;
                 case OP_SCAL_CTA: Pt = cmul(Pt, F[o.c]); break;
+                case OP_CX_PEND:
+                    if ((((tid >> o.b) & 1u) ^ ((o.k >> 1) & 1u)) != 0u) {
+#pragma unroll
+                        for (int k = 0; k < RB; k++)
+                            if (k == o.a) {
+                                Pt = cmul(Pt, R[k]);
+                                R[k] = cinv(R[k]);
+                            }
+                    }
+                    break;
                 case OP_SCAL_TCTA:
                     if ((tid >> o.b) & 1u) Pt = cmul(Pt, F[o.c]);
                     break;

@@ -60,6 +60,10 @@ static __device__ __forceinline__ double2 cmac(double2 acc, double2 m, double2 x
     return acc;
 }
 static __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+static __device__ __forceinline__ double2 cinv(double2 a) {
+    const double d = 1.0 / fma(a.x, a.x, a.y * a.y);
+    return make_double2(a.x * d, -a.y * d);
+}
 static __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
 static __device__ __forceinline__ double2 csel(bool c, double2 x, double2 y) {
     return make_double2(c ? x.x : y.x, c ? x.y : y.y);
@@ -544,6 +548,12 @@ private:
                 o_ << "  R" << a << " = cmul(R" << a << ", __ldg(gt + " << d.c << "u + " << pext(d.b) << "));\n";
                 dirtyR_[a] = true;
                 return;
+            case qkdev::OP_CX_PEND:
+                o_ << "  if ((" << tb(b) << " ^ " << ((d.k >> 1) & 1) << "u) != 0u) { P = cmul(P, R" << a << "); R" << a
+                   << " = cinv(R" << a << "); }\n";
+                dirtyP_ = true;
+                dirtyR_[a] = true;
+                return;
             case qkdev::OP_SCAL_CTA:
                 o_ << "  P = cmul(P, F[" << d.c << "]);\n";
                 dirtyP_ = true;
@@ -698,7 +708,7 @@ private:
 // ---- compile / load / launch -------------------------------------------------
 
 // Bump when the generated code changes for the same PassParams (on-disk cache key).
-constexpr uint64_t kGeneratorVersion = 10;
+constexpr uint64_t kGeneratorVersion = 11;
 
 uint64_t hashPass(const PassParams& P) {
     uint64_t h = 1469598103934665603ull ^ (kGeneratorVersion * 0x9E3779B97F4A7C15ull) ^ (usePrefetch() ? 1u : 0u) ^ (usePersistent() ? 2u : 0u) ^

@@ -71,6 +71,8 @@ enum OpType : uint8_t {
     OP_SCAL_CTA,      // P *= F[c]                          (F = this CTA's factors, see cta_terms)
     OP_PEND_CTA,      // R[a] *= F[c]
     OP_SCAL_TCTA,     // P *= bit_b(thread) ? F[c] : 1
+    OP_CX_PEND,       // before a thread-controlled CX on slot a (control thread bit b, k bit1 = polarity):
+                      // where it fires, P *= R[a]; R[a] = 1 / R[a]  (the pending phase follows the swap)
 };
 
 // Diagonal gates never need their qubits inside the tile: a bit outside the

@@ -312,14 +312,20 @@ private:
                     }
             }
         }
-        // Fill with the highest remaining tile bits (keeps low bits in lanes).
+        // Fill with the highest remaining tile bits (keeps low bits in lanes),
+        // avoiding upcoming CX controls: a thread-resident control lets a
+        // pending phase on the target ride through the swap (OP_CX_PEND).
         std::vector<char> used(static_cast<size_t>(ct_), 0);
         for (int b : regs) used[size_t(b)] = 1;
-        for (int b = ct_ - 1; b >= 0 && int(regs.size()) < rb_; b--)
-            if (!used[size_t(b)]) {
-                used[size_t(b)] = 1;
-                regs.push_back(b);
-            }
+        std::vector<char> ctrl(static_cast<size_t>(ct_), 0);
+        for (size_t j = i; j < tg_.size() && j < i + 96; j++)
+            if (tg_[j].kind == GateKind::CX && tg_[j].controls[0] < ct_) ctrl[size_t(tg_[j].controls[0])] = 1;
+        for (int pass = 0; pass < 2; pass++)
+            for (int b = ct_ - 1; b >= 0 && int(regs.size()) < rb_; b--)
+                if (!used[size_t(b)] && (pass == 1 || !ctrl[size_t(b)])) {
+                    used[size_t(b)] = 1;
+                    regs.push_back(b);
+                }
         // Assign register slots (canonical dense slots already fixed).
         size_t r = 0;
         auto taken = [&](int b) { return std::find(slotBit, slotBit + rb_, b) != slotBit + rb_; };
@@ -679,8 +685,15 @@ private:
             case GateKind::CX: {
                 const int t = inv_[g.targets[0]], c = inv_[g.controls[0]];
                 emitBatch();
-                flushSlot(t);
                 const int pol = flip(c);  // physical control value that means logical 1 is (1 ^ pol)
+                if (!isReg(c) && isReg(t) && pendSlot_[t]) {
+                    // X_t diag(1, r) X_t = r diag(1, 1/r): carry the pending phase
+                    // through the swap per thread instead of flushing 16 amplitudes
+                    emit(OP_CX_PEND, t, c - rb_, pol << 1);
+                    pendScalar_ = true;
+                } else {
+                    flushSlot(t);
+                }
                 if (isReg(c)) emit(OP_CX, t, c, pol << 1);
                 else emit(OP_CX, t, c - rb_, 1 | (pol << 1));
                 return;

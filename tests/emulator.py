@@ -7,7 +7,7 @@ import numpy as np
 
 OPS = ["MAT1", "H", "CX", "DIAG1_R", "DIAG2_RR", "CPHASE_RR", "PEND_R", "PEND_RT", "SCAL", "SCAL_T",
        "SCAL_TT", "FLUSH_SLOT", "FLUSH", "DTABLE", "DENSE", "EXCHANGE", "SCAL_TAB", "PEND_TAB", "SCAL_CTA",
-       "PEND_CTA", "SCAL_TCTA"]
+       "PEND_CTA", "SCAL_TCTA", "CX_PEND"]
 
 
 def pext8(t, m):
@@ -154,6 +154,10 @@ def _run_pass(state, n, P, gt):
                 Pt *= gt[oc + pext8(tid, ob)]
             elif name == "PEND_TAB":
                 R[:, oa] *= gt[oc + pext8(tid, ob)]
+            elif name == "CX_PEND":
+                act = (bit(tid, ob) ^ ((ok >> 1) & 1)) == 1
+                Pt = np.where(act, Pt * R[:, oa], Pt)
+                R[:, oa] = np.where(act, 1 / R[:, oa], R[:, oa])
             elif name == "SCAL_CTA":
                 Pt *= F[oc]
             elif name == "PEND_CTA":
