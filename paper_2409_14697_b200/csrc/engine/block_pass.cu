@@ -45,11 +45,11 @@ __device__ __forceinline__ uint32_t swz(uint32_t u) {
     return u ^ (((u >> 3) ^ (u >> 6) ^ (u >> 9) ^ (u >> 12)) & 7u);
 }
 
-// Bits of t selected by mask m, compacted (PEXT over the 8 thread-index bits).
-__device__ __forceinline__ uint32_t pext8(uint32_t t, uint32_t m) {
+// Bits of t selected by mask m, compacted (PEXT over the <= 9 thread-index bits).
+__device__ __forceinline__ uint32_t pextT(uint32_t t, uint32_t m) {
     uint32_t r = 0, i = 0;
 #pragma unroll
-    for (int j = 0; j < 8; j++)
+    for (int j = 0; j < 9; j++)
         if ((m >> j) & 1u) r |= ((t >> j) & 1u) << i++;
     return r;
 }
@@ -416,7 +416,7 @@ __global__ void __launch_bounds__(1 << (CT - RB), MINB)
                         if (k == o.a) R[k] = cmul(R[k], e);
                     break;
                 }
-                case OP_SCAL_TAB: Pt = cmul(Pt, __ldg(gtab + o.c + pext8(tid, o.b))); break;
+                case OP_SCAL_TAB: Pt = cmul(Pt, __ldg(gtab + o.c + pextT(tid, o.x16))); break;
                 case OP_SCAL_CTA: Pt = cmul(Pt, F[o.c]); break;
                 case OP_CX_PEND:
                     if ((((tid >> o.b) & 1u) ^ ((o.k >> 1) & 1u)) != 0u) {
@@ -439,7 +439,7 @@ __global__ void __launch_bounds__(1 << (CT - RB), MINB)
                     break;
                 }
                 case OP_PEND_TAB: {
-                    const double2 e = __ldg(gtab + o.c + pext8(tid, o.b));
+                    const double2 e = __ldg(gtab + o.c + pextT(tid, o.x16));
 #pragma unroll
                     for (int k = 0; k < RB; k++)
                         if (k == o.a) R[k] = cmul(R[k], e);
@@ -581,7 +581,7 @@ static cudaError_t launchCT(double2* state, const double2* gtab, const PassParam
 
 cudaError_t launchBlockPass(double2* state, const double2* gtab, const PassParams& P, int nLocal, uint64_t basis,
                             cudaStream_t stream) {
-    if (P.rb != regBitsFor(P.ct)) return cudaErrorInvalidValue;
+    if (P.rb != regBitsFor(P.ct) && !(P.ct == 13 && (P.rb == 4 || P.rb == 5))) return cudaErrorInvalidValue;
     const uint64_t ctas = uint64_t(1) << (nLocal - P.ct);
     if (P.ct == 13) return P.rb == 5 ? launchCT<13, 5>(state, gtab, P, ctas, basis, stream)
                                      : launchCT<13, 4>(state, gtab, P, ctas, basis, stream);

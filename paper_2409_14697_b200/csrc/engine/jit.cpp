@@ -471,7 +471,7 @@ private:
     std::string pext(uint32_t mask) const {
         std::string e = "0u";
         int r = 0;
-        for (int j = 0; j < 8; j++)
+        for (int j = 0; j < 16; j++)
             if ((mask >> j) & 1) e += " | (" + tb(j) + " << " + std::to_string(r++) + ")";
         return "(" + e + ")";
     }
@@ -541,11 +541,11 @@ private:
                 dirtyP_ = true;
                 return;
             case qkdev::OP_SCAL_TAB:
-                o_ << "  P = cmul(P, __ldg(gt + " << d.c << "u + " << pext(d.b) << "));\n";
+                o_ << "  P = cmul(P, __ldg(gt + " << d.c << "u + " << pext(d.x16) << "));\n";
                 dirtyP_ = true;
                 return;
             case qkdev::OP_PEND_TAB:
-                o_ << "  R" << a << " = cmul(R" << a << ", __ldg(gt + " << d.c << "u + " << pext(d.b) << "));\n";
+                o_ << "  R" << a << " = cmul(R" << a << ", __ldg(gt + " << d.c << "u + " << pext(d.x16) << "));\n";
                 dirtyR_[a] = true;
                 return;
             case qkdev::OP_CX_PEND:
@@ -708,7 +708,7 @@ private:
 // ---- compile / load / launch -------------------------------------------------
 
 // Bump when the generated code changes for the same PassParams (on-disk cache key).
-constexpr uint64_t kGeneratorVersion = 11;
+constexpr uint64_t kGeneratorVersion = 12;
 
 uint64_t hashPass(const PassParams& P) {
     uint64_t h = 1469598103934665603ull ^ (kGeneratorVersion * 0x9E3779B97F4A7C15ull) ^ (usePrefetch() ? 1u : 0u) ^ (usePersistent() ? 2u : 0u) ^

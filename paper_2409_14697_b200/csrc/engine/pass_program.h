@@ -66,8 +66,8 @@ enum OpType : uint8_t {
     OP_DTABLE,        // fused diagonal: k targets; contrib[c16 .. c16+ct) index map; table at gtab + c
     OP_DENSE,         // fused dense 2^k (k <= 4): targets in canonical slots; matrix at gtab + c
     OP_EXCHANGE,      // shared-memory exchange: map_out[c-1] -> map_in[c] (segment c starts)
-    OP_SCAL_TAB,      // P *= gtab[c + pext(thread, b)]      (b = thread-bit mask)
-    OP_PEND_TAB,      // R[a] *= gtab[c + pext(thread, b)]
+    OP_SCAL_TAB,      // P *= gtab[c + pext(thread, x16)]    (x16 = thread-bit mask)
+    OP_PEND_TAB,      // R[a] *= gtab[c + pext(thread, x16)]
     OP_SCAL_CTA,      // P *= F[c]                          (F = this CTA's factors, see cta_terms)
     OP_PEND_CTA,      // R[a] *= F[c]
     OP_SCAL_TCTA,     // P *= bit_b(thread) ? F[c] : 1

@@ -453,7 +453,10 @@ void prepareJit(const Compiled& c, int device) {
     std::vector<const qkdev::PassParams*> passes;
     for (const CompiledItem& it : c.items)
         for (const qkeng::Step& s : it.steps)
-            if (s.kind == qkeng::Step::Pass) passes.push_back(s.pass.get());
+            if (s.kind == qkeng::Step::Pass) {
+                passes.push_back(s.pass.get());
+                if (s.alt) passes.push_back(s.alt.get());
+            }
     qkjit::prepare(passes, device);
 }
 
@@ -466,10 +469,33 @@ void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_ru
     const bool synthesized = basis != kNoBasis;
     for (const qkeng::Step& s : ci.steps) {
         if (s.kind == qkeng::Step::Pass) {
+            // Register-width autotune: the first two executions of a pass time
+            // each variant (events, synchronous); later ones take the faster.
+            const int v = s.alt ? s.tune->choice() : 0;
+            const qkdev::PassParams& P = v ? *s.alt : *s.pass;
+            const bool timing = s.alt && s.tune->runs[v] == 0;
+            cudaEvent_t e0 = nullptr, e1 = nullptr;
+            if (timing) {
+                cuda(cudaEventCreate(&e0), "event");
+                cuda(cudaEventCreate(&e1), "event");
+                cuda(cudaEventRecord(e0, st->stream), "event");
+            }
             if (useJit(st->nLocal))
-                cuda(qkjit::launch(*s.pass, st->amps, t.gtab, st->nLocal, basis, st->stream), "specialized block pass");
+                cuda(qkjit::launch(P, st->amps, t.gtab, st->nLocal, basis, st->stream), "specialized block pass");
             else
-                cuda(qkdev::launchBlockPass(st->amps, t.gtab, *s.pass, st->nLocal, basis, st->stream), "block pass");
+                cuda(qkdev::launchBlockPass(st->amps, t.gtab, P, st->nLocal, basis, st->stream), "block pass");
+            if (timing) {
+                float ms = 0;
+                cuda(cudaEventRecord(e1, st->stream), "event");
+                cuda(cudaEventSynchronize(e1), "event");
+                cudaEventElapsedTime(&ms, e0, e1);
+                cudaEventDestroy(e0);
+                cudaEventDestroy(e1);
+                s.tune->ms[v] = ms;
+                s.tune->runs[v]++;
+            } else if (s.alt) {
+                s.tune->runs[v]++;
+            }
             basis = kNoBasis;
         } else if (s.kind == qkeng::Step::DiagTable) {
             cuda(qkdev::launchDiagTable(st->amps, t.gtab + s.matOff, st->count, s.targets.data() + 1, s.k, st->stream),

@@ -62,6 +62,13 @@ int regBitsFor(int ct) {
     return ct >= 13 ? rb13 : (ct < 4 ? ct : 4);
 }
 
+// QK_RB13 unset: 2^13-amplitude passes are scheduled both ways (5 and 4
+// register bits) and the runtime keeps the faster per pass.
+bool tuneRegBits() {
+    static const bool v = std::getenv("QK_RB13") == nullptr && envInt("QK_TUNE", 1, 0, 1) != 0;
+    return v;
+}
+
 }  // namespace qkdev
 
 namespace qkeng {
@@ -168,8 +175,9 @@ Amp ratio(Amp num, Amp den) {
 class PassBuilder {
 public:
     PassBuilder(const std::vector<Gate>& tg, const std::vector<Gate>& orig, const std::vector<int>& tilePhys,
-                std::vector<double>& gtab)
-        : tg_(tg), orig_(orig), gtab_(gtab), ct_(int(tilePhys.size())), rb_(regBitsFor(int(tilePhys.size()))) {
+                std::vector<double>& gtab, int rb = -1)
+        : tg_(tg), orig_(orig), gtab_(gtab), ct_(int(tilePhys.size())),
+          rb_(rb > 0 ? rb : regBitsFor(int(tilePhys.size()))) {
         tilePhys_ = tilePhys;
     }
 
@@ -529,7 +537,7 @@ private:
         const int bits = __builtin_popcount(mask);
         for (int i = 0; i < (1 << bits); i++) {
             int t = 0, r = 0;
-            for (int j = 0; j < 8; j++)
+            for (int j = 0; j < 16; j++)
                 if ((mask >> j) & 1) t |= ((i >> r++) & 1) << j;
             out.push_back(full[size_t(t)]);
         }
@@ -548,12 +556,14 @@ private:
         usedP_ = usedP_ && !allOne(tabP_);
         for (int s = 0; s < rb_; s++) usedR_[s] = usedR_[s] && !allOne(tabR_[s]);
         if (usedP_) {
-            emit(OP_SCAL_TAB, 0, int(maskP_), 0, compactTable(tabP_, maskP_));
+            emit(OP_SCAL_TAB, 0, 0, 0, compactTable(tabP_, maskP_));
+            P_->ops[nops_ - 1].x16 = uint16_t(maskP_);  // thread-bit mask (up to 9 bits at 512 threads)
             pendScalar_ = true;
         }
         for (int s = 0; s < rb_; s++)
             if (usedR_[s]) {
-                emit(OP_PEND_TAB, s, int(maskR_[s]), 0, compactTable(tabR_[s], maskR_[s]));
+                emit(OP_PEND_TAB, s, 0, 0, compactTable(tabR_[s], maskR_[s]));
+                P_->ops[nops_ - 1].x16 = uint16_t(maskR_[s]);
                 pendSlot_[s] = true;
             }
         for (const auto& op : regOps_) emit(op.t, op.a, op.b, op.k, addCoef(op.coef));
@@ -805,7 +815,7 @@ Gate remapQubits(const Gate& g, const int* tileOf) {
 }
 
 void compileGroup(const std::vector<Gate>& gates, uint64_t used, int ct, int nLocal, std::vector<double>& gtab,
-                  std::vector<Step>& out) {
+                  std::vector<Step>& out, int rb = -1) {
     // Tile bits: every bit the group touches, padded with the lowest others.
     uint64_t tile = used;
     for (int b = 0; b < nLocal && __builtin_popcountll(tile) < ct; b++) tile |= uint64_t(1) << b;
@@ -819,7 +829,7 @@ void compileGroup(const std::vector<Gate>& gates, uint64_t used, int ct, int nLo
         }
     std::vector<Gate> tg;
     for (const Gate& g : gates) tg.push_back(remapQubits(g, tileOf));
-    PassBuilder pb(tg, gates, phys, gtab);
+    PassBuilder pb(tg, gates, phys, gtab, rb);
     size_t i = 0;
     while (i < gates.size()) {
         Step st;
@@ -899,6 +909,7 @@ std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::
                     taken[size_t(free)] = 1;
                 }
             applyStorePermutation(P, sigma);
+            if (steps[k].alt) applyStorePermutation(*steps[k].alt, sigma);  // same tile, same sigma
             std::vector<int> moved(static_cast<size_t>(nLocal));
             for (int b = 0; b < nLocal; b++) moved[size_t(b)] = b;
             for (int j = 0; j < ct; j++) moved[size_t(P.tile_phys[j])] = P.tile_phys[sigma[size_t(j)]];
@@ -977,6 +988,14 @@ std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::
             }
             const size_t first = steps.size();
             compileGroup(group, used, ct, nLocal, gtab, steps);
+            if (ct == 13 && tuneRegBits() && steps.size() == first + 1 && steps[first].kind == Step::Pass) {
+                std::vector<Step> alt;
+                compileGroup(group, used, ct, nLocal, gtab, alt, regBitsFor(ct) == 5 ? 4 : 5);
+                if (alt.size() == 1 && alt[0].kind == Step::Pass) {
+                    steps[first].alt = alt[0].pass;
+                    steps[first].tune = std::make_shared<Step::Tune>();
+                }
+            }
             route(first);
         }
         run.clear();

@@ -13,6 +13,20 @@ namespace qkeng {
 struct Step {
     enum Kind { Pass, DenseGroup, DiagTable } kind = Pass;
     std::shared_ptr<qkdev::PassParams> pass;  // Kind::Pass
+    // Kind::Pass: the same pass scheduled with the other register width
+    // (2^13 tiles: 32 vs 16 amplitudes per thread); the runtime times both on
+    // their first executions and keeps the faster (`tune`, shared by copies).
+    std::shared_ptr<qkdev::PassParams> alt;
+    struct Tune {
+        float ms[2] = {0, 0};
+        int runs[2] = {0, 0};
+        int choice() const {
+            if (runs[0] == 0) return 0;
+            if (runs[1] == 0) return 1;
+            return ms[1] < ms[0] ? 1 : 0;
+        }
+    };
+    std::shared_ptr<Tune> tune;
     // Kind::DenseGroup / DiagTable: matrix (or diagonal) at gtab offset `matOff`,
     // targets (j -> sub-index bit k-1-j)
     int k = 0;

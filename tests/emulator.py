@@ -13,7 +13,7 @@ OPS = ["MAT1", "H", "CX", "DIAG1_R", "DIAG2_RR", "CPHASE_RR", "PEND_R", "PEND_RT
 def pext8(t, m):
     r = np.zeros_like(t)
     i = 0
-    for j in range(8):
+    for j in range(16):
         if (m >> j) & 1:
             r |= ((t >> j) & 1) << i
             i += 1
@@ -151,9 +151,9 @@ def _run_pass(state, n, P, gt):
             elif name == "PEND_RT":
                 R[:, oa] *= coef[oc + bit(tid, ob)]
             elif name == "SCAL_TAB":
-                Pt *= gt[oc + pext8(tid, ob)]
+                Pt *= gt[oc + pext8(tid, ox16)]
             elif name == "PEND_TAB":
-                R[:, oa] *= gt[oc + pext8(tid, ob)]
+                R[:, oa] *= gt[oc + pext8(tid, ox16)]
             elif name == "CX_PEND":
                 act = (bit(tid, ob) ^ ((ok >> 1) & 1)) == 1
                 Pt = np.where(act, Pt * R[:, oa], Pt)

@@ -148,3 +148,20 @@ def test_grover_closed_form(qk):
     others = np.delete(data, marked)
     assert np.max(np.abs(others - sign * np.cos((2 * k + 1) * th) / np.sqrt(2 ** m - 1))) < TOL
     assert np.max(np.abs(logical[1 << m:])) < TOL  # ancillas back at |0>
+
+
+def test_register_width_autotune_variants_agree(ref, qk):
+    # 2^13-tile passes carry a second schedule (16 vs 32 amplitudes per
+    # thread); run 1 times variant A, run 2 variant B, later runs the faster.
+    # Every run must match the reference.
+    n = 22
+    for kind, a, seed in (("qft", 0, 0), ("random", 200, 3)):
+        cfg_text = config_text(n, 0, 13, fusion=0, diag=0)
+        prog_text = ref.optimize(ref.gen(kind, n, a, seed), cfg_text)
+        want, _, _, _ = ref.simulate(prog_text, cfg_text, n, 0, 3, 8)
+        prog = qk.Program.parse(prog_text, qk.Config.parse(cfg_text))
+        st = qk.State(n)
+        for _ in range(3):
+            st.simulate(prog, 3)
+            assert np.max(np.abs(st.download() - want.view(np.complex128))) < TOL, kind
+        st.close()

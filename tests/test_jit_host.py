@@ -38,6 +38,32 @@ def test_specialized_kernels_on_host(ref, qk, port, kind, n, chunk, fusion, diag
     assert np.max(np.abs(st - want.view(np.complex128))) < 1e-10
 
 
+def test_16_amplitudes_per_thread_variant_on_host():
+    # QK_RB13=4: the other register width the runtime autotunes against
+    code = r"""
+import sys, numpy as np
+sys.path[:0] = [%r, %r, %r]
+import paper_2409_14697_b200 as qk
+from oracle import Ref, Port, config_text
+from jit_host import run_program_jit
+ref, port = Ref(), Port()
+for kind, n, a in (("qft", 16, 0), ("random", 15, 150)):
+    cfg_text = config_text(n, 0, 13, fusion=0, diag=0)
+    pt = ref.optimize(ref.gen(kind, n, a, 3), cfg_text)
+    want = ref.simulate(pt, cfg_text, n, 0, 5, 2)[0].view(np.complex128)
+    prog = qk.Program.parse(pt, qk.Config.parse(cfg_text))
+    assert all(s.get("rb") == 4 for it in prog.debug_compile()["items"] if it["kind"] == 0
+               for s in it["block"]["steps"] if s.get("ct") == 13)
+    st = np.zeros(1 << n, dtype=np.complex128); st[5] = 1
+    run_program_jit(qk, port, prog, n, st)
+    assert np.max(np.abs(st - want)) < 1e-10, kind
+print("ok")
+""" % (ROOT, os.path.join(ROOT, "oracle"), os.path.join(ROOT, "tests"))
+    env = dict(os.environ, QK_RB13="4")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
 def test_tma_pipelined_kernels_on_host():
     # QK_JIT_TMA=1: 2^13 tiles with >= 128-B rows become persistent kernels
     # that stream the next tile into shared memory (cp.async.bulk + mbarrier)
