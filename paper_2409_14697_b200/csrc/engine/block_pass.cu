@@ -255,7 +255,8 @@ __host__ __device__ constexpr int lowBit(int x) { return (x & 1) ? 0 : 1 + lowBi
 // a[s] *= scale * P * prod_{k: bit k of s} R[k]; done as (low 2 slots) x (high slots)
 // factor tables so each amplitude costs ~2 complex multiplies.
 template <int RB>
-__device__ __forceinline__ void flushAll(double2 (&a)[1 << RB], double2 P, double scale, double2 (&R)[RB]) {
+__device__ __forceinline__ void flushAll(double2 (&a)[1 << RB], double2 P, double scale, double2 (&R)[RB],
+                                         const double* D) {
     constexpr int NA = 1 << RB;
     const double2 base = make_double2(P.x * scale, P.y * scale);
     if constexpr (RB < 2) {
@@ -283,6 +284,10 @@ __device__ __forceinline__ void flushAll(double2 (&a)[1 << RB], double2 P, doubl
         for (int h = 0; h < NH; h++)
 #pragma unroll
             for (int l = 0; l < 4; l++) a[h * 4 + l] = cmul(a[h * 4 + l], h ? cmul(lo[l], hi[h]) : lo[l]);
+    }
+    if (D) {  // constant register-pair phases
+#pragma unroll
+        for (int s = 0; s < NA; s++) a[s] = cmul(a[s], make_double2(D[2 * s], D[2 * s + 1]));
     }
 #pragma unroll
     for (int k = 0; k < RB; k++) R[k] = make_double2(1.0, 0.0);
@@ -418,6 +423,25 @@ __global__ void __launch_bounds__(1 << (CT - RB), MINB)
                 }
                 case OP_SCAL_TAB: Pt = cmul(Pt, __ldg(gtab + o.c + pextT(tid, o.x16))); break;
                 case OP_SCAL_CTA: Pt = cmul(Pt, F[o.c]); break;
+                case OP_FLUSH_SLOT_G: {
+                    double2 rk = R[0];
+#pragma unroll
+                    for (int k = 1; k < RB; k++)
+                        if (k == o.a) rk = R[k];
+#pragma unroll
+                    for (int s = 0; s < NA; s++)
+                        if ((s >> o.a) & 1) {
+                            uint32_t idx = 0, q = 0;
+#pragma unroll
+                            for (int k = 0; k < RB; k++)
+                                if ((o.b >> k) & 1u) idx |= uint32_t((s >> k) & 1) << q++;
+                            a[s] = cmul(a[s], cmul(rk, coefAt(P, o.c + idx)));
+                        }
+#pragma unroll
+                    for (int k = 0; k < RB; k++)
+                        if (k == o.a) R[k] = make_double2(1.0, 0.0);
+                    break;
+                }
                 case OP_CX_PEND:
                     if ((((tid >> o.b) & 1u) ^ ((o.k >> 1) & 1u)) != 0u) {
 #pragma unroll
@@ -472,7 +496,7 @@ __global__ void __launch_bounds__(1 << (CT - RB), MINB)
                     break;
                 }
                 case OP_FLUSH:
-                    flushAll<RB>(a, Pt, P.coef[2 * o.c], R);
+                    flushAll<RB>(a, Pt, P.coef[2 * o.c], R, o.c16 ? &P.coef[2 * (o.c16 - 1)] : nullptr);
                     Pt = make_double2(1.0, 0.0);
                     break;
                 case OP_DTABLE: {

@@ -574,8 +574,32 @@ private:
                 dirtyR_[a] = false;
                 return;
             case qkdev::OP_FLUSH:
-                flush(P_.coef[2 * d.c]);
+                flush(P_.coef[2 * d.c], d.c16 ? &P_.coef[2 * (d.c16 - 1)] : nullptr);
                 return;
+            case qkdev::OP_FLUSH_SLOT_G: {
+                // amplitudes with slot-a bit 1 *= R_a * G[pext(s, b)] (G literal)
+                std::vector<int> bits;
+                for (int k = 0; k < rb_; k++)
+                    if ((d.b >> k) & 1) bits.push_back(k);
+                const int ng = 1 << bits.size();
+                o_ << "  {\n";
+                for (int j = 0; j < ng; j++) {
+                    const std::string g = lc(d.c + uint32_t(j));
+                    o_ << "    const double2 h" << j << " = " << (dirtyR_[a] ? "cmul(R" + std::to_string(a) + ", " + g + ")" : g)
+                       << ";\n";
+                }
+                for (int s = 0; s < na_; s++) {
+                    if (!((s >> a) & 1)) continue;
+                    int j = 0;
+                    for (size_t q = 0; q < bits.size(); q++) j |= ((s >> bits[q]) & 1) << q;
+                    o_ << "  ";
+                    mulAmp(s, "h" + std::to_string(j));
+                }
+                o_ << "  }\n";
+                if (dirtyR_[a]) o_ << "  R" << a << " = C2(1.0, 0.0);\n";
+                dirtyR_[a] = false;
+                return;
+            }
             case qkdev::OP_DTABLE: {
                 const uint16_t* cb = &P_.contrib[d.c16];
                 std::string sub = "0u";
@@ -668,9 +692,19 @@ private:
     }
 
     // a[s] *= scale * P * prod_{k: bit k of s} R[k], touching only dirty factors.
-    void flush(double scale) {
+    void flush(double scale, const double* D = nullptr) {
         bool anyR = false;
         for (int k = 0; k < rb_; k++) anyR |= dirtyR_[k];
+        auto dOne = [&](int s) { return !D || (D[2 * s] == 1.0 && D[2 * s + 1] == 0.0); };
+        bool anyD = false;
+        for (int s = 0; s < na_; s++) anyD |= !dOne(s);
+        if (anyD && !anyR && !dirtyP_) {  // constant pair phases (and the scale) only: literal factors
+            for (int s = 0; s < na_; s++) {
+                if (dOne(s) && scale == 1.0) continue;
+                mulAmp(s, c2(D[2 * s] * scale, D[2 * s + 1] * scale));
+            }
+            return;
+        }
         if (!anyR && !dirtyP_) {
             if (scale != 1.0)
                 for (int s = 0; s < na_; s++)
@@ -688,7 +722,9 @@ private:
             if (dirtyR_[hi]) o_ << "    const double2 f" << s << " = cmul(f" << rest << ", R" << hi << ");\n";
             else o_ << "    const double2 f" << s << " = f" << rest << ";\n";
         }
-        for (int s = 0; s < na_; s++) mulAmp(s, "f" + std::to_string(s));
+        for (int s = 0; s < na_; s++)
+            mulAmp(s, dOne(s) ? "f" + std::to_string(s)
+                              : "cmul(f" + std::to_string(s) + ", " + c2(D[2 * s], D[2 * s + 1]) + ")");
         o_ << "  }\n  P = C2(1.0, 0.0);\n";
         for (int k = 0; k < rb_; k++)
             if (dirtyR_[k]) o_ << "  R" << k << " = C2(1.0, 0.0);\n";
@@ -708,7 +744,7 @@ private:
 // ---- compile / load / launch -------------------------------------------------
 
 // Bump when the generated code changes for the same PassParams (on-disk cache key).
-constexpr uint64_t kGeneratorVersion = 12;
+constexpr uint64_t kGeneratorVersion = 13;
 
 uint64_t hashPass(const PassParams& P) {
     uint64_t h = 1469598103934665603ull ^ (kGeneratorVersion * 0x9E3779B97F4A7C15ull) ^ (usePrefetch() ? 1u : 0u) ^ (usePersistent() ? 2u : 0u) ^

@@ -62,7 +62,7 @@ enum OpType : uint8_t {
     OP_SCAL_T,        // P *= coef[c + bit_a(thread)]
     OP_SCAL_TT,       // P *= coef[c + 2 bit_a(thread) + bit_b(thread)]
     OP_FLUSH_SLOT,    // amplitudes with slot-a bit 1 *= R[a]; R[a] = 1
-    OP_FLUSH,         // all amplitudes *= P * coef[c].x * prod_{a: bit a} R[a]; reset
+    OP_FLUSH,         // all amplitudes *= P * coef[c].x * prod_{a: bit a} R[a] (* coef[c16 - 1 + s] if c16); reset
     OP_DTABLE,        // fused diagonal: k targets; contrib[c16 .. c16+ct) index map; table at gtab + c
     OP_DENSE,         // fused dense 2^k (k <= 4): targets in canonical slots; matrix at gtab + c
     OP_EXCHANGE,      // shared-memory exchange: map_out[c-1] -> map_in[c] (segment c starts)
@@ -71,6 +71,7 @@ enum OpType : uint8_t {
     OP_SCAL_CTA,      // P *= F[c]                          (F = this CTA's factors, see cta_terms)
     OP_PEND_CTA,      // R[a] *= F[c]
     OP_SCAL_TCTA,     // P *= bit_b(thread) ? F[c] : 1
+    OP_FLUSH_SLOT_G,  // amplitudes with slot-a bit 1 *= R[a] * coef[c + pext(slot bits, b)]; R[a] = 1
     OP_CX_PEND,       // before a thread-controlled CX on slot a (control thread bit b, k bit1 = polarity):
                       // where it fires, P *= R[a]; R[a] = 1 / R[a]  (the pending phase follows the swap)
 };

@@ -52,6 +52,13 @@ bool wideAccess() {
     return v;
 }
 
+// QK_GTERMS (default 1): register-pair phases are deferred and applied with
+// the slot flush of whichever of their bits is touched first.
+bool deferPairPhases() {
+    static const bool v = envInt("QK_GTERMS", 1, 0, 1) != 0;
+    return v;
+}
+
 bool halfExchanges() {
     static const bool v = envInt("QK_JIT_TMA", 0, 0, 1) != 0;
     return v;
@@ -199,25 +206,28 @@ public:
         std::fill(pendSlot_, pendSlot_ + kMaxRegBits, false);
         flips_ = 0;
         batchReset();
+        gterms_.clear();
+        carry_.clear();
         chooseMap(i, nullptr, wideAccess() && tilePhys_[0] == 0);
         std::memcpy(P_->map_in[0], map_, sizeof map_);
 
         const size_t first = i;
         double flops = 0;
         while (i < tg_.size()) {
-            const int queued = int(regOps_.size());  // ops still held in the diagonal batch
+            const int queued = int(regOps_.size() + gterms_.size() + 2 * carry_.size());  // deferred work
             if (kMaxOps - nops_ - queued < 16 + ct_ || kMaxCoef - ncoef_ - 4 * queued - pendingCtaTerms() < 24 ||
                 kMaxContrib - ncontrib_ < 48 + ct_ || kMaxSegs - seg_ < 3 || kMaxCtaFactors - ncta_ < ct_ + 2 ||
                 kMaxCtaTerms - ncterms_ - pendingCtaTerms() < 12)
                 break;
             if (!satisfied(tg_[i], orig_[i])) {
-                flushAll();
+                flushAll(true);
                 closeSegment();
                 seg_++;
                 chooseMap(i, halfExchanges() ? &P_->xsplit[seg_] : nullptr);
                 if (!halfExchanges()) P_->xsplit[seg_] = 255;
                 std::memcpy(P_->map_in[seg_], map_, sizeof map_);
                 emit(OP_EXCHANGE, 0, 0, 0, uint32_t(seg_));
+                relowerCarried();
             }
             lower(tg_[i], orig_[i]);
             flops += referenceFlopsPerAmp(orig_[i]);
@@ -418,25 +428,93 @@ private:
         o.c16 = c16;
     }
 
-    void flushSlot(int slot) {
-        if (isReg(slot) && pendSlot_[slot]) {
-            emit(OP_FLUSH_SLOT, slot);
-            pendSlot_[slot] = false;
-        }
+    bool slotHasPairPhase(int slot) const {
+        for (const GTerm& g : gterms_)
+            if (g.a == slot || g.b == slot) return true;
+        return false;
     }
 
-    void flushAll() {
+    // Apply everything pending on slot `slot` (its phase R and the pair phases
+    // involving it) to the amplitudes whose slot bit is 1.
+    void flushSlot(int slot) {
+        if (!isReg(slot)) return;
+        std::vector<GTerm> mine, rest;
+        for (const GTerm& g : gterms_) (g.a == slot || g.b == slot ? mine : rest).push_back(g);
+        if (mine.empty()) {
+            if (pendSlot_[slot]) emit(OP_FLUSH_SLOT, slot);
+            pendSlot_[slot] = false;
+            return;
+        }
+        uint32_t mask = 0;  // other slots the pair phases depend on
+        for (const GTerm& g : mine) mask |= 1u << (g.a == slot ? g.b : g.a);
+        // per-thread complex multiplies: one table flush over the slot's half,
+        // or each pair phase on its quarter plus a plain slot flush
+        const int half = 1 << (rb_ - 1), quarter = 1 << (rb_ - 2);
+        const int costTable = half + (pendSlot_[slot] ? (1 << __builtin_popcount(mask)) : 0);
+        const int costSplit = quarter * int(mine.size()) + (pendSlot_[slot] ? half : 0);
+        if (costSplit < costTable) {
+            for (const GTerm& g : mine) {
+                const int lo = std::min(g.a, g.b), hi = std::max(g.a, g.b);
+                emit(OP_CPHASE_RR, lo, hi, 3, addCoef({g.v}));
+            }
+            if (pendSlot_[slot]) emit(OP_FLUSH_SLOT, slot);
+            pendSlot_[slot] = false;
+            gterms_ = rest;
+            return;
+        }
+        std::vector<int> bits;
+        for (int k = 0; k < rb_; k++)
+            if ((mask >> k) & 1u) bits.push_back(k);
+        std::vector<Amp> tab(size_t(1) << bits.size(), Amp(1.0, 0.0));
+        for (size_t idx = 0; idx < tab.size(); idx++)
+            for (const GTerm& g : mine) {
+                const int o = g.a == slot ? g.b : g.a;
+                const size_t j = size_t(std::find(bits.begin(), bits.end(), o) - bits.begin());
+                if ((idx >> j) & 1) tab[idx] *= g.v;
+            }
+        emit(OP_FLUSH_SLOT_G, slot, int(mask), 0, addCoef(tab));
+        pendSlot_[slot] = false;
+        gterms_ = rest;
+    }
+
+    // carry: an exchange follows -- pair phases (constants, known here) are
+    // not applied but re-issued as diagonal gates in the next segment's map.
+    void flushAll(bool carry = false) {
         emitBatch();
         bool any = hcount_ > 0 || pendScalar_;
         for (int s = 0; s < rb_; s++) any |= pendSlot_[s];
+        uint16_t dtab = 0;  // 1 + coef index of a 2^rb pair-phase table, 0: none
+        if (carry) {
+            for (const GTerm& g : gterms_) {  // physical slot bits -> true tile bits
+                std::vector<Amp> dl(4, Amp(1.0, 0.0));
+                dl[size_t(2 * (1 ^ flip(g.a)) + (1 ^ flip(g.b)))] = g.v;
+                carry_.push_back({map_[g.a], map_[g.b], dl});
+            }
+            gterms_.clear();
+        } else if (!gterms_.empty()) {
+            std::vector<Amp> D(size_t(1) << rb_, Amp(1.0, 0.0));
+            for (size_t sidx = 0; sidx < D.size(); sidx++)
+                for (const GTerm& g : gterms_)
+                    if (((sidx >> g.a) & 1) && ((sidx >> g.b) & 1)) D[sidx] *= g.v;
+            dtab = uint16_t(1 + addCoef(D));
+            gterms_.clear();
+            any = true;
+        }
         if (!any) return;
         // (1/sqrt2)^h exactly: a power of two, times 1/sqrt2 when h is odd.
         const double root = 1.0 / std::sqrt(2.0);
         const double scale = std::ldexp(hcount_ % 2 ? root : 1.0, -(hcount_ / 2));
-        emit(OP_FLUSH, 0, 0, 0, addCoef({Amp(scale, 0.0)}));
+        emit(OP_FLUSH, 0, 0, 0, addCoef({Amp(scale, 0.0)}), dtab);
         hcount_ = 0;
         pendScalar_ = false;
         std::fill(pendSlot_, pendSlot_ + kMaxRegBits, false);
+    }
+
+    // Re-issue carried pair phases after an exchange (new map, no flips).
+    void relowerCarried() {
+        std::vector<Carried> c;
+        c.swap(carry_);
+        for (const Carried& x : c) diag2(x.a, x.b, x.d);
     }
 
     void scalar(const std::vector<Amp>& d, OpType t, int a = 0, int b = 0) {
@@ -629,6 +707,20 @@ private:
         std::vector<Amp> d(4);  // physical entries
         for (int b0 = 0; b0 < 2; b0++)
             for (int b1 = 0; b1 < 2; b1++) d[size_t(2 * b0 + b1)] = dl[size_t(2 * (b0 ^ f0) + (b1 ^ f1))];
+        if (isReg(s0) && isReg(s1) && deferPairPhases()) {
+            // d(b0, b1) = d00 (b0 ? r0) (b1 ? r1) (b0 b1 ? g): the constant and
+            // single-slot parts join the pending scalar / slot phases, the pair
+            // part waits (gterms_) for the first non-diagonal op on either slot
+            if (d[0] == Amp(1.0, 0.0) && d[1] == d[0] && d[2] == d[0] && d[3] == d[0]) return;
+            batchAny_ = true;
+            if (d[0] != Amp(1.0, 0.0)) mulP(0, [&](int) { return d[0]; });
+            const Amp r0 = ratio(d[2], d[0]), r1 = ratio(d[1], d[0]);
+            if (r0 != Amp(1.0, 0.0)) mulR(s0, 0, [&](int) { return r0; });
+            if (r1 != Amp(1.0, 0.0)) mulR(s1, 0, [&](int) { return r1; });
+            const Amp g = ratio(d[3], d[0] * r0 * r1);
+            if (g != Amp(1.0, 0.0)) gterms_.push_back({s0, s1, g});
+            return;
+        }
         if (isReg(s0) && isReg(s1)) {
             // one non-unit entry: multiply only that quarter (CP-like)
             int nonUnit = -1, count = 0;
@@ -696,7 +788,7 @@ private:
                 const int t = inv_[g.targets[0]], c = inv_[g.controls[0]];
                 emitBatch();
                 const int pol = flip(c);  // physical control value that means logical 1 is (1 ^ pol)
-                if (!isReg(c) && isReg(t) && pendSlot_[t]) {
+                if (!isReg(c) && isReg(t) && pendSlot_[t] && !slotHasPairPhase(t)) {
                     // X_t diag(1, r) X_t = r diag(1, 1/r): carry the pending phase
                     // through the swap per thread instead of flushing 16 amplitudes
                     emit(OP_CX_PEND, t, c - rb_, pol << 1);
@@ -797,6 +889,16 @@ private:
     uint32_t maskR_[kMaxRegBits] = {};
     bool usedR_[kMaxRegBits] = {};
     std::vector<RegOp> regOps_;
+    struct GTerm {
+        int a, b;  // physical register slots: amplitudes with both slot bits 1 get v
+        Amp v;
+    };
+    std::vector<GTerm> gterms_;
+    struct Carried {
+        int a, b;              // true tile bits
+        std::vector<Amp> d;    // 4-entry diagonal, first bit = MSB
+    };
+    std::vector<Carried> carry_;
     std::vector<Term> ctaP_;            // CTA-dependent factor of every amplitude (this batch)
     std::vector<Term> ctaBit_[16];      // ... of the amplitudes whose tile bit b is 1
     int ncta_ = 0, ncterms_ = 0;

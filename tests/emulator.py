@@ -7,7 +7,7 @@ import numpy as np
 
 OPS = ["MAT1", "H", "CX", "DIAG1_R", "DIAG2_RR", "CPHASE_RR", "PEND_R", "PEND_RT", "SCAL", "SCAL_T",
        "SCAL_TT", "FLUSH_SLOT", "FLUSH", "DTABLE", "DENSE", "EXCHANGE", "SCAL_TAB", "PEND_TAB", "SCAL_CTA",
-       "PEND_CTA", "SCAL_TCTA", "CX_PEND"]
+       "PEND_CTA", "SCAL_TCTA", "FLUSH_SLOT_G", "CX_PEND"]
 
 
 def pext8(t, m):
@@ -154,6 +154,13 @@ def _run_pass(state, n, P, gt):
                 Pt *= gt[oc + pext8(tid, ox16)]
             elif name == "PEND_TAB":
                 R[:, oa] *= gt[oc + pext8(tid, ox16)]
+            elif name == "FLUSH_SLOT_G":
+                bits = [kk for kk in range(rb) if (ob >> kk) & 1]
+                for sv in range(na):
+                    if (sv >> oa) & 1:
+                        j = sum(((sv >> b) & 1) << q for q, b in enumerate(bits))
+                        a[:, sv] *= R[:, oa] * coef[oc + j]
+                R[:, oa] = 1
             elif name == "CX_PEND":
                 act = (bit(tid, ob) ^ ((ok >> 1) & 1)) == 1
                 Pt = np.where(act, Pt * R[:, oa], Pt)
@@ -180,6 +187,8 @@ def _run_pass(state, n, P, gt):
                 for kk in range(rb):
                     sel = bit(s_idx, kk) == 1
                     a[:, sel] *= R[:, kk][:, None]
+                if oc16:
+                    a *= coef[oc16 - 1:oc16 - 1 + na][None, :]
                 R[:] = 1
                 Pt[:] = 1
             elif name == "DTABLE":
