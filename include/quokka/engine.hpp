@@ -74,6 +74,6 @@ private:
 };
 
 // Runs a whole single-rank Program on the device (no host state copy).
-void simulateProgramDevice(DeviceState& st, const Program& p, const Config& cfg);
+void simulateProgramDevice(DeviceState& st, const Program& p, const Config& cfg, Index initial = 0);
 
 }  // namespace quokka

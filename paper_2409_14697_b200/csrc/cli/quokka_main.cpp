@@ -1,0 +1,276 @@
+// `quokka_b200`: command-line drop-in for the reference CLI's hot-path
+// subcommands (proj/tools/main.cpp:290-377), on the B200 engine.
+//
+//   quokka_b200 optimize -i circuit [-o program] --config cfg.ini
+//   quokka_b200 optimize circuit chunk inrank total ims xrs fusion_qbit fusion
+//   quokka_b200 simulate -i cfg.ini -c program [--raw] [--dump-state] [--initial K]
+//   quokka_b200 gen qft|qaoa|bv|gate|random|grover -n N [-o file] [-l L] [-g G]
+//                   [--seed S] [--secret X] [--kind K]
+//
+// Same outputs and exit codes as the reference: program / circuit text,
+// "qubits: / gates: / wall_time_s: / norm:" on stdout, "index re im" lines for
+// --dump-state (<= 20 qubits, logical order), 1 ParseError, 2 ConfigError
+// (also bad command lines), 3 SimulationError.  The simulation runs on cuda:0
+// with the state resident in HBM; simulate's wall time spans initState to the
+// last item (main.cpp:126-145).  No CLI11: a small parser of its own.
+#include <algorithm>
+#include <cctype>
+#include <chrono>
+#include <cstdint>
+#include <cstdlib>
+#include <fstream>
+#include <iostream>
+#include <map>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "qk.h"
+#include "quokka/distributed.hpp"
+#include "quokka/engine.hpp"
+#include "quokka/optimizer.hpp"
+#include "quokka/tools.hpp"
+
+namespace {
+
+using namespace quokka;
+
+struct Args {
+    std::vector<std::string> positional;
+    std::map<std::string, std::string> opts;  // canonical long name -> value ("" for flags)
+};
+
+// name aliases: short -> long, and which options are flags
+Args parseArgs(int argc, char** argv, int first, const std::map<std::string, std::string>& alias,
+               const std::vector<std::string>& flags) {
+    Args a;
+    for (int i = first; i < argc; i++) {
+        std::string t = argv[i];
+        if (t.size() > 1 && t[0] == '-' && !(t.size() > 1 && (std::isdigit(static_cast<unsigned char>(t[1])) != 0))) {
+            std::string name = t, value;
+            const size_t eq = t.find('=');
+            if (eq != std::string::npos) {
+                name = t.substr(0, eq);
+                value = t.substr(eq + 1);
+            }
+            auto it = alias.find(name);
+            if (it == alias.end()) throw ConfigError("unknown option " + name);
+            name = it->second;
+            const bool isFlag = std::find(flags.begin(), flags.end(), name) != flags.end();
+            if (!isFlag && eq == std::string::npos) {
+                if (i + 1 >= argc) throw ConfigError("option " + name + " needs a value");
+                value = argv[++i];
+            }
+            a.opts[name] = value;
+        } else {
+            a.positional.push_back(t);
+        }
+    }
+    return a;
+}
+
+void writeText(const std::string& path, const std::string& text) {
+    if (path.empty()) {
+        std::cout << text;
+        return;
+    }
+    std::ofstream out(path);
+    if (!out) throw ParseError("cannot open output file: " + path);
+    out << text;
+}
+
+long long toInt(const std::string& s, const std::string& what) {
+    try {
+        size_t pos = 0;
+        const long long v = std::stoll(s, &pos, 0);
+        if (pos != s.size()) throw std::invalid_argument(s);
+        return v;
+    } catch (...) {
+        throw ConfigError("bad numeric parameter '" + s + "' for " + what);
+    }
+}
+
+double seconds(std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+    return std::chrono::duration<double>(b - a).count();
+}
+
+int runOptimize(const Args& a) {
+    Config cfg;
+    std::string input = a.opts.count("--input") ? a.opts.at("--input") : "";
+    std::vector<std::string> nums = a.positional;
+    if (a.opts.count("--config")) {
+        if (!nums.empty() && !(input.empty() && nums.size() == 1))
+            throw ConfigError("--config and the positional parameter form are exclusive");
+        if (input.empty() && !nums.empty()) input = nums.front();
+        cfg = parseConfigFile(a.opts.at("--config"));
+    } else {
+        // compatibility form: circuit chunk inrank total ims xrs fusion_qbit fusion
+        if (input.empty() && !nums.empty()) {
+            input = nums.front();
+            nums.erase(nums.begin());
+        }
+        if (nums.size() != 7)
+            throw ConfigError("expected: optimize <circuit> <chunk_qbit> <inrank_qbit> <total_qbit> <ims> <xrs> "
+                              "<fusion_qbit> <fusion>");
+        long long v[7];
+        for (int i = 0; i < 7; i++) v[i] = toInt(nums[size_t(i)], "optimize");
+        cfg.chunkQubits = int(v[0]);
+        cfg.totalQubits = int(v[2]);
+        cfg.rankQubits = int(v[2] - v[1]);
+        cfg.imsEnabled = v[3] != 0;
+        cfg.xrsEnabled = v[4] != 0;
+        cfg.fusionQubits = int(v[5]);
+        cfg.fusionEnabled = v[6] != 0;
+        cfg.diagonalFusionEnabled = v[6] != 0;
+        cfg.finalize();
+    }
+    if (input.empty()) throw ConfigError("no circuit file given");
+    const Circuit c = parseCircuitFile(input, cfg.totalQubits);
+    const auto t0 = std::chrono::steady_clock::now();
+    const Program p = aioOptimize(c, cfg);
+    const auto t1 = std::chrono::steady_clock::now();
+    writeText(a.opts.count("--output") ? a.opts.at("--output") : "", serializeProgram(p));
+    std::cerr << "gates: " << c.gates.size() << " blocks: " << p.blockCount()
+              << " in-memory swaps: " << p.swapCount(SwapOp::InMemory)
+              << " cross-rank swaps: " << p.swapCount(SwapOp::CrossRank) << " wall_time_s: " << seconds(t0, t1)
+              << "\n";
+    return 0;
+}
+
+int runSimulate(const Args& a) {
+    if (!a.opts.count("--config") || !a.opts.count("--circuit"))
+        throw ConfigError("simulate needs -i <config> and -c <program>");
+    const Config cfg = parseConfigFile(a.opts.at("--config"));
+    const Index initial = a.opts.count("--initial") ? Index(toInt(a.opts.at("--initial"), "--initial")) : 0;
+    const bool dump = a.opts.count("--dump-state") != 0;
+    if (dump && cfg.totalQubits > 20) throw ConfigError("state dumps are limited to 20 qubits");
+    size_t gates = 0;
+    double wall = 0, norm = 0;
+    StateVector state;
+    QubitLayout layout = QubitLayout::identity(cfg.totalQubits);
+    if (a.opts.count("--raw")) {  // gate by gate (engine.cpp:299-322 semantics), on the device
+        const Circuit c = parseCircuitFile(a.opts.at("--circuit"), cfg.totalQubits);
+        gates = c.gates.size();
+        const auto t0 = std::chrono::steady_clock::now();
+        state = simulateGateByGate(c, initial);
+        wall = seconds(t0, std::chrono::steady_clock::now());
+        norm = state.norm();
+    } else {
+        const Program p = parseProgramFile(a.opts.at("--circuit"), cfg);
+        gates = p.gateCount();
+        if (cfg.rankQubits > 0) {
+            const auto t0 = std::chrono::steady_clock::now();
+            MultiRankResult r = spawnRanks(p, cfg, initial);
+            wall = seconds(t0, std::chrono::steady_clock::now());
+            state = std::move(r.state);
+            layout = r.layout;
+            size_t sent = 0, peak = 0;
+            for (const RankStats& st : r.stats) {
+                sent += st.bytesSent;
+                peak = std::max(peak, st.peakBufferBytes);
+            }
+            std::cerr << "ranks: " << (1 << cfg.rankQubits) << " bytes_sent: " << sent
+                      << " peak_buffer_bytes: " << peak << "\n";
+            norm = state.norm();
+        } else {
+            DeviceState dev(cfg.totalQubits, 0, 0, 0, cfg.bufferQubits);  // resident: no host copy
+            const auto t0 = std::chrono::steady_clock::now();
+            simulateProgramDevice(dev, p, cfg, initial);
+            wall = seconds(t0, std::chrono::steady_clock::now());
+            norm = dev.norm();
+            layout = p.finalLayout;
+            if (dump) {
+                state.nQubits = cfg.totalQubits;
+                state.amps.resize(size_t(1) << cfg.totalQubits);
+                dev.download(0, state.amps.size(), state.amps.data());
+            }
+        }
+    }
+    std::cout << "qubits: " << cfg.totalQubits << "\n";
+    std::cout << "gates: " << gates << "\n";
+    std::cout << "wall_time_s: " << fmt17(wall) << "\n";
+    std::cout << "norm: " << fmt17(norm) << "\n";
+    if (dump) {
+        const StateVector logical = layoutApply(state, layout);
+        for (Index i = 0; i < Index(logical.amps.size()); i++)
+            std::cout << i << " " << fmt17(logical.amps[i].real()) << " " << fmt17(logical.amps[i].imag()) << "\n";
+    }
+    return 0;
+}
+
+GateKind kindFromName(const std::string& name) {
+    static const std::pair<const char*, GateKind> table[] = {
+        {"H", GateKind::H},   {"U", GateKind::U},     {"X", GateKind::X},   {"CX", GateKind::CX},
+        {"CP", GateKind::CP}, {"SWAP", GateKind::SWAP}, {"RX", GateKind::RX}, {"RY", GateKind::RY},
+        {"RZ", GateKind::RZ}, {"RZZ", GateKind::RZZ},
+    };
+    for (const auto& e : table)
+        if (name == e.first) return e.second;
+    throw ConfigError("unknown gate kind '" + name + "'");
+}
+
+int runGen(const Args& a) {
+    if (a.positional.size() != 1) throw ConfigError("gen needs exactly one generator name");
+    if (!a.opts.count("--qubits")) throw ConfigError("gen needs -n <qubits>");
+    const std::string which = a.positional[0];
+    const int n = int(toInt(a.opts.at("--qubits"), "-n"));
+    auto opt = [&](const char* k, long long d) { return a.opts.count(k) ? toInt(a.opts.at(k), k) : d; };
+    const std::uint64_t seed = std::uint64_t(opt("--seed", 12345));
+    Circuit c;
+    if (which == "qft") c = genQft(n);
+    else if (which == "qaoa") c = genQaoa(n, int(opt("--layers", 1)), seed);
+    else if (which == "bv") c = a.opts.count("--secret") ? genBv(n, std::uint64_t(opt("--secret", 0))) : genBvAllOnes(n);
+    else if (which == "gate") c = genGateBench(kindFromName(a.opts.count("--kind") ? a.opts.at("--kind") : "H"), n);
+    else if (which == "random") c = genRandom(n, int(opt("--gates", 100)), seed);
+    else if (which == "grover") c = genGrover(n, std::uint64_t(opt("--secret", 5)), int(opt("--layers", 0)));
+    else throw ConfigError("unknown generator '" + which + "'");
+    writeText(a.opts.count("--output") ? a.opts.at("--output") : "", serializeCircuit(c));
+    std::cerr << "qubits: " << c.nQubits << " gates: " << c.gates.size() << "\n";
+    return 0;
+}
+
+int usage() {
+    std::cerr << "usage: quokka_b200 optimize|simulate|gen ... (see the header of csrc/cli/quokka_main.cpp)\n";
+    return 2;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+    if (argc < 2) return usage();
+    const std::string cmd = argv[1];
+    try {
+        if (cmd == "optimize")
+            return runOptimize(parseArgs(argc, argv, 2,
+                                         {{"-i", "--input"}, {"--input", "--input"}, {"-o", "--output"},
+                                          {"--output", "--output"}, {"--config", "--config"}},
+                                         {}));
+        if (cmd == "simulate")
+            return runSimulate(parseArgs(argc, argv, 2,
+                                         {{"-i", "--config"}, {"--config", "--config"}, {"-c", "--circuit"},
+                                          {"--circuit", "--circuit"}, {"--raw", "--raw"},
+                                          {"--dump-state", "--dump-state"}, {"--initial", "--initial"},
+                                          {"--threads", "--threads"}},
+                                         {"--raw", "--dump-state"}));
+        if (cmd == "gen")
+            return runGen(parseArgs(argc, argv, 2,
+                                    {{"-n", "--qubits"}, {"--qubits", "--qubits"}, {"-o", "--output"},
+                                     {"--output", "--output"}, {"-l", "--layers"}, {"--layers", "--layers"},
+                                     {"-g", "--gates"}, {"--gates", "--gates"}, {"--seed", "--seed"},
+                                     {"--secret", "--secret"}, {"--kind", "--kind"}},
+                                    {}));
+        return usage();
+    } catch (const ParseError& e) {
+        std::cerr << "error: " << e.what() << "\n";
+        return 1;
+    } catch (const ConfigError& e) {
+        std::cerr << "error: " << e.what() << "\n";
+        return 2;
+    } catch (const SimulationError& e) {
+        std::cerr << "error: " << e.what() << "\n";
+        return 3;
+    } catch (const std::exception& e) {
+        std::cerr << "error: " << e.what() << "\n";
+        return 3;
+    }
+}

@@ -208,10 +208,10 @@ void DeviceState::upload(Index off, Index cnt, const Amp* host) {
 }
 void DeviceState::synchronize() const { check(qk_synchronize(st_)); }
 
-void simulateProgramDevice(DeviceState& st, const Program& p, const Config& cfg) {
+void simulateProgramDevice(DeviceState& st, const Program& p, const Config& cfg, Index initial) {
     ProgramHandle h(p, cfg);
     const qk_config c = toC(cfg);
-    check(qk_simulate(st.handle(), h.p, &c, 0, nullptr));
+    check(qk_simulate(st.handle(), h.p, &c, initial, nullptr));
 }
 
 // ---- multi-rank (distributed.hpp) -------------------------------------------------
