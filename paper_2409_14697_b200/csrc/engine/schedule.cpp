@@ -59,6 +59,14 @@ bool deferPairPhases() {
     return v;
 }
 
+// QK_WIDE_FORCE=1: reserve a register slot for memory bit 0 even when the
+// first segment's gates could use all slots (costs an exchange, saves half
+// the load instructions).  Default: only use a free slot.
+bool wideLoadsForceSlot() {
+    static const bool v = envInt("QK_WIDE_FORCE", 0, 0, 1) != 0;
+    return v;
+}
+
 bool halfExchanges() {
     static const bool v = envInt("QK_JIT_TMA", 0, 0, 1) != 0;
     return v;
@@ -319,7 +327,7 @@ private:
         if (wantBit0 && std::find(regs.begin(), regs.end(), 0) == regs.end()) {
             if (int(regs.size()) < rb_) {
                 regs.push_back(0);
-            } else {
+            } else if (wideLoadsForceSlot()) {
                 std::vector<char> must(static_cast<size_t>(ct_), 0);
                 if (i < tg_.size())
                     for (int b : regNeeds(tg_[i], orig_[i])) must[size_t(b)] = 1;
