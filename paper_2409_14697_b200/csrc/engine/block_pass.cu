@@ -423,6 +423,11 @@ __global__ void __launch_bounds__(1 << (CT - RB), MINB)
                 }
                 case OP_SCAL_TAB: Pt = cmul(Pt, __ldg(gtab + o.c + pextT(tid, o.x16))); break;
                 case OP_SCAL_CTA: Pt = cmul(Pt, F[o.c]); break;
+                case OP_RESET:
+                    Pt = make_double2(1.0, 0.0);
+#pragma unroll
+                    for (int k = 0; k < RB; k++) R[k] = make_double2(1.0, 0.0);
+                    break;
                 case OP_FLUSH_SLOT_G: {
                     double2 rk = R[0];
 #pragma unroll

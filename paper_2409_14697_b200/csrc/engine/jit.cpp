@@ -576,6 +576,13 @@ private:
             case qkdev::OP_FLUSH:
                 flush(P_.coef[2 * d.c], d.c16 ? &P_.coef[2 * (d.c16 - 1)] : nullptr);
                 return;
+            case qkdev::OP_RESET:
+                if (dirtyP_) o_ << "  P = C2(1.0, 0.0);\n";
+                for (int k = 0; k < rb_; k++)
+                    if (dirtyR_[k]) o_ << "  R" << k << " = C2(1.0, 0.0);\n";
+                dirtyP_ = false;
+                for (int k = 0; k < rb_; k++) dirtyR_[k] = false;
+                return;
             case qkdev::OP_FLUSH_SLOT_G: {
                 // amplitudes with slot-a bit 1 *= R_a * G[pext(s, b)] (G literal)
                 std::vector<int> bits;
@@ -744,7 +751,7 @@ private:
 // ---- compile / load / launch -------------------------------------------------
 
 // Bump when the generated code changes for the same PassParams (on-disk cache key).
-constexpr uint64_t kGeneratorVersion = 13;
+constexpr uint64_t kGeneratorVersion = 14;
 
 uint64_t hashPass(const PassParams& P) {
     uint64_t h = 1469598103934665603ull ^ (kGeneratorVersion * 0x9E3779B97F4A7C15ull) ^ (usePrefetch() ? 1u : 0u) ^ (usePersistent() ? 2u : 0u) ^

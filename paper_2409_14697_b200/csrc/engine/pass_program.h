@@ -72,6 +72,7 @@ enum OpType : uint8_t {
     OP_PEND_CTA,      // R[a] *= F[c]
     OP_SCAL_TCTA,     // P *= bit_b(thread) ? F[c] : 1
     OP_FLUSH_SLOT_G,  // amplitudes with slot-a bit 1 *= R[a] * coef[c + pext(slot bits, b)]; R[a] = 1
+    OP_RESET,         // P = 1, R[*] = 1 (the pending factors are re-issued for the next segment)
     OP_CX_PEND,       // before a thread-controlled CX on slot a (control thread bit b, k bit1 = polarity):
                       // where it fires, P *= R[a]; R[a] = 1 / R[a]  (the pending phase follows the swap)
 };

@@ -67,6 +67,14 @@ bool wideLoadsForceSlot() {
     return v;
 }
 
+// QK_CARRY (default 1): at an exchange, pending diagonal factors are not
+// applied; the per-thread accumulators are reset and the pending diagonal
+// gates re-issued in the next segment's map (no per-amplitude flush).
+bool carryPending() {
+    static const bool v = envInt("QK_CARRY", 1, 0, 1) != 0;
+    return v;
+}
+
 bool halfExchanges() {
     static const bool v = envInt("QK_JIT_TMA", 0, 0, 1) != 0;
     return v;
@@ -216,13 +224,17 @@ public:
         batchReset();
         gterms_.clear();
         carry_.clear();
+        pend_.clear();
+        pendConst_ = Amp(1.0, 0.0);
+        carryOk_ = true;
+        carried_ = false;
         chooseMap(i, nullptr, wideAccess() && tilePhys_[0] == 0);
         std::memcpy(P_->map_in[0], map_, sizeof map_);
 
         const size_t first = i;
         double flops = 0;
         while (i < tg_.size()) {
-            const int queued = int(regOps_.size() + gterms_.size() + 2 * carry_.size());  // deferred work
+            const int queued = int(regOps_.size() + gterms_.size() + 2 * carry_.size() + 3 * pend_.size());
             if (kMaxOps - nops_ - queued < 16 + ct_ || kMaxCoef - ncoef_ - 4 * queued - pendingCtaTerms() < 24 ||
                 kMaxContrib - ncontrib_ < 48 + ct_ || kMaxSegs - seg_ < 3 || kMaxCtaFactors - ncta_ < ct_ + 2 ||
                 kMaxCtaTerms - ncterms_ - pendingCtaTerms() < 12)
@@ -446,6 +458,7 @@ private:
     // involving it) to the amplitudes whose slot bit is 1.
     void flushSlot(int slot) {
         if (!isReg(slot)) return;
+        consumeSlot(slot);
         std::vector<GTerm> mine, rest;
         for (const GTerm& g : gterms_) (g.a == slot || g.b == slot ? mine : rest).push_back(g);
         if (mine.empty()) {
@@ -488,6 +501,23 @@ private:
     // carry: an exchange follows -- pair phases (constants, known here) are
     // not applied but re-issued as diagonal gates in the next segment's map.
     void flushAll(bool carry = false) {
+        if (carry && carryOk_ && carryPending() && deferPairPhases()) {
+            // nothing is applied: drop the accumulators and the unemitted batch;
+            // reissuePending() re-lowers every pending gate in the next map
+            batchReset();
+            gterms_.clear();
+            bool any = pendScalar_;
+            for (int s = 0; s < rb_; s++) any |= pendSlot_[s];
+            if (any) emit(OP_RESET);
+            pendScalar_ = false;
+            std::fill(pendSlot_, pendSlot_ + kMaxRegBits, false);
+            carried_ = true;
+            return;
+        }
+        carried_ = false;
+        pend_.clear();  // everything below is applied
+        pendConst_ = Amp(1.0, 0.0);
+        carryOk_ = true;
         emitBatch();
         bool any = hcount_ > 0 || pendScalar_;
         for (int s = 0; s < rb_; s++) any |= pendSlot_[s];
@@ -518,11 +548,19 @@ private:
         std::fill(pendSlot_, pendSlot_ + kMaxRegBits, false);
     }
 
-    // Re-issue carried pair phases after an exchange (new map, no flips).
+    // Re-issue carried pair phases (or every pending gate) after an exchange
+    // (new map, no flips).
     void relowerCarried() {
+        if (carried_) {
+            carried_ = false;
+            carryOk_ = true;
+            carry_.clear();
+            reissuePending();
+            return;
+        }
         std::vector<Carried> c;
         c.swap(carry_);
-        for (const Carried& x : c) diag2(x.a, x.b, x.d);
+        for (const Carried& x : c) gate2(x.a, x.b, x.d);
     }
 
     void scalar(const std::vector<Amp>& d, OpType t, int a = 0, int b = 0) {
@@ -656,6 +694,70 @@ private:
         batchReset();
     }
 
+    // ---- pending diagonal gates (carried across exchanges) -----------------
+    struct PendGate {
+        int q0, q1;             // logical tile bits or kCta + memory bit; q1 < 0: one-qubit
+        std::vector<Amp> d;     // logical diagonal (q0 = MSB)
+    };
+    std::vector<PendGate> pend_;
+    Amp pendConst_ = Amp(1.0, 0.0);
+    bool carryOk_ = true;
+
+    void gate1(int q, const std::vector<Amp>& d) {
+        pend_.push_back({q, -1, d});
+        diag1(q, d);
+    }
+    void gate2(int q0, int q1, const std::vector<Amp>& d) {
+        pend_.push_back({q0, q1, d});
+        diag2(q0, q1, d);
+    }
+    bool touchesPending(int q) const {
+        for (const PendGate& pg : pend_)
+            if (pg.q0 == q || pg.q1 == q) return true;
+        return false;
+    }
+    // The slot-`slot` part of every pending gate has just been applied to the
+    // amplitudes (physical slot bit 1 half): what stays pending is the gate
+    // restricted to physical bit 0, i.e. logical value flip(slot).
+    void consumeSlot(int slot) {
+        const int q = map_[slot], v = flip(slot);
+        std::vector<PendGate> keep;
+        for (PendGate& pg : pend_) {
+            if (pg.q0 != q && pg.q1 != q) {
+                keep.push_back(pg);
+                continue;
+            }
+            if (pg.q1 < 0) {
+                pendConst_ *= pg.d[size_t(v)];
+                continue;
+            }
+            // restrict the 2-qubit diagonal: remaining one-qubit gate on the other bit
+            const bool msb = pg.q0 == q;
+            const int other = msb ? pg.q1 : pg.q0;
+            std::vector<Amp> r(2);
+            for (int x = 0; x < 2; x++) r[size_t(x)] = msb ? pg.d[size_t(2 * v + x)] : pg.d[size_t(2 * x + v)];
+            if (r[0] == r[1]) pendConst_ *= r[0];
+            else keep.push_back({other, -1, r});
+        }
+        pend_.swap(keep);
+    }
+    // After an exchange: the accumulators were reset; re-issue what is pending.
+    void reissuePending() {
+        std::vector<PendGate> p;
+        p.swap(pend_);
+        const Amp c = pendConst_;
+        pendConst_ = Amp(1.0, 0.0);
+        if (c != Amp(1.0, 0.0)) {
+            batchAny_ = true;
+            mulP(0, [&](int) { return c; });
+            pendConst_ = c;
+        }
+        for (const PendGate& pg : p) {
+            if (pg.q1 < 0) gate1(pg.q0, pg.d);
+            else gate2(pg.q0, pg.q1, pg.d);
+        }
+    }
+
     // amplitude *= d[logical bit q].  Slot semantics are physical: a flipped
     // slot holds the logical bit inverted, so the entry pair swaps.
     void diag1(int q, std::vector<Amp> d) {
@@ -778,18 +880,19 @@ private:
                 hcount_++;
                 if (flip(s)) {  // H on a flipped slot leaves it unflipped with the |1> half negated
                     flips_ ^= 1u << s;
-                    pending(s, {Amp(-1.0, 0.0)}, OP_PEND_R);
+                    gate1(g.targets[0], {Amp(1.0, 0.0), Amp(-1.0, 0.0)});
                 }
                 return;
             }
             case GateKind::X:  // relabel: no data moves
+                if (touchesPending(g.targets[0])) carryOk_ = false;  // pending factors would need X conjugation
                 flips_ ^= 1u << inv_[g.targets[0]];
                 return;
             case GateKind::U:
             case GateKind::RX:
             case GateKind::RY: {
                 const std::vector<Amp> m = quokka::gateMatrix(orig);
-                if (diagonalMatrix(m)) return diag1(g.targets[0], {m[0], m[3]});
+                if (diagonalMatrix(m)) return gate1(g.targets[0], {m[0], m[3]});
                 return mat1(g.targets[0], m);
             }
             case GateKind::CX: {
@@ -801,6 +904,7 @@ private:
                     // through the swap per thread instead of flushing 16 amplitudes
                     emit(OP_CX_PEND, t, c - rb_, pol << 1);
                     pendScalar_ = true;
+                    carryOk_ = false;  // thread-conditional rewrite of the pending factors
                 } else {
                     flushSlot(t);
                 }
@@ -814,23 +918,28 @@ private:
                 map_[sb] = uint8_t(a);
                 inv_[a] = sb;
                 inv_[b] = sa;
+                for (PendGate& pg : pend_)  // the data that was logical a is now logical b
+                    for (int* q : {&pg.q0, &pg.q1}) {
+                        if (*q == a) *q = b;
+                        else if (*q == b) *q = a;
+                    }
                 return;
             }
             case GateKind::RZ:
-                diag1(g.targets[0], quokka::gateDiagonal(orig));
+                gate1(g.targets[0], quokka::gateDiagonal(orig));
                 return;
             case GateKind::CP:
-                diag2(g.controls[0], g.targets[0], quokka::gateDiagonal(orig));
+                gate2(g.controls[0], g.targets[0], quokka::gateDiagonal(orig));
                 return;
             case GateKind::RZZ: {
                 const std::vector<int> qs = g.qubits();
-                diag2(qs[0], qs[1], quokka::gateDiagonal(orig));
+                gate2(qs[0], qs[1], quokka::gateDiagonal(orig));
                 return;
             }
             case GateKind::FusedDiag: {
                 const int k = int(g.targets.size());
-                if (k == 1) return diag1(g.targets[0], orig.payload);
-                if (k == 2) return diag2(g.targets[0], g.targets[1], orig.payload);
+                if (k == 1) return gate1(g.targets[0], orig.payload);
+                if (k == 2) return gate2(g.targets[0], g.targets[1], orig.payload);
                 const uint16_t c16 = uint16_t(ncontrib_);
                 uint32_t x = 0;
                 for (int s = 0; s < ct_; s++) P_->contrib[ncontrib_ + s] = 0;
@@ -858,7 +967,7 @@ private:
             case GateKind::FusedDense: {
                 const int k = int(g.targets.size());
                 if (k == 1) {
-                    if (diagonalMatrix(orig.payload)) return diag1(g.targets[0], {orig.payload[0], orig.payload[3]});
+                    if (diagonalMatrix(orig.payload)) return gate1(g.targets[0], {orig.payload[0], orig.payload[3]});
                     return mat1(g.targets[0], orig.payload);
                 }
                 // canonical slots: sub-index bit b <-> slot b; flipped slots permute the matrix
@@ -907,6 +1016,7 @@ private:
         std::vector<Amp> d;    // 4-entry diagonal, first bit = MSB
     };
     std::vector<Carried> carry_;
+    bool carried_ = false;
     std::vector<Term> ctaP_;            // CTA-dependent factor of every amplitude (this batch)
     std::vector<Term> ctaBit_[16];      // ... of the amplitudes whose tile bit b is 1
     int ncta_ = 0, ncterms_ = 0;

@@ -7,7 +7,7 @@ import numpy as np
 
 OPS = ["MAT1", "H", "CX", "DIAG1_R", "DIAG2_RR", "CPHASE_RR", "PEND_R", "PEND_RT", "SCAL", "SCAL_T",
        "SCAL_TT", "FLUSH_SLOT", "FLUSH", "DTABLE", "DENSE", "EXCHANGE", "SCAL_TAB", "PEND_TAB", "SCAL_CTA",
-       "PEND_CTA", "SCAL_TCTA", "FLUSH_SLOT_G", "CX_PEND"]
+       "PEND_CTA", "SCAL_TCTA", "FLUSH_SLOT_G", "RESET", "CX_PEND"]
 
 
 def pext8(t, m):
@@ -154,6 +154,9 @@ def _run_pass(state, n, P, gt):
                 Pt *= gt[oc + pext8(tid, ox16)]
             elif name == "PEND_TAB":
                 R[:, oa] *= gt[oc + pext8(tid, ox16)]
+            elif name == "RESET":
+                Pt[:] = 1
+                R[:] = 1
             elif name == "FLUSH_SLOT_G":
                 bits = [kk for kk in range(rb) if (ob >> kk) & 1]
                 for sv in range(na):
