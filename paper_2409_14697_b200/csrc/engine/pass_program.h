@@ -36,8 +36,8 @@ constexpr int kMaxOps = 700;
 constexpr int kMaxCoef = 860;               // complex coefficients (double2)
 constexpr int kMaxSegs = 96;
 constexpr int kMaxContrib = 512;            // uint16 words for fused-diagonal index maps
-constexpr int kMaxCtaFactors = 64;          // per-CTA diagonal factors (functions of non-tile bits)
-constexpr int kMaxCtaTerms = 320;
+constexpr int kMaxCtaFactors = 128;         // per-CTA diagonal factors (functions of non-tile bits)
+constexpr int kMaxCtaTerms = 640;
 
 // Register bits used for a tile of ct bits: 16 amplitudes per thread up to
 // ct = 12 (<= 256 threads, no register cap), 32 per thread at ct = 13 (256

@@ -24,6 +24,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -234,11 +235,21 @@ public:
         const size_t first = i;
         double flops = 0;
         while (i < tg_.size()) {
-            const int queued = int(regOps_.size() + gterms_.size() + 2 * carry_.size() + 3 * pend_.size());
-            if (kMaxOps - nops_ - queued < 16 + ct_ || kMaxCoef - ncoef_ - 4 * queued - pendingCtaTerms() < 24 ||
-                kMaxContrib - ncontrib_ < 48 + ct_ || kMaxSegs - seg_ < 3 || kMaxCtaFactors - ncta_ < ct_ + 2 ||
-                kMaxCtaTerms - ncterms_ - pendingCtaTerms() < 12)
+            // room for what is still queued: batched register ops, pair-phase
+            // flushes, and one re-issue of the pending gates (tables fold into
+            // <= rb + 2 ops; CTA-bit gates add up to 2 terms / coefficients each)
+            const int pendCta = carryAffordable() ? pendCtaCost() : 0;
+            const int queuedOps = int(regOps_.size() + gterms_.size() + 2 * carry_.size()) + (pend_.empty() ? 0 : rb_ + ct_ + 4);
+            const int queuedCoef = int(4 * regOps_.size() + 17 * gterms_.size() + 8 * carry_.size()) + pendCta;
+            if (kMaxOps - nops_ - queuedOps < 16 + ct_ || kMaxCoef - ncoef_ - queuedCoef - pendingCtaTerms() < 40 ||
+                kMaxContrib - ncontrib_ < 48 + ct_ || kMaxSegs - seg_ < 3 || kMaxCtaFactors - ncta_ < 2 * ct_ + 4 ||
+                kMaxCtaTerms - ncterms_ - pendingCtaTerms() - pendCta < 12) {
+                if (std::getenv("QK_DEBUG_SPLIT"))
+                    std::fprintf(stderr, "pass split at gate %zu: ops %d+%d coef %d+%d+%d cta %d terms %d+%d+%d\n", i, nops_,
+                                 queuedOps, ncoef_, queuedCoef, pendingCtaTerms(), ncta_, ncterms_, pendingCtaTerms(),
+                                 pendCta);
                 break;
+            }
             if (!satisfied(tg_[i], orig_[i])) {
                 flushAll(true);
                 closeSegment();
@@ -501,7 +512,7 @@ private:
     // carry: an exchange follows -- pair phases (constants, known here) are
     // not applied but re-issued as diagonal gates in the next segment's map.
     void flushAll(bool carry = false) {
-        if (carry && carryOk_ && carryPending() && deferPairPhases()) {
+        if (carry && carryOk_ && carryPending() && deferPairPhases() && carryAffordable()) {
             // nothing is applied: drop the accumulators and the unemitted batch;
             // reissuePending() re-lowers every pending gate in the next map
             batchReset();
@@ -711,6 +722,14 @@ private:
         pend_.push_back({q0, q1, d});
         diag2(q0, q1, d);
     }
+    // Re-issuing CTA-bit gates rebuilds their per-CTA terms: carry only while
+    // that stays small (else flush at the exchange as usual).
+    int pendCtaCost() const {
+        int c = 0;
+        for (const PendGate& pg : pend_) c += (isCtaBit(pg.q0) || (pg.q1 >= 0 && isCtaBit(pg.q1))) ? 2 : 0;
+        return c;
+    }
+    bool carryAffordable() const { return pendCtaCost() <= 64 && int(pend_.size()) <= 96; }
     bool touchesPending(int q) const {
         for (const PendGate& pg : pend_)
             if (pg.q0 == q || pg.q1 == q) return true;
