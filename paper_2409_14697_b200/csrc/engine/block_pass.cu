@@ -313,6 +313,15 @@ __global__ void __launch_bounds__(1 << (CT - RB), MINB)
     }
 
     double2 a[NA];
+    if (basis != ~uint64_t(0) && ((basis ^ base) & ~P.tile_mask) != 0) {
+        // first pass of a run, tile without the basis index: zeros in, zeros out
+        uint64_t off, st[RB];
+        globalLayout<CT, RB>(P, P.map_in[0], tid, off, st);
+        off |= base;
+#pragma unroll
+        for (int s = 0; s < NA; s++) __stcs(state + (off | slotOffset<RB>(s, st)), make_double2(0.0, 0.0));
+        return;
+    }
     {
         uint64_t off, st[RB];
         globalLayout<CT, RB>(P, P.map_in[0], tid, off, st);

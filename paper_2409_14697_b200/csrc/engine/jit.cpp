@@ -219,6 +219,7 @@ public:
            << ";\n  const u32 tid = threadIdx.x;\n";
         o_ << "  for (u32 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {\n";
         o_ << "  " << deposit("base", "(u64)tile") << "\n";
+        zeroTile();
         std::string decl = "  double2 ";
         for (int s = 0; s < na_; s++) decl += (s ? ", a" : "a") + std::to_string(s);
         o_ << decl << ";\n  double2 P = C2(1.0, 0.0);\n" << pendDecl();
@@ -287,6 +288,7 @@ public:
         issueTile("blockIdx.x", L);
         o_ << "  }\n  for (u32 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {\n"
            << "  " << deposit("base", "(u64)tile") << "\n";
+        zeroTile();
         std::string decl = "  double2 ";
         for (int s = 0; s < na_; s++) decl += (s ? ", a" : "a") + std::to_string(s);
         o_ << decl << ";\n  double2 P = C2(1.0, 0.0);\n" << pendDecl();
@@ -317,6 +319,23 @@ public:
     }
 
 private:
+    // First pass of a run (|basis> synthesized): a tile that does not hold the
+    // basis index is all zeros and stays all zeros under the pass's linear
+    // map -- write the zeros, skip the arithmetic.
+    void zeroTile() {
+        o_ << "  if (basis != ~0ull && ((basis ^ base) & " << (~P_.tile_mask) << "ull) != 0ull) {\n"
+           << "    const u64 zoff = base | " << threadGlobal(P_.map_in[0]) << ";\n";
+        const int kl = slotOfMem0(P_.map_in[0]);
+        for (int s = 0; s < na_; s++) {
+            if (kl >= 0) {
+                if (!((s >> kl) & 1))
+                    o_ << "    st256(st + (zoff | " << regGlobal(P_.map_in[0], s) << "ull), C2(0.0, 0.0), C2(0.0, 0.0));\n";
+                continue;
+            }
+            o_ << "    __stcs(st + (zoff | " << regGlobal(P_.map_in[0], s) << "ull), C2(0.0, 0.0));\n";
+        }
+        o_ << "    continue;\n  }\n";
+    }
     // Warp 0 streams tile `t` into PB: one cp.async.bulk per contiguous row.
     void issueTile(const std::string& t, int Lrun) {
         const int L = std::min(Lrun, 8);  // rows of <= 4 KB, spread over warp 0's lanes
@@ -751,7 +770,7 @@ private:
 // ---- compile / load / launch -------------------------------------------------
 
 // Bump when the generated code changes for the same PassParams (on-disk cache key).
-constexpr uint64_t kGeneratorVersion = 14;
+constexpr uint64_t kGeneratorVersion = 15;
 
 uint64_t hashPass(const PassParams& P) {
     uint64_t h = 1469598103934665603ull ^ (kGeneratorVersion * 0x9E3779B97F4A7C15ull) ^ (usePrefetch() ? 1u : 0u) ^ (usePersistent() ? 2u : 0u) ^
