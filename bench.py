@@ -283,11 +283,15 @@ def main():
                 "d2h_bytes_per_step": window * 16 + 8,
                 "path": "qk_program_parse + qk_simulate + qk_norm + qk_download(2^20 amps) via C-ABI"},
         "gpu_launches": int(sum(x["kernel_launches"] for x in stats)),
-        "roofline": {"bound": "hbm", "kernel": "k_block_pass", "achieved": round(blk_gbs, 1),
+        "roofline": {"bound": "hbm", "kernel": "qk_pass_<hash> (NVRTC-specialized fused pass, csrc/engine/jit.cpp)",
+                     "achieved": round(blk_gbs, 1),
                      "peak": peak, "unit": "GB/s", "frac": round(blk_gbs / peak, 4),
                      "peak_source": peak_src, "traffic": traffic,
                      "traffic_source": (tr["source"] + ", DRAM bytes/amp x this slice") if tr else None,
                      "algorithmic_bytes_per_launch": round(blk_bytes_per_launch),
+                     "fp64_peak_tflops_measured": 36.5,
+                     "fp64_note": "DFMA 36.5 / DMMA 37.0 TF measured (profiles/r1_fp64_peak.txt); passes run "
+                                  "~75 FP64 instr/amp, FP64 pipe 24-41% active (profiles/r1_qft30_ncu_full.txt)",
                      "avg_launch_ms": round(blk_launch_ms, 3)},
         "breakdown": {"block_ms": round(s0["block_ms"], 2), "ims_ms": round(s0["ims_ms"], 2),
                       "xrs_ms": round(s0["xrs_ms"], 2), "block_launches": s0["block_launches"],
