@@ -88,6 +88,11 @@ int qk_set_basis(qk_state* st, uint64_t global_index);          /* initState */
 int qk_upload(qk_state* st, uint64_t offset, uint64_t count, const double* host);
 int qk_download(qk_state* st, uint64_t offset, uint64_t count, double* host);
 int qk_norm(qk_state* st, double* out);                          /* StateVector::norm */
+/* Marginal probabilities of this slice over k <= 10 of its bits (physical
+ * positions): out[v] = sum |a_i|^2 over i whose bits[j] equal bit j of v
+ * (2^k doubles).  One HBM read of the slice; block partials folded in a fixed
+ * order (the in-block accumulation order may vary at the last ulp). */
+int qk_marginal(qk_state* st, const int* bits, int k, double* out);
 int qk_synchronize(qk_state* st);
 int qk_stream(qk_state* st, void** cuda_stream);                 /* for interop */
 int qk_set_profiling(qk_state* st, int on);

@@ -109,6 +109,7 @@ def lib():
         "qk_upload": ([P, U64, U64, P], I),
         "qk_download": ([P, U64, U64, P], I),
         "qk_norm": ([P, C.POINTER(D)], I),
+        "qk_marginal": ([P, C.POINTER(I), I, C.POINTER(D)], I),
         "qk_synchronize": ([P], I),
         "qk_stream": ([P, C.POINTER(P)], I),
         "qk_set_profiling": ([P, I], I),
@@ -305,6 +306,13 @@ class State:
         v = C.c_double()
         _check(lib().qk_norm(self._h, C.byref(v)))
         return v.value
+
+    def marginal(self, bits) -> np.ndarray:
+        """Probabilities over the given slice bits (physical positions): 2^k values."""
+        arr = (C.c_int * max(1, len(bits)))(*bits)
+        out = np.empty(1 << len(bits), dtype=np.float64)
+        _check(lib().qk_marginal(self._h, arr, len(bits), out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
 
     def synchronize(self) -> None:
         _check(lib().qk_synchronize(self._h))

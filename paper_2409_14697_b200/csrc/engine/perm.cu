@@ -289,6 +289,42 @@ __global__ void k_norm_final(const double* __restrict__ part, int nb, double* __
 
 __global__ void k_set_basis(double2* a, uint64_t idx) { a[idx] = make_double2(1.0, 0.0); }
 
+// Marginal probabilities over k <= 10 slice bits: part[block][v] = sum of
+// |a_i|^2 over this block's range with bits(i) = v (bit j of v = slice bit
+// bits[j]).  Shared-memory atomics within a block; blocks fold in order.
+struct MargSpec {
+    int k;
+    int bits[10];
+};
+__global__ void __launch_bounds__(256) k_marginal_partial(const double2* __restrict__ a, uint64_t n,
+                                                          const __grid_constant__ MargSpec m, double* __restrict__ part) {
+    __shared__ double bins[1024];
+    const int nb = 1 << m.k;
+    for (int v = threadIdx.x; v < nb; v += blockDim.x) bins[v] = 0.0;
+    __syncthreads();
+    const uint64_t per = (n + gridDim.x - 1) / gridDim.x;
+    const uint64_t lo = per * blockIdx.x, hi = lo + per < n ? lo + per : n;
+    for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        const double2 x = __ldcs(a + i);
+        int v = 0;
+        for (int j = 0; j < m.k; j++) v |= int((i >> m.bits[j]) & 1u) << j;
+        atomicAdd(&bins[v], fma(x.x, x.x, x.y * x.y));
+    }
+    __syncthreads();
+    for (int v = threadIdx.x; v < nb; v += blockDim.x) part[uint64_t(blockIdx.x) * nb + v] = bins[v];
+}
+__global__ void k_marginal_final(const double* __restrict__ part, int nblocks, int nb, double* __restrict__ out) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nb; v += gridDim.x * blockDim.x) {
+        double s = 0.0, c = 0.0;  // compensated, fixed block order
+        for (int b = 0; b < nblocks; b++) {
+            const double y = part[uint64_t(b) * nb + v] - c, t = s + y;
+            c = (t - s) - y;
+            s = t;
+        }
+        out[v] = s;
+    }
+}
+
 // ---- launchers ----------------------------------------------------------------
 
 static unsigned gridFor(uint64_t work, unsigned threads, unsigned cap) {
@@ -463,6 +499,18 @@ cudaError_t launchNorm(const double2* a, uint64_t n, double* scratch, double* ou
     return cudaGetLastError();
 }
 size_t normScratchDoubles() { return 2 * kNormBlocks; }
+
+constexpr int kMargBlocks = 1184;
+size_t marginalScratchDoubles(int k) { return size_t(kMargBlocks) << k; }
+cudaError_t launchMarginal(const double2* a, uint64_t n, const int* bits, int k, double* scratch, double* out,
+                           cudaStream_t st) {
+    MargSpec m{};
+    m.k = k;
+    for (int j = 0; j < k; j++) m.bits[j] = bits[j];
+    k_marginal_partial<<<kMargBlocks, 256, 0, st>>>(a, n, m, scratch);
+    k_marginal_final<<<((1 << k) + 255) / 256, 256, 0, st>>>(scratch, kMargBlocks, 1 << k, out);
+    return cudaGetLastError();
+}
 
 cudaError_t launchSetBasis(double2* a, uint64_t idx, cudaStream_t st) {
     k_set_basis<<<1, 1, 0, st>>>(a, idx);

@@ -38,6 +38,8 @@ cudaError_t launchDiagTable(double2*, const double2*, uint64_t, const int*, int,
 cudaError_t launchNorm(const double2*, uint64_t, double*, double*, cudaStream_t);
 size_t normScratchDoubles();
 cudaError_t launchSetBasis(double2*, uint64_t, cudaStream_t);
+cudaError_t launchMarginal(const double2*, uint64_t, const int*, int, double*, double*, cudaStream_t);
+size_t marginalScratchDoubles(int k);
 }  // namespace qkdev
 
 using quokka::ConfigError;
@@ -878,6 +880,23 @@ int qk_norm(qk_state* st, double* out) {
         cuda(qkdev::launchNorm(st->amps, st->count, st->normScratch, st->normOut, st->stream), "norm");
         cuda(cudaMemcpyAsync(out, st->normOut, sizeof(double), cudaMemcpyDeviceToHost, st->stream), "norm copy");
         cuda(cudaStreamSynchronize(st->stream), "norm sync");
+    });
+}
+
+int qk_marginal(qk_state* st, const int* bits, int k, double* out) {
+    return guard([&] {
+        if (k < 0 || k > 10) throw SimulationError("marginal: 0 <= k <= 10 bits");
+        for (int j = 0; j < k; j++)
+            if (bits[j] < 0 || bits[j] >= st->nLocal) throw SimulationError("marginal: bit outside the slice");
+        DeviceGuard g(st->device);
+        double *scratch = nullptr, *dout = nullptr;
+        cuda(cudaMallocAsync(&scratch, qkdev::marginalScratchDoubles(k) * sizeof(double), st->stream), "marginal");
+        cuda(cudaMallocAsync(&dout, sizeof(double) << k, st->stream), "marginal");
+        cuda(qkdev::launchMarginal(st->amps, st->count, bits, k, scratch, dout, st->stream), "marginal");
+        cuda(cudaMemcpyAsync(out, dout, sizeof(double) << k, cudaMemcpyDeviceToHost, st->stream), "marginal copy");
+        cuda(cudaFreeAsync(scratch, st->stream), "marginal");
+        cuda(cudaFreeAsync(dout, st->stream), "marginal");
+        cuda(cudaStreamSynchronize(st->stream), "marginal sync");
     });
 }
 

@@ -230,3 +230,21 @@ def test_norm_and_basis(qk):
     st.upload(a)
     want = np.sum(np.abs(a) ** 2)
     assert abs(st.norm() - want) / want < 1e-14
+
+
+def test_marginal_probabilities(qk):
+    n = 16
+    rng = np.random.default_rng(9)
+    st = rng.standard_normal(2 << n).view(np.complex128)
+    st /= np.linalg.norm(st)
+    d = qk.State(n)
+    d.upload(st)
+    p = np.abs(st) ** 2
+    idx = np.arange(1 << n)
+    for bits in ([0], [3, 11], [15, 0, 7, 2], list(range(10))):
+        v = np.zeros(1 << n, dtype=np.int64)
+        for j, b in enumerate(bits):
+            v |= ((idx >> b) & 1) << j
+        want = np.bincount(v, weights=p, minlength=1 << len(bits))
+        assert np.max(np.abs(d.marginal(bits) - want)) < 1e-14
+    d.close()
