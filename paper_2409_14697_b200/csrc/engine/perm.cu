@@ -89,13 +89,13 @@ __global__ void __launch_bounds__(256) k_ims(double2* __restrict__ a, int logN, 
 struct ImsTileSpec {
     int k;                 // tile bits
     int n;                 // slice bits
-    int tbit[6];           // tile coordinate r -> memory bit (ascending)
-    int pi[6];             // tile coordinate r -> coordinate of P(bit)
+    int tbit[8];           // tile coordinate r -> memory bit (ascending)
+    int pi[8];             // tile coordinate r -> coordinate of P(bit)
     int nfree;             // non-tile bits, ascending
     int fbit[58];
     int nhp;               // pairs among non-tile bits (memory bits)
     int ho[29], hi[29];
-    int swz[3];            // staging swizzle: coordinate bit 3+i XORs swz[i] into bits 0..2
+    int swz[5];            // staging swizzle: coordinate bit 3+i XORs swz[i] into bits 0..2
     int a;                 // 2^a warps; warp w walks g = w | (k << a)
     uint64_t hstep[58];    // dep(trailing-ones mask j+1, shifted by a): h(k+1) = h(k) ^ hstep[tz(~k)]
     uint64_t pstep[58];    // P(hstep[j])
@@ -107,20 +107,25 @@ struct ImsTileSpec {
 __device__ __forceinline__ int stageIdx(int u, const ImsTileSpec& sp) {
     int x = u;
 #pragma unroll
-    for (int i = 0; i < 3; i++)
+    for (int i = 0; i < 5; i++)
         if ((u >> (3 + i)) & 1) x ^= sp.swz[i];
     return x;
 }
 
+// PER amplitudes per lane per tile (tiles of 32 * PER = 2^k amplitudes), U
+// orbits per trip; each warp stages one tile pair at a time.
+template <int PER, int U>
 __global__ void __launch_bounds__(256) k_ims_tiled(double2* __restrict__ a, const __grid_constant__ ImsTileSpec sp) {
-    __shared__ double2 buf[8][4][64];
+    extern __shared__ double2 tbuf[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int per = (1 << sp.k) >> 5;  // amplitudes per lane per tile (1 or 2)
-    // tile coordinates handled by this lane, their memory offsets, and the
-    // memory offsets of the permuted coordinates
-    uint64_t off[2];
-    int tpi[2], sidx[2];
-    _Pragma("unroll") for (int e = 0; e < 2; e++) if (e < per) {
+    double2* const bufA = tbuf + size_t(w) * 2 * 32 * PER;
+    double2* const bufB = bufA + 32 * PER;
+    // tile coordinates handled by this lane: their memory offsets, staging
+    // slots, and the staging slot of the permuted source coordinate
+    uint64_t off[PER];
+    int tpi[PER], sidx[PER];
+#pragma unroll
+    for (int e = 0; e < PER; e++) {
         const int t = lane + 32 * e;
         uint64_t o = 0;
         int u = 0;
@@ -143,11 +148,12 @@ __global__ void __launch_bounds__(256) k_ims_tiled(double2* __restrict__ a, cons
         const uint64_t d = ((ph >> sp.ho[j]) ^ (ph >> sp.hi[j])) & 1u;
         ph ^= (d << sp.ho[j]) | (d << sp.hi[j]);
     }
-    // Two orbits per trip (k, k+1): 8 independent 16-B loads per lane in flight.
     const uint64_t K = uint64_t(1) << (sp.nfree - sp.a);
-    for (uint64_t k = 0; k < K; k += 2) {
-        uint64_t hs[2], ps[2];
-        _Pragma("unroll") for (int q = 0; q < 2; q++) {
+    for (uint64_t k = 0; k < K; k += U) {
+        uint64_t hs[U], ps[U];
+        bool lead[U];
+#pragma unroll
+        for (int q = 0; q < U; q++) {
             const uint64_t kk = k + q;
             if (kk) {
                 const int tz = __ffsll((long long)(~(kk - 1))) - 1;
@@ -156,29 +162,35 @@ __global__ void __launch_bounds__(256) k_ims_tiled(double2* __restrict__ a, cons
             }
             hs[q] = h;
             ps[q] = ph;
+            lead[q] = kk < K && ph >= h;  // the orbit's smaller member does the work
         }
-        const bool lead[2] = {ps[0] >= hs[0], K > 1 && ps[1] >= hs[1]};  // smaller member does the work
-        double2 va[2][2], vb[2][2];
-        _Pragma("unroll") for (int q = 0; q < 2; q++) if (lead[q]) {
-            _Pragma("unroll") for (int e = 0; e < 2; e++) if (e < per) va[q][e] = __ldcs(a + (hs[q] | off[e]));
-            if (ps[q] != hs[q])
-                _Pragma("unroll") for (int e = 0; e < 2; e++) if (e < per) vb[q][e] = __ldcs(a + (ps[q] | off[e]));
-        }
-        _Pragma("unroll") for (int q = 0; q < 2; q++) if (lead[q]) {
-            _Pragma("unroll") for (int e = 0; e < 2; e++) if (e < per) {
-                buf[w][2 * q][sidx[e]] = va[q][e];
-                if (ps[q] != hs[q]) buf[w][2 * q + 1][sidx[e]] = vb[q][e];
+        double2 va[U][PER], vb[U][PER];  // every load of the trip in flight at once
+#pragma unroll
+        for (int q = 0; q < U; q++)
+            if (lead[q]) {
+#pragma unroll
+                for (int e = 0; e < PER; e++) va[q][e] = __ldcs(a + (hs[q] | off[e]));
+                if (ps[q] != hs[q])
+#pragma unroll
+                    for (int e = 0; e < PER; e++) vb[q][e] = __ldcs(a + (ps[q] | off[e]));
             }
-        }
-        __syncwarp();
-        // tile(ph)[t] <- tile(h)[pi(t)];  tile(h)[t] <- tile(ph)[pi(t)]
-        _Pragma("unroll") for (int q = 0; q < 2; q++) if (lead[q]) {
-            _Pragma("unroll") for (int e = 0; e < 2; e++) if (e < per) __stcs(a + (ps[q] | off[e]), buf[w][2 * q][tpi[e]]);
+#pragma unroll
+        for (int q = 0; q < U; q++) {
+            if (!lead[q]) continue;  // warp-uniform
+#pragma unroll
+            for (int e = 0; e < PER; e++) {
+                bufA[sidx[e]] = va[q][e];
+                if (ps[q] != hs[q]) bufB[sidx[e]] = vb[q][e];
+            }
+            __syncwarp();
+            // tile(ph)[t] <- tile(h)[pi(t)];  tile(h)[t] <- tile(ph)[pi(t)]
+#pragma unroll
+            for (int e = 0; e < PER; e++) __stcs(a + (ps[q] | off[e]), bufA[tpi[e]]);
             if (ps[q] != hs[q])
-                _Pragma("unroll") for (int e = 0; e < 2; e++) if (e < per)
-                    __stcs(a + (hs[q] | off[e]), buf[w][2 * q + 1][tpi[e]]);
+#pragma unroll
+                for (int e = 0; e < PER; e++) __stcs(a + (hs[q] | off[e]), bufB[tpi[e]]);
+            __syncwarp();
         }
-        __syncwarp();
     }
 }
 
@@ -358,16 +370,18 @@ static bool imsTileSpec(int logN, const int* outs, const int* ins, int s, ImsTil
         partner[outs[j]] = ins[j];
         partner[ins[j]] = outs[j];
     }
+    // T: memory bits 0..2 and their partners, then the lowest bits (with
+    // partners) up to 8 bits: longer contiguous rows (bits 0..L-1) first.
     uint64_t T = 0;
     for (int b = 0; b < 3; b++) T |= (uint64_t(1) << b) | (uint64_t(1) << partner[b]);
-    if (__builtin_popcountll(T) > 6) return false;
-    for (int b = 0; b < logN && __builtin_popcountll(T) < 6; b++) {
+    if (__builtin_popcountll(T) > 8) return false;
+    for (int b = 0; b < logN && __builtin_popcountll(T) < 8; b++) {
         if ((T >> b) & 1) continue;
         const uint64_t add = (uint64_t(1) << b) | (uint64_t(1) << partner[b]);
-        if (__builtin_popcountll(T | add) <= 6) T |= add;
+        if (__builtin_popcountll(T | add) <= 8) T |= add;
     }
     const int k = __builtin_popcountll(T);
-    if (k < 5) return false;
+    if (k < 5 || k > logN - 1) return false;
     sp = ImsTileSpec{};
     sp.k = k;
     sp.n = logN;
@@ -410,11 +424,11 @@ static bool imsTileSpec(int logN, const int* outs, const int* ins, int s, ImsTil
     // 0..2, always) and of the permuted reads (span of pi(0..2)).
     int img[3];
     for (int i = 0; i < 3; i++) img[i] = 1 << sp.pi[i];
-    for (int m = 0; m < 512; m++) {
-        const int z[3] = {m & 7, (m >> 3) & 7, (m >> 6) & 7};
+    for (int m = 0; m < (1 << 15); m++) {
+        const int z[5] = {m & 7, (m >> 3) & 7, (m >> 6) & 7, (m >> 9) & 7, (m >> 12) & 7};
         auto bank = [&](int u) {
             int x = u & 7;
-            for (int i = 0; i < 3; i++)
+            for (int i = 0; i < 5; i++)
                 if ((u >> (3 + i)) & 1) x ^= z[i];
             return x;
         };
@@ -426,7 +440,7 @@ static bool imsTileSpec(int logN, const int* outs, const int* ins, int s, ImsTil
             ok = bank(u) != 0;
         }
         if (ok) {
-            for (int i = 0; i < 3; i++) sp.swz[i] = z[i];
+            for (int i = 0; i < 5; i++) sp.swz[i] = z[i];
             break;
         }
     }
@@ -453,7 +467,19 @@ cudaError_t launchIms(double2* a, int logN, const int* outs, const int* ins, int
     if (mode == 0 || (mode == 2 && !lowPair) || !imsTileSpec(logN, outs, ins, s, sp))
         return launchImsGeneric(a, logN, outs, ins, s, st);
     const uint64_t ctas = ((uint64_t(1) << sp.a) + 7) / 8;  // 8 warps per CTA
-    k_ims_tiled<<<unsigned(ctas), sp.a >= 3 ? 256 : (32 << sp.a), 0, st>>>(a, sp);
+    const unsigned threads = sp.a >= 3 ? 256 : (32 << sp.a);
+    const int per = 1 << (sp.k - 5);
+    const size_t smem = size_t(threads / 32) * 2 * 32 * per * sizeof(double2);
+    switch (per) {
+        case 1: k_ims_tiled<1, 4><<<unsigned(ctas), threads, smem, st>>>(a, sp); break;
+        case 2: k_ims_tiled<2, 2><<<unsigned(ctas), threads, smem, st>>>(a, sp); break;
+        case 4: k_ims_tiled<4, 1><<<unsigned(ctas), threads, smem, st>>>(a, sp); break;
+        default: {
+            cudaError_t e = cudaFuncSetAttribute(k_ims_tiled<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+            if (e != cudaSuccess) return e;
+            k_ims_tiled<8, 1><<<unsigned(ctas), threads, smem, st>>>(a, sp);
+        }
+    }
     return cudaGetLastError();
 }
 
