@@ -214,10 +214,10 @@ public:
         o_ << kPrologue;
         ctaTables();
         o_ << "extern \"C\" __global__ void __launch_bounds__(" << nt_ << "," << minb << ") " << name
-           << "(double2* __restrict__ st, const double2* __restrict__ gt, const u32 ntiles, const u64 basis) {\n";
+           << "(double2* __restrict__ st, const double2* __restrict__ gt, const u32 ntiles, const u64 basis, const u32 tile0) {\n";
         o_ << "  extern __shared__ double2 sm[];\n  double2* const F = sm + " << (1 << ct_)
            << ";\n  const u32 tid = threadIdx.x;\n";
-        o_ << "  for (u32 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {\n";
+        o_ << "  for (u32 tile = blockIdx.x + tile0; tile < ntiles; tile += gridDim.x) {\n";
         o_ << "  " << deposit("base", "(u64)tile") << "\n";
         zeroTile();
         std::string decl = "  double2 ";
@@ -278,7 +278,7 @@ public:
         o_ << kPrologue;
         ctaTables();
         o_ << "extern \"C\" __global__ void __launch_bounds__(" << nt_ << ",1) " << name
-           << "(double2* __restrict__ st, const double2* __restrict__ gt, const u32 ntiles, const u64 basis) {\n"
+           << "(double2* __restrict__ st, const double2* __restrict__ gt, const u32 ntiles, const u64 basis, const u32 tile0) {\n"
            << "  extern __shared__ double2 sm[];  // PB: next tile (linear tile coordinates) | XS | F | mbarrier\n"
            << "  double2* const XS = sm + 8192;\n  double2* const F = sm + 12288;\n"
            << "  u64* const mbar = (u64*)(sm + 12352);\n  const u32 tid = threadIdx.x;\n"
@@ -286,7 +286,7 @@ public:
            << "  if (tid == 0) mbar_init(mbar);\n  __syncthreads();\n"
            << "  if (tma && blockIdx.x < ntiles) {\n";
         issueTile("blockIdx.x", L);
-        o_ << "  }\n  for (u32 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {\n"
+        o_ << "  }\n  for (u32 tile = blockIdx.x + tile0; tile < ntiles; tile += gridDim.x) {\n"
            << "  " << deposit("base", "(u64)tile") << "\n";
         zeroTile();
         std::string decl = "  double2 ";
@@ -770,7 +770,7 @@ private:
 // ---- compile / load / launch -------------------------------------------------
 
 // Bump when the generated code changes for the same PassParams (on-disk cache key).
-constexpr uint64_t kGeneratorVersion = 15;
+constexpr uint64_t kGeneratorVersion = 16;
 
 uint64_t hashPass(const PassParams& P) {
     uint64_t h = 1469598103934665603ull ^ (kGeneratorVersion * 0x9E3779B97F4A7C15ull) ^ (usePrefetch() ? 1u : 0u) ^ (usePersistent() ? 2u : 0u) ^
@@ -1001,13 +1001,29 @@ cudaError_t launch(const PassParams& P, double2* state, const double2* gtab, int
     cudaGetDevice(&dev);
     void* fn = functionFor(P, hashPass(P), dev);
     unsigned ntiles = unsigned(uint64_t(1) << (nLocal - P.ct));
-    const unsigned resident = unsigned(smCount(dev) * blocksPerSm(P.ct, P.rb));
+    unsigned tile0 = 0;
+    unsigned ctas;
     const bool pipe = pipelined(P);
-    const unsigned ctas = (ntiles < resident || !(usePersistent() || pipe)) ? ntiles : resident;
+    if (basis != ~uint64_t(0)) {
+        // First pass of a run: every tile but the one holding |basis> is zeros
+        // in and zeros out -- memset the slice, compute that one tile.
+        const cudaError_t e = cudaMemsetAsync(state, 0, sizeof(double2) << nLocal, stream);
+        if (e != cudaSuccess) return e;
+        if (basis >> nLocal) return cudaSuccess;  // the basis state lives on another rank
+        uint32_t t = 0, q = 0;  // tile index = the basis's non-tile bits, compacted
+        for (int b = 0; b < nLocal; b++)
+            if (!((P.tile_mask >> b) & 1)) t |= uint32_t((basis >> b) & 1) << q++;
+        tile0 = t;
+        ntiles = t + 1;
+        ctas = 1;
+    } else {
+        const unsigned resident = unsigned(smCount(dev) * blocksPerSm(P.ct, P.rb));
+        ctas = (ntiles < resident || !(usePersistent() || pipe)) ? ntiles : resident;
+    }
     const unsigned nt = 1u << (P.ct - P.rb);
     const unsigned smem = pipe ? unsigned(sizeof(double2) * kPipeSmemAmps)
                                : unsigned((sizeof(double2) << P.ct) + sizeof(double2) * qkdev::kMaxCtaFactors);
-    void* args[] = {&state, &gtab, &ntiles, &basis};
+    void* args[] = {&state, &gtab, &ntiles, &basis, &tile0};
     if (driver().launchKernel(fn, ctas, 1, 1, nt, 1, 1, smem, stream, args, nullptr) != 0)
         return cudaErrorLaunchFailure;
     return cudaSuccess;

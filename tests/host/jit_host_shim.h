@@ -79,7 +79,7 @@ extern "C" double2 sm[1 << 14];
                 ts.emplace_back([=] {                                                         \
                     qk_tl_tid = t;                                                            \
                     qk_tl_bid = b;                                                            \
-                    KERNEL(st, gt, ntiles, basis);                                            \
+                    KERNEL(st, gt, ntiles, basis, 0u);                                        \
                 });                                                                           \
             for (auto& th : ts) th.join();                                                    \
         }                                                                                     \
