@@ -49,7 +49,7 @@ __device__ __forceinline__ uint32_t swz(uint32_t u) {
 __device__ __forceinline__ uint32_t pextT(uint32_t t, uint32_t m) {
     uint32_t r = 0, i = 0;
 #pragma unroll
-    for (int j = 0; j < 9; j++)
+    for (int j = 0; j < 10; j++)
         if ((m >> j) & 1u) r |= ((t >> j) & 1u) << i++;
     return r;
 }
@@ -601,7 +601,7 @@ __global__ void k_dense_group(double2* __restrict__ state, const double2* __rest
 
 // CT <= 12: 16 amplitudes per thread, two CTAs per SM at CT = 12 (128 KiB of
 // smem, 128 registers); CT = 13: RB = 5 (256 threads x 255 registers, one CTA
-// per SM) or RB = 4 (512 threads x 128 registers).
+// per SM), RB = 4 (512 threads x 128 registers) or RB = 3 (1024 threads).
 template <int CT, int RB = (CT < 4 ? CT : 4)>
 static cudaError_t launchCT(double2* state, const double2* gtab, const PassParams& P, uint64_t ctas,
                             uint64_t basis, cudaStream_t stream) {
@@ -619,10 +619,11 @@ static cudaError_t launchCT(double2* state, const double2* gtab, const PassParam
 
 cudaError_t launchBlockPass(double2* state, const double2* gtab, const PassParams& P, int nLocal, uint64_t basis,
                             cudaStream_t stream) {
-    if (P.rb != regBitsFor(P.ct) && !(P.ct == 13 && (P.rb == 4 || P.rb == 5))) return cudaErrorInvalidValue;
+    if (P.rb != regBitsFor(P.ct) && !(P.ct == 13 && P.rb >= 3 && P.rb <= 5)) return cudaErrorInvalidValue;
     const uint64_t ctas = uint64_t(1) << (nLocal - P.ct);
-    if (P.ct == 13) return P.rb == 5 ? launchCT<13, 5>(state, gtab, P, ctas, basis, stream)
-                                     : launchCT<13, 4>(state, gtab, P, ctas, basis, stream);
+    if (P.ct == 13) return P.rb == 5   ? launchCT<13, 5>(state, gtab, P, ctas, basis, stream)
+                           : P.rb == 4 ? launchCT<13, 4>(state, gtab, P, ctas, basis, stream)
+                                       : launchCT<13, 3>(state, gtab, P, ctas, basis, stream);
     switch (P.ct) {
         case 4: return launchCT<4>(state, gtab, P, ctas, basis, stream);
         case 5: return launchCT<5>(state, gtab, P, ctas, basis, stream);

@@ -457,7 +457,7 @@ void prepareJit(const Compiled& c, int device) {
         for (const qkeng::Step& s : it.steps)
             if (s.kind == qkeng::Step::Pass) {
                 passes.push_back(s.pass.get());
-                if (s.alt) passes.push_back(s.alt.get());
+                for (const auto& a : s.alts) passes.push_back(a.get());
             }
     qkjit::prepare(passes, device);
 }
@@ -473,9 +473,10 @@ void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_ru
         if (s.kind == qkeng::Step::Pass) {
             // Register-width autotune: the first two executions of a pass time
             // each variant (events, synchronous); later ones take the faster.
-            const int v = s.alt ? s.tune->choice() : 0;
-            const qkdev::PassParams& P = v ? *s.alt : *s.pass;
-            const bool timing = s.alt && s.tune->runs[v] == 0;
+            const int nv = 1 + int(s.alts.size());
+            const int v = s.tune ? s.tune->choice(nv) : 0;
+            const qkdev::PassParams& P = v ? *s.alts[size_t(v - 1)] : *s.pass;
+            const bool timing = s.tune && s.tune->runs[v] == 0;
             cudaEvent_t e0 = nullptr, e1 = nullptr;
             if (timing) {
                 cuda(cudaEventCreate(&e0), "event");
@@ -495,7 +496,7 @@ void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_ru
                 cudaEventDestroy(e1);
                 s.tune->ms[v] = ms;
                 s.tune->runs[v]++;
-            } else if (s.alt) {
+            } else if (s.tune) {
                 s.tune->runs[v]++;
             }
             basis = kNoBasis;

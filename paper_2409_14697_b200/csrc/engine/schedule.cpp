@@ -82,7 +82,7 @@ bool halfExchanges() {
 }
 
 int regBitsFor(int ct) {
-    static const int rb13 = envInt("QK_RB13", 5, 4, 5);
+    static const int rb13 = envInt("QK_RB13", 5, 3, 5);
     return ct >= 13 ? rb13 : (ct < 4 ? ct : 4);
 }
 
@@ -1148,7 +1148,7 @@ std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::
                     taken[size_t(free)] = 1;
                 }
             applyStorePermutation(P, sigma);
-            if (steps[k].alt) applyStorePermutation(*steps[k].alt, sigma);  // same tile, same sigma
+            for (auto& a : steps[k].alts) applyStorePermutation(*a, sigma);  // same tile, same sigma
             std::vector<int> moved(static_cast<size_t>(nLocal));
             for (int b = 0; b < nLocal; b++) moved[size_t(b)] = b;
             for (int j = 0; j < ct; j++) moved[size_t(P.tile_phys[j])] = P.tile_phys[sigma[size_t(j)]];
@@ -1228,12 +1228,12 @@ std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::
             const size_t first = steps.size();
             compileGroup(group, used, ct, nLocal, gtab, steps);
             if (ct == 13 && tuneRegBits() && steps.size() == first + 1 && steps[first].kind == Step::Pass) {
-                std::vector<Step> alt;
-                compileGroup(group, used, ct, nLocal, gtab, alt, regBitsFor(ct) == 5 ? 4 : 5);
-                if (alt.size() == 1 && alt[0].kind == Step::Pass) {
-                    steps[first].alt = alt[0].pass;
-                    steps[first].tune = std::make_shared<Step::Tune>();
+                for (int rbAlt : {4, 3}) {  // 16 and 8 amplitudes per thread (512 / 1024 threads)
+                    std::vector<Step> alt;
+                    compileGroup(group, used, ct, nLocal, gtab, alt, rbAlt);
+                    if (alt.size() == 1 && alt[0].kind == Step::Pass) steps[first].alts.push_back(alt[0].pass);
                 }
+                if (!steps[first].alts.empty()) steps[first].tune = std::make_shared<Step::Tune>();
             }
             route(first);
         }

@@ -13,17 +13,21 @@ namespace qkeng {
 struct Step {
     enum Kind { Pass, DenseGroup, DiagTable } kind = Pass;
     std::shared_ptr<qkdev::PassParams> pass;  // Kind::Pass
-    // Kind::Pass: the same pass scheduled with the other register width
-    // (2^13 tiles: 32 vs 16 amplitudes per thread); the runtime times both on
-    // their first executions and keeps the faster (`tune`, shared by copies).
-    std::shared_ptr<qkdev::PassParams> alt;
+    // Kind::Pass: the same pass scheduled with other register widths (2^13
+    // tiles: 32, 16 or 8 amplitudes per thread); the runtime times each on its
+    // first execution and keeps the fastest (`tune`, shared by copies).
+    std::vector<std::shared_ptr<qkdev::PassParams>> alts;
     struct Tune {
-        float ms[2] = {0, 0};
-        int runs[2] = {0, 0};
-        int choice() const {
-            if (runs[0] == 0) return 0;
-            if (runs[1] == 0) return 1;
-            return ms[1] < ms[0] ? 1 : 0;
+        static constexpr int kMax = 3;
+        float ms[kMax] = {0, 0, 0};
+        int runs[kMax] = {0, 0, 0};
+        int choice(int n) const {  // n = 1 + alts
+            for (int v = 0; v < n; v++)
+                if (runs[v] == 0) return v;
+            int best = 0;
+            for (int v = 1; v < n; v++)
+                if (ms[v] < ms[best]) best = v;
+            return best;
         }
     };
     std::shared_ptr<Tune> tune;

@@ -38,8 +38,10 @@ def test_specialized_kernels_on_host(ref, qk, port, kind, n, chunk, fusion, diag
     assert np.max(np.abs(st - want.view(np.complex128))) < 1e-10
 
 
-def test_16_amplitudes_per_thread_variant_on_host():
-    # QK_RB13=4: the other register width the runtime autotunes against
+@pytest.mark.parametrize("rb", [4, 3])
+def test_other_register_width_variants_on_host(rb):
+    # QK_RB13=4 / 3: the register widths the runtime autotunes against
+    # (16 / 8 amplitudes per thread, 512 / 1024 threads per 2^13 tile)
     code = r"""
 import sys, numpy as np
 sys.path[:0] = [%r, %r, %r]
@@ -52,14 +54,14 @@ for kind, n, a in (("qft", 16, 0), ("random", 15, 150)):
     pt = ref.optimize(ref.gen(kind, n, a, 3), cfg_text)
     want = ref.simulate(pt, cfg_text, n, 0, 5, 2)[0].view(np.complex128)
     prog = qk.Program.parse(pt, qk.Config.parse(cfg_text))
-    assert all(s.get("rb") == 4 for it in prog.debug_compile()["items"] if it["kind"] == 0
+    assert all(s.get("rb") == RB for it in prog.debug_compile()["items"] if it["kind"] == 0
                for s in it["block"]["steps"] if s.get("ct") == 13)
     st = np.zeros(1 << n, dtype=np.complex128); st[5] = 1
     run_program_jit(qk, port, prog, n, st)
     assert np.max(np.abs(st - want)) < 1e-10, kind
 print("ok")
-""" % (ROOT, os.path.join(ROOT, "oracle"), os.path.join(ROOT, "tests"))
-    env = dict(os.environ, QK_RB13="4")
+""".replace("RB", str(rb)) % (ROOT, os.path.join(ROOT, "oracle"), os.path.join(ROOT, "tests"))
+    env = dict(os.environ, QK_RB13=str(rb))
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
 
