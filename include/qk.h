@@ -71,6 +71,7 @@ typedef struct qk_run_stats {
     double block_ms, ims_ms, xrs_ms, total_ms;
     uint64_t block_launches, ims_launches, xrs_rounds, kernel_launches;
     double block_bytes, block_flops, ims_bytes, xrs_bytes;
+    uint64_t tuning_runs; /* schedule variants timed during this call (autotune still settling) */
 } qk_run_stats;
 
 typedef struct qk_state qk_state;      /* one rank slice in HBM + its stream */

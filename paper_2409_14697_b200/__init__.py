@@ -79,7 +79,8 @@ class _RunStats(C.Structure):
                 ("total_ms", C.c_double), ("block_launches", C.c_uint64),
                 ("ims_launches", C.c_uint64), ("xrs_rounds", C.c_uint64),
                 ("kernel_launches", C.c_uint64), ("block_bytes", C.c_double),
-                ("block_flops", C.c_double), ("ims_bytes", C.c_double), ("xrs_bytes", C.c_double)]
+                ("block_flops", C.c_double), ("ims_bytes", C.c_double), ("xrs_bytes", C.c_double),
+                ("tuning_runs", C.c_uint64)]
 
 
 def build(quiet: bool = True) -> None:

@@ -158,7 +158,7 @@ bool literalFactors() {
 }
 
 // Resident CTAs per SM of a pass kernel (register / shared-memory bound).
-int blocksPerSm(int ct, int rb) { return (ct == 12 && rb == 4) ? 2 : ct <= 11 ? 2 : 1; }
+int blocksPerSm(int ct, int rb) { return (ct == 12 && rb >= 4) ? 2 : ct <= 11 ? 2 : 1; }
 
 int smCount(int dev) {
     static std::mutex mu;

@@ -200,9 +200,27 @@ struct CompiledItem {
     uint64_t denseTargetsOff = 0;    // int offset into the device target table
 };
 
+// Tile-size autotune (qkdev::tileTune): items [first, last) of `items` (a
+// gate stream scheduled with 2^13 tiles plus its materialization) have an
+// alternative `b` (the same stream with 2^12 tiles).  Run 1 times A, run 2
+// times B; once A's per-pass register-width tuning has settled, the faster
+// schedule is kept.
+struct ChoiceTune {
+    int runs = 0;
+    float msA = -1, msB = -1;  // group device time: A's first run, B's run
+    int choice = -1;
+};
+
+struct Alternative {
+    size_t first = 0, last = 0;
+    std::vector<CompiledItem> b;
+    std::shared_ptr<ChoiceTune> tune = std::make_shared<ChoiceTune>();
+};
+
 struct Compiled {
     int nLocal = 0;
     std::vector<CompiledItem> items;
+    std::vector<Alternative> alts;  // sorted by first
     std::vector<double> gtab;     // host copy of device tables
     std::vector<int> targets;     // dense-group target lists
 };
@@ -299,6 +317,8 @@ std::vector<std::vector<std::pair<int, int>>> materializePairs(const std::vector
     return out;
 }
 
+bool useJit(int nLocal);
+
 std::shared_ptr<Compiled> compileFor(qk_program* p, int nLocal) {
     std::lock_guard<std::mutex> lk(p->mu);
     auto it = p->compiled.find(nLocal);
@@ -317,7 +337,7 @@ std::shared_ptr<Compiled> compileFor(qk_program* p, int nLocal) {
     for (int b = 0; b < nLocal; b++) mem[size_t(b)] = b;
     const bool lazy = lazyIms();
     std::vector<quokka::Gate> stream;
-    auto flushStream = [&](bool beforeMaterialize) {
+    auto flushStream = [&](bool beforeMaterialize, int tileBits = 0) {
         if (stream.empty()) return;
         CompiledItem ci;
         ci.kind = CompiledItem::Block;
@@ -325,10 +345,10 @@ std::shared_ptr<Compiled> compileFor(qk_program* p, int nLocal) {
             // route the data toward the program's physical order (mem = identity)
             std::vector<int> dest(static_cast<size_t>(nLocal)), moved;
             for (int q = 0; q < nLocal; q++) dest[size_t(mem[size_t(q)])] = q;
-            ci.steps = qkeng::compileBlock(stream, nLocal, c->gtab, &dest, &moved);
+            ci.steps = qkeng::compileBlock(stream, nLocal, c->gtab, &dest, &moved, tileBits);
             for (int q = 0; q < nLocal; q++) mem[size_t(q)] = moved[size_t(mem[size_t(q)])];
         } else {
-            ci.steps = qkeng::compileBlock(stream, nLocal, c->gtab);
+            ci.steps = qkeng::compileBlock(stream, nLocal, c->gtab, nullptr, nullptr, tileBits);
         }
         for (qkeng::Step& s : ci.steps) {
             ci.flopsPerAmp += s.flopsPerAmp;
@@ -339,7 +359,6 @@ std::shared_ptr<Compiled> compileFor(qk_program* p, int nLocal) {
             }
         }
         c->items.push_back(std::move(ci));
-        stream.clear();
     };
     auto materialize = [&] {
         for (const auto& pairs : materializePairs(mem)) {
@@ -352,6 +371,40 @@ std::shared_ptr<Compiled> compileFor(qk_program* p, int nLocal) {
             c->items.push_back(std::move(ci));
         }
         for (int b = 0; b < nLocal; b++) mem[size_t(b)] = b;
+    };
+    // A stream, routed and materialized (mem ends as the identity); with tile
+    // autotune also the 2^12-tile alternative of the same range.
+    auto flushAndMaterialize = [&] {
+        const size_t first = c->items.size();
+        const std::vector<int> mem0 = mem;
+        flushStream(true);
+        materialize();
+        if (lazy && !stream.empty() && qkdev::tileTune() && useJit(nLocal) && nLocal > 13) {
+            const size_t last = c->items.size();
+            std::vector<CompiledItem> a(std::make_move_iterator(c->items.begin() + long(first)),
+                                        std::make_move_iterator(c->items.end()));
+            c->items.resize(first);
+            mem = mem0;
+            try {
+                flushStream(true, 12);
+                materialize();
+                Alternative alt;
+                alt.first = first;
+                alt.last = last;
+                alt.b.assign(std::make_move_iterator(c->items.begin() + long(first)),
+                             std::make_move_iterator(c->items.end()));
+                const auto firstIsPass = [](const std::vector<CompiledItem>& v) {
+                    return !v.empty() && v[0].kind == CompiledItem::Block && !v[0].steps.empty() &&
+                           v[0].steps[0].kind == qkeng::Step::Pass;
+                };
+                if (firstIsPass(alt.b) == firstIsPass(a)) c->alts.push_back(std::move(alt));
+            } catch (const SimulationError&) {
+            }
+            c->items.resize(first);
+            for (auto& x : a) c->items.push_back(std::move(x));
+            for (int b = 0; b < nLocal; b++) mem[size_t(b)] = b;
+        }
+        stream.clear();
     };
     const auto& items = p->prog.items;
     for (size_t idx = 0; idx < items.size(); idx++) {
@@ -375,8 +428,12 @@ std::shared_ptr<Compiled> compileFor(qk_program* p, int nLocal) {
             continue;
         }
         const bool cross = item.swap.kind == quokka::SwapOp::CrossRank;
-        flushStream(cross);
-        if (cross) materialize();
+        if (cross) {
+            flushAndMaterialize();
+        } else {
+            flushStream(false);
+            stream.clear();
+        }
         CompiledItem ci;
         ci.kind = cross ? CompiledItem::Xrs : CompiledItem::Ims;
         for (const auto& [o, i] : item.swap.pairs) {
@@ -385,8 +442,7 @@ std::shared_ptr<Compiled> compileFor(qk_program* p, int nLocal) {
         }
         c->items.push_back(std::move(ci));
     }
-    flushStream(true);
-    materialize();
+    flushAndMaterialize();
     p->compiled[nLocal] = c;
     return c;
 }
@@ -453,12 +509,16 @@ bool useJit(int nLocal) { return qkjit::minQubits() >= 0 && nLocal >= qkjit::min
 void prepareJit(const Compiled& c, int device) {
     if (!useJit(c.nLocal)) return;
     std::vector<const qkdev::PassParams*> passes;
-    for (const CompiledItem& it : c.items)
-        for (const qkeng::Step& s : it.steps)
-            if (s.kind == qkeng::Step::Pass) {
-                passes.push_back(s.pass.get());
-                for (const auto& a : s.alts) passes.push_back(a.get());
-            }
+    auto add = [&](const std::vector<CompiledItem>& items) {
+        for (const CompiledItem& it : items)
+            for (const qkeng::Step& s : it.steps)
+                if (s.kind == qkeng::Step::Pass) {
+                    passes.push_back(s.pass.get());
+                    for (const auto& a : s.alts) passes.push_back(a.get());
+                }
+    };
+    add(c.items);
+    for (const Alternative& a : c.alts) add(a.b);
     qkjit::prepare(passes, device);
 }
 
@@ -496,6 +556,7 @@ void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_ru
                 cudaEventDestroy(e1);
                 s.tune->ms[v] = ms;
                 s.tune->runs[v]++;
+                rs.tuning_runs++;
             } else if (s.tune) {
                 s.tune->runs[v]++;
             }
@@ -1213,6 +1274,31 @@ int qk_circuit_generate(const char* kind, int n, int64_t a, uint64_t seed, char*
     });
 }
 
+// Tile-size choice for one alternative range (ChoiceTune): A first, then B,
+// then A until its passes' register-width variants are all timed; then the
+// faster of B and A's best estimate (A's first run with every pass replaced
+// by its fastest variant).
+int chooseTileVariant(const Compiled& c, const Alternative& alt) {
+    ChoiceTune& t = *alt.tune;
+    if (t.choice >= 0) return t.choice;
+    if (t.msA < 0) return 0;
+    if (t.msB < 0) return 1;
+    double est = t.msA;
+    for (size_t k = alt.first; k < alt.last; k++)
+        for (const qkeng::Step& s : c.items[k].steps) {
+            if (!s.tune) continue;
+            const int nv = 1 + int(s.alts.size());
+            float best = s.tune->ms[0];
+            for (int v = 0; v < nv; v++) {
+                if (s.tune->runs[v] == 0) return 0;  // A still tuning its register widths
+                best = std::min(best, s.tune->ms[v]);
+            }
+            est += double(best) - double(s.tune->ms[0]);
+        }
+    t.choice = t.msB < est ? 1 : 0;
+    return t.choice;
+}
+
 int qk_simulate(qk_state* st, const qk_program* cp, const qk_config* cfg, uint64_t initial, qk_run_stats* stats) {
     return guard([&] {
         qk_program* p = const_cast<qk_program*>(cp);
@@ -1237,7 +1323,7 @@ int qk_simulate(qk_state* st, const qk_program* cp, const qk_config* cfg, uint64
         uint64_t basis = kNoBasis;
         if (synth) basis = (initial >> st->nLocal) == Index(st->rank) ? (initial & (st->count - 1)) : st->count;
         else setBasis(st, initial);
-        for (const CompiledItem& it : comp->items) {
+        auto runItem = [&](const CompiledItem& it) {
             if (it.kind == CompiledItem::Block) {
                 timer.time(0, [&] { runBlock(st, it, t, rs, basis); });
                 basis = kNoBasis;
@@ -1250,6 +1336,38 @@ int qk_simulate(qk_state* st, const qk_program* cp, const qk_config* cfg, uint64
                 const XrsPlan plan = planXrs(op, st->n, st->R, st->B);
                 timer.time(2, [&] { runXrsNccl(st, plan, rs); });
             }
+        };
+        size_t nextAlt = 0;
+        for (size_t i = 0; i < comp->items.size();) {
+            if (nextAlt < comp->alts.size() && comp->alts[nextAlt].first == i) {
+                const Alternative& alt = comp->alts[nextAlt++];
+                const int v = chooseTileVariant(*comp, alt);
+                const bool timing = alt.tune->choice < 0 && ((v == 0 && alt.tune->msA < 0) || v == 1);
+                cudaEvent_t a0 = nullptr, a1 = nullptr;
+                if (timing) {
+                    cuda(cudaEventCreate(&a0), "event");
+                    cuda(cudaEventCreate(&a1), "event");
+                    cuda(cudaEventRecord(a0, st->stream), "event");
+                    rs.tuning_runs++;
+                }
+                if (v == 1)
+                    for (const CompiledItem& it : alt.b) runItem(it);
+                else
+                    for (size_t k = alt.first; k < alt.last; k++) runItem(comp->items[k]);
+                if (timing) {
+                    float ms = 0;
+                    cuda(cudaEventRecord(a1, st->stream), "event");
+                    cuda(cudaEventSynchronize(a1), "event");
+                    cudaEventElapsedTime(&ms, a0, a1);
+                    cudaEventDestroy(a0);
+                    cudaEventDestroy(a1);
+                    (v == 1 ? alt.tune->msB : alt.tune->msA) = ms;
+                }
+                alt.tune->runs++;
+                i = alt.last;
+                continue;
+            }
+            runItem(comp->items[i++]);
         }
         cuda(cudaEventRecord(e1, st->stream), "event");
         cuda(cudaEventSynchronize(e1), "simulate");

@@ -44,6 +44,15 @@ int maxTileBits() {
     return v;
 }
 
+// QK_TUNE_TILE (default 1): a gate stream is also scheduled with 2^12
+// tiles (two CTAs per SM overlap one tile's loads with the other's math) and
+// the runtime keeps whichever schedule ran faster.
+bool tileTune() {
+    static const bool v = maxTileBits() == kMaxTileBits && envInt("QK_TUNE_TILE", 1, 0, 1) != 0 &&
+                          envInt("QK_TUNE", 1, 0, 1) != 0;
+    return v;
+}
+
 // QK_JIT_TMA=1: specialized kernels stream the next tile through shared
 // memory, so exchanges must be splittable into halves (see chooseMap).
 // QK_WIDE_ACCESS (default 1): first segments hold memory bit 0 in a register
@@ -83,7 +92,8 @@ bool halfExchanges() {
 
 int regBitsFor(int ct) {
     static const int rb13 = envInt("QK_RB13", 5, 3, 5);
-    return ct >= 13 ? rb13 : (ct < 4 ? ct : 4);
+    static const int rb12 = envInt("QK_RB12", 4, 3, 5);
+    return ct >= 13 ? rb13 : ct == 12 ? rb12 : (ct < 4 ? ct : 4);
 }
 
 // QK_RB13 unset: 2^13-amplitude passes are scheduled both ways (5 and 4
@@ -1103,7 +1113,7 @@ void applyStorePermutation(PassParams& P, const std::vector<int>& sigma) {
 }
 
 std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::vector<double>& gtab,
-                               const std::vector<int>* dest, std::vector<int>* relabel) {
+                               const std::vector<int>* dest, std::vector<int>* relabel, int tileBits) {
     std::vector<Step> steps;
     // Routing (dest given): memory bit b's data should end at memory bit
     // dest[b].  Each pass stores its tile with the permutation that puts every
@@ -1179,7 +1189,7 @@ std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::
         for (const Gate& g : gates) denseStep(quokka::gateMatrix(g), g.qubits(), referenceFlopsPerAmp(g));
         return steps;
     }
-    const int ct = std::min(maxTileBits(), nLocal);
+    const int ct = std::min(tileBits > 0 ? tileBits : maxTileBits(), nLocal);
     const int rb = regBitsFor(ct);
     // Cut each run of gates (between wide dense steps) into passes by dynamic
     // programming over cut points.  A pass costs one HBM round trip, more when

@@ -48,9 +48,10 @@ struct Step {
 // With `dest` (memory bit -> memory bit where its data should end up), the
 // passes also route data toward dest with free in-tile store permutations;
 // `relabel` receives the resulting move (data that started at memory bit b is
-// now at relabel[b]).
+// now at relabel[b]).  tileBits > 0 overrides the tile size (QK_MAX_TILE_BITS).
 std::vector<Step> compileBlock(const std::vector<quokka::Gate>& gates, int nLocal, std::vector<double>& gtab,
-                               const std::vector<int>* dest = nullptr, std::vector<int>* relabel = nullptr);
+                               const std::vector<int>* dest = nullptr, std::vector<int>* relabel = nullptr,
+                               int tileBits = 0);
 
 // Reference-formula flops per amplitude for one gate.
 double referenceFlopsPerAmp(const quokka::Gate& g);

@@ -150,10 +150,11 @@ def test_grover_closed_form(qk):
     assert np.max(np.abs(logical[1 << m:])) < TOL  # ancillas back at |0>
 
 
-def test_register_width_autotune_variants_agree(ref, qk):
-    # 2^13-tile passes carry a second schedule (16 vs 32 amplitudes per
-    # thread); run 1 times variant A, run 2 variant B, later runs the faster.
-    # Every run must match the reference.
+def test_autotune_variants_agree(ref, qk):
+    # 2^13-tile passes carry register-width variants (32/16/8 amplitudes per
+    # thread) and each gate stream a 2^12-tile schedule; the first runs time
+    # the variants (2^13 rb=5, 2^12, 2^13 rb=4, 2^13 rb=3), later runs keep
+    # the fastest.  Every run must match the reference.
     n = 22
     for kind, a, seed in (("qft", 0, 0), ("random", 200, 3)):
         cfg_text = config_text(n, 0, 13, fusion=0, diag=0)
@@ -161,7 +162,9 @@ def test_register_width_autotune_variants_agree(ref, qk):
         want, _, _, _ = ref.simulate(prog_text, cfg_text, n, 0, 3, 8)
         prog = qk.Program.parse(prog_text, qk.Config.parse(cfg_text))
         st = qk.State(n)
-        for _ in range(3):
-            st.simulate(prog, 3)
+        tuning = []
+        for _ in range(6):
+            tuning.append(st.simulate(prog, 3)["tuning_runs"])
             assert np.max(np.abs(st.download() - want.view(np.complex128))) < TOL, kind
+        assert all(tuning[:4]) and not any(tuning[4:]), tuning
         st.close()
