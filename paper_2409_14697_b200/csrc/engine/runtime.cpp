@@ -319,10 +319,72 @@ std::vector<std::vector<std::pair<int, int>>> materializePairs(const std::vector
 
 bool useJit(int nLocal);
 
+// Process-wide schedule cache (a plan cache): programs with identical items
+// on the same slice size share one compiled schedule, its device-independent
+// tables and its autotune state, so re-parsing a program text does not
+// re-schedule or re-tune it.  Keyed by the items' binary content.
+std::string scheduleKey(const quokka::Program& prog, int nLocal) {
+    std::string k;
+    auto put = [&](const void* d, size_t n) { k.append(static_cast<const char*>(d), n); };
+    auto putInts = [&](const std::vector<int>& v) {
+        const uint32_t n = uint32_t(v.size());
+        put(&n, sizeof n);
+        put(v.data(), v.size() * sizeof(int));
+    };
+    put(&nLocal, sizeof nLocal);
+    for (const quokka::ProgramItem& it : prog.items) {
+        const int t = int(it.type);
+        put(&t, sizeof t);
+        if (it.type == quokka::ProgramItem::Block) {
+            const uint32_t n = uint32_t(it.block.gates.size());
+            put(&n, sizeof n);
+            for (const quokka::Gate& g : it.block.gates) {
+                const int kind = int(g.kind);
+                put(&kind, sizeof kind);
+                putInts(g.targets);
+                putInts(g.controls);
+                const uint32_t np = uint32_t(g.params.size()), na = uint32_t(g.payload.size());
+                put(&np, sizeof np);
+                put(g.params.data(), g.params.size() * sizeof(double));
+                put(&na, sizeof na);
+                put(g.payload.data(), g.payload.size() * sizeof(quokka::Amp));
+            }
+        } else {
+            const int kind = int(it.swap.kind);
+            put(&kind, sizeof kind);
+            for (const auto& [a, b] : it.swap.pairs) {
+                put(&a, sizeof a);
+                put(&b, sizeof b);
+            }
+            const int end = -1;
+            put(&end, sizeof end);
+        }
+    }
+    return k;
+}
+
+struct ScheduleCache {
+    std::mutex mu;
+    std::map<std::string, std::shared_ptr<Compiled>> byKey;
+    std::vector<std::string> order;  // insertion order (evict the oldest)
+    static constexpr size_t kMax = 32;
+};
+ScheduleCache& scheduleCache() {
+    static ScheduleCache c;
+    return c;
+}
+
 std::shared_ptr<Compiled> compileFor(qk_program* p, int nLocal) {
     std::lock_guard<std::mutex> lk(p->mu);
     auto it = p->compiled.find(nLocal);
     if (it != p->compiled.end()) return it->second;
+    const std::string key = scheduleKey(p->prog, nLocal);
+    {
+        ScheduleCache& sc = scheduleCache();
+        std::lock_guard<std::mutex> g(sc.mu);
+        auto hit = sc.byKey.find(key);
+        if (hit != sc.byKey.end()) return p->compiled[nLocal] = hit->second;
+    }
     auto c = std::make_shared<Compiled>();
     c->nLocal = nLocal;
     // Lazy in-memory swaps: an SQS (and a SWAP gate) only relabels which
@@ -444,6 +506,17 @@ std::shared_ptr<Compiled> compileFor(qk_program* p, int nLocal) {
     }
     flushAndMaterialize();
     p->compiled[nLocal] = c;
+    {
+        ScheduleCache& sc = scheduleCache();
+        std::lock_guard<std::mutex> g(sc.mu);
+        if (sc.byKey.emplace(key, c).second) {
+            sc.order.push_back(key);
+            if (sc.order.size() > ScheduleCache::kMax) {
+                sc.byKey.erase(sc.order.front());
+                sc.order.erase(sc.order.begin());
+            }
+        }
+    }
     return c;
 }
 
