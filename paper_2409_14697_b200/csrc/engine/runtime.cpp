@@ -219,6 +219,9 @@ struct Alternative {
 
 struct Compiled {
     int nLocal = 0;
+    // Initial memory layout (program position p of the slice at memory bit
+    // mem0[p]); identity unless compiled for a run from a basis state.
+    std::vector<int> mem0;
     std::vector<CompiledItem> items;
     std::vector<Alternative> alts;  // sorted by first
     std::vector<double> gtab;     // host copy of device tables
@@ -319,6 +322,15 @@ std::vector<std::vector<std::pair<int, int>>> materializePairs(const std::vector
 
 bool useJit(int nLocal);
 
+// QK_BASIS_LAYOUT (default 1): see compileFor(fromBasis).
+bool basisLayout() {
+    static const bool v = [] {
+        const char* e = std::getenv("QK_BASIS_LAYOUT");
+        return !e || std::atoi(e) != 0;
+    }();
+    return v;
+}
+
 // Process-wide schedule cache (a plan cache): programs with identical items
 // on the same slice size share one compiled schedule, its device-independent
 // tables and its autotune state, so re-parsing a program text does not
@@ -374,17 +386,19 @@ ScheduleCache& scheduleCache() {
     return c;
 }
 
-std::shared_ptr<Compiled> compileFor(qk_program* p, int nLocal) {
-    std::lock_guard<std::mutex> lk(p->mu);
-    auto it = p->compiled.find(nLocal);
-    if (it != p->compiled.end()) return it->second;
-    const std::string key = scheduleKey(p->prog, nLocal);
-    {
-        ScheduleCache& sc = scheduleCache();
-        std::lock_guard<std::mutex> g(sc.mu);
-        auto hit = sc.byKey.find(key);
-        if (hit != sc.byKey.end()) return p->compiled[nLocal] = hit->second;
-    }
+// Estimated cost of a compiled program in slice sweeps: every step of a
+// block and every IMS / XRS item reads and writes the slice once; a block
+// step runs at ~1.5x the time of an IMS (B200: ~73 vs ~44 ms at 2^33), so
+// steps weigh 3 and permutations 2.
+size_t sweeps(const Compiled& c) {
+    size_t n = 0;
+    for (const CompiledItem& it : c.items) n += it.kind == CompiledItem::Block ? 3 * it.steps.size() : 2;
+    return n;
+}
+
+// One compilation of p's items for a slice of 2^nLocal amplitudes, starting
+// from memory layout mem0 (program position p at memory bit mem0[p]).
+std::shared_ptr<Compiled> compileLayout(qk_program* p, int nLocal, const std::vector<int>& mem0) {
     auto c = std::make_shared<Compiled>();
     c->nLocal = nLocal;
     // Lazy in-memory swaps: an SQS (and a SWAP gate) only relabels which
@@ -395,9 +409,9 @@ std::shared_ptr<Compiled> compileFor(qk_program* p, int nLocal) {
     // relabeling is materialized (<= 2 IMS passes) only before a cross-rank
     // swap and at the end, so the final state is in the program's physical
     // order.
-    std::vector<int> mem(static_cast<size_t>(nLocal));
-    for (int b = 0; b < nLocal; b++) mem[size_t(b)] = b;
+    std::vector<int> mem = mem0;
     const bool lazy = lazyIms();
+    c->mem0 = mem;
     std::vector<quokka::Gate> stream;
     auto flushStream = [&](bool beforeMaterialize, int tileBits = 0) {
         if (stream.empty()) return;
@@ -505,7 +519,52 @@ std::shared_ptr<Compiled> compileFor(qk_program* p, int nLocal) {
         c->items.push_back(std::move(ci));
     }
     flushAndMaterialize();
-    p->compiled[nLocal] = c;
+    return c;
+}
+
+// fromBasis: the run starts from a basis state (qk_simulate), whose memory
+// layout is free: |x> with its bits permuted is just another basis state.
+// The slice then starts in the layout that the first gate stream's lazy
+// SQS / SWAP relabels carry to the program's physical order, so that stream
+// ends with nothing to materialize (no IMS pass).  Runs on an existing state
+// (qk_apply_block) start from the identity layout.
+std::shared_ptr<Compiled> compileFor(qk_program* p, int nLocal, bool fromBasis = true) {
+    std::lock_guard<std::mutex> lk(p->mu);
+    const int slot = fromBasis ? nLocal : -1 - nLocal;
+    auto it = p->compiled.find(slot);
+    if (it != p->compiled.end()) return it->second;
+    const std::string key = scheduleKey(p->prog, slot);
+    {
+        ScheduleCache& sc = scheduleCache();
+        std::lock_guard<std::mutex> g(sc.mu);
+        auto hit = sc.byKey.find(key);
+        if (hit != sc.byKey.end()) return p->compiled[slot] = hit->second;
+    }
+    std::vector<int> ident(static_cast<size_t>(nLocal));
+    for (int b = 0; b < nLocal; b++) ident[size_t(b)] = b;
+    std::shared_ptr<Compiled> c = compileLayout(p, nLocal, ident);
+    if (lazyIms() && fromBasis && basisLayout()) {
+        // sim = the first stream's relabels applied to the identity; starting
+        // from its inverse, mem is the identity when that stream ends.  The
+        // layout changes the scheduler's tiles too, so keep whichever
+        // compilation costs fewer weighted sweeps (ties: the free layout).
+        std::vector<int> sim = ident, mem0(static_cast<size_t>(nLocal));
+        for (const quokka::ProgramItem& item : p->prog.items) {
+            if (item.type == quokka::ProgramItem::Block) {
+                for (const quokka::Gate& g : item.block.gates)
+                    if (g.kind == quokka::GateKind::SWAP) std::swap(sim[size_t(g.targets[0])], sim[size_t(g.targets[1])]);
+                continue;
+            }
+            if (item.swap.kind != quokka::SwapOp::InMemory) break;
+            for (const auto& [o, i] : item.swap.pairs) std::swap(sim[size_t(o)], sim[size_t(i)]);
+        }
+        for (int q = 0; q < nLocal; q++) mem0[size_t(sim[size_t(q)])] = q;
+        if (mem0 != ident) {
+            std::shared_ptr<Compiled> b = compileLayout(p, nLocal, mem0);
+            if (sweeps(*b) <= sweeps(*c)) c = b;
+        }
+    }
+    p->compiled[slot] = c;
     {
         ScheduleCache& sc = scheduleCache();
         std::lock_guard<std::mutex> g(sc.mu);
@@ -922,11 +981,20 @@ void checkProgramAgainst(const quokka::Program& prog, const quokka::Config& cfg,
     }
 }
 
-void setBasis(qk_state* st, Index global) {
+// Slice-local index of a basis state in the memory layout `mem0` (program
+// position p at memory bit mem0[p]).
+uint64_t layoutIndex(uint64_t local, const std::vector<int>& mem0) {
+    uint64_t x = 0;
+    for (size_t p = 0; p < mem0.size(); p++) x |= ((local >> p) & 1) << mem0[p];
+    return x;
+}
+
+void setBasis(qk_state* st, Index global, const std::vector<int>* mem0 = nullptr) {
     if (global >= (Index(1) << st->n)) throw SimulationError("initial basis state out of range");
     cuda(cudaMemsetAsync(st->amps, 0, st->count * sizeof(double2), st->stream), "memset");
-    if ((global >> st->nLocal) == Index(st->rank))
-        cuda(qkdev::launchSetBasis(st->amps, global & (st->count - 1), st->stream), "set basis");
+    uint64_t local = global & (st->count - 1);
+    if (mem0) local = layoutIndex(local, *mem0);
+    if ((global >> st->nLocal) == Index(st->rank)) cuda(qkdev::launchSetBasis(st->amps, local, st->stream), "set basis");
 }
 
 }  // namespace
@@ -1060,7 +1128,7 @@ int qk_apply_block(qk_state* st, const qk_gate* gates, int ngates, int chunk) {
         qk_program prog;
         prog.prog = std::move(p);
         DeviceGuard g(st->device);
-        auto c = compileFor(&prog, st->nLocal);
+        auto c = compileFor(&prog, st->nLocal, false);
         DeviceTables t = tablesFor(&prog, *c, st->device);
         prepareJit(*c, st->device);
         qk_run_stats rs{};
@@ -1106,7 +1174,7 @@ int qk_debug_jit_compile(const qk_gate* gates, int ngates, int nLocal, char** so
 int qk_debug_jit_program(const qk_program* cp, int nLocal, char** sources) {
     return guard([&] {
         qk_program* p = const_cast<qk_program*>(cp);
-        auto c = compileFor(p, nLocal);
+        auto c = compileFor(p, nLocal, std::getenv("QK_DEBUG_FROM_BASIS") != nullptr);
         std::string all;
         int k = 0;
         for (const CompiledItem& it : c->items)
@@ -1125,7 +1193,7 @@ int qk_debug_jit_program(const qk_program* cp, int nLocal, char** sources) {
 int qk_debug_compile_program(const qk_program* cp, int nLocal, char** json) {
     return guard([&] {
         qk_program* p = const_cast<qk_program*>(cp);
-        auto c = compileFor(p, nLocal);
+        auto c = compileFor(p, nLocal, std::getenv("QK_DEBUG_FROM_BASIS") != nullptr);
         std::ostringstream o;
         o << "{\"items\":[";
         for (size_t i = 0; i < c->items.size(); i++) {
@@ -1394,8 +1462,10 @@ int qk_simulate(qk_state* st, const qk_program* cp, const qk_config* cfg, uint64
         const bool synth = !comp->items.empty() && comp->items[0].kind == CompiledItem::Block &&
                            !comp->items[0].steps.empty() && comp->items[0].steps[0].kind == qkeng::Step::Pass;
         uint64_t basis = kNoBasis;
-        if (synth) basis = (initial >> st->nLocal) == Index(st->rank) ? (initial & (st->count - 1)) : st->count;
-        else setBasis(st, initial);
+        if (synth)
+            basis = (initial >> st->nLocal) == Index(st->rank) ? layoutIndex(initial & (st->count - 1), comp->mem0)
+                                                              : st->count;
+        else setBasis(st, initial, &comp->mem0);
         auto runItem = [&](const CompiledItem& it) {
             if (it.kind == CompiledItem::Block) {
                 timer.time(0, [&] { runBlock(st, it, t, rs, basis); });
@@ -1477,7 +1547,7 @@ int qk_simulate_local(qk_state** sl, int ns, const qk_program* cp, const qk_conf
             tabs.push_back(tablesFor(p, *comp, sl[k]->device));
             DeviceGuard g(sl[k]->device);
             prepareJit(*comp, sl[k]->device);
-            setBasis(sl[k], initial);
+            setBasis(sl[k], initial, &comp->mem0);
         }
         if (stats)
             for (int k = 0; k < ns; k++) stats[k] = qk_xrs_stats{};
