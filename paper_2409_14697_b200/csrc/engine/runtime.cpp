@@ -398,7 +398,7 @@ size_t sweeps(const Compiled& c) {
 
 // One compilation of p's items for a slice of 2^nLocal amplitudes, starting
 // from memory layout mem0 (program position p at memory bit mem0[p]).
-std::shared_ptr<Compiled> compileLayout(qk_program* p, int nLocal, const std::vector<int>& mem0) {
+std::shared_ptr<Compiled> compileLayout(qk_program* p, int nLocal, const std::vector<int>& mem0, bool synthFirst) {
     auto c = std::make_shared<Compiled>();
     c->nLocal = nLocal;
     // Lazy in-memory swaps: an SQS (and a SWAP gate) only relabels which
@@ -421,10 +421,11 @@ std::shared_ptr<Compiled> compileLayout(qk_program* p, int nLocal, const std::ve
             // route the data toward the program's physical order (mem = identity)
             std::vector<int> dest(static_cast<size_t>(nLocal)), moved;
             for (int q = 0; q < nLocal; q++) dest[size_t(mem[size_t(q)])] = q;
-            ci.steps = qkeng::compileBlock(stream, nLocal, c->gtab, &dest, &moved, tileBits);
+            ci.steps = qkeng::compileBlock(stream, nLocal, c->gtab, &dest, &moved, tileBits, synthFirst && c->items.empty());
             for (int q = 0; q < nLocal; q++) mem[size_t(q)] = moved[size_t(mem[size_t(q)])];
         } else {
-            ci.steps = qkeng::compileBlock(stream, nLocal, c->gtab, nullptr, nullptr, tileBits);
+            ci.steps = qkeng::compileBlock(stream, nLocal, c->gtab, nullptr, nullptr, tileBits,
+                                           synthFirst && c->items.empty());
         }
         for (qkeng::Step& s : ci.steps) {
             ci.flopsPerAmp += s.flopsPerAmp;
@@ -542,7 +543,7 @@ std::shared_ptr<Compiled> compileFor(qk_program* p, int nLocal, bool fromBasis =
     }
     std::vector<int> ident(static_cast<size_t>(nLocal));
     for (int b = 0; b < nLocal; b++) ident[size_t(b)] = b;
-    std::shared_ptr<Compiled> c = compileLayout(p, nLocal, ident);
+    std::shared_ptr<Compiled> c = compileLayout(p, nLocal, ident, fromBasis);
     if (lazyIms() && fromBasis && basisLayout()) {
         // sim = the first stream's relabels applied to the identity; starting
         // from its inverse, mem is the identity when that stream ends.  The
@@ -560,7 +561,7 @@ std::shared_ptr<Compiled> compileFor(qk_program* p, int nLocal, bool fromBasis =
         }
         for (int q = 0; q < nLocal; q++) mem0[size_t(sim[size_t(q)])] = q;
         if (mem0 != ident) {
-            std::shared_ptr<Compiled> b = compileLayout(p, nLocal, mem0);
+            std::shared_ptr<Compiled> b = compileLayout(p, nLocal, mem0, fromBasis);
             if (sweeps(*b) <= sweeps(*c)) c = b;
         }
     }

@@ -1113,7 +1113,8 @@ void applyStorePermutation(PassParams& P, const std::vector<int>& sigma) {
 }
 
 std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::vector<double>& gtab,
-                               const std::vector<int>* dest, std::vector<int>* relabel, int tileBits) {
+                               const std::vector<int>* dest, std::vector<int>* relabel, int tileBits,
+                               bool synthFirst) {
     std::vector<Step> steps;
     // Routing (dest given): memory bit b's data should end at memory bit
     // dest[b].  Each pass stores its tile with the permutation that puts every
@@ -1207,6 +1208,7 @@ std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::
     auto cutRun = [&] {
         const size_t m = run.size();
         if (!m) return;
+        const bool synthRun = synthFirst && steps.empty();
         std::vector<uint64_t> mask(m);
         for (size_t k = 0; k < m; k++) mask[k] = isDiagonalGate(run[k]) ? 0 : run[k].depMask();
         std::vector<double> best(m + 1, 1e300);
@@ -1217,7 +1219,7 @@ std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::
             for (size_t j = i; j-- > 0;) {
                 used |= mask[j];
                 if (__builtin_popcountll(used) > ct) break;
-                const double c = best[j] + passCost(used);
+                const double c = best[j] + ((synthRun && j == 0) ? 1.0 : passCost(used));
                 if (c < best[i] - 1e-9) {
                     best[i] = c;
                     from[i] = j;

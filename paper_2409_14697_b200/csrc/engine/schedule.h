@@ -49,9 +49,12 @@ struct Step {
 // passes also route data toward dest with free in-tile store permutations;
 // `relabel` receives the resulting move (data that started at memory bit b is
 // now at relabel[b]).  tileBits > 0 overrides the tile size (QK_MAX_TILE_BITS).
+// synthFirst: the first pass will synthesize its input from a basis state
+// (one tile computed, the rest zero-filled), so its tile needs no coalescing
+// padding with the lowest memory bits.
 std::vector<Step> compileBlock(const std::vector<quokka::Gate>& gates, int nLocal, std::vector<double>& gtab,
                                const std::vector<int>* dest = nullptr, std::vector<int>* relabel = nullptr,
-                               int tileBits = 0);
+                               int tileBits = 0, bool synthFirst = false);
 
 // Reference-formula flops per amplitude for one gate.
 double referenceFlopsPerAmp(const quokka::Gate& g);
