@@ -12,8 +12,7 @@ timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; echo "bench rc $?";
 if [ "${SKIP_NCU:-0}" = "0" ]; then
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv \
    python bench.py --steps 1 --warmup 1 --no-cpu-baseline > $O/bench_ncu.log 2>&1; echo "ncu-list rc $?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:qk_pass -s 0 -c 3 -o $O/prof_block \
-   python tools/run_qft.py 30 > $O/ncu_full.log 2>&1; echo "ncu-full rc $?"; tail -3 $O/ncu_full.log
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_ims -s 0 -c 2 -o $O/prof_ims \
-   python tools/run_qft.py 30 > $O/ncu_ims.log 2>&1; echo "ncu-ims rc $?"
+# the two full-state passes of QFT-31 (launch 0 is the synthesized single-tile pass)
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:qk_pass -s 1 -c 2 -o $O/prof_block \
+   python tools/run_qft.py 31 > $O/ncu_full.log 2>&1; echo "ncu-full rc $?"; tail -3 $O/ncu_full.log
 fi
