@@ -59,6 +59,16 @@ static __device__ __forceinline__ double2 cmac(double2 acc, double2 m, double2 x
     acc.y = fma(m.x, x.y, acc.y); acc.y = fma(m.y, x.x, acc.y);
     return acc;
 }
+// Literal coefficients with a zero part (the generator picks these): real r,
+// imaginary i.  Same results as cmul / cmac up to the sign of zero.
+static __device__ __forceinline__ double2 cmulr(double2 a, double r) { return make_double2(a.x * r, a.y * r); }
+static __device__ __forceinline__ double2 cmuli(double2 a, double i) { return make_double2(-(a.y * i), a.x * i); }
+static __device__ __forceinline__ double2 cmacr(double2 acc, double r, double2 x) {
+    return make_double2(fma(r, x.x, acc.x), fma(r, x.y, acc.y));
+}
+static __device__ __forceinline__ double2 cmaci(double2 acc, double i, double2 x) {
+    return make_double2(fma(-i, x.y, acc.x), fma(i, x.x, acc.y));
+}
 static __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 static __device__ __forceinline__ double2 cinv(double2 a) {
     const double d = 1.0 / fma(a.x, a.x, a.y * a.y);
@@ -483,6 +493,24 @@ private:
     }
 
     std::string lc(uint32_t i) const { return c2(P_.coef[2 * i], P_.coef[2 * i + 1]); }
+    // x * (re + i im) for a literal coefficient, specialized when a part is 0.
+    static std::string mulK(const std::string& x, double re, double im) {
+        if (re == 0.0 && im == 0.0) return "C2(0.0, 0.0)";
+        if (im == 0.0) return re == 1.0 ? x : "cmulr(" + x + ", " + lit(re) + ")";
+        if (re == 0.0) return "cmuli(" + x + ", " + lit(im) + ")";
+        return "cmul(" + x + ", " + c2(re, im) + ")";
+    }
+    // acc + (re + i im) * x
+    static std::string macK(const std::string& acc, double re, double im, const std::string& x) {
+        if (re == 0.0 && im == 0.0) return acc;
+        if (im == 0.0) return "cmacr(" + acc + ", " + lit(re) + ", " + x + ")";
+        if (re == 0.0) return "cmaci(" + acc + ", " + lit(im) + ", " + x + ")";
+        return "cmac(" + acc + ", " + c2(re, im) + ", " + x + ")";
+    }
+    std::string mulC(const std::string& x, uint32_t i) const { return mulK(x, P_.coef[2 * i], P_.coef[2 * i + 1]); }
+    std::string macC(const std::string& acc, uint32_t i, const std::string& x) const {
+        return macK(acc, P_.coef[2 * i], P_.coef[2 * i + 1], x);
+    }
     std::string A(int s) const { return "a" + std::to_string(nm_[size_t(s)]); }
 
     void mulAmp(int s, const std::string& e) { o_ << "  " << A(s) << " = cmul(" << A(s) << ", " << e << ");\n"; }
@@ -507,9 +535,9 @@ private:
             case qkdev::OP_MAT1:
                 for (int s = 0; s < na_; s++)
                     if (!(s & K))
-                        o_ << "  { const double2 x = " << A(s) << ", y = " << A(s | K) << "; " << A(s) << " = cmac(cmul("
-                           << lc(d.c) << ", x), " << lc(d.c + 1) << ", y); " << A(s | K) << " = cmac(cmul("
-                           << lc(d.c + 2) << ", x), " << lc(d.c + 3) << ", y); }\n";
+                        o_ << "  { const double2 x = " << A(s) << ", y = " << A(s | K) << "; " << A(s) << " = "
+                           << macC(mulC("x", d.c), d.c + 1, "y") << "; " << A(s | K) << " = "
+                           << macC(mulC("x", d.c + 2), d.c + 3, "y") << "; }\n";
                 return;
             case qkdev::OP_CX: {
                 const int pol = (d.k >> 1) & 1;
@@ -527,7 +555,10 @@ private:
                 return;
             }
             case qkdev::OP_DIAG1_R:
-                for (int s = 0; s < na_; s++) mulAmp(s, lc(d.c + ((s >> a) & 1)));
+                for (int s = 0; s < na_; s++) {
+                    const std::string e = mulC(A(s), d.c + ((s >> a) & 1));
+                    if (e != A(s)) o_ << "  " << A(s) << " = " << e << ";\n";
+                }
                 return;
             case qkdev::OP_DIAG2_RR:
                 for (int s = 0; s < na_; s++) mulAmp(s, lc(d.c + ((((s >> a) & 1) << 1) | ((s >> b) & 1))));
@@ -611,7 +642,7 @@ private:
                 o_ << "  {\n";
                 for (int j = 0; j < ng; j++) {
                     const std::string g = lc(d.c + uint32_t(j));
-                    o_ << "    const double2 h" << j << " = " << (dirtyR_[a] ? "cmul(R" + std::to_string(a) + ", " + g + ")" : g)
+                    o_ << "    const double2 h" << j << " = " << (dirtyR_[a] ? mulC("R" + std::to_string(a), d.c + uint32_t(j)) : g)
                        << ";\n";
                 }
                 for (int s = 0; s < na_; s++) {
@@ -749,8 +780,7 @@ private:
             else o_ << "    const double2 f" << s << " = f" << rest << ";\n";
         }
         for (int s = 0; s < na_; s++)
-            mulAmp(s, dOne(s) ? "f" + std::to_string(s)
-                              : "cmul(f" + std::to_string(s) + ", " + c2(D[2 * s], D[2 * s + 1]) + ")");
+            mulAmp(s, dOne(s) ? "f" + std::to_string(s) : mulK("f" + std::to_string(s), D[2 * s], D[2 * s + 1]));
         o_ << "  }\n  P = C2(1.0, 0.0);\n";
         for (int k = 0; k < rb_; k++)
             if (dirtyR_[k]) o_ << "  R" << k << " = C2(1.0, 0.0);\n";
@@ -770,7 +800,7 @@ private:
 // ---- compile / load / launch -------------------------------------------------
 
 // Bump when the generated code changes for the same PassParams (on-disk cache key).
-constexpr uint64_t kGeneratorVersion = 16;
+constexpr uint64_t kGeneratorVersion = 17;
 
 uint64_t hashPass(const PassParams& P) {
     uint64_t h = 1469598103934665603ull ^ (kGeneratorVersion * 0x9E3779B97F4A7C15ull) ^ (usePrefetch() ? 1u : 0u) ^ (usePersistent() ? 2u : 0u) ^
