@@ -224,7 +224,7 @@ public:
         o_ << kPrologue;
         ctaTables();
         o_ << "extern \"C\" __global__ void __launch_bounds__(" << nt_ << "," << minb << ") " << name
-           << "(double2* __restrict__ st, const double2* __restrict__ gt, const u32 ntiles, const u64 basis, const u32 tile0) {\n";
+           << "(double2* __restrict__ st, const double2* __restrict__ gt, const u32 ntiles, const u64 basis, const u32 tile0, double* __restrict__ np) {\n";
         o_ << "  extern __shared__ double2 sm[];\n  double2* const F = sm + " << (1 << ct_)
            << ";\n  const u32 tid = threadIdx.x;\n";
         o_ << "  for (u32 tile = blockIdx.x + tile0; tile < ntiles; tile += gridDim.x) {\n";
@@ -263,6 +263,16 @@ public:
         // threads may still be loading the addresses this thread stores to.
         if (P_.nsegs == 1 && (std::memcmp(P_.map_in[0], P_.map_out[0], sizeof P_.map_in[0]) != 0 || P_.xmask_out[0]))
             o_ << "  __syncthreads();\n";
+        if (P_.norm_out) {
+            // sum |a|^2 of the output tile (fixed order: slots, xor butterfly, warps)
+            o_ << "  { double s_ = 0.0;\n";
+            for (int s = 0; s < na_; s++) o_ << "    s_ = fma(" << A(s) << ".x, " << A(s) << ".x, fma(" << A(s) << ".y, " << A(s) << ".y, s_));\n";
+            o_ << "    for (int o_ = 16; o_ > 0; o_ >>= 1) s_ += __shfl_xor_sync(0xffffffffu, s_, o_);\n"
+               << "    double* const red = reinterpret_cast<double*>(F + " << qkdev::kMaxCtaFactors << ");\n"
+               << "    if ((tid & 31u) == 0u) red[tid >> 5] = s_;\n    __syncthreads();\n"
+               << "    if (tid == 0u) { double t_ = 0.0; for (u32 w = 0; w < " << (nt_ / 32 > 0 ? nt_ / 32 : 1)
+               << "u; w++) t_ += red[w]; np[tile] = t_; }\n  }\n";
+        }
         o_ << "  { const u64 off = (base | " << threadGlobal(P_.map_out[last]) << ") ^ " << gx << "ull;\n";
         const int ks = slotOfMem0(P_.map_out[last]);
         for (int s = 0; s < na_; s++) {
@@ -288,7 +298,7 @@ public:
         o_ << kPrologue;
         ctaTables();
         o_ << "extern \"C\" __global__ void __launch_bounds__(" << nt_ << ",1) " << name
-           << "(double2* __restrict__ st, const double2* __restrict__ gt, const u32 ntiles, const u64 basis, const u32 tile0) {\n"
+           << "(double2* __restrict__ st, const double2* __restrict__ gt, const u32 ntiles, const u64 basis, const u32 tile0, double* __restrict__ np) {\n"
            << "  extern __shared__ double2 sm[];  // PB: next tile (linear tile coordinates) | XS | F | mbarrier\n"
            << "  double2* const XS = sm + 8192;\n  double2* const F = sm + 12288;\n"
            << "  u64* const mbar = (u64*)(sm + 12352);\n  const u32 tid = threadIdx.x;\n"
@@ -800,7 +810,7 @@ private:
 // ---- compile / load / launch -------------------------------------------------
 
 // Bump when the generated code changes for the same PassParams (on-disk cache key).
-constexpr uint64_t kGeneratorVersion = 17;
+constexpr uint64_t kGeneratorVersion = 18;
 
 uint64_t hashPass(const PassParams& P) {
     uint64_t h = 1469598103934665603ull ^ (kGeneratorVersion * 0x9E3779B97F4A7C15ull) ^ (usePrefetch() ? 1u : 0u) ^ (usePersistent() ? 2u : 0u) ^
@@ -888,7 +898,7 @@ void* functionFor(const PassParams& P, uint64_t h, int device) {
     if (d.moduleLoadData(&mod, e.cubin.data()) != 0) throw SimulationError("jit: cuModuleLoadData failed");
     if (d.moduleGetFunction(&fn, mod, kernelName(h).c_str()) != 0) throw SimulationError("jit: cuModuleGetFunction failed");
     const int smem = pipelined(P) ? int(sizeof(double2) * kPipeSmemAmps)
-                                  : int((sizeof(double2) << P.ct) + sizeof(double2) * qkdev::kMaxCtaFactors);
+                                  : int((sizeof(double2) << P.ct) + sizeof(double2) * qkdev::kMaxCtaFactors + 256);
     if (smem > 48 * 1024 && d.funcSetAttribute(fn, 8 /*CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES*/, smem) != 0)
         throw SimulationError("jit: cuFuncSetAttribute failed");
     e.func[device] = fn;
@@ -1026,7 +1036,7 @@ void prepare(const std::vector<const PassParams*>& passes, int device) {
 }
 
 cudaError_t launch(const PassParams& P, double2* state, const double2* gtab, int nLocal, uint64_t basis,
-                   cudaStream_t stream) {
+                   cudaStream_t stream, double* np) {
     int dev = 0;
     cudaGetDevice(&dev);
     void* fn = functionFor(P, hashPass(P), dev);
@@ -1052,8 +1062,8 @@ cudaError_t launch(const PassParams& P, double2* state, const double2* gtab, int
     }
     const unsigned nt = 1u << (P.ct - P.rb);
     const unsigned smem = pipe ? unsigned(sizeof(double2) * kPipeSmemAmps)
-                               : unsigned((sizeof(double2) << P.ct) + sizeof(double2) * qkdev::kMaxCtaFactors);
-    void* args[] = {&state, &gtab, &ntiles, &basis, &tile0};
+                               : unsigned((sizeof(double2) << P.ct) + sizeof(double2) * qkdev::kMaxCtaFactors + 256);
+    void* args[] = {&state, &gtab, &ntiles, &basis, &tile0, &np};
     if (driver().launchKernel(fn, ctas, 1, 1, nt, 1, 1, smem, stream, args, nullptr) != 0)
         return cudaErrorLaunchFailure;
     return cudaSuccess;

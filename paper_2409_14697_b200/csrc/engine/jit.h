@@ -26,8 +26,9 @@ void prepare(const std::vector<const qkdev::PassParams*>& passes, int device);
 // Launch the specialized kernel of P (prepare()d for the current device).
 // basis != ~0: synthesize the basis state |basis> (slice index) instead of
 // loading the slice (the first pass of a simulation needs no initState).
+// np: per-tile sums of |a|^2 when P.norm_out (one double per tile).
 cudaError_t launch(const qkdev::PassParams& P, double2* state, const double2* gtab, int nLocal, uint64_t basis,
-                   cudaStream_t stream);
+                   cudaStream_t stream, double* np = nullptr);
 
 // Slices with at least this many local qubits use specialized kernels
 // (QK_JIT_MIN_QUBITS, default 22; -1 disables).

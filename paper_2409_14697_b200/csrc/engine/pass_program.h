@@ -115,6 +115,7 @@ struct PassParams {
     int32_t ncta;                     // CTA factors (0: none)
     uint16_t cta_end[kMaxCtaFactors];
     CtaTerm cta_terms[kMaxCtaTerms];
+    int32_t norm_out;  // specialized kernels: also write sum |a|^2 of each output tile to np[tile]
 };
 
 static_assert(sizeof(PassParams) <= 32000, "kernel parameter limit");

@@ -302,6 +302,32 @@ __global__ void k_norm_final(const double* __restrict__ part, int nb, double* __
     }
 }
 
+// Fold of per-tile sums of |a|^2 (written by a specialized pass with
+// norm_out): same compensated fixed-order tree as k_norm_partial.
+__global__ void __launch_bounds__(256) k_sum_partial(const double* __restrict__ x, uint64_t n, double* __restrict__ part) {
+    __shared__ double ss[256], sc[256];
+    const uint64_t per = (n + gridDim.x - 1) / gridDim.x;
+    const uint64_t lo = per * blockIdx.x, hi = lo + per < n ? lo + per : n;
+    double s = 0, c = 0;
+    for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) twoSum(s, c, x[i]);
+    ss[threadIdx.x] = s;
+    sc[threadIdx.x] = c;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) {
+            double s2 = ss[threadIdx.x], c2 = sc[threadIdx.x] + sc[threadIdx.x + w];
+            twoSum(s2, c2, ss[threadIdx.x + w]);
+            ss[threadIdx.x] = s2;
+            sc[threadIdx.x] = c2;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        part[2 * blockIdx.x] = ss[0];
+        part[2 * blockIdx.x + 1] = sc[0];
+    }
+}
+
 __global__ void k_set_basis(double2* a, uint64_t idx) { a[idx] = make_double2(1.0, 0.0); }
 
 // Marginal probabilities over k <= 10 slice bits: part[block][v] = sum of
@@ -529,6 +555,12 @@ cudaError_t launchNorm(const double2* a, uint64_t n, double* scratch, double* ou
     return cudaGetLastError();
 }
 size_t normScratchDoubles() { return 2 * kNormBlocks; }
+
+cudaError_t launchSumTiles(const double* x, uint64_t n, double* scratch, double* out, cudaStream_t st) {
+    k_sum_partial<<<kNormBlocks, 256, 0, st>>>(x, n, scratch);
+    k_norm_final<<<1, 32, 0, st>>>(scratch, kNormBlocks, out);
+    return cudaGetLastError();
+}
 
 constexpr int kMargBlocks = 1184;
 size_t marginalScratchDoubles(int k) { return size_t(kMargBlocks) << k; }

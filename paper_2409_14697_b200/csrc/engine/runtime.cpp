@@ -36,6 +36,7 @@ cudaError_t launchWindowPack(double2*, const double2*, uint64_t, uint64_t, const
 cudaError_t launchWindowUnpack(double2*, const double2*, uint64_t, uint64_t, const int*, int, cudaStream_t);
 cudaError_t launchDiagTable(double2*, const double2*, uint64_t, const int*, int, cudaStream_t);
 cudaError_t launchNorm(const double2*, uint64_t, double*, double*, cudaStream_t);
+cudaError_t launchSumTiles(const double*, uint64_t, double*, double*, cudaStream_t);
 size_t normScratchDoubles();
 cudaError_t launchSetBasis(double2*, uint64_t, cudaStream_t);
 cudaError_t launchMarginal(const double2*, uint64_t, const int*, int, double*, double*, cudaStream_t);
@@ -265,6 +266,11 @@ struct qk_state {
     ncclComm_t comm = nullptr;
     bool profiling = false;
     qk_run_stats last{};
+    // Fused norm: the program's last pass wrote per-tile sums of |a|^2 and
+    // normOut holds their fold; valid until the state changes again.
+    double* normTiles = nullptr;
+    uint64_t normTilesCap = 0;
+    bool normValid = false;
 };
 
 namespace {
@@ -520,6 +526,20 @@ std::shared_ptr<Compiled> compileLayout(qk_program* p, int nLocal, const std::ve
         c->items.push_back(std::move(ci));
     }
     flushAndMaterialize();
+    // The program's last pass also writes per-tile sums of |a|^2, so the norm
+    // after a run needs no extra sweep of the slice (qk_norm).  Not for the
+    // synthesized single-tile first pass, nor the TMA-pipelined kernels.
+    auto markNorm = [&](std::vector<CompiledItem>& items, bool firstIsSynth) {
+        if (items.empty() || items.back().kind != CompiledItem::Block || items.back().steps.empty()) return;
+        qkeng::Step& s = items.back().steps.back();
+        if (s.kind != qkeng::Step::Pass || qkdev::halfExchanges()) return;
+        if (firstIsSynth && items.size() == 1 && items[0].steps.size() == 1) return;
+        s.pass->norm_out = 1;
+        for (auto& a : s.alts) a->norm_out = 1;
+    };
+    for (Alternative& alt : c->alts)
+        if (alt.last == c->items.size()) markNorm(alt.b, synthFirst && alt.first == 0);
+    markNorm(c->items, synthFirst);
     return c;
 }
 
@@ -663,6 +683,7 @@ void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_ru
               uint64_t basis = kNoBasis) {
     const bool synthesized = basis != kNoBasis;
     for (const qkeng::Step& s : ci.steps) {
+        st->normValid = false;
         if (s.kind == qkeng::Step::Pass) {
             // Register-width autotune: the first two executions of a pass time
             // each variant (events, synchronous); later ones take the faster.
@@ -676,8 +697,20 @@ void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_ru
                 cuda(cudaEventCreate(&e1), "event");
                 cuda(cudaEventRecord(e0, st->stream), "event");
             }
+            const bool fusedNorm = P.norm_out && useJit(st->nLocal) && basis == kNoBasis;
+            if (P.norm_out && useJit(st->nLocal)) {
+                const uint64_t tiles = st->count >> P.ct;
+                if (st->normTilesCap < tiles) {
+                    cudaFree(st->normTiles);
+                    st->normTiles = nullptr;
+                    cuda(cudaMalloc(&st->normTiles, tiles * sizeof(double)), "cudaMalloc(norm tiles)");
+                    st->normTilesCap = tiles;
+                }
+            }
             if (useJit(st->nLocal))
-                cuda(qkjit::launch(P, st->amps, t.gtab, st->nLocal, basis, st->stream), "specialized block pass");
+                cuda(qkjit::launch(P, st->amps, t.gtab, st->nLocal, basis, st->stream,
+                                   P.norm_out ? st->normTiles : nullptr),
+                     "specialized block pass");
             else
                 cuda(qkdev::launchBlockPass(st->amps, t.gtab, P, st->nLocal, basis, st->stream), "block pass");
             if (timing) {
@@ -692,6 +725,11 @@ void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_ru
                 rs.tuning_runs++;
             } else if (s.tune) {
                 s.tune->runs[v]++;
+            }
+            if (fusedNorm) {
+                cuda(qkdev::launchSumTiles(st->normTiles, st->count >> P.ct, st->normScratch, st->normOut, st->stream),
+                     "norm fold");
+                st->normValid = true;
             }
             basis = kNoBasis;
         } else if (s.kind == qkeng::Step::DiagTable) {
@@ -714,6 +752,7 @@ void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_ru
 }
 
 void runIms(qk_state* st, const std::vector<int>& outs, const std::vector<int>& ins, qk_run_stats& rs) {
+    st->normValid = false;
     if (outs.empty()) return;
     cuda(qkdev::launchIms(st->amps, st->nLocal, outs.data(), ins.data(), int(outs.size()), st->stream), "ims");
     rs.kernel_launches++;
@@ -781,6 +820,7 @@ struct XrsRank {
 // NCCL XRS for this rank (one process per GPU): per window round, one grouped
 // ncclSend/ncclRecv per partner into a single receive buffer, then copy-back.
 void runXrsNccl(qk_state* st, const XrsPlan& p, qk_run_stats& rs) {
+    st->normValid = false;
     if (!st->comm) throw SimulationError("cross-rank swap needs a communicator (qk_comm_init) or qk_simulate_local");
     if (p.s == 0) return;
     XrsRank x(st, p);
@@ -806,6 +846,7 @@ void runXrsNccl(qk_state* st, const XrsPlan& p, qk_run_stats& rs) {
 // round, as NCCL's grouped point-to-point does).  Test hook for the NCCL
 // path's plan, pack and copy-back kernels on a single GPU.
 void runXrsLoopback(qk_state** sl, int ns, const XrsPlan& p) {
+    for (int k = 0; k < ns; k++) sl[k]->normValid = false;
     if (p.s == 0) return;
     std::vector<std::unique_ptr<XrsRank>> rk;
     for (int r = 0; r < ns; r++) rk.push_back(std::make_unique<XrsRank>(sl[r], p));
@@ -850,6 +891,7 @@ void runXrsLoopback(qk_state** sl, int ns, const XrsPlan& p) {
 // In-process XRS: every slab pair swapped in place by one kernel reading and
 // writing both slices (same device or peer-mapped).  No buffer, no copy-back.
 void runXrsLocal(qk_state** sl, int ns, const XrsPlan& p) {
+    for (int k = 0; k < ns; k++) sl[k]->normValid = false;
     for (int k = 0; k < ns; k++) cuda(cudaStreamSynchronize(sl[k]->stream), "xrs pre-sync");
     const int slabs = 1 << p.s;
     for (int r = 0; r < ns; r++) {
@@ -991,6 +1033,7 @@ uint64_t layoutIndex(uint64_t local, const std::vector<int>& mem0) {
 }
 
 void setBasis(qk_state* st, Index global, const std::vector<int>* mem0 = nullptr) {
+    st->normValid = false;
     if (global >= (Index(1) << st->n)) throw SimulationError("initial basis state out of range");
     cuda(cudaMemsetAsync(st->amps, 0, st->count * sizeof(double2), st->stream), "memset");
     uint64_t local = global & (st->count - 1);
@@ -1046,6 +1089,7 @@ int qk_destroy(qk_state* st) {
         cudaFree(st->amps);
         cudaFree(st->normScratch);
         cudaFree(st->normOut);
+        cudaFree(st->normTiles);
         cudaFree(st->recvBuf);
         cudaFree(st->packBuf);
         cudaStreamDestroy(st->stream);
@@ -1062,6 +1106,7 @@ int qk_set_basis(qk_state* st, uint64_t global) {
 
 int qk_upload(qk_state* st, uint64_t off, uint64_t cnt, const double* host) {
     return guard([&] {
+        st->normValid = false;
         if (off + cnt > st->count) throw SimulationError("upload range outside the slice");
         DeviceGuard g(st->device);
         cuda(cudaMemcpyAsync(st->amps + off, host, cnt * sizeof(double2), cudaMemcpyHostToDevice, st->stream), "upload");
@@ -1081,7 +1126,8 @@ int qk_download(qk_state* st, uint64_t off, uint64_t cnt, double* host) {
 int qk_norm(qk_state* st, double* out) {
     return guard([&] {
         DeviceGuard g(st->device);
-        cuda(qkdev::launchNorm(st->amps, st->count, st->normScratch, st->normOut, st->stream), "norm");
+        if (!st->normValid)  // else the last pass already folded sum |a|^2 into normOut
+            cuda(qkdev::launchNorm(st->amps, st->count, st->normScratch, st->normOut, st->stream), "norm");
         cuda(cudaMemcpyAsync(out, st->normOut, sizeof(double), cudaMemcpyDeviceToHost, st->stream), "norm copy");
         cuda(cudaStreamSynchronize(st->stream), "norm sync");
     });

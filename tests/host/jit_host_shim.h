@@ -63,6 +63,8 @@ extern "C" double2 sm[1 << 14];
     extern "C" void qk_host_launch(double2* st, const double2* gt, int nLocal, int ct, int rb,    \
                                    unsigned long long basis) {                              \
         const unsigned ntiles = 1u << (nLocal - ct), nt = 1u << (ct - rb);                   \
+        std::vector<double> npv(ntiles); /* per-tile sums of |a|^2 (norm_out passes) */        \
+        double* const np = npv.data();                                                        \
         qk_grid = ntiles < 3u ? ntiles : 3u;                                                  \
         for (unsigned b = 0; b < qk_grid; b++) {                                              \
             std::barrier<> bar(nt);                                                           \
@@ -79,7 +81,7 @@ extern "C" double2 sm[1 << 14];
                 ts.emplace_back([=] {                                                         \
                     qk_tl_tid = t;                                                            \
                     qk_tl_bid = b;                                                            \
-                    KERNEL(st, gt, ntiles, basis, 0u);                                        \
+                    KERNEL(st, gt, ntiles, basis, 0u, np);                                    \
                 });                                                                           \
             for (auto& th : ts) th.join();                                                    \
         }                                                                                     \

@@ -172,3 +172,22 @@ def test_autotune_variants_agree(ref, qk):
         assert st.simulate(again, 3)["tuning_runs"] == 0
         assert np.max(np.abs(st.download() - want.view(np.complex128))) < TOL, kind
         st.close()
+
+
+def test_fused_norm_after_run(ref, qk):
+    # The last specialized pass folds sum |a|^2 per tile (norm_out); qk_norm
+    # returns it until the state changes, then sweeps the slice again.
+    n = 22
+    for kind, a, seed in (("qft", 0, 0), ("random", 120, 5)):
+        cfg_text = config_text(n, 0, 13, fusion=0, diag=0)
+        prog = qk.Program.parse(ref.optimize(ref.gen(kind, n, a, seed), cfg_text), qk.Config.parse(cfg_text))
+        st = qk.State(n)
+        st.simulate(prog, 7)
+        host = st.download()
+        want = float(np.sum(np.abs(host) ** 2))
+        assert abs(st.norm() - want) < 1e-12 and abs(want - 1.0) < 1e-12
+        half = host.copy()
+        half[: 1 << (n - 1)] = 0
+        st.upload(half)
+        assert abs(st.norm() - float(np.sum(np.abs(half) ** 2))) < 1e-12
+        st.close()
