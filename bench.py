@@ -296,8 +296,9 @@ def main():
                      "traffic_source": (tr["source"] + ", DRAM bytes/amp x this slice") if tr else None,
                      "algorithmic_bytes_per_launch": round(blk_bytes_per_launch),
                      "fp64_peak_tflops_measured": 36.5,
-                     "fp64_note": "DFMA 36.5 / DMMA 37.0 TF measured (profiles/r1_fp64_peak.txt); passes run "
-                                  "~75 FP64 instr/amp, FP64 pipe 24-41% active (profiles/r1_qft30_ncu_full.txt)",
+                     "fp64_note": "DFMA 36.5 / DMMA 37.0 TF measured (profiles/r1_fp64_peak.txt); QFT passes "
+                                  "run ~50-60 FP64 instr/amp, FP64 pipe 24-32% active at 8 warps/SM "
+                                  "(profiles/r1_qft31_ncu_full.txt)",
                      "avg_launch_ms": round(blk_launch_ms, 3)},
         "breakdown": {"block_ms": round(s0["block_ms"], 2), "ims_ms": round(s0["ims_ms"], 2),
                       "xrs_ms": round(s0["xrs_ms"], 2), "block_launches": s0["block_launches"],

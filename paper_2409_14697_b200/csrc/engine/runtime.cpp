@@ -208,7 +208,8 @@ struct CompiledItem {
 // schedule is kept.
 struct ChoiceTune {
     int runs = 0;
-    float msA = -1, msB = -1;  // group device time: A's first run, B's run
+    float msA = -1, msB = -1;  // group device time: A's first run, B's fastest run
+    int runsB = 0;             // B is timed twice (a first run can be slow)
     int choice = -1;
 };
 
@@ -1463,14 +1464,14 @@ int qk_circuit_generate(const char* kind, int n, int64_t a, uint64_t seed, char*
 }
 
 // Tile-size choice for one alternative range (ChoiceTune): A first, then B,
-// then A until its passes' register-width variants are all timed; then the
-// faster of B and A's best estimate (A's first run with every pass replaced
-// by its fastest variant).
+// then A until its passes' register-width variants are all timed, then B
+// once more; then the faster of B (its better run) and A's best estimate
+// (A's first run with every pass replaced by its fastest variant).
 int chooseTileVariant(const Compiled& c, const Alternative& alt) {
     ChoiceTune& t = *alt.tune;
     if (t.choice >= 0) return t.choice;
     if (t.msA < 0) return 0;
-    if (t.msB < 0) return 1;
+    if (t.runsB == 0) return 1;
     double est = t.msA;
     for (size_t k = alt.first; k < alt.last; k++)
         for (const qkeng::Step& s : c.items[k].steps) {
@@ -1483,7 +1484,11 @@ int chooseTileVariant(const Compiled& c, const Alternative& alt) {
             }
             est += double(best) - double(s.tune->ms[0]);
         }
+    if (t.runsB < 2) return 1;
     t.choice = t.msB < est ? 1 : 0;
+    if (std::getenv("QK_DEBUG_TUNE"))
+        std::fprintf(stderr, "tile tune [%zu,%zu): A first run %.2f ms, A best estimate %.2f ms, B (2^12) %.2f ms -> %s\n",
+                     alt.first, alt.last, double(t.msA), est, double(t.msB), t.choice ? "B" : "A");
     return t.choice;
 }
 
@@ -1551,7 +1556,12 @@ int qk_simulate(qk_state* st, const qk_program* cp, const qk_config* cfg, uint64
                     cudaEventElapsedTime(&ms, a0, a1);
                     cudaEventDestroy(a0);
                     cudaEventDestroy(a1);
-                    (v == 1 ? alt.tune->msB : alt.tune->msA) = ms;
+                    if (v == 1) {
+                        alt.tune->msB = alt.tune->runsB ? std::min(alt.tune->msB, ms) : ms;
+                        alt.tune->runsB++;
+                    } else {
+                        alt.tune->msA = ms;
+                    }
                 }
                 alt.tune->runs++;
                 i = alt.last;
