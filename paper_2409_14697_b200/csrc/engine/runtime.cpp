@@ -1257,6 +1257,8 @@ int qk_debug_compile_program(const qk_program* cp, int nLocal, char** json) {
             }
             o << "}";
         }
+        o << "],\"mem0\":[";
+        for (size_t q = 0; q < c->mem0.size(); q++) o << (q ? "," : "") << c->mem0[q];
         o << "]}";
         *json = dupText(o.str());
     });

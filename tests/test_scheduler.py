@@ -101,10 +101,13 @@ def test_pass_capacity_split(qk, port):
 
 
 def run_compiled(qk, port, prog, n, initial):
-    """Replay the engine's compiled item list (lazy IMS included) on the CPU."""
+    """Replay the engine's compiled item list (lazy IMS included) on the CPU.
+    The run starts in the compiled initial layout mem0 (program position p at
+    memory bit mem0[p]); identity unless compiled for a basis-state run."""
+    compiled = prog.debug_compile(n)
     st = np.zeros(1 << n, dtype=np.complex128)
-    st[initial] = 1
-    for it in prog.debug_compile(n)["items"]:
+    st[sum(((initial >> p) & 1) << m for p, m in enumerate(compiled["mem0"]))] = 1
+    for it in compiled["items"]:
         if it["kind"] == 0:
             run_steps(st, n, it["block"])
         elif it["kind"] == 1:
@@ -123,6 +126,29 @@ def test_compiled_programs_match_golden(qk, port, name):
         got = run_compiled(qk, port, prog, case["n"], initial)
         want = G[f"{name}/init{initial}/state"].view(np.complex128)
         assert np.max(np.abs(got - want)) < 1e-10
+
+
+@pytest.mark.parametrize("name", sorted(k for k in P if "program" in P[k] and P[k]["r"] == 0))
+def test_free_initial_layout_programs_match_golden(qk, port, name, monkeypatch):
+    # compiled as qk_simulate compiles them (run from a basis state): the
+    # slice starts in the layout that ends the first stream in physical order
+    monkeypatch.setenv("QK_DEBUG_FROM_BASIS", "1")
+    case = P[name]
+    prog = qk.Program.parse(case["program"], qk.Config.parse(case["config"]))
+    for initial in (0, 5):
+        got = run_compiled(qk, port, prog, case["n"], initial)
+        want = G[f"{name}/init{initial}/state"].view(np.complex128)
+        assert np.max(np.abs(got - want)) < 1e-10
+
+
+def test_free_initial_layout_needs_no_materialization(qk, monkeypatch):
+    monkeypatch.setenv("QK_DEBUG_FROM_BASIS", "1")
+    n = 16
+    cfg = qk.Config.make(n, 0, chunk=8, fusion=0, diag=0)
+    prog = qk.Program.optimize(qk.generate("qft", n), cfg)
+    compiled = prog.debug_compile()
+    assert prog.counts()["sqs"] > 2 and not [it for it in compiled["items"] if it["kind"] == 1]
+    assert sorted(compiled["mem0"]) == list(range(n)) and compiled["mem0"] != list(range(n))
 
 
 def test_lazy_ims_removes_swap_passes(qk):
