@@ -197,8 +197,7 @@ int lowRun(const PassParams& P) {
 // the same register slot (schedule.cpp guarantees one).  Needs 2^13 tiles, 32
 // amplitudes per thread and >= 128-B rows.
 bool pipelined(const PassParams& P) {
-    static const bool on = qkdev::halfExchanges();
-    if (!on || P.ct != 13 || P.rb != 5 || lowRun(P) < 3) return false;
+    if (!P.half_x || P.ct != 13 || P.rb != 5 || lowRun(P) < 3) return false;
     for (int c = 1; c < P.nsegs; c++) {
         const int k = P.xsplit[c];
         if (k >= P.rb || P.map_out[c - 1][k] != P.map_in[c][k] || P.map_out[c - 1][k] < 3) return false;
@@ -301,7 +300,7 @@ public:
            << "(double2* __restrict__ st, const double2* __restrict__ gt, const u32 ntiles, const u64 basis, const u32 tile0, double* __restrict__ np) {\n"
            << "  extern __shared__ double2 sm[];  // PB: next tile (linear tile coordinates) | XS | F | mbarrier\n"
            << "  double2* const XS = sm + 8192;\n  double2* const F = sm + 12288;\n"
-           << "  u64* const mbar = (u64*)(sm + 12352);\n  const u32 tid = threadIdx.x;\n"
+           << "  u64* const mbar = (u64*)(sm + " << (12288 + qkdev::kMaxCtaFactors) << ");\n  const u32 tid = threadIdx.x;\n"
            << "  const bool tma = basis == ~0ull;\n  u32 phase = 0u;\n"
            << "  if (tid == 0) mbar_init(mbar);\n  __syncthreads();\n"
            << "  if (tma && blockIdx.x < ntiles) {\n";
@@ -358,11 +357,11 @@ private:
     }
     // Warp 0 streams tile `t` into PB: one cp.async.bulk per contiguous row.
     void issueTile(const std::string& t, int Lrun) {
-        const int L = std::min(Lrun, 8);  // rows of <= 4 KB, spread over warp 0's lanes
+        const int L = std::min(Lrun, 8);  // rows of <= 4 KB, spread over all threads
         const int rows = 1 << (ct_ - L);
-        o_ << "    if (tid < 32u) {\n      " << deposit("nb", "(u64)(" + t + ")") << "\n"
+        o_ << "    {\n      " << deposit("nb", "(u64)(" + t + ")") << "\n"
            << "      fence_async();\n      if (tid == 0u) mbar_expect_tx(mbar, " << (16u << ct_) << "u);\n"
-           << "      __syncwarp();\n      for (u32 r = tid; r < " << rows << "u; r += 32u) {\n        u64 o = nb;\n";
+           << "      __syncthreads();\n      for (u32 r = tid; r < " << rows << "u; r += " << nt_ << "u) {\n        u64 o = nb;\n";
         for (int j = L; j < ct_; j++)
             o_ << "        o |= (u64)((r >> " << (j - L) << ") & 1u) << " << int(P_.tile_phys[j]) << ";\n";
         o_ << "        bulk_g2s(sm + (r << " << L << "), st + o, " << (16u << L) << "u, mbar);\n      }\n    }\n";
@@ -810,7 +809,7 @@ private:
 // ---- compile / load / launch -------------------------------------------------
 
 // Bump when the generated code changes for the same PassParams (on-disk cache key).
-constexpr uint64_t kGeneratorVersion = 18;
+constexpr uint64_t kGeneratorVersion = 20;
 
 uint64_t hashPass(const PassParams& P) {
     uint64_t h = 1469598103934665603ull ^ (kGeneratorVersion * 0x9E3779B97F4A7C15ull) ^ (usePrefetch() ? 1u : 0u) ^ (usePersistent() ? 2u : 0u) ^

@@ -116,6 +116,7 @@ struct PassParams {
     uint16_t cta_end[kMaxCtaFactors];
     CtaTerm cta_terms[kMaxCtaTerms];
     int32_t norm_out;  // specialized kernels: also write sum |a|^2 of each output tile to np[tile]
+    int32_t half_x;    // exchanges scheduled splittable in halves (xsplit): TMA-pipelined kernel eligible
 };
 
 static_assert(sizeof(PassParams) <= 32000, "kernel parameter limit");

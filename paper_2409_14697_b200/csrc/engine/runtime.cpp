@@ -533,10 +533,11 @@ std::shared_ptr<Compiled> compileLayout(qk_program* p, int nLocal, const std::ve
     auto markNorm = [&](std::vector<CompiledItem>& items, bool firstIsSynth) {
         if (items.empty() || items.back().kind != CompiledItem::Block || items.back().steps.empty()) return;
         qkeng::Step& s = items.back().steps.back();
-        if (s.kind != qkeng::Step::Pass || qkdev::halfExchanges()) return;
+        if (s.kind != qkeng::Step::Pass) return;
         if (firstIsSynth && items.size() == 1 && items[0].steps.size() == 1) return;
-        s.pass->norm_out = 1;
-        for (auto& a : s.alts) a->norm_out = 1;
+        if (!s.pass->half_x) s.pass->norm_out = 1;
+        for (auto& a : s.alts)
+            if (!a->half_x) a->norm_out = 1;  // the TMA-pipelined kernel has no norm epilogue
     };
     for (Alternative& alt : c->alts)
         if (alt.last == c->items.size()) markNorm(alt.b, synthFirst && alt.first == 0);

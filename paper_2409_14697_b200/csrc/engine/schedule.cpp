@@ -209,9 +209,9 @@ Amp ratio(Amp num, Amp den) {
 class PassBuilder {
 public:
     PassBuilder(const std::vector<Gate>& tg, const std::vector<Gate>& orig, const std::vector<int>& tilePhys,
-                std::vector<double>& gtab, int rb = -1)
+                std::vector<double>& gtab, int rb = -1, bool halfX = false)
         : tg_(tg), orig_(orig), gtab_(gtab), ct_(int(tilePhys.size())),
-          rb_(rb > 0 ? rb : regBitsFor(int(tilePhys.size()))) {
+          rb_(rb > 0 ? rb : regBitsFor(int(tilePhys.size()))), halfX_(halfX || halfExchanges()) {
         tilePhys_ = tilePhys;
     }
 
@@ -220,6 +220,7 @@ public:
         auto P = std::make_shared<PassParams>();
         std::memset(P.get(), 0, sizeof(PassParams));
         P_ = P.get();
+        P_->half_x = halfX_ ? 1 : 0;
         P_->ct = ct_;
         P_->rb = rb_;
         for (int j = 0; j < ct_; j++) {
@@ -264,8 +265,8 @@ public:
                 flushAll(true);
                 closeSegment();
                 seg_++;
-                chooseMap(i, halfExchanges() ? &P_->xsplit[seg_] : nullptr);
-                if (!halfExchanges()) P_->xsplit[seg_] = 255;
+                chooseMap(i, halfX_ ? &P_->xsplit[seg_] : nullptr);
+                if (!halfX_) P_->xsplit[seg_] = 255;
                 std::memcpy(P_->map_in[seg_], map_, sizeof map_);
                 emit(OP_EXCHANGE, 0, 0, 0, uint32_t(seg_));
                 relowerCarried();
@@ -1018,6 +1019,7 @@ private:
     std::vector<double>& gtab_;
     std::vector<int> tilePhys_;
     int ct_, rb_;
+    bool halfX_;
     PassParams* P_ = nullptr;
     int nops_ = 0, ncoef_ = 0, ncontrib_ = 0, seg_ = 0, hcount_ = 0;
     bool pendScalar_ = false;
@@ -1064,7 +1066,7 @@ Gate remapQubits(const Gate& g, const int* tileOf) {
 }
 
 void compileGroup(const std::vector<Gate>& gates, uint64_t used, int ct, int nLocal, std::vector<double>& gtab,
-                  std::vector<Step>& out, int rb = -1) {
+                  std::vector<Step>& out, int rb = -1, bool halfX = false) {
     // Tile bits: every bit the group touches, padded with the lowest others.
     uint64_t tile = used;
     for (int b = 0; b < nLocal && __builtin_popcountll(tile) < ct; b++) tile |= uint64_t(1) << b;
@@ -1078,7 +1080,7 @@ void compileGroup(const std::vector<Gate>& gates, uint64_t used, int ct, int nLo
         }
     std::vector<Gate> tg;
     for (const Gate& g : gates) tg.push_back(remapQubits(g, tileOf));
-    PassBuilder pb(tg, gates, phys, gtab, rb);
+    PassBuilder pb(tg, gates, phys, gtab, rb, halfX);
     size_t i = 0;
     while (i < gates.size()) {
         Step st;
@@ -1243,6 +1245,11 @@ std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::
                 for (int rbAlt : {4, 3}) {  // 16 and 8 amplitudes per thread (512 / 1024 threads)
                     std::vector<Step> alt;
                     compileGroup(group, used, ct, nLocal, gtab, alt, rbAlt);
+                    if (alt.size() == 1 && alt[0].kind == Step::Pass) steps[first].alts.push_back(alt[0].pass);
+                }
+                if (!halfExchanges()) {  // 32 per thread, half-splittable exchanges: the TMA-pipelined kernel
+                    std::vector<Step> alt;
+                    compileGroup(group, used, ct, nLocal, gtab, alt, 5, true);
                     if (alt.size() == 1 && alt[0].kind == Step::Pass) steps[first].alts.push_back(alt[0].pass);
                 }
                 if (!steps[first].alts.empty()) steps[first].tune = std::make_shared<Step::Tune>();

@@ -18,9 +18,9 @@ struct Step {
     // first execution and keeps the fastest (`tune`, shared by copies).
     std::vector<std::shared_ptr<qkdev::PassParams>> alts;
     struct Tune {
-        static constexpr int kMax = 3;
-        float ms[kMax] = {0, 0, 0};
-        int runs[kMax] = {0, 0, 0};
+        static constexpr int kMax = 4;  // rb 5 / 4 / 3, rb 5 with half-splittable exchanges (TMA-pipelined)
+        float ms[kMax] = {0, 0, 0, 0};
+        int runs[kMax] = {0, 0, 0, 0};
         int choice(int n) const {  // n = 1 + alts
             for (int v = 0; v < n; v++)
                 if (runs[v] == 0) return v;
