@@ -535,9 +535,8 @@ std::shared_ptr<Compiled> compileLayout(qk_program* p, int nLocal, const std::ve
         qkeng::Step& s = items.back().steps.back();
         if (s.kind != qkeng::Step::Pass) return;
         if (firstIsSynth && items.size() == 1 && items[0].steps.size() == 1) return;
-        if (!s.pass->half_x) s.pass->norm_out = 1;
-        for (auto& a : s.alts)
-            if (!a->half_x) a->norm_out = 1;  // the TMA-pipelined kernel has no norm epilogue
+        s.pass->norm_out = 1;
+        for (auto& a : s.alts) a->norm_out = 1;
     };
     for (Alternative& alt : c->alts)
         if (alt.last == c->items.size()) markNorm(alt.b, synthFirst && alt.first == 0);
