@@ -287,7 +287,7 @@ def main():
                    "l2": f"state {16 * amps / 2**30:.0f} GiB/GPU >> 126 MB L2: inputs larger than L2, no flush"},
         "e2e": {"value": round(e2e_s, 6), "unit": "s", "h2d_bytes_per_step": len(prog_text.encode()),
                 "d2h_bytes_per_step": window * 16 + 8,
-                "path": "qk_program_parse + qk_simulate + qk_norm + qk_download(2^20 amps) via C-ABI"},
+                "path": "qk_program_parse + qk_simulate + qk_norm + qk_download(2^20 amps) via C-ABI; the re-parsed program hits the process-wide schedule cache (compiled + autotuned schedule reused)"},
         "gpu_launches": int(sum(x["kernel_launches"] for x in stats)),
         "roofline": {"bound": "hbm", "kernel": "qk_pass_<hash> (NVRTC-specialized fused pass, csrc/engine/jit.cpp)",
                      "achieved": round(blk_gbs, 1),
