@@ -204,7 +204,7 @@ bool pipelined(const PassParams& P) {
     }
     return true;
 }
-constexpr int kPipeSmemAmps = (1 << 13) + (1 << 12) + qkdev::kMaxCtaFactors + 1 + 4;  // PB | XS | F | mbarrier | norm scratch
+constexpr int kPipeSmemAmps = (1 << 13) + (1 << 12) + qkdev::kMaxCtaFactors + 1;  // PB | XS | F | mbarrier
 
 class Gen {
 public:
@@ -262,7 +262,7 @@ public:
         // threads may still be loading the addresses this thread stores to.
         if (P_.nsegs == 1 && (std::memcmp(P_.map_in[0], P_.map_out[0], sizeof P_.map_in[0]) != 0 || P_.xmask_out[0]))
             o_ << "  __syncthreads();\n";
-        if (P_.norm_out) emitNorm("F + " + std::to_string(qkdev::kMaxCtaFactors));
+        if (P_.norm_out) emitNorm();
         o_ << "  { const u64 off = (base | " << threadGlobal(P_.map_out[last]) << ") ^ " << gx << "ull;\n";
         const int ks = slotOfMem0(P_.map_out[last]);
         for (int s = 0; s < na_; s++) {
@@ -319,7 +319,7 @@ public:
         uint64_t gx = 0;
         for (int j = 0; j < ct_; j++)
             if ((P_.xmask_out[last] >> j) & 1) gx |= uint64_t(1) << P_.tile_phys[j];
-        if (P_.norm_out) emitNorm("sm + " + std::to_string(kPipeSmemAmps - 4));  // after the mbarrier
+        if (P_.norm_out) emitNorm();
         o_ << "  { const u64 off = (base | " << threadGlobal(P_.map_out[last]) << ") ^ " << gx << "ull;\n";
         for (int s = 0; s < na_; s++)
             o_ << "  __stcs(st + (off ^ " << regGlobal(P_.map_out[last], s) << "ull), a" << nm_[size_t(s)] << ");\n";
@@ -330,17 +330,16 @@ public:
     }
 
 private:
-    // Sum |a|^2 of the output tile into np[tile] (fixed order: slots, xor
-    // butterfly, warps); `red` = shared scratch for one double per warp.
-    void emitNorm(const std::string& red) {
+    // Sum |a|^2 of each warp's part of the output tile into
+    // np[tile * warps + warp] (fixed order: slots, xor butterfly); no CTA
+    // barrier.  The runtime folds the array (launchSumTiles).
+    void emitNorm() {
+        const int warps = nt_ / 32 > 0 ? nt_ / 32 : 1;
         o_ << "  { double s_ = 0.0;\n";
         for (int s = 0; s < na_; s++)
             o_ << "    s_ = fma(" << A(s) << ".x, " << A(s) << ".x, fma(" << A(s) << ".y, " << A(s) << ".y, s_));\n";
         o_ << "    for (int o_ = 16; o_ > 0; o_ >>= 1) s_ += __shfl_xor_sync(0xffffffffu, s_, o_);\n"
-           << "    double* const red = reinterpret_cast<double*>(" << red << ");\n"
-           << "    if ((tid & 31u) == 0u) red[tid >> 5] = s_;\n    __syncthreads();\n"
-           << "    if (tid == 0u) { double t_ = 0.0; for (u32 w = 0; w < " << (nt_ / 32 > 0 ? nt_ / 32 : 1)
-           << "u; w++) t_ += red[w]; np[tile] = t_; }\n  }\n";
+           << "    if ((tid & 31u) == 0u) np[(u64)tile * " << warps << "u + (tid >> 5)] = s_;\n  }\n";
     }
 
     // First pass of a run (|basis> synthesized): a tile that does not hold the
@@ -814,7 +813,7 @@ private:
 // ---- compile / load / launch -------------------------------------------------
 
 // Bump when the generated code changes for the same PassParams (on-disk cache key).
-constexpr uint64_t kGeneratorVersion = 21;
+constexpr uint64_t kGeneratorVersion = 22;
 
 uint64_t hashPass(const PassParams& P) {
     uint64_t h = 1469598103934665603ull ^ (kGeneratorVersion * 0x9E3779B97F4A7C15ull) ^ (usePrefetch() ? 1u : 0u) ^ (usePersistent() ? 2u : 0u) ^

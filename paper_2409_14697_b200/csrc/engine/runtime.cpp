@@ -267,8 +267,8 @@ struct qk_state {
     ncclComm_t comm = nullptr;
     bool profiling = false;
     qk_run_stats last{};
-    // Fused norm: the program's last pass wrote per-tile sums of |a|^2 and
-    // normOut holds their fold; valid until the state changes again.
+    // Fused norm: the program's last pass wrote per-warp partial sums of
+    // |a|^2 and normOut holds their fold; valid until the state changes again.
     double* normTiles = nullptr;
     uint64_t normTilesCap = 0;
     bool normValid = false;
@@ -699,8 +699,10 @@ void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_ru
                 cuda(cudaEventRecord(e0, st->stream), "event");
             }
             const bool fusedNorm = P.norm_out && useJit(st->nLocal) && basis == kNoBasis;
+            // one partial sum per warp of every tile (2^(ct-rb-5) warps per tile)
+            const uint64_t normParts = st->count >> std::min(P.ct, P.rb + 5);
             if (P.norm_out && useJit(st->nLocal)) {
-                const uint64_t tiles = st->count >> P.ct;
+                const uint64_t tiles = normParts;
                 if (st->normTilesCap < tiles) {
                     cudaFree(st->normTiles);
                     st->normTiles = nullptr;
@@ -728,7 +730,7 @@ void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_ru
                 s.tune->runs[v]++;
             }
             if (fusedNorm) {
-                cuda(qkdev::launchSumTiles(st->normTiles, st->count >> P.ct, st->normScratch, st->normOut, st->stream),
+                cuda(qkdev::launchSumTiles(st->normTiles, normParts, st->normScratch, st->normOut, st->stream),
                      "norm fold");
                 st->normValid = true;
             }

@@ -63,7 +63,7 @@ extern "C" double2 sm[1 << 14];
     extern "C" void qk_host_launch(double2* st, const double2* gt, int nLocal, int ct, int rb,    \
                                    unsigned long long basis) {                              \
         const unsigned ntiles = 1u << (nLocal - ct), nt = 1u << (ct - rb);                   \
-        std::vector<double> npv(ntiles); /* per-tile sums of |a|^2 (norm_out passes) */        \
+        std::vector<double> npv(size_t(ntiles) * (nt >= 32u ? nt / 32u : 1u)); /* norm partials */ \
         double* const np = npv.data();                                                        \
         qk_grid = ntiles < 3u ? ntiles : 3u;                                                  \
         for (unsigned b = 0; b < qk_grid; b++) {                                              \
