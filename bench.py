@@ -39,7 +39,10 @@ def parse_args():
     ap.add_argument("--circuit", default="qft", help="qft | bvones | qaoa | random | grover")
     ap.add_argument("--per-gpu-qubits", type=int, default=PER_GPU_QUBITS)
     ap.add_argument("--chunk", type=int, default=13)
-    ap.add_argument("--cpu-sample-qubits", type=int, default=25)
+    ap.add_argument("--cpu-sample-qubits", type=int, default=28,
+                    help="measured reference run for cpu_baseline (same-size GPU/CPU pair)")
+    ap.add_argument("--ref-sample-qubits", type=int, default=26,
+                    help="--impl reference: per-step reference sample size")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -118,51 +121,89 @@ def ncu_traffic():
 
 # ------------------------------------------------------------------ CPU baseline
 
-def cpu_reference_sample(kind, n_target, chunk, n_sample, threads):
-    """Reference simulateProgram (oracle/_ref, the unmodified reference build) on
-    the same circuit family at n_sample qubits with the same config family,
-    scaled to n_target by amplitude-passes: the reference's cost per item is
-    linear in the slice size (every block / IMS item sweeps every amplitude)."""
+def ref_circuit(ref, kind, n):
+    """Circuit text for the reference path.  The reference's own generators
+    (tools.cpp:169-272) for its kinds; Grover (which the reference lacks, its
+    tools.hpp:38-48) is written by a separate process so that the process
+    timing the reference never loads this repo's library."""
+    a, seed = circuit_args(kind, n)
+    if kind != "grover":
+        return ref.gen(kind, n, a, seed)
+    code = ("import sys; sys.path.insert(0, %r); import paper_2409_14697_b200 as qk; "
+            "sys.stdout.write(qk.generate('grover', %d, %d, %d))" % (ROOT, n, a, seed))
+    return subprocess.run([sys.executable, "-c", code], check=True, capture_output=True, text=True).stdout
+
+
+def program_items(text):
+    """Items (blocks + SQS + CSQS) of a program text (circuit.cpp:394-460)."""
+    lines = [ln for ln in text.splitlines() if ln.strip()]
+    items = i = 0
+    while i < len(lines):
+        k = int(lines[i].split()[0])
+        items += 1
+        i += 1 + k
+    return items
+
+
+def cpu_reference_run(kind, n, chunk, threads, initial=0):
+    """The reference's simulateProgram (oracle/_ref: /root/reference/proj/src
+    compiled unmodified) on an n-qubit program with `threads` host threads.
+    Timed region = initState .. last item (proj/tools/main.cpp:126-145); the
+    shim's copy-out of the state is outside it.  Returns (seconds, items)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     from oracle import Ref, config_text
-    import paper_2409_14697_b200 as qk
     ref = Ref()
-    a, seed = circuit_args(kind, n_sample)
-    cfg_s = config_text(n_sample, 0, min(chunk, n_sample), fusion=0, diag=0)
-    # circuit text from this repo's generators: byte-identical to the
-    # reference's for its kinds (tests/test_host_formats.py), plus grover
-    prog_s = ref.optimize(qk.generate(kind, n_sample, a, seed), cfg_s)
-    t0 = time.perf_counter()
-    _, _, _, sec = ref.simulate(prog_s, cfg_s, n_sample, 0, 0, threads)
-    wall = time.perf_counter() - t0
-    # amplitude-passes of the sample and of the target program
-    def passes(text):
-        blocks = swaps = 0
-        lines = text.splitlines()
-        i = 0
-        while i < len(lines):
-            k = int(lines[i])
-            if lines[i + 1].startswith(("SQS", "CSQS")):
-                swaps += 1
-            else:
-                blocks += 1
-            i += 1 + k
-        return blocks + swaps
-    a2, seed2 = circuit_args(kind, n_target)
-    cfg_t = qk.Config.make(n_target, 0, chunk=chunk, fusion=0, diag=0)
-    prog_t = qk.Program.optimize(qk.generate(kind, n_target, a2, seed2), cfg_t).text()
-    scale = (2.0 ** n_target * passes(prog_t)) / (2.0 ** n_sample * passes(prog_s))
-    return sec * scale, sec, wall, scale, passes(prog_s), passes(prog_t)
+    cfg = config_text(n, 0, min(chunk, n), fusion=0, diag=0)
+    prog = ref.optimize(ref_circuit(ref, kind, n), cfg)
+    _, _, _, sec = ref.simulate(prog, cfg, n, 0, initial, threads)
+    return sec, program_items(prog), prog
+
+
+def extrapolate(kind, n_sample, sec, items_sample, n_target, chunk, R=0):
+    """Scale a measured reference run to the target size by amplitude-passes:
+    every reference item (applyBlock / imsSwap, engine.cpp:262-297) sweeps the
+    whole state once, so its time is linear in 2^n x items."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import Ref, config_text
+    ref = Ref()
+    cfg = config_text(n_target, 0, chunk, fusion=0, diag=0)
+    items_t = program_items(ref.optimize(ref_circuit(ref, kind, n_target), cfg))
+    scale = (2.0 ** n_target * items_t) / (2.0 ** n_sample * items_sample)
+    return sec * scale, scale, items_t
 
 
 # ------------------------------------------------------------------ main
+
+def spawn_ranks_self(args):
+    """`python bench.py --gpus N` without torchrun: launch N ranks (one process
+    per GPU) through torch.distributed.run on 127.0.0.1 and pass on the exit code."""
+    import socket
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(json.dumps({"metric": METRIC, "error": f"--gpus {args.gpus} needs {args.gpus} visible GPUs, "
+                                                     f"found {have} (one process per GPU, 2^{args.per_gpu_qubits} "
+                                                     "amplitudes each)"}), flush=True)
+        return 2
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
 
 def main():
     args = parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus and world > 1:
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        if args.impl == "reference":
+            world = 1  # the reference arm runs on rank 0's host cores only
+        else:
+            sys.exit(spawn_ranks_self(args))
+    if world > 1:
         args.gpus = world
     R = int(round(math.log2(max(1, args.gpus))))
     n = args.per_gpu_qubits + R
@@ -171,6 +212,7 @@ def main():
     if args.impl == "reference":
         return run_reference(args, rank, n, R, kind)
 
+    import numpy as np
     import torch
     import torch.distributed as dist
     import paper_2409_14697_b200 as qk
@@ -189,7 +231,13 @@ def main():
     prog_text = prog.text()
 
     st = qk.State(n, R, rank, cfg.buffer_qubits, local_rank)
-    if world > 1:
+    transport = os.environ.get("QK_XRS", "nccl")
+    if world > 1 and transport == "ipc":
+        # peer-memory rank group: in-place swap kernels over NVLink, no buffer
+        job = [f"bench{os.getpid()}_{time.time_ns()}" if rank == 0 else None]
+        dist.broadcast_object_list(job, 0)
+        st.ipc_init(job[0], world, rank)
+    elif world > 1:
         uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
         if rank == 0:
             uid.copy_(torch.frombuffer(bytearray(qk.comm_unique_id()), dtype=torch.uint8))
@@ -203,11 +251,18 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    # Cold first call of a new program: NVRTC specialization of every pass,
+    # table upload and the first autotune run (wall clock, synchronous).
+    barrier()
+    t1 = time.perf_counter()
+    tuning = st.simulate(prog, 0)["tuning_runs"]
+    cold_s = time.perf_counter() - t1
     # Schedule autotune (register widths per pass, tile size per gate stream)
     # settles over the first few runs of a program; finish it before the
     # warm-up so the timed steps run the tuned schedule.
-    tune_runs = 0
-    while tune_runs < 8 and st.simulate(prog, 0)["tuning_runs"]:
+    tune_runs = 1
+    while tune_runs < 8 and tuning:
+        tuning = st.simulate(prog, 0)["tuning_runs"]
         tune_runs += 1
     for _ in range(args.warmup):
         st.simulate(prog, 0)
@@ -234,7 +289,6 @@ def main():
 
     # End to end through the C-ABI with host buffers: program text -> parse ->
     # device tables (H2D) -> simulate -> norm + 2^20-amplitude window (D2H).
-    import numpy as np
     window = 1 << 20
     host = torch.empty(window * 2, dtype=torch.float64).pin_memory().numpy().view(np.complex128)
     e2e = []
@@ -249,24 +303,28 @@ def main():
         e2e.append(time.perf_counter() - t1)
         del p2
     e2e_s = sorted(e2e)[len(e2e) // 2]
-    et = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+    et = torch.tensor([e2e_s, cold_s], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(et, op=dist.ReduceOp.MAX)
-    e2e_s = float(et.item())
+    e2e_s, cold_s = float(et[0].item()), float(et[1].item())
 
-    # Roofline of the dominant kernel (the fused block pass): algorithmic
-    # 32 B/amplitude per launch over its event-timed average.
-    s0 = stats[-1]
+    # Roofline of the dominant kernel, the fused block pass over the whole
+    # slice: algorithmic 32 B/amplitude per launch over its
+    # event-timed average launch.  The first pass of a run (memset + the one
+    # tile holding |initial>) is reported apart as init.
     amps = 1 << (n - R)
     peak, peak_src = measured_peaks()
-    blk_launch_ms = s0["block_ms"] / max(1, s0["block_launches"])
-    blk_bytes_per_launch = s0["block_bytes"] / max(1, s0["block_launches"])  # 32 B/amp; 16 for the pass that
-    blk_gbs = blk_bytes_per_launch / (blk_launch_ms * 1e-3) / 1e9            # synthesizes |initial> (write only)
-    ims_launch_ms = s0["ims_ms"] / max(1, s0["ims_launches"]) if s0["ims_launches"] else 0.0
+    fp_launches = sum(x["full_pass_launches"] for x in stats)
+    fp_ms = sum(x["full_pass_ms"] for x in stats)
+    fp_bytes = sum(x["full_pass_bytes"] for x in stats)
+    pass_launch_ms = fp_ms / max(1, fp_launches)
+    pass_bytes_per_launch = fp_bytes / max(1, fp_launches)
+    pass_gbs = pass_bytes_per_launch / (pass_launch_ms * 1e-3) / 1e9 if fp_launches else 0.0
+    s0 = stats[-1]
     tr = ncu_traffic()
-    traffic = round(tr["dram_bytes_per_amp"] / 32.0 * blk_bytes_per_launch) if tr else None
+    traffic = round(tr["dram_bytes_per_amp"] * amps) if tr else None
     # program-level roofline: T_roof = sum over items, HBM-bound
-    t_roof = (s0["block_bytes"] + s0["ims_bytes"]) / (peak * 1e9) + s0["xrs_bytes"] / 770e9
+    t_roof = (s0["block_bytes"] + s0["ims_bytes"]) / (peak * 1e9) + s0["xrs_bytes"] / 900e9
 
     out = {
         "metric": METRIC,
@@ -283,29 +341,41 @@ def main():
         "data": "synthetic: generated circuit, |0> initial state",
         "config": {"workload": f"{kind.upper()}-{n} ({kind}, {n} qubits, {1 << R} GPU(s), 2^{n - R} amps/GPU)",
                    "n_qubits": n, "rank_qubits": R, "chunk_qubits": args.chunk, "fusion": 0,
+                   "xrs": (transport + (" (grouped ncclSend/ncclRecv, 2^B receive buffer, copy-back)"
+                                        if transport == "nccl" else " (cudaIpc-mapped peer slices, in-place swap)"))
+                   if world > 1 else None,
                    "diagonal_fusion": 0, "program": counts, "optimize_s": round(opt_s, 3),
                    "l2": f"state {16 * amps / 2**30:.0f} GiB/GPU >> 126 MB L2: inputs larger than L2, no flush"},
         "e2e": {"value": round(e2e_s, 6), "unit": "s", "h2d_bytes_per_step": len(prog_text.encode()),
                 "d2h_bytes_per_step": window * 16 + 8,
-                "path": "qk_program_parse + qk_simulate + qk_norm + qk_download(2^20 amps) via C-ABI; the re-parsed program hits the process-wide schedule cache (compiled + autotuned schedule reused)"},
+                "path": "qk_program_parse + qk_simulate + qk_norm + qk_download(2^20 amps) via C-ABI; the "
+                        "re-parsed program hits the process-wide schedule cache (compiled + autotuned schedule "
+                        "reused)",
+                "cold_first_call_s": round(cold_s, 3),
+                "cold_note": "first qk_simulate of the program in this process: NVRTC specialization of every "
+                             "pass variant (disk cache empty on a fresh box), table upload, first autotune run"},
         "gpu_launches": int(sum(x["kernel_launches"] for x in stats)),
-        "roofline": {"bound": "hbm", "kernel": "qk_pass_<hash> (NVRTC-specialized fused pass, csrc/engine/jit.cpp)",
-                     "achieved": round(blk_gbs, 1),
-                     "peak": peak, "unit": "GB/s", "frac": round(blk_gbs / peak, 4),
+        "roofline": {"bound": "hbm", "kernel": "qk_pass_<hash> (NVRTC-specialized fused pass over the whole "
+                                               "slice, csrc/engine/jit.cpp)",
+                     "achieved": round(pass_gbs, 1),
+                     "peak": peak, "unit": "GB/s", "frac": round(pass_gbs / peak, 4),
                      "peak_source": peak_src, "traffic": traffic,
                      "traffic_source": (tr["source"] + ", DRAM bytes/amp x this slice") if tr else None,
-                     "algorithmic_bytes_per_launch": round(blk_bytes_per_launch),
+                     "algorithmic_bytes_per_launch": round(pass_bytes_per_launch),
+                     "launches_per_step": fp_launches // max(1, args.steps),
+                     "avg_launch_ms": round(pass_launch_ms, 3),
+                     "excludes": "the run's first pass (memset of the slice + the single tile holding |initial>), "
+                                 "reported as breakdown.init_ms",
                      "fp64_peak_tflops_measured": 36.5,
-                     "fp64_note": "DFMA 36.5 / DMMA 37.0 TF measured (profiles/r1_fp64_peak.txt); QFT passes "
-                                  "run ~50-60 FP64 instr/amp, FP64 pipe 24-32% active at 8 warps/SM "
-                                  "(profiles/r1_qft31_ncu_full.txt)",
-                     "avg_launch_ms": round(blk_launch_ms, 3)},
-        "breakdown": {"block_ms": round(s0["block_ms"], 2), "ims_ms": round(s0["ims_ms"], 2),
+                     "fp64_note": "DFMA 36.5 / DMMA 37.0 TF measured (profiles/r1_fp64_peak.txt)"},
+        "breakdown": {"block_ms": round(s0["block_ms"], 2), "full_pass_ms": round(s0["full_pass_ms"], 2),
+                      "init_ms": round(s0["init_ms"], 2), "ims_ms": round(s0["ims_ms"], 2),
                       "xrs_ms": round(s0["xrs_ms"], 2), "block_launches": s0["block_launches"],
                       "ims_launches": s0["ims_launches"], "xrs_rounds": s0["xrs_rounds"],
-                      "ims_avg_launch_ms": round(ims_launch_ms, 3),
                       "ims_gbs": round(s0["ims_bytes"] / max(1e-9, s0["ims_ms"] * 1e-3) / 1e9, 1)
                       if s0["ims_ms"] else None,
+                      "xrs_nvlink_gbs_per_direction": round(s0["xrs_bytes"] / max(1e-9, s0["xrs_ms"] * 1e-3) / 1e9, 1)
+                      if s0["xrs_ms"] else None,
                       "program_roofline_s": round(t_roof, 4),
                       "program_roofline_frac": round(t_roof / (ms_per_step / 1e3), 4),
                       "autotune_runs": tune_runs,
@@ -314,13 +384,7 @@ def main():
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            threads = os.cpu_count() or 1
-            v, sec, wall, scale, ps, pt = cpu_reference_sample(kind, n, args.chunk, args.cpu_sample_qubits, threads)
-            out["cpu_baseline"] = {"value": round(v, 3), "unit": "s", "cores": threads, "kind": "reference",
-                                   "sample": f"reference simulateProgram (oracle/_ref) on {kind.upper()}-"
-                                             f"{args.cpu_sample_qubits} (C={min(args.chunk, args.cpu_sample_qubits)}, "
-                                             f"unfused, {ps} items) = {sec:.3f} s, scaled x{scale:.1f} by "
-                                             f"amplitude-passes to the {n}-qubit program ({pt} items)"}
+            out["cpu_baseline"] = cpu_baseline(args, kind, n, st, qk)
         except Exception as e:  # noqa: BLE001
             out["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
     if rank == 0:
@@ -330,17 +394,65 @@ def main():
         dist.destroy_process_group()
 
 
+def gpu_time_program(qk, kind, n, chunk, reps=5):
+    """Device-timed steps (CUDA events inside qk_simulate) of this engine on the
+    same program, after its autotune settled; median of `reps`."""
+    cfg = qk.Config.make(n, 0, chunk=chunk, fusion=0, diag=0)
+    a, seed = circuit_args(kind, n)
+    prog = qk.Program.optimize(qk.generate(kind, n, a, seed), cfg)
+    st = qk.State(n)
+    try:
+        for _ in range(8):
+            if not st.simulate(prog, 0)["tuning_runs"]:
+                break
+        ts = sorted(st.simulate(prog, 0)["total_ms"] for _ in range(reps))
+        return ts[len(ts) // 2] / 1e3
+    finally:
+        st.close()
+
+
+def cpu_baseline(args, kind, n, st, qk):
+    """The reference's simulateProgram on this box's host cores: one measured
+    run at --cpu-sample-qubits (the same program family: chunk_qbit, fusion
+    off), extrapolated to the n-qubit workload by amplitude-passes, plus the
+    same-size GPU/CPU pair measured in this run."""
+    threads = os.cpu_count() or 1
+    ns = min(args.cpu_sample_qubits, n)
+    sec, items_s, _ = cpu_reference_run(kind, ns, args.chunk, threads)
+    v, scale, items_t = extrapolate(kind, ns, sec, items_s, n, args.chunk)
+    gpu_s = gpu_time_program(qk, kind, ns, min(args.chunk, ns))
+    return {"value": round(v, 3), "unit": "s", "cores": threads, "kind": "reference",
+            "extrapolated": ns != n,
+            "sample": f"reference simulateProgram (oracle/_ref, unmodified reference sources) on {kind.upper()}-{ns} "
+                      f"(chunk_qbit {min(args.chunk, ns)}, fusion off, {items_s} items), {threads} threads: "
+                      f"{sec:.3f} s measured, x{scale:.1f} by amplitude-passes to the {n}-qubit program "
+                      f"({items_t} items); a {n}-qubit host state needs {16 * 2**n / 2**30:.0f} GiB",
+            "measured_pair": {"workload": f"{kind.upper()}-{ns}, same program, this box",
+                              "cpu_s": round(sec, 3), "gpu_s": round(gpu_s, 5),
+                              "cpu_over_gpu": round(sec / gpu_s, 1) if gpu_s else None}}
+
+
 def run_reference(args, rank, n, R, kind):
     """--impl reference: the reference's own CPU implementation (oracle/_ref =
-    /root/reference/proj/src compiled unmodified) on the host cores, rank 0 only."""
+    /root/reference/proj/src compiled unmodified) on the host cores, rank 0
+    only.  This process never loads libqk_b200.so.  Each step is a bounded
+    sample: simulateProgram at --ref-sample-qubits, extrapolated to n qubits
+    by amplitude-passes (the whole --steps/--warmup run stays within minutes)."""
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    vals = []
+    ns = min(args.ref_sample_qubits, n)
+    vals, secs = [], []
+    items_s = None
     for i in range(args.warmup + args.steps):
-        v, sec, wall, scale, ps, pt = cpu_reference_sample(kind, n, args.chunk, args.cpu_sample_qubits, threads)
-        if i >= args.warmup:
-            vals.append(v)
+        warm = i < args.warmup
+        sec, items, _ = cpu_reference_run(kind, min(20, ns) if warm else ns, args.chunk, threads)
+        if not warm:
+            secs.append(sec)
+            items_s = items
+    sec = sorted(secs)[len(secs) // 2]
+    v, scale, items_t = extrapolate(kind, ns, sec, items_s, n, args.chunk)
+    vals = [x * scale for x in secs]
     v = sum(vals) / len(vals)
     out = {
         "impl": "reference",
@@ -351,8 +463,10 @@ def run_reference(args, rank, n, R, kind):
         "config": {"workload": f"{kind.upper()}-{n} ({kind}, {n} qubits, {1 << R} GPU(s) equivalent)",
                    "n_qubits": n, "chunk_qubits": args.chunk, "fusion": 0, "diagonal_fusion": 0},
         "cpu_baseline": {"value": round(v, 3), "unit": "s", "cores": threads, "kind": "reference",
-                         "sample": f"reference simulateProgram on {kind.upper()}-{args.cpu_sample_qubits} "
-                                   f"({ps} items) x{scale:.1f} amplitude-pass scale to {n} qubits ({pt} items)"},
+                         "extrapolated": ns != n,
+                         "sample": f"each step: reference simulateProgram on {kind.upper()}-{ns} ({items_s} items, "
+                                   f"median {sec:.3f} s measured) x{scale:.1f} amplitude-pass scale to {n} qubits "
+                                   f"({items_t} items); warm-up steps run {kind.upper()}-{min(20, ns)}"},
         "e2e": {"value": round(v, 3), "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)

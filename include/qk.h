@@ -72,6 +72,14 @@ typedef struct qk_run_stats {
     uint64_t block_launches, ims_launches, xrs_rounds, kernel_launches;
     double block_bytes, block_flops, ims_bytes, xrs_bytes;
     uint64_t tuning_runs; /* schedule variants timed during this call (autotune still settling) */
+    /* Fused passes over the whole slice only (not the first pass of a run,
+     * which is a memset + one tile holding |initial>): their event-timed sum,
+     * launches and algorithmic bytes (32 B/amp each).  init_ms = that first
+     * pass (memset + one tile), or initState's memset when there is none. */
+    double full_pass_ms;
+    uint64_t full_pass_launches;
+    double full_pass_bytes;
+    double init_ms;
 } qk_run_stats;
 
 typedef struct qk_state qk_state;      /* one rank slice in HBM + its stream */
@@ -121,6 +129,10 @@ int qk_apply_gate(qk_state* st, const qk_gate* gate);
 /* engine.cpp:86-101 imsSwap: a[bitswap(i)] <- a[i], in place.  cache_line_qubits
  * is accepted for signature parity; the device kernel picks its own tiling. */
 int qk_ims_swap(qk_state* st, const int* outs, const int* ins, int s, int cache_line_qubits);
+/* IMS kernel selection (test / A-B hook; default from QK_IMS_TILED, else 1):
+ * 0 = per-element k_ims, 1 = tiled k_ims_tiled whenever a tile exists,
+ * 2 = tiled only for pairs that move memory bit 0 or 1. */
+int qk_set_ims_mode(int mode);
 /* distributed.cpp:124-138 xrsSwap over slices owned by THIS process (one
  * device, or several with peer access): in-place pairwise slab swap, no
  * exchange buffer.  slices[k] must be rank k.  stats: one entry per slice, in
@@ -146,7 +158,21 @@ int qk_xrs_slab_index(int n_qubits, int rank_qubits, const int* outs, int s, int
                       uint64_t offset, uint64_t* index);
 int qk_comm_unique_id(unsigned char id[128]);
 int qk_comm_init(qk_state* st, const unsigned char id[128], int nranks, int rank);
+/* Multi-process XRS over CUDA peer memory instead of NCCL: one process per
+ * GPU on one node (NVLink / NVSwitch P2P), or several processes sharing a
+ * GPU.  Collective over the 2^R ranks that call it with the same `job` name
+ * (node-local POSIX shared memory carries the cudaIpc handles and a host
+ * barrier; pick a name unique to the run).  Afterwards every CSQS of
+ * qk_simulate / qk_xrs_swap on this state is one in-place slab-swap kernel
+ * over the mapped peer slices, bracketed by two barriers: no exchange buffer
+ * and no copy-back (same permutation and RankStats as distributed.cpp:76-138).
+ * Waits at most QK_IPC_TIMEOUT seconds (default 600) for the other ranks. */
+int qk_ipc_init(qk_state* st, const char* job, int nranks, int rank);
 int qk_xrs_swap(qk_state* st, const int* outs, const int* ins, int s, qk_xrs_stats* stats);
+/* Host-only test hook for qk_ipc_init's rendezvous: joins the shared-memory
+ * barrier of `job` as `rank` of `nranks` and passes it `rounds` times.
+ * Fails with QK_ERR_SIM after timeout_s seconds without the others. */
+int qk_debug_host_barrier(const char* job, int nranks, int rank, int rounds, double timeout_s);
 /* Test hook: every rank's qk_xrs_swap schedule (plan, pack, single receive
  * buffer, copy-back kernels) for slices owned by this process, with the NCCL
  * transfers replaced by device copies matched peer-to-peer per round. */

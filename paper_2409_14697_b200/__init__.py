@@ -80,7 +80,9 @@ class _RunStats(C.Structure):
                 ("ims_launches", C.c_uint64), ("xrs_rounds", C.c_uint64),
                 ("kernel_launches", C.c_uint64), ("block_bytes", C.c_double),
                 ("block_flops", C.c_double), ("ims_bytes", C.c_double), ("xrs_bytes", C.c_double),
-                ("tuning_runs", C.c_uint64)]
+                ("tuning_runs", C.c_uint64), ("full_pass_ms", C.c_double),
+                ("full_pass_launches", C.c_uint64), ("full_pass_bytes", C.c_double),
+                ("init_ms", C.c_double)]
 
 
 def build(quiet: bool = True) -> None:
@@ -122,6 +124,7 @@ def lib():
         "qk_debug_jit_program": ([P, I, C.POINTER(P)], I),
         "qk_set_jit_min_qubits": ([I], I),
         "qk_ims_swap": ([P, C.POINTER(I), C.POINTER(I), I, I], I),
+        "qk_set_ims_mode": ([I], I),
         "qk_xrs_swap_local": ([C.POINTER(P), I, C.POINTER(I), C.POINTER(I), I, C.POINTER(_XrsStats)], I),
         "qk_xrs_plan": ([I, I, I, I, C.POINTER(I), C.POINTER(I), I, C.POINTER(_XrsMsg), I,
                          C.POINTER(I)], I),
@@ -129,6 +132,8 @@ def lib():
         "qk_comm_unique_id": ([C.c_char_p], I),
         "qk_comm_init": ([P, C.c_char_p, I, I], I),
         "qk_xrs_swap": ([P, C.POINTER(I), C.POINTER(I), I, C.POINTER(_XrsStats)], I),
+        "qk_ipc_init": ([P, C.c_char_p, I, I], I),
+        "qk_debug_host_barrier": ([C.c_char_p, I, I, I, D], I),
         "qk_xrs_swap_loopback": ([C.POINTER(P), I, C.POINTER(I), C.POINTER(I), I, C.POINTER(_XrsStats)], I),
         "qk_config_parse": ([C.c_char_p, C.POINTER(_Config)], I),
         "qk_config_finalize": ([C.POINTER(_Config)], I),
@@ -329,13 +334,18 @@ class State:
     def comm_init(self, unique_id: bytes, nranks: int, rank: int) -> None:
         _check(lib().qk_comm_init(self._h, unique_id, nranks, rank))
 
+    def ipc_init(self, job: str, nranks: int, rank: int) -> None:
+        """Join the node-local peer-memory rank group `job` (collective): CSQS
+        items then run as in-place swaps over the mapped peer slices."""
+        _check(lib().qk_ipc_init(self._h, job.encode(), nranks, rank))
+
     def simulate(self, prog: Program, initial: int = 0) -> dict:
         rs = _RunStats()
         _check(lib().qk_simulate(self._h, prog._h, C.byref(prog.cfg._c), initial, C.byref(rs)))
         return {k: getattr(rs, k) for k, _ in _RunStats._fields_}
 
     def xrs_swap(self, pairs):
-        """Multi-process XRS over this rank's communicator (NCCL)."""
+        """Multi-process XRS over this rank's group (peer memory if ipc_init, else NCCL)."""
         outs, ins, s = _pairs(pairs)
         st = _XrsStats()
         _check(lib().qk_xrs_swap(self._h, outs, ins, s, C.byref(st)))
@@ -358,6 +368,11 @@ def xrs_slab_index(n: int, r: int, outs, slab: int, offset: int) -> int:
     out = C.c_uint64()
     _check(lib().qk_xrs_slab_index(n, r, arr, len(outs), slab, offset, C.byref(out)))
     return out.value
+
+
+def debug_host_barrier(job: str, nranks: int, rank: int, rounds: int, timeout_s: float = 60.0) -> None:
+    """Pass qk_ipc_init's shared-memory barrier `rounds` times (host-only test hook)."""
+    _check(lib().qk_debug_host_barrier(job.encode(), nranks, rank, rounds, timeout_s))
 
 
 def comm_unique_id() -> bytes:
@@ -453,6 +468,12 @@ def ims_swap(state: State, pairs, cache_line_qubits: int = 2) -> None:
     """imsSwap (engine.cpp:86-101) on a device slice."""
     outs, ins, s = _pairs(pairs)
     _check(lib().qk_ims_swap(state._h, outs, ins, s, cache_line_qubits))
+
+
+def set_ims_mode(mode: int) -> None:
+    """IMS kernel choice: 0 per-element, 1 tiled when possible (default), 2 tiled
+    only for pairs moving memory bit 0/1."""
+    _check(lib().qk_set_ims_mode(mode))
 
 
 def xrs_swap(slices, pairs):

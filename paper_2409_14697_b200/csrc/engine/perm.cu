@@ -211,15 +211,47 @@ __device__ __forceinline__ uint64_t depositAround(uint64_t o, const SlabSpec& sp
     return o;
 }
 
-// Swap slab elements pairwise: A[dep(o)] <-> B[dep(o)] for o < count, where A
-// and B already point at their slab's bit pattern (may be peer memory).
-__global__ void __launch_bounds__(256) k_slab_swap(double2* A, double2* B, uint64_t count, const __grid_constant__ SlabSpec sp) {
-    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-    for (uint64_t o = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; o < count; o += stride) {
-        const uint64_t i = depositAround(o, sp);
-        const double2 x = A[i], y = B[i];
-        A[i] = y;
-        B[i] = x;
+// Swap slab elements pairwise: A[dep(o)] <-> B[dep(o)] for o in [o0, o0 + cnt),
+// where A and B already point at their slab's bit pattern (B may be peer
+// memory: NVLink loads/stores, or another process's slice on this GPU).  Up
+// to kSwapJobs slab pairs per launch (blockIdx.y); 4 elements per thread per
+// trip, every load in flight before the stores.
+constexpr int kSwapJobs = 8;
+struct SwapJobs {
+    int n;
+    double2* A[kSwapJobs];
+    double2* B[kSwapJobs];
+    uint64_t o0[kSwapJobs], cnt[kSwapJobs];
+    SlabSpec sp;
+};
+
+__global__ void __launch_bounds__(256) k_slab_swap(const __grid_constant__ SwapJobs j) {
+    constexpr int U = 4;
+    const int job = blockIdx.y;
+    double2* const A = j.A[job];
+    double2* const B = j.B[job];
+    const uint64_t o0 = j.o0[job], cnt = j.cnt[job];
+    const uint64_t tile = uint64_t(blockDim.x) * U;
+    for (uint64_t base = uint64_t(blockIdx.x) * tile; base < cnt; base += uint64_t(gridDim.x) * tile) {
+        uint64_t idx[U];
+        double2 x[U], y[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const uint64_t o = base + threadIdx.x + uint64_t(u) * blockDim.x;
+            idx[u] = o < cnt ? depositAround(o0 + o, j.sp) : ~uint64_t(0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++)
+            if (idx[u] != ~uint64_t(0)) {
+                x[u] = A[idx[u]];
+                y[u] = B[idx[u]];
+            }
+#pragma unroll
+        for (int u = 0; u < U; u++)
+            if (idx[u] != ~uint64_t(0)) {
+                A[idx[u]] = y[u];
+                B[idx[u]] = x[u];
+            }
     }
 }
 
@@ -481,13 +513,15 @@ static bool imsTileSpec(int logN, const int* outs, const int* ins, int s, ImsTil
 // QK_IMS_TILED: 0 = always the per-element kernel, 1 (default) = tiled
 // whenever possible (2^8-amplitude tiles: 6.2-6.5 TB/s on every pair pattern
 // measured), 2 = tiled only when a pair moves memory bit 0 or 1.
+static int g_imsMode = -1;  // -1: not set yet (QK_IMS_TILED, default 1)
 static int imsMode() {
-    static const int v = [] {
+    if (g_imsMode < 0) {
         const char* e = std::getenv("QK_IMS_TILED");
-        return e ? std::atoi(e) : 1;
-    }();
-    return v;
+        g_imsMode = e ? std::atoi(e) : 1;
+    }
+    return g_imsMode;
 }
+void setImsMode(int v) { g_imsMode = v; }
 
 cudaError_t launchIms(double2* a, int logN, const int* outs, const int* ins, int s, cudaStream_t st) {
     ImsTileSpec sp;
@@ -513,12 +547,29 @@ cudaError_t launchIms(double2* a, int logN, const int* outs, const int* ins, int
     return cudaGetLastError();
 }
 
-cudaError_t launchSlabSwap(double2* A, double2* B, uint64_t count, const int* outsSorted, int s, cudaStream_t st) {
-    SlabSpec sp{};
-    sp.s = s;
-    for (int j = 0; j < s; j++) sp.outs[j] = outsSorted[j];
-    k_slab_swap<<<gridFor(count, 256, 148 * 16), 256, 0, st>>>(A, B, count, sp);
-    return cudaGetLastError();
+// n slab pairs (A[k], B[k]) swapped over element ranges [o0[k], o0[k] + cnt[k]).
+cudaError_t launchSlabSwap(int n, double2* const* A, double2* const* B, const uint64_t* o0, const uint64_t* cnt,
+                           const int* outsSorted, int s, cudaStream_t st) {
+    for (int first = 0; first < n; first += kSwapJobs) {
+        SwapJobs j{};
+        j.n = n - first < kSwapJobs ? n - first : kSwapJobs;
+        j.sp.s = s;
+        for (int q = 0; q < s; q++) j.sp.outs[q] = outsSorted[q];
+        uint64_t most = 0;
+        for (int k = 0; k < j.n; k++) {
+            j.A[k] = A[first + k];
+            j.B[k] = B[first + k];
+            j.o0[k] = o0[first + k];
+            j.cnt[k] = cnt[first + k];
+            if (j.cnt[k] > most) most = j.cnt[k];
+        }
+        if (!most) continue;
+        const unsigned gx = gridFor((most + 3) / 4, 256, (148u * 8u + unsigned(j.n) - 1) / unsigned(j.n));
+        k_slab_swap<<<dim3(gx, unsigned(j.n)), 256, 0, st>>>(j);
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 cudaError_t launchWindowPack(double2* buf, const double2* S, uint64_t w0, uint64_t cnt, const int* outsSorted, int s,

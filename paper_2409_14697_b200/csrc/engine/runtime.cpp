@@ -24,6 +24,7 @@
 #include "quokka/circuit.hpp"
 #include "quokka/optimizer.hpp"
 #include "quokka/tools.hpp"
+#include "ipc.h"
 #include "jit.h"
 #include "schedule.h"
 
@@ -31,7 +32,9 @@ namespace qkdev {
 cudaError_t launchBlockPass(double2*, const double2*, const PassParams&, int, uint64_t, cudaStream_t);
 cudaError_t launchDenseGroup(double2*, const double2*, int, const int*, uint64_t, int, cudaStream_t);
 cudaError_t launchIms(double2*, int, const int*, const int*, int, cudaStream_t);
-cudaError_t launchSlabSwap(double2*, double2*, uint64_t, const int*, int, cudaStream_t);
+void setImsMode(int);
+cudaError_t launchSlabSwap(int, double2* const*, double2* const*, const uint64_t*, const uint64_t*, const int*, int,
+                           cudaStream_t);
 cudaError_t launchWindowPack(double2*, const double2*, uint64_t, uint64_t, const int*, int, cudaStream_t);
 cudaError_t launchWindowUnpack(double2*, const double2*, uint64_t, uint64_t, const int*, int, cudaStream_t);
 cudaError_t launchDiagTable(double2*, const double2*, uint64_t, const int*, int, cudaStream_t);
@@ -265,6 +268,7 @@ struct qk_state {
     double2* packBuf = nullptr;
     uint64_t bufAmps = 0;
     ncclComm_t comm = nullptr;
+    qkipc::Group* ipc = nullptr;  // peer-memory rank group (qk_ipc_init)
     bool profiling = false;
     qk_run_stats last{};
     // Fused norm: the program's last pass wrote per-warp partial sums of
@@ -621,7 +625,9 @@ DeviceTables tablesFor(qk_program* p, const Compiled& c, int device) {
 // Profiling: CUDA events on the state's stream around each launch class.
 struct Timer {
     qk_state* st;
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[3];
+    // classes: 0 block items, 1 IMS, 2 XRS, 3 full-slice fused passes, 4 init (first pass / memset)
+    static constexpr int kClasses = 5;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[kClasses];
     explicit Timer(qk_state* s) : st(s) {}
     template <class F>
     void time(int cls, F&& f) {
@@ -637,8 +643,8 @@ struct Timer {
         cuda(cudaEventRecord(b, st->stream), "event record");
         ev[cls].emplace_back(a, b);
     }
-    void collect(double out[3]) {
-        for (int c = 0; c < 3; c++) {
+    void collect(double out[kClasses]) {
+        for (int c = 0; c < kClasses; c++) {
             out[c] = 0;
             for (auto& [a, b] : ev[c]) {
                 float ms = 0;
@@ -646,7 +652,8 @@ struct Timer {
                 cudaEventElapsedTime(&ms, a, b);
                 out[c] += ms;
                 static const bool perItem = std::getenv("QK_PROFILE_ITEMS") != nullptr;
-                if (perItem) std::fprintf(stderr, "qk item %s %.3f ms\n", c == 0 ? "pass" : c == 1 ? "ims" : "xrs", ms);
+                static const char* names[kClasses] = {"block", "ims", "xrs", "pass", "init"};
+                if (perItem) std::fprintf(stderr, "qk item %s %.3f ms\n", names[c], ms);
                 cudaEventDestroy(a);
                 cudaEventDestroy(b);
             }
@@ -681,7 +688,7 @@ constexpr uint64_t kNoBasis = ~uint64_t(0);
 // basis != kNoBasis: the first step is a pass that synthesizes |basis> (slice
 // index) instead of reading the slice (replaces initState's memset + store).
 void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_run_stats& rs,
-              uint64_t basis = kNoBasis) {
+              uint64_t basis = kNoBasis, Timer* timer = nullptr) {
     const bool synthesized = basis != kNoBasis;
     for (const qkeng::Step& s : ci.steps) {
         st->normValid = false;
@@ -710,12 +717,20 @@ void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_ru
                     st->normTilesCap = tiles;
                 }
             }
-            if (useJit(st->nLocal))
-                cuda(qkjit::launch(P, st->amps, t.gtab, st->nLocal, basis, st->stream,
-                                   P.norm_out ? st->normTiles : nullptr),
-                     "specialized block pass");
-            else
-                cuda(qkdev::launchBlockPass(st->amps, t.gtab, P, st->nLocal, basis, st->stream), "block pass");
+            auto launchPass = [&] {
+                if (useJit(st->nLocal))
+                    cuda(qkjit::launch(P, st->amps, t.gtab, st->nLocal, basis, st->stream,
+                                       P.norm_out ? st->normTiles : nullptr),
+                         "specialized block pass");
+                else
+                    cuda(qkdev::launchBlockPass(st->amps, t.gtab, P, st->nLocal, basis, st->stream), "block pass");
+            };
+            if (timer) timer->time(basis == kNoBasis ? 3 : 4, launchPass);
+            else launchPass();
+            if (basis == kNoBasis) {
+                rs.full_pass_launches++;
+                rs.full_pass_bytes += 32.0 * double(st->count);
+            }
             if (timing) {
                 float ms = 0;
                 cuda(cudaEventRecord(e1, st->stream), "event");
@@ -824,7 +839,8 @@ struct XrsRank {
 // ncclSend/ncclRecv per partner into a single receive buffer, then copy-back.
 void runXrsNccl(qk_state* st, const XrsPlan& p, qk_run_stats& rs) {
     st->normValid = false;
-    if (!st->comm) throw SimulationError("cross-rank swap needs a communicator (qk_comm_init) or qk_simulate_local");
+    if (!st->comm)
+        throw SimulationError("cross-rank swap needs a communicator (qk_comm_init / qk_ipc_init) or qk_simulate_local");
     if (p.s == 0) return;
     XrsRank x(st, p);
     for (size_t a = 0; a < x.msgs.size();) {
@@ -891,6 +907,26 @@ void runXrsLoopback(qk_state** sl, int ns, const XrsPlan& p) {
     }
 }
 
+// Slices of one process on different GPUs: map every pair of their devices
+// for peer loads/stores (NVLink) so the slab-swap kernel can reach both.
+void enablePeers(qk_state** sl, int ns) {
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
+    for (int a = 0; a < ns; a++)
+        for (int b = 0; b < ns; b++) {
+            const int da = sl[a]->device, db = sl[b]->device;
+            if (da == db) continue;
+            int can = 0;
+            cuda(cudaDeviceCanAccessPeer(&can, da, db), "cudaDeviceCanAccessPeer");
+            if (!can) throw SimulationError("devices " + std::to_string(da) + " and " + std::to_string(db) +
+                                            " have no peer access: use one process per GPU (qk_comm_init)");
+            DeviceGuard g(da);
+            const cudaError_t e = cudaDeviceEnablePeerAccess(db, 0);
+            if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+            else cuda(e, "cudaDeviceEnablePeerAccess");
+        }
+}
+
 // In-process XRS: every slab pair swapped in place by one kernel reading and
 // writing both slices (same device or peer-mapped).  No buffer, no copy-back.
 void runXrsLocal(qk_state** sl, int ns, const XrsPlan& p) {
@@ -899,19 +935,58 @@ void runXrsLocal(qk_state** sl, int ns, const XrsPlan& p) {
     const int slabs = 1 << p.s;
     for (int r = 0; r < ns; r++) {
         const int own = ownSlab(r, p);
+        std::vector<double2*> A, B;
         for (int pa = 0; pa < slabs; pa++) {
             if (pa == own) continue;
             const int q = partnerOf(r, pa, p);
             if (q < r) continue;  // each unordered slab pair once
-            DeviceGuard g(sl[r]->device);
-            cuda(qkdev::launchSlabSwap(sl[r]->amps + slabBits(pa, p), sl[q]->amps + slabBits(own, p), p.slabOffsets,
-                                       p.outs.data(), p.s, sl[r]->stream),
-                 "xrs slab swap");
+            A.push_back(sl[r]->amps + slabBits(pa, p));
+            B.push_back(sl[q]->amps + slabBits(own, p));
         }
+        if (A.empty()) continue;
+        const std::vector<uint64_t> o0(A.size(), 0), cnt(A.size(), p.slabOffsets);
+        DeviceGuard g(sl[r]->device);
+        cuda(qkdev::launchSlabSwap(int(A.size()), A.data(), B.data(), o0.data(), cnt.data(), p.outs.data(), p.s,
+                                   sl[r]->stream),
+             "xrs slab swap");
     }
     for (int k = 0; k < ns; k++) cuda(cudaStreamSynchronize(sl[k]->stream), "xrs post-sync");
 }
 
+// Multi-process XRS over peer memory (qk_ipc_init): every rank maps every
+// other rank's slice, so a CSQS is one in-place swap kernel per rank over all
+// its partner slab pairs -- no exchange buffer, no copy-back pass.  Each
+// unordered slab pair is split in halves: the lower rank swaps the first
+// half of its elements, the higher rank the second, so both directions of
+// every link carry half the slab.  Host barriers bracket the kernel: every
+// rank's earlier items are done before any peer touches its slice, and every
+// swap is done before any rank goes on.
+void runXrsIpc(qk_state* st, const XrsPlan& p, qk_run_stats& rs) {
+    st->normValid = false;
+    if (p.s == 0) return;
+    cuda(cudaStreamSynchronize(st->stream), "xrs pre-sync");
+    qkipc::barrier(st->ipc);
+    const int own = ownSlab(st->rank, p), slabs = 1 << p.s;
+    const uint64_t half = p.slabOffsets / 2;
+    std::vector<double2*> A, B;
+    std::vector<uint64_t> o0, cnt;
+    for (int pa = 0; pa < slabs; pa++) {
+        if (pa == own) continue;
+        const int q = partnerOf(st->rank, pa, p);
+        A.push_back(st->amps + slabBits(pa, p));
+        B.push_back(static_cast<double2*>(qkipc::peer(st->ipc, q)) + slabBits(own, p));
+        o0.push_back(st->rank < q ? 0 : half);
+        cnt.push_back(st->rank < q ? half : p.slabOffsets - half);
+    }
+    cuda(qkdev::launchSlabSwap(int(A.size()), A.data(), B.data(), o0.data(), cnt.data(), p.outs.data(), p.s,
+                               st->stream),
+         "xrs peer swap");
+    rs.kernel_launches += (A.size() + 7) / 8;
+    cuda(cudaStreamSynchronize(st->stream), "xrs peer swap");
+    qkipc::barrier(st->ipc);
+    rs.xrs_rounds++;
+    rs.xrs_bytes += 16.0 * double(st->count) * (1.0 - std::ldexp(1.0, -p.s));
+}
 
 // qk_gate[] -> quokka::Gate list (matrix order: controls first), validating
 // arity and the chunk bound (engine.cpp:264-268).
@@ -1089,6 +1164,7 @@ int qk_destroy(qk_state* st) {
         DeviceGuard g(st->device);
         cudaStreamSynchronize(st->stream);
         if (st->comm) ncclCommDestroy(st->comm);
+        qkipc::leave(st->ipc);
         cudaFree(st->amps);
         cudaFree(st->normScratch);
         cudaFree(st->normOut);
@@ -1282,6 +1358,13 @@ int qk_ims_swap(qk_state* st, const int* outs, const int* ins, int s, int /*cach
     });
 }
 
+int qk_set_ims_mode(int mode) {
+    return guard([&] {
+        if (mode < 0 || mode > 2) throw ConfigError("ims mode must be 0, 1 or 2");
+        qkdev::setImsMode(mode);
+    });
+}
+
 int qk_xrs_swap_local(qk_state** sl, int ns, const int* outs, const int* ins, int s, qk_xrs_stats* stats) {
     return guard([&] {
         if (ns < 1) throw SimulationError("no slices");
@@ -1295,6 +1378,7 @@ int qk_xrs_swap_local(qk_state** sl, int ns, const int* outs, const int* ins, in
         const XrsPlan p = planXrs(op, n, R, B);
         if (stats)
             for (int k = 0; k < ns; k++) accountXrs(p, &stats[k]);
+        enablePeers(sl, ns);
         if (p.s) runXrsLocal(sl, ns, p);
     });
 }
@@ -1318,6 +1402,30 @@ int qk_comm_init(qk_state* st, const unsigned char id[128], int nranks, int rank
     });
 }
 
+int qk_ipc_init(qk_state* st, const char* job, int nranks, int rank) {
+    return guard([&] {
+        if (nranks != (1 << st->R) || rank != st->rank) throw ConfigError("rank group does not match the rank split");
+        if (st->ipc) throw SimulationError("ipc group already joined");
+        const char* t = std::getenv("QK_IPC_TIMEOUT");
+        DeviceGuard g(st->device);
+        cuda(cudaStreamSynchronize(st->stream), "ipc init");
+        st->ipc = qkipc::join(job ? job : "", nranks, rank, st->amps, st->device, t ? std::atof(t) : 600.0);
+    });
+}
+
+int qk_debug_host_barrier(const char* job, int nranks, int rank, int rounds, double timeout_s) {
+    return guard([&] {
+        qkipc::Barrier* b = qkipc::barrierOpen(job ? job : "", nranks, rank, timeout_s);
+        try {
+            for (int i = 0; i < rounds; i++) qkipc::barrierWait(b);
+        } catch (...) {
+            qkipc::barrierClose(b);
+            throw;
+        }
+        qkipc::barrierClose(b);
+    });
+}
+
 int qk_xrs_swap(qk_state* st, const int* outs, const int* ins, int s, qk_xrs_stats* stats) {
     return guard([&] {
         quokka::SwapOp op;
@@ -1327,7 +1435,8 @@ int qk_xrs_swap(qk_state* st, const int* outs, const int* ins, int s, qk_xrs_sta
         accountXrs(p, stats);
         DeviceGuard g(st->device);
         qk_run_stats rs{};
-        runXrsNccl(st, p, rs);
+        if (st->ipc) runXrsIpc(st, p, rs);
+        else runXrsNccl(st, p, rs);
         cuda(cudaStreamSynchronize(st->stream), "xrs");
     });
 }
@@ -1521,10 +1630,10 @@ int qk_simulate(qk_state* st, const qk_program* cp, const qk_config* cfg, uint64
         if (synth)
             basis = (initial >> st->nLocal) == Index(st->rank) ? layoutIndex(initial & (st->count - 1), comp->mem0)
                                                               : st->count;
-        else setBasis(st, initial, &comp->mem0);
+        else timer.time(4, [&] { setBasis(st, initial, &comp->mem0); });
         auto runItem = [&](const CompiledItem& it) {
             if (it.kind == CompiledItem::Block) {
-                timer.time(0, [&] { runBlock(st, it, t, rs, basis); });
+                timer.time(0, [&] { runBlock(st, it, t, rs, basis, &timer); });
                 basis = kNoBasis;
             }
             else if (it.kind == CompiledItem::Ims) timer.time(1, [&] { runIms(st, it.outs, it.ins, rs); });
@@ -1533,7 +1642,10 @@ int qk_simulate(qk_state* st, const qk_program* cp, const qk_config* cfg, uint64
                 op.kind = quokka::SwapOp::CrossRank;
                 for (size_t j = 0; j < it.outs.size(); j++) op.pairs.emplace_back(it.outs[j], it.ins[j]);
                 const XrsPlan plan = planXrs(op, st->n, st->R, st->B);
-                timer.time(2, [&] { runXrsNccl(st, plan, rs); });
+                timer.time(2, [&] {
+                    if (st->ipc) runXrsIpc(st, plan, rs);
+                    else runXrsNccl(st, plan, rs);
+                });
             }
         };
         size_t nextAlt = 0;
@@ -1579,11 +1691,13 @@ int qk_simulate(qk_state* st, const qk_program* cp, const qk_config* cfg, uint64
         cudaEventElapsedTime(&ms, e0, e1);
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
-        double cls[3];
+        double cls[Timer::kClasses];
         timer.collect(cls);
         rs.block_ms = cls[0];
         rs.ims_ms = cls[1];
         rs.xrs_ms = cls[2];
+        rs.full_pass_ms = cls[3];
+        rs.init_ms = cls[4];
         rs.total_ms = ms;
         st->last = rs;
         if (stats) *stats = rs;
@@ -1602,6 +1716,7 @@ int qk_simulate_local(qk_state** sl, int ns, const qk_program* cp, const qk_conf
         }
         if (initial >= (Index(1) << c.totalQubits)) throw SimulationError("initial basis state out of range");
         auto comp = compileFor(p, sl[0]->nLocal);
+        enablePeers(sl, ns);
         std::vector<DeviceTables> tabs;
         for (int k = 0; k < ns; k++) {
             sl[k]->B = c.bufferQubits;

@@ -185,6 +185,8 @@ bool isDiagonalGate(const Gate& g) {
     }
 }
 
+double passCodeBudget();
+
 namespace {
 
 // Tile bits that must sit in register slots when `g` runs.
@@ -244,8 +246,12 @@ public:
         std::memcpy(P_->map_in[0], map_, sizeof map_);
 
         const size_t first = i;
-        double flops = 0;
+        double flops = 0, code = 0;
         while (i < tg_.size()) {
+            if (code > passCodeBudget() && i > first) {  // NVRTC time grows super-linearly with a pass's length
+                if (std::getenv("QK_DEBUG_SPLIT")) std::fprintf(stderr, "pass split at gate %zu: code %.0f\n", i, code);
+                break;
+            }
             // room for what is still queued: batched register ops, pair-phase
             // flushes, and one re-issue of the pending gates (tables fold into
             // <= rb + 2 ops; CTA-bit gates add up to 2 terms / coefficients each)
@@ -273,6 +279,7 @@ public:
             }
             lower(tg_[i], orig_[i]);
             flops += referenceFlopsPerAmp(orig_[i]);
+            code += codeWork(orig_[i]);
             i++;
         }
         flushAll();
@@ -288,6 +295,17 @@ public:
     }
 
 private:
+    // Straight-line code a gate adds per thread, in complex multiply-adds:
+    // a dense k-qubit gate is a 2^k x 2^k matvec on each of the 2^(rb-k)
+    // register groups; diagonals mostly fold into phase tables.
+    double codeWork(const Gate& g) const {
+        const double slots = double(1 << rb_);
+        if (isDiagonalGate(g)) return 0.25 * slots;
+        if (g.kind == GateKind::CX || g.kind == GateKind::SWAP || g.kind == GateKind::X) return 0.0;
+        const int k = g.kind == GateKind::FusedDense ? int(g.targets.size()) : 1;
+        return slots * double(1 << k);
+    }
+
     bool isReg(int slot) const { return slot < rb_; }
     // Slot holds its tile bit inverted (an X was applied as a relabel).
     int flip(int slot) const { return int((flips_ >> slot) & 1u); }
@@ -1091,6 +1109,22 @@ void compileGroup(const std::vector<Gate>& gates, uint64_t used, int ct, int nLo
 
 }  // namespace
 
+// QK_PASS_WORK (default 3000): most reference-formula flops per amplitude
+// one pass may carry.  NVRTC's time on a straight-line
+// pass grows super-linearly with its length (QFT-33's ~1300-flop passes
+// compile in ~1 s, a 150-gate U3 stream at n = 13 took minutes); a pass
+// this heavy is FP64-bound, so the extra HBM sweep of a cut costs < 10 %.
+double passWorkBudget() {
+    static const double v = envInt("QK_PASS_WORK", 3000, 50, 1 << 30);
+    return v;
+}
+// QK_PASS_CODE (default 4096): most complex multiply-adds of straight-line
+// code per thread in one pass (PassBuilder::codeWork); the pass is cut there.
+double passCodeBudget() {
+    static const double v = envInt("QK_PASS_CODE", 4096, 64, 1 << 30);
+    return v;
+}
+
 int lowTileBits() {
     static const int v = envInt("QK_TILE_LOW", 3, 0, 8);
     return v;
@@ -1213,14 +1247,19 @@ std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::
         const bool synthRun = synthFirst && steps.empty();
         std::vector<uint64_t> mask(m);
         for (size_t k = 0; k < m; k++) mask[k] = isDiagonalGate(run[k]) ? 0 : run[k].depMask();
+        std::vector<double> work(m);  // reference-formula flops/amp: bounds a pass's straight-line code
+        for (size_t k = 0; k < m; k++) work[k] = referenceFlopsPerAmp(run[k]);
         std::vector<double> best(m + 1, 1e300);
         std::vector<size_t> from(m + 1, 0);
         best[0] = 0;
         for (size_t i = 1; i <= m; i++) {
             uint64_t used = 0;
+            double w = 0;
             for (size_t j = i; j-- > 0;) {
                 used |= mask[j];
+                w += work[j];
                 if (__builtin_popcountll(used) > ct) break;
+                if (w > passWorkBudget() && j + 1 < i) break;
                 const double c = best[j] + ((synthRun && j == 0) ? 1.0 : passCost(used));
                 if (c < best[i] - 1e-9) {
                     best[i] = c;

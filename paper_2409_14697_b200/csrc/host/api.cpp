@@ -228,6 +228,9 @@ StateVector gatherState(const std::vector<std::vector<Amp>>& slices, int nQubits
 
 namespace {
 
+// Rank r's slice lives on device r mod (visible devices): one GPU per rank
+// when there are enough (the runtime enables peer access between them for
+// the in-place slab swap), else several slices share a device.
 struct SliceSet {
     std::vector<std::unique_ptr<Slice>> owned;
     std::vector<qk_state*> raw;
@@ -236,19 +239,45 @@ struct SliceSet {
         check(qk_device_count(&ndev));
         const int ranks = 1 << cfg.rankQubits;
         for (int r = 0; r < ranks; r++) {
-            owned.push_back(std::make_unique<Slice>(cfg.totalQubits, cfg.rankQubits, r, cfg.bufferQubits, 0));
+            owned.push_back(std::make_unique<Slice>(cfg.totalQubits, cfg.rankQubits, r, cfg.bufferQubits,
+                                                    ndev > 0 ? r % ndev : 0));
             raw.push_back(owned.back()->st);
         }
     }
 };
 
-void fillStats(const std::vector<qk_xrs_stats>& cs, std::vector<RankStats>& out) {
-    out.resize(cs.size());
-    for (size_t k = 0; k < cs.size(); k++) {
-        out[k].bytesSent = cs[k].bytes_sent;
-        out[k].bytesReceived = cs[k].bytes_received;
-        out[k].peakBufferBytes = cs[k].peak_buffer_bytes;
-        out[k].rounds = cs[k].rounds;
+// The reference's RankStats for one cross-rank swap, added to `out` the way
+// xrsFill / xrsDeliver accumulate them (distributed.cpp:87-93, 116-119): per
+// window round, bytes sent (= received) and one perRound entry.  The round
+// structure is the runtime's own message plan (qk_xrs_plan).
+void accountSwap(const SwapOp& op, const Config& cfg, std::vector<RankStats>& out) {
+    const int ranks = 1 << cfg.rankQubits;
+    if (int(out.size()) != ranks) out.resize(size_t(ranks));
+    std::vector<int> outs, ins;
+    for (const auto& [a, b] : op.pairs) {
+        outs.push_back(a);
+        ins.push_back(b);
+    }
+    const int s = int(outs.size());
+    const Index slabOffsets = Index(1) << (cfg.rankRegion() - s);
+    const Index window = std::min(slabOffsets, Index(1) << (cfg.bufferQubits - s));
+    const Index rounds = (slabOffsets + window - 1) / window;
+    const int slabsOut = (1 << s) - 1;
+    std::vector<qk_xrs_msg> msgs(size_t(slabsOut) * size_t(rounds) + 1);
+    for (int r = 0; r < ranks; r++) {
+        int nm = 0;
+        check(qk_xrs_plan(cfg.totalQubits, cfg.rankQubits, cfg.bufferQubits, r, outs.data(), ins.data(), s,
+                          msgs.data(), int(msgs.size()), &nm));
+        RankStats& st = out[size_t(r)];
+        std::vector<std::size_t> perRound(size_t(rounds), 0);
+        for (int m = 0; m < nm; m++) perRound[size_t(msgs[size_t(m)].round)] += msgs[size_t(m)].count * sizeof(Amp);
+        for (std::size_t bytes : perRound) {
+            st.bytesSent += bytes;
+            st.bytesReceived += bytes;
+            st.peakBufferBytes = std::max<std::size_t>(st.peakBufferBytes, std::size_t(slabsOut) * window * sizeof(Amp));
+            st.rounds++;
+            st.perRound.emplace_back(bytes, bytes);
+        }
     }
 }
 
@@ -270,7 +299,9 @@ MultiRankResult spawnRanks(const Program& p, const Config& cfg, Index initial) {
     }
     r.state = gatherState(slices, p.nQubits);
     r.layout = p.finalLayout;
-    fillStats(cs, r.stats);
+    r.stats.assign(set.raw.size(), RankStats{});
+    for (const ProgramItem& it : p.items)
+        if (it.type == ProgramItem::Swap && it.swap.kind == SwapOp::CrossRank) accountSwap(it.swap, cfg, r.stats);
     return r;
 }
 
@@ -288,7 +319,7 @@ void xrsSwap(std::vector<std::vector<Amp>>& slices, const SwapOp& op, const Conf
     std::vector<qk_xrs_stats> cs(slices.size());
     check(qk_xrs_swap_local(set.raw.data(), int(set.raw.size()), outs.data(), ins.data(), int(outs.size()), cs.data()));
     for (size_t k = 0; k < slices.size(); k++) set.owned[k]->down(slices[k]);
-    if (stats) fillStats(cs, *stats);
+    if (stats) accountSwap(op, cfg, *stats);
 }
 
 }  // namespace quokka
