@@ -125,6 +125,7 @@ def lib():
         "qk_set_jit_min_qubits": ([I], I),
         "qk_ims_swap": ([P, C.POINTER(I), C.POINTER(I), I, I], I),
         "qk_set_ims_mode": ([I], I),
+        "qk_set_dense_mode": ([I], I),
         "qk_xrs_swap_local": ([C.POINTER(P), I, C.POINTER(I), C.POINTER(I), I, C.POINTER(_XrsStats)], I),
         "qk_xrs_plan": ([I, I, I, I, C.POINTER(I), C.POINTER(I), I, C.POINTER(_XrsMsg), I,
                          C.POINTER(I)], I),
@@ -474,6 +475,11 @@ def set_ims_mode(mode: int) -> None:
     """IMS kernel choice: 0 per-element, 1 tiled when possible (default), 2 tiled
     only for pairs moving memory bit 0/1."""
     _check(lib().qk_set_ims_mode(mode))
+
+
+def set_dense_mode(mode: int) -> None:
+    """Fused U5 kernel: 0 DFMA, 1 DMMA (FP64 tensor cores), -1 autotune (default)."""
+    _check(lib().qk_set_dense_mode(mode))
 
 
 def xrs_swap(slices, pairs):

@@ -1,0 +1,246 @@
+// Fused dense U5 (the reference's default fusion_qbit = 5) over the whole
+// slice: y_g = M x_g for every group g of 32 amplitudes that differ only in
+// the 5 target bits (proj/src/engine.cpp:228-251: gather 2^k, row-major
+// matvec, scatter; sub-index bit k-1-j = target j, engine.cpp:176-182).
+//
+// A CTA stages a 2^12-amplitude tile (the 5 target bits + the 7 lowest other
+// bits, so rows are coalesced) in shared memory as two planes, re and im,
+// [s][g] (s = target sub-index, g = one of the tile's 128 groups), applies M
+// to its 128 groups and writes the tile back: one HBM round trip per U5
+// (32 B/amp) and 128 complex multiply-adds per amplitude (FP64-bound on
+// B200: 36.5 TF vs 6.5 TB/s).  Two ways to do the math, chosen by timing:
+//   FMA  -- each thread holds one group's 32 inputs in registers and forms
+//           its 32 outputs with DFMA, M broadcast from shared memory;
+//   MMA  -- the tile as a real GEMM on the FP64 tensor cores (DMMA,
+//           mma.sync.m8n8k4.f64): Y(64x128) = A(64x64) X(64x128) with
+//           A = [[Mr, -Mi], [Mi, Mr]] staged in shared memory in fragment order.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace qkdev {
+
+namespace {
+
+constexpr int kDk = 5;                       // target bits
+constexpr int kDct = 12;                     // tile bits
+constexpr int kDgroups = 1 << (kDct - kDk);  // 128 groups per tile
+constexpr int kDstride = kDgroups + 8;       // plane row stride (doubles): rows 16 banks apart
+constexpr int kDplane = 32 * kDstride;
+
+struct DenseSpec {
+    int tbit[kDct];      // tile index bit j -> memory bit
+    int vslot[kDct];     // tile index bit j -> plane offset contribution (s row or g column)
+    int nfree;           // memory bits outside the tile (ascending)
+    int fbit[40];
+};
+
+__device__ __forceinline__ double2 cmacD(double2 acc, double2 m, double2 x) {
+    acc.x = fma(m.x, x.x, acc.x);
+    acc.x = fma(-m.y, x.y, acc.x);
+    acc.y = fma(m.x, x.y, acc.y);
+    acc.y = fma(m.y, x.x, acc.y);
+    return acc;
+}
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+// Real block matrix A[i][k] of the complex M (row-major 32x32 double2).
+__device__ __forceinline__ double blockA(const double2* __restrict__ M, int i, int k) {
+    const double2 m = __ldg(M + (i & 31) * 32 + (k & 31));
+    if (i < 32) return k < 32 ? m.x : -m.y;
+    return k < 32 ? m.y : m.x;
+}
+
+// FMA: 128 threads, one group each (its 32 inputs in registers, outputs
+// written back into its own plane column: no other thread reads it), two
+// CTAs per SM.  MMA: 256 threads, 8 warps each owning a 16 x 64 block of Y.
+template <bool MMA>
+__global__ void __launch_bounds__(MMA ? 256 : 128, 2) k_dense_tile(double2* __restrict__ st, const double2* __restrict__ M,
+                                                                  const __grid_constant__ DenseSpec sp, uint64_t ntiles) {
+    constexpr int LOGNT = MMA ? 8 : 7;
+    constexpr int NT = 1 << LOGNT;
+    constexpr int PER = (1 << kDct) / NT;  // amplitudes per thread in the load / store phases
+    constexpr int HI = kDct - LOGNT;
+    extern __shared__ double smd[];
+    double* const Xr = smd;
+    double* const Xi = smd + kDplane;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+
+    // this thread's part of every tile: t = tid | i << LOGNT
+    uint64_t depLo = 0;
+    int slotLo = 0;
+#pragma unroll
+    for (int j = 0; j < LOGNT; j++)
+        if ((tid >> j) & 1) {
+            depLo |= uint64_t(1) << sp.tbit[j];
+            slotLo += sp.vslot[j];
+        }
+
+    // MMA: A = [[Mr, -Mi], [Mi, Mr]] (64 x 64) in shared memory, stored in
+    // fragment order: As[(rowTile * 16 + kk) * 32 + lane] is lane's element
+    // of the A fragment for rows 8 rowTile.., k-step kk (conflict-free loads).
+    // FMA: M itself, read as warp-wide broadcasts.
+    double* const As = smd + 2 * kDplane;
+    double2* const Ms = reinterpret_cast<double2*>(smd + 2 * kDplane);
+    if (MMA) {
+        for (int e = tid; e < 8 * 16 * 32; e += NT) {
+            const int l = e & 31, kk = (e >> 5) & 15, rt = e >> 9;
+            As[e] = blockA(M, 8 * rt + (l >> 2), 4 * kk + (l & 3));
+        }
+    } else {
+        for (int e = tid; e < 32 * 32; e += NT) Ms[e] = __ldg(M + e);
+    }
+    uint64_t depHi[HI];
+    int slotHi[HI];
+#pragma unroll
+    for (int j = 0; j < HI; j++) {
+        depHi[j] = uint64_t(1) << sp.tbit[LOGNT + j];
+        slotHi[j] = sp.vslot[LOGNT + j];
+    }
+
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        uint64_t base = 0;
+        for (int j = 0; j < sp.nfree; j++) base |= ((tile >> j) & 1) << sp.fbit[j];
+        __syncthreads();  // the previous tile's stores read the planes
+        base |= depLo;
+#pragma unroll
+        for (int b8 = 0; b8 < PER; b8 += 8) {  // 8 loads in flight per thread per batch
+            double2 v[8];
+#pragma unroll
+            for (int i = 0; i < 8; i++) {
+                const int ii = b8 + i;
+                uint64_t a = base;
+#pragma unroll
+                for (int j = 0; j < HI; j++)
+                    if ((ii >> j) & 1) a |= depHi[j];
+                v[i] = __ldcs(st + a);
+            }
+#pragma unroll
+            for (int i = 0; i < 8; i++) {
+                const int ii = b8 + i;
+                int slot = slotLo;
+#pragma unroll
+                for (int j = 0; j < HI; j++)
+                    if ((ii >> j) & 1) slot += slotHi[j];
+                Xr[slot] = v[i].x;
+                Xi[slot] = v[i].y;
+            }
+        }
+        __syncthreads();
+        if (!MMA) {
+            const int g = tid;
+            double2 x[32];
+#pragma unroll
+            for (int s = 0; s < 32; s++) x[s] = make_double2(Xr[s * kDstride + g], Xi[s * kDstride + g]);
+#pragma unroll 1
+            for (int r0 = 0; r0 < 32; r0 += 4) {
+                double2 acc[4];
+#pragma unroll
+                for (int q = 0; q < 4; q++) acc[q] = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int s = 0; s < 32; s++)
+#pragma unroll
+                    for (int q = 0; q < 4; q++) acc[q] = cmacD(acc[q], Ms[(r0 + q) * 32 + s], x[s]);
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    Xr[(r0 + q) * kDstride + g] = acc[q].x;
+                    Xi[(r0 + q) * kDstride + g] = acc[q].y;
+                }
+            }
+        } else {
+            const int rp = w & 3, ch = w >> 2;
+            double acc[2][8][2];
+#pragma unroll
+            for (int rt = 0; rt < 2; rt++)
+#pragma unroll
+                for (int c = 0; c < 8; c++) acc[rt][c][0] = acc[rt][c][1] = 0.0;
+#pragma unroll
+            for (int kk = 0; kk < 16; kk++) {
+                const int k = 4 * kk + (lane & 3);
+                const double* const plane = k < 32 ? Xr : Xi;
+                double b[8];
+#pragma unroll
+                for (int c = 0; c < 8; c++) b[c] = plane[(k & 31) * kDstride + 8 * (8 * ch + c) + (lane >> 2)];
+                const double a0 = As[((2 * rp) * 16 + kk) * 32 + lane];
+                const double a1 = As[((2 * rp + 1) * 16 + kk) * 32 + lane];
+#pragma unroll
+                for (int c = 0; c < 8; c++) dmma(acc[0][c][0], acc[0][c][1], a0, b[c]);
+#pragma unroll
+                for (int c = 0; c < 8; c++) dmma(acc[1][c][0], acc[1][c][1], a1, b[c]);
+            }
+            __syncthreads();  // every warp has read X before Y overwrites it
+#pragma unroll
+            for (int rt = 0; rt < 2; rt++) {
+                const int i = 8 * (2 * rp + rt) + (lane >> 2);
+                double* const plane = i < 32 ? Xr : Xi;
+#pragma unroll
+                for (int c = 0; c < 8; c++) {
+                    const int col = 8 * (8 * ch + c) + 2 * (lane & 3);
+                    plane[(i & 31) * kDstride + col] = acc[rt][c][0];
+                    plane[(i & 31) * kDstride + col + 1] = acc[rt][c][1];
+                }
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < PER; i++) {
+            uint64_t a = base;
+            int slot = slotLo;
+#pragma unroll
+            for (int j = 0; j < HI; j++)
+                if ((i >> j) & 1) {
+                    a |= depHi[j];
+                    slot += slotHi[j];
+                }
+            __stcs(st + a, make_double2(Xr[slot], Xi[slot]));
+        }
+    }
+}
+
+}  // namespace
+
+// U5 over a slice of 2^nLocal >= 2^12 amplitudes; targets[j] = memory bit of
+// sub-index bit (4 - j).  mode 0 = DFMA, 1 = DMMA.
+cudaError_t launchDenseTile(double2* state, const double2* M, const int* targets, int k, int nLocal, int mode,
+                            int smCount, cudaStream_t stream) {
+    if (k != kDk || nLocal < kDct) return cudaErrorInvalidValue;
+    DenseSpec sp{};
+    uint64_t tmask = 0;
+    for (int j = 0; j < k; j++) tmask |= uint64_t(1) << targets[j];
+    uint64_t tile = tmask;
+    for (int b = 0; b < nLocal && __builtin_popcountll(tile) < kDct; b++) tile |= uint64_t(1) << b;
+    int j = 0, gbit = 0;
+    for (int b = 0; b < nLocal; b++) {
+        if (!((tile >> b) & 1)) {
+            sp.fbit[sp.nfree++] = b;
+            continue;
+        }
+        sp.tbit[j] = b;
+        int q = -1;
+        for (int t = 0; t < k; t++)
+            if (targets[t] == b) q = t;
+        sp.vslot[j] = q >= 0 ? (1 << (k - 1 - q)) * kDstride : (1 << gbit++);
+        j++;
+    }
+    const uint64_t ntiles = uint64_t(1) << (nLocal - kDct);
+    const size_t smem = sizeof(double) * 2 * kDplane + (mode ? sizeof(double) * 64 * 64 : sizeof(double2) * 32 * 32);
+    const uint64_t resident = uint64_t(smCount) * 2;
+    const unsigned grid = unsigned(ntiles < resident ? ntiles : resident);
+    cudaError_t e;
+    if (mode) {
+        e = cudaFuncSetAttribute(k_dense_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return e;
+        k_dense_tile<true><<<grid, 256, smem, stream>>>(state, M, sp, ntiles);  // 8 warps x (16 rows x 64 groups)
+    } else {
+        e = cudaFuncSetAttribute(k_dense_tile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return e;
+        k_dense_tile<false><<<grid, 128, smem, stream>>>(state, M, sp, ntiles);  // one group per thread
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace qkdev

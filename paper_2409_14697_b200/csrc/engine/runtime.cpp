@@ -10,6 +10,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -31,6 +32,7 @@
 namespace qkdev {
 cudaError_t launchBlockPass(double2*, const double2*, const PassParams&, int, uint64_t, cudaStream_t);
 cudaError_t launchDenseGroup(double2*, const double2*, int, const int*, uint64_t, int, cudaStream_t);
+cudaError_t launchDenseTile(double2*, const double2*, const int*, int, int, int, int, cudaStream_t);
 cudaError_t launchIms(double2*, int, const int*, const int*, int, cudaStream_t);
 void setImsMode(int);
 cudaError_t launchSlabSwap(int, double2* const*, double2* const*, const uint64_t*, const uint64_t*, const int*, int,
@@ -685,6 +687,28 @@ void prepareJit(const Compiled& c, int device) {
 
 constexpr uint64_t kNoBasis = ~uint64_t(0);
 
+// QK_DENSE_MODE: 0 = DFMA, 1 = DMMA (FP64 tensor cores) for the U5 tile
+// kernel; unset = time both on a step's first executions, keep the faster.
+std::atomic<int>& denseModeVar() {
+    static std::atomic<int> v{[] {
+        const char* e = std::getenv("QK_DENSE_MODE");
+        return e ? std::atoi(e) : -1;
+    }()};
+    return v;
+}
+int denseMode() { return denseModeVar().load(); }
+
+int smCountOf(int device) {
+    static std::mutex mu;
+    static std::map<int, int> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(device);
+    if (it != cache.end()) return it->second;
+    int n = 148;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
+    return cache[device] = n;
+}
+
 // basis != kNoBasis: the first step is a pass that synthesizes |basis> (slice
 // index) instead of reading the slice (replaces initState's memset + store).
 void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_run_stats& rs,
@@ -753,6 +777,34 @@ void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_ru
         } else if (s.kind == qkeng::Step::DiagTable) {
             cuda(qkdev::launchDiagTable(st->amps, t.gtab + s.matOff, st->count, s.targets.data() + 1, s.k, st->stream),
                  "diag table");
+        } else if (s.k == 5 && st->nLocal >= 12) {
+            // U5 tile kernel, DFMA or DMMA: the first two executions time
+            // both (events, synchronous), later ones take the faster
+            int v = denseMode();
+            const bool timing = v < 0 && s.tune && s.tune->runs[s.tune->choice(2)] == 0;
+            if (v < 0) v = s.tune ? s.tune->choice(2) : 0;
+            cudaEvent_t e0 = nullptr, e1 = nullptr;
+            if (timing) {
+                cuda(cudaEventCreate(&e0), "event");
+                cuda(cudaEventCreate(&e1), "event");
+                cuda(cudaEventRecord(e0, st->stream), "event");
+            }
+            cuda(qkdev::launchDenseTile(st->amps, t.gtab + s.matOff, s.targets.data() + 1, s.k, st->nLocal, v,
+                                        smCountOf(st->device), st->stream),
+                 "dense U5 tile");
+            if (timing) {
+                float ms = 0;
+                cuda(cudaEventRecord(e1, st->stream), "event");
+                cuda(cudaEventSynchronize(e1), "event");
+                cudaEventElapsedTime(&ms, e0, e1);
+                cudaEventDestroy(e0);
+                cudaEventDestroy(e1);
+                s.tune->ms[v] = ms;
+                rs.tuning_runs++;
+                if (std::getenv("QK_DEBUG_TUNE"))
+                    std::fprintf(stderr, "dense U5 %s: %.3f ms\n", v ? "DMMA" : "DFMA", double(ms));
+            }
+            if (s.tune) s.tune->runs[v]++;
         } else {
             uint64_t mask = 0;
             for (size_t j = 1; j < s.targets.size(); j++) mask |= uint64_t(1) << s.targets[j];
@@ -1355,6 +1407,13 @@ int qk_ims_swap(qk_state* st, const int* outs, const int* ins, int s, int /*cach
         qk_run_stats rs{};
         runIms(st, std::vector<int>(outs, outs + s), std::vector<int>(ins, ins + s), rs);
         cuda(cudaStreamSynchronize(st->stream), "ims");
+    });
+}
+
+int qk_set_dense_mode(int mode) {
+    return guard([&] {
+        if (mode < -1 || mode > 1) throw ConfigError("dense mode must be -1, 0 or 1");
+        denseModeVar().store(mode);
     });
 }
 

@@ -1218,6 +1218,7 @@ std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::
         s.targets = targets;
         s.flopsPerAmp = flops;
         s.gates = 1;
+        if (s.k == 5) s.tune = std::make_shared<Step::Tune>();  // DFMA / DMMA tile kernels
         steps.push_back(std::move(s));
     };
 

@@ -248,3 +248,28 @@ def test_marginal_probabilities(qk):
         want = np.bincount(v, weights=p, minlength=1 << len(bits))
         assert np.max(np.abs(d.marginal(bits) - want)) < 1e-14
     d.close()
+
+
+@pytest.mark.parametrize("mode", [0, 1, -1])
+def test_u5_tile_kernel_vs_reference(ref, qk, mode):
+    # fused dense U5 (reference fusion_qbit = 5, engine.cpp:228-251) through
+    # the tile kernel: DFMA (0), DMMA FP64 tensor cores (1), autotuned (-1);
+    # targets on low, high and mixed bits, in every order (first = MSB)
+    n = 15
+    rng = np.random.default_rng(55 + mode)
+    cases = [[0, 1, 2, 3, 4], [14, 13, 12, 11, 10], [3, 9, 0, 14, 6], [7, 2, 12, 5, 1], [1, 0, 13, 4, 8]]
+    qk.set_dense_mode(mode)
+    try:
+        for tg in cases:
+            m = rng.standard_normal((32, 32)) + 1j * rng.standard_normal((32, 32))
+            q, _ = np.linalg.qr(m)
+            line = "U5 " + " ".join(map(str, tg)) + " " + " ".join(f"{v.real!r} {v.imag!r}" for v in q.reshape(-1))
+            st = np.random.default_rng(len(tg) + tg[0]).standard_normal(2 << n)
+            st /= np.linalg.norm(st)
+            want = st.copy()
+            ref.apply_block(want, n, [line], n, 4)
+            for _ in range(3):  # autotune: the first two runs time DFMA and DMMA
+                got = run_block(qk, st, n, [line], n)
+                assert np.max(np.abs(got - cx(want))) < TOL, (tg, mode)
+    finally:
+        qk.set_dense_mode(-1)
