@@ -135,7 +135,8 @@ int qk_ims_swap(qk_state* st, const int* outs, const int* ins, int s, int cache_
 int qk_set_ims_mode(int mode);
 /* Fused dense U5 kernel (A/B hook; default from QK_DENSE_MODE, else -1):
  * 0 = DFMA on the CUDA cores, 1 = DMMA (mma.sync.m8n8k4.f64, FP64 tensor
- * cores), -1 = time both on a step's first two executions, keep the faster. */
+ * cores), -1 = time both on a step's first two executions, keep the faster,
+ * 2 = the generic per-group kernel (k_dense_group, the round-1 path; A/B only). */
 int qk_set_dense_mode(int mode);
 /* distributed.cpp:124-138 xrsSwap over slices owned by THIS process (one
  * device, or several with peer access): in-place pairwise slab swap, no

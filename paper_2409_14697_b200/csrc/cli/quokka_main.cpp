@@ -4,8 +4,11 @@
 //   quokka_b200 optimize -i circuit [-o program] --config cfg.ini
 //   quokka_b200 optimize circuit chunk inrank total ims xrs fusion_qbit fusion
 //   quokka_b200 simulate -i cfg.ini -c program [--raw] [--dump-state] [--initial K]
+//   quokka_b200 validate circuit program [-i cfg.ini]
 //   quokka_b200 gen qft|qaoa|bv|gate|random|grover -n N [-o file] [-l L] [-g G]
 //                   [--seed S] [--secret X] [--kind K]
+//   quokka_b200 bench [-n N] [-g G] [--seed S] [--engine blockwise|gate_by_gate]
+//                     [--compare] [--repeats R] [--circuit random|qft|qaoa] [--threads T]
 //
 // Same outputs and exit codes as the reference: program / circuit text,
 // "qubits: / gates: / wall_time_s: / norm:" on stdout, "index re im" lines for
@@ -79,10 +82,24 @@ void writeText(const std::string& path, const std::string& text) {
     out << text;
 }
 
+// Base-10 parsing like the reference (std::stoi / CLI11's integral options).
 long long toInt(const std::string& s, const std::string& what) {
     try {
         size_t pos = 0;
-        const long long v = std::stoll(s, &pos, 0);
+        const long long v = std::stoll(s, &pos, 10);
+        if (pos != s.size()) throw std::invalid_argument(s);
+        return v;
+    } catch (...) {
+        throw ConfigError("bad numeric parameter '" + s + "' for " + what);
+    }
+}
+
+// uint64 options (--initial, --seed, --secret): the full unsigned range.
+std::uint64_t toU64(const std::string& s, const std::string& what) {
+    try {
+        size_t pos = 0;
+        if (!s.empty() && s[0] == '-') throw std::invalid_argument(s);
+        const unsigned long long v = std::stoull(s, &pos, 10);
         if (pos != s.size()) throw std::invalid_argument(s);
         return v;
     } catch (...) {
@@ -141,9 +158,9 @@ int runSimulate(const Args& a) {
     if (!a.opts.count("--config") || !a.opts.count("--circuit"))
         throw ConfigError("simulate needs -i <config> and -c <program>");
     const Config cfg = parseConfigFile(a.opts.at("--config"));
-    const Index initial = a.opts.count("--initial") ? Index(toInt(a.opts.at("--initial"), "--initial")) : 0;
+    const Index initial = a.opts.count("--initial") ? Index(toU64(a.opts.at("--initial"), "--initial")) : 0;
     const bool dump = a.opts.count("--dump-state") != 0;
-    if (dump && cfg.totalQubits > 20) throw ConfigError("state dumps are limited to 20 qubits");
+    const bool dumpable = dump && cfg.totalQubits <= 20;  // the limit is reported after the summary (main.cpp:151-152)
     size_t gates = 0;
     double wall = 0, norm = 0;
     StateVector state;
@@ -179,7 +196,7 @@ int runSimulate(const Args& a) {
             wall = seconds(t0, std::chrono::steady_clock::now());
             norm = dev.norm();
             layout = p.finalLayout;
-            if (dump) {
+            if (dumpable) {
                 state.nQubits = cfg.totalQubits;
                 state.amps.resize(size_t(1) << cfg.totalQubits);
                 dev.download(0, state.amps.size(), state.amps.data());
@@ -191,6 +208,7 @@ int runSimulate(const Args& a) {
     std::cout << "wall_time_s: " << fmt17(wall) << "\n";
     std::cout << "norm: " << fmt17(norm) << "\n";
     if (dump) {
+        if (!dumpable) throw ConfigError("state dumps are limited to 20 qubits");
         const StateVector logical = layoutApply(state, layout);
         for (Index i = 0; i < Index(logical.amps.size()); i++)
             std::cout << i << " " << fmt17(logical.amps[i].real()) << " " << fmt17(logical.amps[i].imag()) << "\n";
@@ -215,22 +233,108 @@ int runGen(const Args& a) {
     const std::string which = a.positional[0];
     const int n = int(toInt(a.opts.at("--qubits"), "-n"));
     auto opt = [&](const char* k, long long d) { return a.opts.count(k) ? toInt(a.opts.at(k), k) : d; };
-    const std::uint64_t seed = std::uint64_t(opt("--seed", 12345));
+    auto optU = [&](const char* k, std::uint64_t d) { return a.opts.count(k) ? toU64(a.opts.at(k), k) : d; };
+    const std::uint64_t seed = optU("--seed", 12345);
     Circuit c;
     if (which == "qft") c = genQft(n);
     else if (which == "qaoa") c = genQaoa(n, int(opt("--layers", 1)), seed);
-    else if (which == "bv") c = a.opts.count("--secret") ? genBv(n, std::uint64_t(opt("--secret", 0))) : genBvAllOnes(n);
+    else if (which == "bv") c = a.opts.count("--secret") ? genBv(n, optU("--secret", 0)) : genBvAllOnes(n);
     else if (which == "gate") c = genGateBench(kindFromName(a.opts.count("--kind") ? a.opts.at("--kind") : "H"), n);
     else if (which == "random") c = genRandom(n, int(opt("--gates", 100)), seed);
-    else if (which == "grover") c = genGrover(n, std::uint64_t(opt("--secret", 5)), int(opt("--layers", 0)));
+    else if (which == "grover") c = genGrover(n, optU("--secret", 5), int(opt("--layers", 0)));
     else throw ConfigError("unknown generator '" + which + "'");
     writeText(a.opts.count("--output") ? a.opts.at("--output") : "", serializeCircuit(c));
     std::cerr << "qubits: " << c.nQubits << " gates: " << c.gates.size() << "\n";
     return 0;
 }
 
+// validate <circuit> <program> [-i cfg.ini] (main.cpp:167-192): exit 4 and
+// "validation failed: ..." on stderr when the program is not a faithful
+// reordering of the raw circuit.
+int runValidate(const Args& a) {
+    if (a.positional.size() != 2) throw ConfigError("validate needs <circuit> <program>");
+    Config cfg;
+    Circuit raw;
+    Program p;
+    if (a.opts.count("--config")) {
+        cfg = parseConfigFile(a.opts.at("--config"));
+        raw = parseCircuitFile(a.positional[0], cfg.totalQubits);
+        p = parseProgramFile(a.positional[1], cfg);
+    } else {
+        raw = parseCircuitFile(a.positional[0]);
+        cfg.totalQubits = raw.nQubits;
+        cfg.rankQubits = 0;
+        cfg.chunkQubits = raw.nQubits;
+        cfg.cacheLineQubits = 0;
+        cfg.fusionQubits = raw.nQubits;
+        cfg.bufferQubits = raw.nQubits;
+        p = parseProgramFile(a.positional[1], cfg, /*lenient=*/true);
+    }
+    const OrderReport rep = validateOrder(raw, p);
+    if (!rep.ok) {
+        std::cerr << "validation failed: " << rep.message << "\n";
+        return 4;
+    }
+    std::cout << "Passed all circuit order validations\n";
+    return 0;
+}
+
+// bench (main.cpp:236-286): the same CSV schema, median of --repeats timed
+// runs per engine; "blockwise" = simulateProgram of the unfused Program,
+// "gate_by_gate" = simulateGateByGate, both on the device here.
+int runBench(const Args& a) {
+    auto opt = [&](const char* k, long long d) { return a.opts.count(k) ? toInt(a.opts.at(k), k) : d; };
+    const int n = int(opt("--qubits", 24)), ngates = int(opt("--gates", 200)), repeats = int(opt("--repeats", 10));
+    const std::uint64_t seed = a.opts.count("--seed") ? toU64(a.opts.at("--seed"), "--seed") : 12345;
+    const std::string circuit = a.opts.count("--circuit") ? a.opts.at("--circuit") : "random";
+    Circuit c;
+    if (circuit == "random") c = genRandom(n, ngates, seed);
+    else if (circuit == "qft") c = genQft(n);
+    else if (circuit == "qaoa") c = genQaoa(n, 1, seed);
+    else throw ConfigError("unknown bench circuit '" + circuit + "'");
+    Config cfg;
+    cfg.totalQubits = n;
+    cfg.rankQubits = 0;
+    cfg.fusionEnabled = false;
+    cfg.diagonalFusionEnabled = false;
+    cfg.finalize();
+    std::vector<std::string> engines;
+    if (a.opts.count("--compare")) engines = {"blockwise", "gate_by_gate"};
+    else engines = {a.opts.count("--engine") ? a.opts.at("--engine") : "blockwise"};
+    std::cout << "name,n_qubits,ranks,gates,engine,wall_time_s,time_per_gate_s\n";
+    double blockTime = 0.0, rawTime = 0.0;
+    for (const std::string& eng : engines) {
+        std::vector<double> times;
+        if (eng == "blockwise") {
+            const Program p = aioOptimize(c, cfg);
+            for (int r = 0; r < repeats; r++) {
+                const auto t0 = std::chrono::steady_clock::now();
+                SimResult res = simulateProgram(p, cfg, 0, 0);
+                times.push_back(seconds(t0, std::chrono::steady_clock::now()));
+            }
+        } else if (eng == "gate_by_gate") {
+            for (int r = 0; r < repeats; r++) {
+                const auto t0 = std::chrono::steady_clock::now();
+                StateVector res = simulateGateByGate(c, 0, 0);
+                times.push_back(seconds(t0, std::chrono::steady_clock::now()));
+            }
+        } else {
+            throw ConfigError("unknown engine '" + eng + "' (blockwise, gate_by_gate)");
+        }
+        std::sort(times.begin(), times.end());
+        const size_t m = times.size() / 2;
+        const double med = times.empty() ? 0.0 : times.size() % 2 ? times[m] : 0.5 * (times[m - 1] + times[m]);
+        (eng == "blockwise" ? blockTime : rawTime) = med;
+        std::cout << circuit << "," << n << ",1," << c.gates.size() << "," << eng << "," << fmt17(med) << ","
+                  << fmt17(med / double(c.gates.size())) << "\n";
+    }
+    if (engines.size() == 2 && blockTime > 0.0) std::cerr << "speedup: " << fmt17(rawTime / blockTime) << "\n";
+    return 0;
+}
+
 int usage() {
-    std::cerr << "usage: quokka_b200 optimize|simulate|gen ... (see the header of csrc/cli/quokka_main.cpp)\n";
+    std::cerr << "usage: quokka_b200 optimize|simulate|validate|gen|bench ... (see the header of "
+                 "csrc/cli/quokka_main.cpp)\n";
     return 2;
 }
 
@@ -252,6 +356,15 @@ int main(int argc, char** argv) {
                                           {"--dump-state", "--dump-state"}, {"--initial", "--initial"},
                                           {"--threads", "--threads"}},
                                          {"--raw", "--dump-state"}));
+        if (cmd == "validate")
+            return runValidate(parseArgs(argc, argv, 2, {{"-i", "--config"}, {"--config", "--config"}}, {}));
+        if (cmd == "bench")
+            return runBench(parseArgs(argc, argv, 2,
+                                      {{"-n", "--qubits"}, {"--qubits", "--qubits"}, {"-g", "--gates"},
+                                       {"--gates", "--gates"}, {"--seed", "--seed"}, {"--engine", "--engine"},
+                                       {"--compare", "--compare"}, {"--repeats", "--repeats"},
+                                       {"--circuit", "--circuit"}, {"--threads", "--threads"}},
+                                      {"--compare"}));
         if (cmd == "gen")
             return runGen(parseArgs(argc, argv, 2,
                                     {{"-n", "--qubits"}, {"--qubits", "--qubits"}, {"-o", "--output"},

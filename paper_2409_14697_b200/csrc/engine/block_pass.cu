@@ -599,14 +599,16 @@ __global__ void k_dense_group(double2* __restrict__ state, const double2* __rest
 
 // ---- launchers --------------------------------------------------------------
 
-// CT <= 12: 16 amplitudes per thread, two CTAs per SM at CT = 12 (128 KiB of
-// smem, 128 registers); CT = 13: RB = 5 (256 threads x 255 registers, one CTA
-// per SM), RB = 4 (512 threads x 128 registers) or RB = 3 (1024 threads).
-template <int CT, int RB = (CT < 4 ? CT : 4)>
+// The interpreter runs tiles of <= 2^12 amplitudes, 8 per thread (RB = 3):
+// 512 threads and 128 registers at CT = 12, two CTAs per SM below.  Its
+// register budget then holds the amplitudes, pending phases and op operands
+// without spilling (the specialized kernels, not this one, serve slices
+// >= 2^22).
+template <int CT, int RB = (CT < 3 ? CT : 3)>
 static cudaError_t launchCT(double2* state, const double2* gtab, const PassParams& P, uint64_t ctas,
                             uint64_t basis, cudaStream_t stream) {
     constexpr int NT = 1 << (CT - RB);
-    constexpr int MINB = (CT == 12 && RB == 4) ? 2 : 1;
+    constexpr int MINB = CT <= 11 ? 2 : 1;
     const size_t smem = (sizeof(double2) << CT) + sizeof(double2) * kMaxCtaFactors;
     if (smem > 48 * 1024) {  // per-device attribute; cheap to re-apply
         cudaError_t e = cudaFuncSetAttribute(k_block_pass<CT, RB, MINB>,
@@ -619,11 +621,9 @@ static cudaError_t launchCT(double2* state, const double2* gtab, const PassParam
 
 cudaError_t launchBlockPass(double2* state, const double2* gtab, const PassParams& P, int nLocal, uint64_t basis,
                             cudaStream_t stream) {
-    if (P.rb != regBitsFor(P.ct) && !(P.ct == 13 && P.rb >= 3 && P.rb <= 5)) return cudaErrorInvalidValue;
+    if (P.rb != (P.ct < 3 ? P.ct : 3))
+        return cudaErrorInvalidValue;  // compiled for the specialized kernels (compileBlock interp = false)
     const uint64_t ctas = uint64_t(1) << (nLocal - P.ct);
-    if (P.ct == 13) return P.rb == 5   ? launchCT<13, 5>(state, gtab, P, ctas, basis, stream)
-                           : P.rb == 4 ? launchCT<13, 4>(state, gtab, P, ctas, basis, stream)
-                                       : launchCT<13, 3>(state, gtab, P, ctas, basis, stream);
     switch (P.ct) {
         case 4: return launchCT<4>(state, gtab, P, ctas, basis, stream);
         case 5: return launchCT<5>(state, gtab, P, ctas, basis, stream);
@@ -634,7 +634,7 @@ cudaError_t launchBlockPass(double2* state, const double2* gtab, const PassParam
         case 10: return launchCT<10>(state, gtab, P, ctas, basis, stream);
         case 11: return launchCT<11>(state, gtab, P, ctas, basis, stream);
         case 12: return launchCT<12>(state, gtab, P, ctas, basis, stream);
-        default: return cudaErrorInvalidValue;
+        default: return cudaErrorInvalidValue;  // interpreter tiles are <= 2^12 (compileBlock interp)
     }
 }
 

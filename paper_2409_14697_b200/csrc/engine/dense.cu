@@ -13,7 +13,7 @@
 //           its 32 outputs with DFMA, M broadcast from shared memory;
 //   MMA  -- the tile as a real GEMM on the FP64 tensor cores (DMMA,
 //           mma.sync.m8n8k4.f64): Y(64x128) = A(64x64) X(64x128) with
-//           A = [[Mr, -Mi], [Mi, Mr]] staged in shared memory in fragment order.
+//           A = [[Mr, -Mi], [Mi, Mr]] in register fragments.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -21,15 +21,21 @@ namespace qkdev {
 
 namespace {
 
-constexpr int kDk = 5;                       // target bits
-constexpr int kDct = 12;                     // tile bits
-constexpr int kDgroups = 1 << (kDct - kDk);  // 128 groups per tile
-constexpr int kDstride = kDgroups + 8;       // plane row stride (doubles): rows 16 banks apart
-constexpr int kDplane = 32 * kDstride;
+constexpr int kDk = 5;      // target bits
+constexpr int kDctMax = 12;  // tile bits: 12 (DFMA, 128 groups), 11 (DMMA, 64 groups)
+// Plane row stride (doubles).  DFMA (128 groups): +8, rows 16 banks apart.
+// DMMA (64 groups): +4, rows 8 banks apart, so each half-warp of a B-fragment
+// load (4 k-rows x 4 columns of doubles) hits 16 distinct bank pairs.
+template <int CT>
+struct TileShape {
+    static constexpr int groups = 1 << (CT - kDk);
+    static constexpr int stride = groups + (CT == 11 ? 4 : 8);
+    static constexpr int plane = 32 * stride;
+};
 
 struct DenseSpec {
-    int tbit[kDct];      // tile index bit j -> memory bit
-    int vslot[kDct];     // tile index bit j -> plane offset contribution (s row or g column)
+    int tbit[kDctMax];   // tile index bit j -> memory bit
+    int vslot[kDctMax];  // tile index bit j -> plane offset contribution (s row or g column)
     int nfree;           // memory bits outside the tile (ascending)
     int fbit[40];
 };
@@ -57,14 +63,21 @@ __device__ __forceinline__ double blockA(const double2* __restrict__ M, int i, i
 
 // FMA: 128 threads, one group each (its 32 inputs in registers, outputs
 // written back into its own plane column: no other thread reads it), two
-// CTAs per SM.  MMA: 256 threads, 8 warps each owning a 16 x 64 block of Y.
+// CTAs per SM.  MMA: 2^11-amplitude tiles (64 groups), 256 threads, 8 warps
+// each owning an 8 x 64 block of Y, three CTAs per SM (80 registers, 34 KiB
+// of planes + 32 KiB of A fragments each) so some CTAs' loads and stores
+// overlap the others' tensor-core work.
 template <bool MMA>
-__global__ void __launch_bounds__(MMA ? 256 : 128, 2) k_dense_tile(double2* __restrict__ st, const double2* __restrict__ M,
+__global__ void __launch_bounds__(MMA ? 256 : 128, MMA ? 3 : 2) k_dense_tile(double2* __restrict__ st, const double2* __restrict__ M,
                                                                   const __grid_constant__ DenseSpec sp, uint64_t ntiles) {
+    constexpr int CT = MMA ? 11 : 12;
+    constexpr int kDstride = TileShape<CT>::stride;
+    constexpr int kDplane = TileShape<CT>::plane;
+    constexpr int kDgroups = TileShape<CT>::groups;
     constexpr int LOGNT = MMA ? 8 : 7;
     constexpr int NT = 1 << LOGNT;
-    constexpr int PER = (1 << kDct) / NT;  // amplitudes per thread in the load / store phases
-    constexpr int HI = kDct - LOGNT;
+    constexpr int PER = (1 << CT) / NT;  // amplitudes per thread in the load / store phases
+    constexpr int HI = CT - LOGNT;
     extern __shared__ double smd[];
     double* const Xr = smd;
     double* const Xi = smd + kDplane;
@@ -80,12 +93,12 @@ __global__ void __launch_bounds__(MMA ? 256 : 128, 2) k_dense_tile(double2* __re
             slotLo += sp.vslot[j];
         }
 
-    // MMA: A = [[Mr, -Mi], [Mi, Mr]] (64 x 64) in shared memory, stored in
-    // fragment order: As[(rowTile * 16 + kk) * 32 + lane] is lane's element
-    // of the A fragment for rows 8 rowTile.., k-step kk (conflict-free loads).
-    // FMA: M itself, read as warp-wide broadcasts.
-    double* const As = smd + 2 * kDplane;
+    // MMA: A = [[Mr, -Mi], [Mi, Mr]] (64 x 64) in shared memory in fragment
+    // order, As[(rowTile * 16 + kk) * 32 + lane] = lane's A element for the
+    // 8-row tile rowTile at k-step kk (one conflict-free LDS per k-step).
+    // FMA: M itself in shared memory, read as warp-wide broadcasts.
     double2* const Ms = reinterpret_cast<double2*>(smd + 2 * kDplane);
+    double* const As = smd + 2 * kDplane;
     if (MMA) {
         for (int e = tid; e < 8 * 16 * 32; e += NT) {
             const int l = e & 31, kk = (e >> 5) & 15, rt = e >> 9;
@@ -107,7 +120,7 @@ __global__ void __launch_bounds__(MMA ? 256 : 128, 2) k_dense_tile(double2* __re
         for (int j = 0; j < sp.nfree; j++) base |= ((tile >> j) & 1) << sp.fbit[j];
         __syncthreads();  // the previous tile's stores read the planes
         base |= depLo;
-#pragma unroll
+#pragma unroll 1
         for (int b8 = 0; b8 < PER; b8 += 8) {  // 8 loads in flight per thread per batch
             double2 v[8];
 #pragma unroll
@@ -137,66 +150,63 @@ __global__ void __launch_bounds__(MMA ? 256 : 128, 2) k_dense_tile(double2* __re
 #pragma unroll
             for (int s = 0; s < 32; s++) x[s] = make_double2(Xr[s * kDstride + g], Xi[s * kDstride + g]);
 #pragma unroll 1
-            for (int r0 = 0; r0 < 32; r0 += 4) {
-                double2 acc[4];
+            for (int r0 = 0; r0 < 32; r0 += 8) {  // 8 rows: 16 independent FMA chains per thread
+                double2 acc[8];
 #pragma unroll
-                for (int q = 0; q < 4; q++) acc[q] = make_double2(0.0, 0.0);
+                for (int q = 0; q < 8; q++) acc[q] = make_double2(0.0, 0.0);
 #pragma unroll
                 for (int s = 0; s < 32; s++)
 #pragma unroll
-                    for (int q = 0; q < 4; q++) acc[q] = cmacD(acc[q], Ms[(r0 + q) * 32 + s], x[s]);
+                    for (int q = 0; q < 8; q++) acc[q] = cmacD(acc[q], Ms[(r0 + q) * 32 + s], x[s]);
 #pragma unroll
-                for (int q = 0; q < 4; q++) {
+                for (int q = 0; q < 8; q++) {
                     Xr[(r0 + q) * kDstride + g] = acc[q].x;
                     Xi[(r0 + q) * kDstride + g] = acc[q].y;
                 }
             }
         } else {
-            const int rp = w & 3, ch = w >> 2;
-            double acc[2][8][2];
+            constexpr int CTILES = kDgroups / 8;  // 8 column tiles of Y per warp
+            double acc[CTILES][2];
 #pragma unroll
-            for (int rt = 0; rt < 2; rt++)
-#pragma unroll
-                for (int c = 0; c < 8; c++) acc[rt][c][0] = acc[rt][c][1] = 0.0;
-#pragma unroll
+            for (int c = 0; c < CTILES; c++) acc[c][0] = acc[c][1] = 0.0;
+#pragma unroll 1
             for (int kk = 0; kk < 16; kk++) {
                 const int k = 4 * kk + (lane & 3);
-                const double* const plane = k < 32 ? Xr : Xi;
-                double b[8];
+                const double afr = As[(w * 16 + kk) * 32 + lane];
+                const double* const row = (k < 32 ? Xr : Xi) + (k & 31) * kDstride + (lane >> 2);
+                double b[CTILES];
 #pragma unroll
-                for (int c = 0; c < 8; c++) b[c] = plane[(k & 31) * kDstride + 8 * (8 * ch + c) + (lane >> 2)];
-                const double a0 = As[((2 * rp) * 16 + kk) * 32 + lane];
-                const double a1 = As[((2 * rp + 1) * 16 + kk) * 32 + lane];
+                for (int c = 0; c < CTILES; c++) b[c] = row[8 * c];
 #pragma unroll
-                for (int c = 0; c < 8; c++) dmma(acc[0][c][0], acc[0][c][1], a0, b[c]);
-#pragma unroll
-                for (int c = 0; c < 8; c++) dmma(acc[1][c][0], acc[1][c][1], a1, b[c]);
+                for (int c = 0; c < CTILES; c++) dmma(acc[c][0], acc[c][1], afr, b[c]);
             }
             __syncthreads();  // every warp has read X before Y overwrites it
+            {
+                const int i = 8 * w + (lane >> 2);
+                double* const plane = (i < 32 ? Xr : Xi) + (i & 31) * kDstride + 2 * (lane & 3);
 #pragma unroll
-            for (int rt = 0; rt < 2; rt++) {
-                const int i = 8 * (2 * rp + rt) + (lane >> 2);
-                double* const plane = i < 32 ? Xr : Xi;
-#pragma unroll
-                for (int c = 0; c < 8; c++) {
-                    const int col = 8 * (8 * ch + c) + 2 * (lane & 3);
-                    plane[(i & 31) * kDstride + col] = acc[rt][c][0];
-                    plane[(i & 31) * kDstride + col + 1] = acc[rt][c][1];
+                for (int c = 0; c < CTILES; c++) {
+                    plane[8 * c] = acc[c][0];
+                    plane[8 * c + 1] = acc[c][1];
                 }
             }
         }
         __syncthreads();
+#pragma unroll 1
+        for (int b8 = 0; b8 < PER; b8 += 8) {  // batches of 8 stores (bounded register use)
 #pragma unroll
-        for (int i = 0; i < PER; i++) {
-            uint64_t a = base;
-            int slot = slotLo;
+            for (int i = 0; i < 8; i++) {
+                const int ii = b8 + i;
+                uint64_t a = base;
+                int slot = slotLo;
 #pragma unroll
-            for (int j = 0; j < HI; j++)
-                if ((i >> j) & 1) {
-                    a |= depHi[j];
-                    slot += slotHi[j];
-                }
-            __stcs(st + a, make_double2(Xr[slot], Xi[slot]));
+                for (int j = 0; j < HI; j++)
+                    if ((ii >> j) & 1) {
+                        a |= depHi[j];
+                        slot += slotHi[j];
+                    }
+                __stcs(st + a, make_double2(Xr[slot], Xi[slot]));
+            }
         }
     }
 }
@@ -207,7 +217,10 @@ __global__ void __launch_bounds__(MMA ? 256 : 128, 2) k_dense_tile(double2* __re
 // sub-index bit (4 - j).  mode 0 = DFMA, 1 = DMMA.
 cudaError_t launchDenseTile(double2* state, const double2* M, const int* targets, int k, int nLocal, int mode,
                             int smCount, cudaStream_t stream) {
+    const int kDct = mode ? 11 : 12;
     if (k != kDk || nLocal < kDct) return cudaErrorInvalidValue;
+    const int kDstride = mode ? TileShape<11>::stride : TileShape<12>::stride;
+    const int kDplane = 32 * kDstride;
     DenseSpec sp{};
     uint64_t tmask = 0;
     for (int j = 0; j < k; j++) tmask |= uint64_t(1) << targets[j];
@@ -228,13 +241,13 @@ cudaError_t launchDenseTile(double2* state, const double2* M, const int* targets
     }
     const uint64_t ntiles = uint64_t(1) << (nLocal - kDct);
     const size_t smem = sizeof(double) * 2 * kDplane + (mode ? sizeof(double) * 64 * 64 : sizeof(double2) * 32 * 32);
-    const uint64_t resident = uint64_t(smCount) * 2;
+    const uint64_t resident = uint64_t(smCount) * (mode ? 3 : 2);
     const unsigned grid = unsigned(ntiles < resident ? ntiles : resident);
     cudaError_t e;
     if (mode) {
         e = cudaFuncSetAttribute(k_dense_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         if (e != cudaSuccess) return e;
-        k_dense_tile<true><<<grid, 256, smem, stream>>>(state, M, sp, ntiles);  // 8 warps x (16 rows x 64 groups)
+        k_dense_tile<true><<<grid, 256, smem, stream>>>(state, M, sp, ntiles);  // 8 warps x (8 rows x 64 groups)
     } else {
         e = cudaFuncSetAttribute(k_dense_tile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         if (e != cudaSuccess) return e;

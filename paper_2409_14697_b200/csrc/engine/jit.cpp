@@ -11,10 +11,13 @@
 #include "jit.h"
 
 #include <dlfcn.h>
+#include <sys/stat.h>
+#include <unistd.h>
 #include <nvrtc.h>
 
 #include <algorithm>
 #include <atomic>
+#include <cerrno>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -865,25 +868,86 @@ std::string kernelName(uint64_t h) {
     return buf;
 }
 
-std::string cacheDir() {
-    const char* d = std::getenv("QK_JIT_CACHE");
-    return d ? d : "/tmp/qk_jit_cache";
+// On-disk cubin cache.  Directory: QK_JIT_CACHE, else $XDG_CACHE_HOME/qk_jit,
+// else $HOME/.cache/qk_jit, else /tmp/qk_jit_cache_<uid>; created 0700 and
+// used only if this user owns it and nobody else can write it.  Each file
+// carries a header (magic, NVRTC version, target arch, hash of the generated
+// source, length and FNV-1a checksum of the cubin) that must match before the
+// cubin is loaded; anything else is recompiled.  Files are written to a temp
+// name and renamed into place only after a complete, checked write.
+uint64_t fnv1a(const char* p, size_t n) {
+    uint64_t h = 1469598103934665603ull;
+    for (size_t i = 0; i < n; i++) h = (h ^ uint64_t(uint8_t(p[i]))) * 1099511628211ull;
+    return h;
 }
 
-std::vector<char> cubinFor(const PassParams& P, uint64_t h) {
-    const std::string path = cacheDir() + "/" + kernelName(h) + ".cubin";
-    {
-        std::ifstream in(path, std::ios::binary);
-        if (in) return std::vector<char>((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+struct CacheHeader {
+    char magic[8];        // "QKJIT02\0"
+    int32_t nvrtcMajor, nvrtcMinor;
+    char arch[16];        // "sm_100a"
+    uint64_t sourceHash;  // FNV-1a of the generated CUDA source
+    uint64_t size;        // cubin bytes
+    uint64_t checksum;    // FNV-1a of the cubin
+};
+
+bool makePrivateDir(const std::string& dir) {
+    std::string cur;
+    for (size_t i = 0; i <= dir.size(); i++) {
+        if (i < dir.size() && dir[i] != '/') continue;
+        cur = dir.substr(0, i);
+        if (cur.empty()) continue;
+        if (mkdir(cur.c_str(), 0700) != 0 && errno != EEXIST) return false;
     }
-    std::vector<char> bin = compileToCubin(generatePassSource(P, kernelName(h)), kernelName(h));
-    std::string mk = "mkdir -p '" + cacheDir() + "'";
-    if (std::system(mk.c_str()) == 0) {
-        const std::string tmp = path + ".tmp" + std::to_string(reinterpret_cast<uintptr_t>(&bin));
-        std::ofstream out(tmp, std::ios::binary);
-        out.write(bin.data(), std::streamsize(bin.size()));
-        out.close();
-        std::rename(tmp.c_str(), path.c_str());
+    struct stat sb;
+    if (stat(dir.c_str(), &sb) != 0 || !S_ISDIR(sb.st_mode)) return false;
+    return sb.st_uid == getuid() && (sb.st_mode & (S_IWGRP | S_IWOTH)) == 0;
+}
+
+const std::string& cacheDir() {  // "" = no disk cache
+    static const std::string dir = [] {
+        std::string d;
+        if (const char* e = std::getenv("QK_JIT_CACHE")) d = e;
+        else if (const char* x = std::getenv("XDG_CACHE_HOME")) d = std::string(x) + "/qk_jit";
+        else if (const char* h = std::getenv("HOME")) d = std::string(h) + "/.cache/qk_jit";
+        else d = "/tmp/qk_jit_cache_" + std::to_string(getuid());
+        return makePrivateDir(d) ? d : std::string();
+    }();
+    return dir;
+}
+
+CacheHeader headerFor(const std::string& src, const std::vector<char>& bin);
+
+std::vector<char> cubinFor(const PassParams& P, uint64_t h) {
+    const std::string src = generatePassSource(P, kernelName(h));
+    const std::string& dir = cacheDir();
+    const std::string path = dir.empty() ? std::string() : dir + "/" + kernelName(h) + ".cubin";
+    if (!path.empty()) {
+        std::ifstream in(path, std::ios::binary);
+        CacheHeader hd{};
+        if (in && in.read(reinterpret_cast<char*>(&hd), sizeof hd)) {
+            std::vector<char> bin(hd.size < (uint64_t(1) << 30) ? size_t(hd.size) : 0);
+            const CacheHeader want = headerFor(src, bin);
+            if (!bin.empty() && in.read(bin.data(), std::streamsize(bin.size())) &&
+                std::memcmp(hd.magic, want.magic, sizeof hd.magic) == 0 && hd.nvrtcMajor == want.nvrtcMajor &&
+                hd.nvrtcMinor == want.nvrtcMinor && std::memcmp(hd.arch, want.arch, sizeof hd.arch) == 0 &&
+                hd.sourceHash == want.sourceHash && hd.checksum == fnv1a(bin.data(), bin.size()))
+                return bin;
+        }
+    }
+    std::vector<char> bin = compileToCubin(src, kernelName(h));
+    if (!path.empty()) {
+        const CacheHeader hd = headerFor(src, bin);
+        const std::string tmp = path + ".tmp" + std::to_string(getpid()) + "_" +
+                                std::to_string(reinterpret_cast<uintptr_t>(&bin));
+        bool ok;
+        {
+            std::ofstream out(tmp, std::ios::binary | std::ios::trunc);
+            out.write(reinterpret_cast<const char*>(&hd), sizeof hd);
+            out.write(bin.data(), std::streamsize(bin.size()));
+            out.close();
+            ok = bool(out);
+        }
+        if (!ok || std::rename(tmp.c_str(), path.c_str()) != 0) std::remove(tmp.c_str());
     }
     return bin;
 }
@@ -953,6 +1017,18 @@ struct Nvrtc {
 Nvrtc& nvrtc() {
     static Nvrtc n;
     return n;
+}
+
+CacheHeader headerFor(const std::string& src, const std::vector<char>& bin) {
+    CacheHeader h{};
+    std::memcpy(h.magic, "QKJIT02", 8);
+    h.nvrtcMajor = nvrtc().major;
+    h.nvrtcMinor = nvrtc().minor;
+    std::snprintf(h.arch, sizeof h.arch, "%s", "sm_100a");
+    h.sourceHash = fnv1a(src.data(), src.size());
+    h.size = bin.size();
+    h.checksum = fnv1a(bin.data(), bin.size());
+    return h;
 }
 }  // namespace
 

@@ -266,9 +266,11 @@ struct qk_state {
     cudaStream_t stream = nullptr;
     double* normScratch = nullptr;
     double* normOut = nullptr;
-    double2* recvBuf = nullptr;
+    double2* recvBuf = nullptr;   // two halves of bufAmps / 2: round k receives into half k % 2
     double2* packBuf = nullptr;
     uint64_t bufAmps = 0;
+    cudaStream_t aux = nullptr;   // NCCL XRS: copy-back of round k overlaps the transfer of round k + 1
+    cudaEvent_t xrsDone[2] = {nullptr, nullptr}, unpackDone[2] = {nullptr, nullptr};
     ncclComm_t comm = nullptr;
     qkipc::Group* ipc = nullptr;  // peer-memory rank group (qk_ipc_init)
     bool profiling = false;
@@ -411,7 +413,8 @@ size_t sweeps(const Compiled& c) {
 
 // One compilation of p's items for a slice of 2^nLocal amplitudes, starting
 // from memory layout mem0 (program position p at memory bit mem0[p]).
-std::shared_ptr<Compiled> compileLayout(qk_program* p, int nLocal, const std::vector<int>& mem0, bool synthFirst) {
+std::shared_ptr<Compiled> compileLayout(qk_program* p, int nLocal, const std::vector<int>& mem0, bool synthFirst,
+                                        bool interp) {
     auto c = std::make_shared<Compiled>();
     c->nLocal = nLocal;
     // Lazy in-memory swaps: an SQS (and a SWAP gate) only relabels which
@@ -434,11 +437,12 @@ std::shared_ptr<Compiled> compileLayout(qk_program* p, int nLocal, const std::ve
             // route the data toward the program's physical order (mem = identity)
             std::vector<int> dest(static_cast<size_t>(nLocal)), moved;
             for (int q = 0; q < nLocal; q++) dest[size_t(mem[size_t(q)])] = q;
-            ci.steps = qkeng::compileBlock(stream, nLocal, c->gtab, &dest, &moved, tileBits, synthFirst && c->items.empty());
+            ci.steps = qkeng::compileBlock(stream, nLocal, c->gtab, &dest, &moved, tileBits, synthFirst && c->items.empty(),
+                                           interp);
             for (int q = 0; q < nLocal; q++) mem[size_t(q)] = moved[size_t(mem[size_t(q)])];
         } else {
             ci.steps = qkeng::compileBlock(stream, nLocal, c->gtab, nullptr, nullptr, tileBits,
-                                           synthFirst && c->items.empty());
+                                           synthFirst && c->items.empty(), interp);
         }
         for (qkeng::Step& s : ci.steps) {
             ci.flopsPerAmp += s.flopsPerAmp;
@@ -469,7 +473,7 @@ std::shared_ptr<Compiled> compileLayout(qk_program* p, int nLocal, const std::ve
         const std::vector<int> mem0 = mem;
         flushStream(true);
         materialize();
-        if (lazy && !stream.empty() && qkdev::tileTune() && useJit(nLocal) && nLocal > 13) {
+        if (lazy && !stream.empty() && qkdev::tileTune() && !interp && nLocal > 13) {
             const size_t last = c->items.size();
             std::vector<CompiledItem> a(std::make_move_iterator(c->items.begin() + long(first)),
                                         std::make_move_iterator(c->items.end()));
@@ -556,9 +560,13 @@ std::shared_ptr<Compiled> compileLayout(qk_program* p, int nLocal, const std::ve
 // SQS / SWAP relabels carry to the program's physical order, so that stream
 // ends with nothing to materialize (no IMS pass).  Runs on an existing state
 // (qk_apply_block) start from the identity layout.
-std::shared_ptr<Compiled> compileFor(qk_program* p, int nLocal, bool fromBasis = true) {
+// jit: schedule for the specialized kernels (1), the interpreter (0), or
+// whichever runs a 2^nLocal slice (-1).  The two get different schedules
+// (interpreter: rb = 3, tiles <= 2^12).
+std::shared_ptr<Compiled> compileFor(qk_program* p, int nLocal, bool fromBasis = true, int jit = -1) {
     std::lock_guard<std::mutex> lk(p->mu);
-    const int slot = fromBasis ? nLocal : -1 - nLocal;
+    const bool interp = jit < 0 ? !useJit(nLocal) : jit == 0;
+    const int slot = (fromBasis ? nLocal : -1 - nLocal) * 2 + (interp ? 1 : 0);
     auto it = p->compiled.find(slot);
     if (it != p->compiled.end()) return it->second;
     const std::string key = scheduleKey(p->prog, slot);
@@ -570,7 +578,7 @@ std::shared_ptr<Compiled> compileFor(qk_program* p, int nLocal, bool fromBasis =
     }
     std::vector<int> ident(static_cast<size_t>(nLocal));
     for (int b = 0; b < nLocal; b++) ident[size_t(b)] = b;
-    std::shared_ptr<Compiled> c = compileLayout(p, nLocal, ident, fromBasis);
+    std::shared_ptr<Compiled> c = compileLayout(p, nLocal, ident, fromBasis, interp);
     if (lazyIms() && fromBasis && basisLayout()) {
         // sim = the first stream's relabels applied to the identity; starting
         // from its inverse, mem is the identity when that stream ends.  The
@@ -588,7 +596,7 @@ std::shared_ptr<Compiled> compileFor(qk_program* p, int nLocal, bool fromBasis =
         }
         for (int q = 0; q < nLocal; q++) mem0[size_t(sim[size_t(q)])] = q;
         if (mem0 != ident) {
-            std::shared_ptr<Compiled> b = compileLayout(p, nLocal, mem0, fromBasis);
+            std::shared_ptr<Compiled> b = compileLayout(p, nLocal, mem0, fromBasis, interp);
             if (sweeps(*b) <= sweeps(*c)) c = b;
         }
     }
@@ -687,6 +695,14 @@ void prepareJit(const Compiled& c, int device) {
 
 constexpr uint64_t kNoBasis = ~uint64_t(0);
 
+// Autotune state (Step::Tune, ChoiceTune) lives in schedules shared through
+// the process-wide cache; one host thread per GPU may run the same schedule
+// concurrently, so every read-modify-write of it holds this lock.
+std::mutex& tuneMu() {
+    static std::mutex m;
+    return m;
+}
+
 // QK_DENSE_MODE: 0 = DFMA, 1 = DMMA (FP64 tensor cores) for the U5 tile
 // kernel; unset = time both on a step's first executions, keep the faster.
 std::atomic<int>& denseModeVar() {
@@ -720,9 +736,14 @@ void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_ru
             // Register-width autotune: the first two executions of a pass time
             // each variant (events, synchronous); later ones take the faster.
             const int nv = 1 + int(s.alts.size());
-            const int v = s.tune ? s.tune->choice(nv) : 0;
+            int v = 0;
+            bool timing = false;
+            if (s.tune) {
+                std::lock_guard<std::mutex> lk(tuneMu());
+                v = s.tune->choice(nv);
+                timing = s.tune->runs[v] == 0;
+            }
             const qkdev::PassParams& P = v ? *s.alts[size_t(v - 1)] : *s.pass;
-            const bool timing = s.tune && s.tune->runs[v] == 0;
             cudaEvent_t e0 = nullptr, e1 = nullptr;
             if (timing) {
                 cuda(cudaEventCreate(&e0), "event");
@@ -762,10 +783,12 @@ void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_ru
                 cudaEventElapsedTime(&ms, e0, e1);
                 cudaEventDestroy(e0);
                 cudaEventDestroy(e1);
+                std::lock_guard<std::mutex> lk(tuneMu());
                 s.tune->ms[v] = ms;
                 s.tune->runs[v]++;
                 rs.tuning_runs++;
             } else if (s.tune) {
+                std::lock_guard<std::mutex> lk(tuneMu());
                 s.tune->runs[v]++;
             }
             if (fusedNorm) {
@@ -777,12 +800,16 @@ void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_ru
         } else if (s.kind == qkeng::Step::DiagTable) {
             cuda(qkdev::launchDiagTable(st->amps, t.gtab + s.matOff, st->count, s.targets.data() + 1, s.k, st->stream),
                  "diag table");
-        } else if (s.k == 5 && st->nLocal >= 12) {
+        } else if (s.k == 5 && st->nLocal >= 12 && denseMode() != 2) {
             // U5 tile kernel, DFMA or DMMA: the first two executions time
             // both (events, synchronous), later ones take the faster
             int v = denseMode();
-            const bool timing = v < 0 && s.tune && s.tune->runs[s.tune->choice(2)] == 0;
-            if (v < 0) v = s.tune ? s.tune->choice(2) : 0;
+            bool timing = false;
+            if (v < 0) {
+                std::lock_guard<std::mutex> lk(tuneMu());
+                timing = s.tune && s.tune->runs[s.tune->choice(2)] == 0;
+                v = s.tune ? s.tune->choice(2) : 0;
+            }
             cudaEvent_t e0 = nullptr, e1 = nullptr;
             if (timing) {
                 cuda(cudaEventCreate(&e0), "event");
@@ -799,12 +826,16 @@ void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_ru
                 cudaEventElapsedTime(&ms, e0, e1);
                 cudaEventDestroy(e0);
                 cudaEventDestroy(e1);
+                std::lock_guard<std::mutex> lk(tuneMu());
                 s.tune->ms[v] = ms;
                 rs.tuning_runs++;
                 if (std::getenv("QK_DEBUG_TUNE"))
                     std::fprintf(stderr, "dense U5 %s: %.3f ms\n", v ? "DMMA" : "DFMA", double(ms));
             }
-            if (s.tune) s.tune->runs[v]++;
+            if (s.tune) {
+                std::lock_guard<std::mutex> lk(tuneMu());
+                s.tune->runs[v]++;
+            }
         } else {
             uint64_t mask = 0;
             for (size_t j = 1; j < s.targets.size(); j++) mask |= uint64_t(1) << s.targets[j];
@@ -854,7 +885,7 @@ struct XrsRank {
     std::vector<qk_xrs_msg> msgs;
     XrsRank(qk_state* s, const XrsPlan& plan) : st(s), p(plan) {
         for (int j = 0; j < p.s; j++) contiguous &= p.outs[size_t(j)] == st->nLocal - p.s + j;
-        ensureXrsBuffers(st, uint64_t((1 << p.s) - 1) * p.window, !contiguous);
+        ensureXrsBuffers(st, 2 * uint64_t((1 << p.s) - 1) * p.window, !contiguous);  // two receive halves
         msgs = xrsMessages(p, st->rank);
     }
     const double2* sendSrc(const qk_xrs_msg& x) const {
@@ -871,11 +902,11 @@ struct XrsRank {
             rs.kernel_launches++;
         }
     }
-    void unpack(size_t a, size_t b, qk_run_stats& rs) {
+    void unpack(size_t a, size_t b, qk_run_stats& rs, cudaStream_t on = nullptr, uint64_t bufOffset = 0) {
         for (size_t m = a; m < b; m++) {
             const qk_xrs_msg& x = msgs[m];
-            cuda(qkdev::launchWindowUnpack(st->amps + slabBits(x.slab, p), recvDst(x), x.w0, x.count, p.outs.data(), p.s,
-                                           st->stream),
+            cuda(qkdev::launchWindowUnpack(st->amps + slabBits(x.slab, p), recvDst(x) + bufOffset, x.w0, x.count,
+                                           p.outs.data(), p.s, on ? on : st->stream),
                  "xrs copy-back");
             rs.kernel_launches++;
         }
@@ -888,27 +919,52 @@ struct XrsRank {
 };
 
 // NCCL XRS for this rank (one process per GPU): per window round, one grouped
-// ncclSend/ncclRecv per partner into a single receive buffer, then copy-back.
+// ncclSend/ncclRecv per partner into the receive buffer, then copy-back
+// (distributed.cpp:183-191).  The buffer is double-buffered: round k lands
+// in half k % 2 and its copy-back runs on a second stream, overlapping the
+// transfer of round k + 1; round k + 2 waits for that copy-back before it
+// reuses the half.  Sends read the slab windows in place when the outs are
+// the AIO-staged top S positions (else a pack kernel fills packBuf).
 void runXrsNccl(qk_state* st, const XrsPlan& p, qk_run_stats& rs) {
     st->normValid = false;
     if (!st->comm)
         throw SimulationError("cross-rank swap needs a communicator (qk_comm_init / qk_ipc_init) or qk_simulate_local");
     if (p.s == 0) return;
     XrsRank x(st, p);
-    for (size_t a = 0; a < x.msgs.size();) {
+    if (!st->aux) {
+        cuda(cudaStreamCreateWithFlags(&st->aux, cudaStreamNonBlocking), "xrs copy-back stream");
+        for (int h = 0; h < 2; h++) {
+            cuda(cudaEventCreateWithFlags(&st->xrsDone[h], cudaEventDisableTiming), "event");
+            cuda(cudaEventCreateWithFlags(&st->unpackDone[h], cudaEventDisableTiming), "event");
+        }
+    }
+    const uint64_t half = uint64_t((1 << p.s) - 1) * p.window;  // one round's receive sections
+    bool used[2] = {false, false};
+    int round = 0;
+    for (size_t a = 0; a < x.msgs.size(); round++) {
         const size_t b = x.roundEnd(a);
+        const int h = round & 1;
+        if (used[h]) cuda(cudaStreamWaitEvent(st->stream, st->unpackDone[h], 0), "xrs wait copy-back");
         x.pack(a, b, rs);
         nccl(ncclGroupStart(), "ncclGroupStart");
         for (size_t m = a; m < b; m++) {
             const qk_xrs_msg& msg = x.msgs[m];
             nccl(ncclSend(x.sendSrc(msg), 2 * msg.count, ncclDouble, msg.peer, st->comm, st->stream), "ncclSend");
-            nccl(ncclRecv(x.recvDst(msg), 2 * msg.count, ncclDouble, msg.peer, st->comm, st->stream), "ncclRecv");
+            nccl(ncclRecv(x.recvDst(msg) + uint64_t(h) * half, 2 * msg.count, ncclDouble, msg.peer, st->comm,
+                          st->stream),
+                 "ncclRecv");
         }
         nccl(ncclGroupEnd(), "ncclGroupEnd");
-        x.unpack(a, b, rs);
+        cuda(cudaEventRecord(st->xrsDone[h], st->stream), "event");
+        cuda(cudaStreamWaitEvent(st->aux, st->xrsDone[h], 0), "xrs copy-back wait");
+        x.unpack(a, b, rs, st->aux, uint64_t(h) * half);
+        cuda(cudaEventRecord(st->unpackDone[h], st->aux), "event");
+        used[h] = true;
         rs.xrs_rounds++;
         a = b;
     }
+    for (int h = 0; h < 2; h++)
+        if (used[h]) cuda(cudaStreamWaitEvent(st->stream, st->unpackDone[h], 0), "xrs join copy-back");
     rs.xrs_bytes += 16.0 * double(st->count) * (1.0 - std::ldexp(1.0, -p.s));
 }
 
@@ -1223,6 +1279,11 @@ int qk_destroy(qk_state* st) {
         cudaFree(st->normTiles);
         cudaFree(st->recvBuf);
         cudaFree(st->packBuf);
+        for (int h = 0; h < 2; h++) {
+            if (st->xrsDone[h]) cudaEventDestroy(st->xrsDone[h]);
+            if (st->unpackDone[h]) cudaEventDestroy(st->unpackDone[h]);
+        }
+        if (st->aux) cudaStreamDestroy(st->aux);
         cudaStreamDestroy(st->stream);
         delete st;
     });
@@ -1352,7 +1413,7 @@ int qk_debug_jit_compile(const qk_gate* gates, int ngates, int nLocal, char** so
 int qk_debug_jit_program(const qk_program* cp, int nLocal, char** sources) {
     return guard([&] {
         qk_program* p = const_cast<qk_program*>(cp);
-        auto c = compileFor(p, nLocal, std::getenv("QK_DEBUG_FROM_BASIS") != nullptr);
+        auto c = compileFor(p, nLocal, std::getenv("QK_DEBUG_FROM_BASIS") != nullptr, 1);  // specialized-kernel schedule
         std::string all;
         int k = 0;
         for (const CompiledItem& it : c->items)
@@ -1412,7 +1473,7 @@ int qk_ims_swap(qk_state* st, const int* outs, const int* ins, int s, int /*cach
 
 int qk_set_dense_mode(int mode) {
     return guard([&] {
-        if (mode < -1 || mode > 1) throw ConfigError("dense mode must be -1, 0 or 1");
+        if (mode < -1 || mode > 2) throw ConfigError("dense mode must be -1, 0, 1 or 2");
         denseModeVar().store(mode);
     });
 }
@@ -1711,8 +1772,13 @@ int qk_simulate(qk_state* st, const qk_program* cp, const qk_config* cfg, uint64
         for (size_t i = 0; i < comp->items.size();) {
             if (nextAlt < comp->alts.size() && comp->alts[nextAlt].first == i) {
                 const Alternative& alt = comp->alts[nextAlt++];
-                const int v = chooseTileVariant(*comp, alt);
-                const bool timing = alt.tune->choice < 0 && ((v == 0 && alt.tune->msA < 0) || v == 1);
+                int v;
+                bool timing;
+                {
+                    std::lock_guard<std::mutex> lk(tuneMu());
+                    v = chooseTileVariant(*comp, alt);
+                    timing = alt.tune->choice < 0 && ((v == 0 && alt.tune->msA < 0) || v == 1);
+                }
                 cudaEvent_t a0 = nullptr, a1 = nullptr;
                 if (timing) {
                     cuda(cudaEventCreate(&a0), "event");
@@ -1731,6 +1797,7 @@ int qk_simulate(qk_state* st, const qk_program* cp, const qk_config* cfg, uint64
                     cudaEventElapsedTime(&ms, a0, a1);
                     cudaEventDestroy(a0);
                     cudaEventDestroy(a1);
+                    std::lock_guard<std::mutex> lk(tuneMu());
                     if (v == 1) {
                         alt.tune->msB = alt.tune->runsB ? std::min(alt.tune->msB, ms) : ms;
                         alt.tune->runsB++;
@@ -1738,7 +1805,10 @@ int qk_simulate(qk_state* st, const qk_program* cp, const qk_config* cfg, uint64
                         alt.tune->msA = ms;
                     }
                 }
-                alt.tune->runs++;
+                {
+                    std::lock_guard<std::mutex> lk(tuneMu());
+                    alt.tune->runs++;
+                }
                 i = alt.last;
                 continue;
             }

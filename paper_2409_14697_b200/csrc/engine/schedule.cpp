@@ -23,6 +23,7 @@
 #include "schedule.h"
 
 #include <algorithm>
+#include <sstream>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -1125,6 +1126,32 @@ double passCodeBudget() {
     return v;
 }
 
+// Pass cost model of the DP (units: one HBM sweep of the slice).  Row
+// penalty by the number L of contiguous lowest memory bits in the tile
+// (QK_ROW_PEN="p0,p1,p2,p3"): measured on B200 at 2^33 amplitudes, a pass
+// with L = 0 (16-B rows, lanes 2^12 amplitudes apart) ran 2.7x a coalesced
+// one, L = 3 about 1.3x.  QK_XCHG_COST: cost of one extra segment (a smem
+// exchange of the whole tile, ~10 ms of a ~45 ms pass).
+const double* rowPenalty() {
+    static const std::vector<double> v = [] {
+        std::vector<double> p = {1.7, 1.0, 0.4, 0.1};
+        if (const char* e = std::getenv("QK_ROW_PEN")) {
+            std::istringstream in(e);
+            std::string tok;
+            for (size_t i = 0; i < p.size() && std::getline(in, tok, ','); i++) p[i] = std::atof(tok.c_str());
+        }
+        return p;
+    }();
+    return v.data();
+}
+double exchangeCost() {
+    static const double v = [] {
+        const char* e = std::getenv("QK_XCHG_COST");
+        return e ? std::atof(e) : 0.2;
+    }();
+    return v;
+}
+
 int lowTileBits() {
     static const int v = envInt("QK_TILE_LOW", 3, 0, 8);
     return v;
@@ -1150,7 +1177,7 @@ void applyStorePermutation(PassParams& P, const std::vector<int>& sigma) {
 
 std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::vector<double>& gtab,
                                const std::vector<int>* dest, std::vector<int>* relabel, int tileBits,
-                               bool synthFirst) {
+                               bool synthFirst, bool interp) {
     std::vector<Step> steps;
     // Routing (dest given): memory bit b's data should end at memory bit
     // dest[b].  Each pass stores its tile with the permutation that puts every
@@ -1228,7 +1255,8 @@ std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::
         return steps;
     }
     const int ct = std::min(tileBits > 0 ? tileBits : maxTileBits(), nLocal);
-    const int rb = regBitsFor(ct);
+    const int rb = interp ? std::min(ct, 3) : regBitsFor(ct);
+    if (interp && ct > 12) return compileBlock(gates, nLocal, gtab, dest, relabel, 12, synthFirst, true);
     // Cut each run of gates (between wide dense steps) into passes by dynamic
     // programming over cut points.  A pass costs one HBM round trip, more when
     // its tile cannot start with >= 3 contiguous low memory bits (rows under
@@ -1238,8 +1266,14 @@ std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::
         for (int b = 0; b < nLocal && __builtin_popcountll(tile) < ct; b++) tile |= uint64_t(1) << b;
         int L = 0;
         while (L < ct && ((tile >> L) & 1)) L++;
-        static const double pen[4] = {1.0, 0.6, 0.3, 0.0};
-        return 1.0 + pen[std::min(L, lowTileBits())];
+        const double* pen = rowPenalty();
+        double c = 1.0 + pen[std::min(L, lowTileBits())];
+        // exchanges: the register window holds rb of the tile's bits, so a
+        // pass whose non-diagonal gates touch u bits needs >= ceil(u / rb)
+        // segments; each extra one is a shared-memory round trip of the tile
+        const int u = __builtin_popcountll(used);
+        c += exchangeCost() * double(std::max(0, (u + rb - 1) / rb - 1));
+        return c;
     };
     std::vector<Gate> run;
     auto cutRun = [&] {
@@ -1280,8 +1314,8 @@ std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::
                 if (mask[k]) used |= group.back().depMask();
             }
             const size_t first = steps.size();
-            compileGroup(group, used, ct, nLocal, gtab, steps);
-            if (ct == 13 && tuneRegBits() && steps.size() == first + 1 && steps[first].kind == Step::Pass) {
+            compileGroup(group, used, ct, nLocal, gtab, steps, interp ? rb : -1);
+            if (!interp && ct == 13 && tuneRegBits() && steps.size() == first + 1 && steps[first].kind == Step::Pass) {
                 for (int rbAlt : {4, 3}) {  // 16 and 8 amplitudes per thread (512 / 1024 threads)
                     std::vector<Step> alt;
                     compileGroup(group, used, ct, nLocal, gtab, alt, rbAlt);

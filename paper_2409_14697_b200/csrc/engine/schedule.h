@@ -52,9 +52,12 @@ struct Step {
 // synthFirst: the first pass will synthesize its input from a basis state
 // (one tile computed, the rest zero-filled), so its tile needs no coalescing
 // padding with the lowest memory bits.
+// interp: the passes will run on the pass interpreter (k_block_pass, slices
+// below the specialization threshold): 8 amplitudes per thread (rb = 3), no
+// register-width variants, so its registers never spill.
 std::vector<Step> compileBlock(const std::vector<quokka::Gate>& gates, int nLocal, std::vector<double>& gtab,
                                const std::vector<int>* dest = nullptr, std::vector<int>* relabel = nullptr,
-                               int tileBits = 0, bool synthFirst = false);
+                               int tileBits = 0, bool synthFirst = false, bool interp = false);
 
 // Reference-formula flops per amplitude for one gate.
 double referenceFlopsPerAmp(const quokka::Gate& g);

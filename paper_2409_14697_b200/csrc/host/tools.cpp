@@ -5,6 +5,9 @@
 // and optimized Programs are identical; tests/test_host_formats.py compares
 // the serialized text.  genGrover is this framework's addition.
 #include <cmath>
+#include <map>
+#include <string>
+#include <vector>
 
 #include "quokka/tools.hpp"
 
@@ -170,6 +173,88 @@ void multiZ(Circuit& c, long& id, int m) {
 }
 
 }  // namespace
+
+// validateOrder: each logical qubit keeps a cursor into the ids of its raw
+// gates; replaying the program (SQS / CSQS move the layout, fused gates expand
+// into their constituents) must advance every cursor by exactly the gate it
+// meets, and finish with every cursor at its end.
+OrderReport validateOrder(const Circuit& raw, const Program& p) {
+    OrderReport rep;
+    auto fail = [&rep](const std::string& msg, int qubit, long expected, long got) {
+        if (!rep.ok) return;  // keep the first divergence
+        rep = OrderReport{false, msg, qubit, expected, got};
+    };
+    if (raw.nQubits != p.nQubits) {
+        fail("qubit count mismatch", -1, -1, -1);
+        return rep;
+    }
+    std::vector<std::vector<long>> order(static_cast<size_t>(raw.nQubits));
+    std::map<long, const Gate*> byId;
+    for (const Gate& g : raw.gates) {
+        byId[g.id] = &g;
+        for (int q : g.qubits()) order[size_t(q)].push_back(g.id);
+    }
+    std::vector<size_t> cursor(static_cast<size_t>(raw.nQubits), 0);
+    QubitLayout layout = QubitLayout::identity(raw.nQubits);
+    auto visit = [&](const Gate& g) {
+        std::vector<int> logical;
+        for (int q : g.qubits()) logical.push_back(layout.physToLog[size_t(q)]);
+        const int first = logical.empty() ? -1 : logical[0];
+        const auto it = byId.find(g.id);
+        if (it == byId.end()) {
+            fail("gate id " + std::to_string(g.id) + " does not appear in the raw circuit", first, -1, g.id);
+            return;
+        }
+        const Gate& want = *it->second;
+        if (g.kind != want.kind || g.params != want.params || logical != want.qubits()) {
+            fail("gate " + std::to_string(g.id) + " differs from its raw form", first, g.id, g.id);
+            return;
+        }
+        for (int q : logical) {
+            const std::vector<long>& ids = order[size_t(q)];
+            size_t& c = cursor[size_t(q)];
+            if (c >= ids.size()) {
+                fail("qubit " + std::to_string(q) + " sees extra gate " + std::to_string(g.id), q, -1, g.id);
+                return;
+            }
+            if (ids[c] != g.id) {
+                fail("qubit " + std::to_string(q) + " expected gate " + std::to_string(ids[c]) + " but found " +
+                         std::to_string(g.id),
+                     q, ids[c], g.id);
+                return;
+            }
+            c++;
+        }
+    };
+    for (const ProgramItem& it : p.items) {
+        if (!rep.ok) break;
+        if (it.type == ProgramItem::Swap) {
+            layout.applyPairs(it.swap.pairs);
+            continue;
+        }
+        for (const Gate& g : it.block.gates) {
+            if (!rep.ok) break;
+            const bool fused = g.kind == GateKind::FusedDiag || g.kind == GateKind::FusedDense;
+            if (!fused) {
+                visit(g);
+                continue;
+            }
+            if (g.constituents.empty()) {
+                fail("fused gate " + std::to_string(g.id) + " carries no constituent records", -1, -1, g.id);
+                break;
+            }
+            for (const Gate& c : g.constituents) {
+                visit(c);
+                if (!rep.ok) break;
+            }
+        }
+    }
+    for (int q = 0; rep.ok && q < raw.nQubits; q++)
+        if (cursor[size_t(q)] != order[size_t(q)].size())
+            fail("qubit " + std::to_string(q) + " is missing gate " + std::to_string(order[size_t(q)][cursor[size_t(q)]]),
+                 q, order[size_t(q)][cursor[size_t(q)]], -1);
+    return rep;
+}
 
 Circuit genGrover(int n, std::uint64_t marked, int iterations) {
     if (n < 2) throw ConfigError("grover needs at least 2 qubits");

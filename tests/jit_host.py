@@ -41,7 +41,11 @@ def run_program_jit(qk, port, prog, n_local, state, basis=None):
     the oracle for IMS items.  basis: the first pass synthesizes |basis>
     instead of reading `state` (the engine's folded initState)."""
     first = NO_BASIS if basis is None else basis
-    items = prog.debug_compile(n_local)["items"]
+    qk.set_jit_min_qubits(0)  # the schedule the specialized kernels run (the interpreter's differs)
+    try:
+        items = prog.debug_compile(n_local)["items"]
+    finally:
+        qk.set_jit_min_qubits(22)
     if basis is not None and not (items and items[0]["kind"] == 0 and items[0]["block"]["steps"][0]["kind"] == 0):
         state[:] = 0  # the engine folds initState only into a leading pass
         state[basis] = 1

@@ -250,7 +250,7 @@ def test_marginal_probabilities(qk):
     d.close()
 
 
-@pytest.mark.parametrize("mode", [0, 1, -1])
+@pytest.mark.parametrize("mode", [0, 1, -1, 2])
 def test_u5_tile_kernel_vs_reference(ref, qk, mode):
     # fused dense U5 (reference fusion_qbit = 5, engine.cpp:228-251) through
     # the tile kernel: DFMA (0), DMMA FP64 tensor cores (1), autotuned (-1);
@@ -263,7 +263,7 @@ def test_u5_tile_kernel_vs_reference(ref, qk, mode):
         for tg in cases:
             m = rng.standard_normal((32, 32)) + 1j * rng.standard_normal((32, 32))
             q, _ = np.linalg.qr(m)
-            line = "U5 " + " ".join(map(str, tg)) + " " + " ".join(f"{v.real!r} {v.imag!r}" for v in q.reshape(-1))
+            line = "U5 " + " ".join(map(str, tg)) + " " + " ".join(f"{float(v.real)!r} {float(v.imag)!r}" for v in q.reshape(-1))
             st = np.random.default_rng(len(tg) + tg[0]).standard_normal(2 << n)
             st /= np.linalg.norm(st)
             want = st.copy()
