@@ -207,6 +207,9 @@ bool pipelined(const PassParams& P) {
     }
     return true;
 }
+}  // namespace
+bool pipelinedPass(const PassParams& P) { return pipelined(P); }
+namespace {
 constexpr int kPipeSmemAmps = (1 << 13) + (1 << 12) + qkdev::kMaxCtaFactors + 1;  // PB | XS | F | mbarrier
 
 class Gen {

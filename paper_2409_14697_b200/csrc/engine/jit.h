@@ -35,6 +35,10 @@ cudaError_t launch(const qkdev::PassParams& P, double2* state, const double2* gt
 int minQubits();
 void setMinQubits(int v);
 
+// P runs as the TMA-pipelined persistent kernel (next tile streamed into
+// shared memory while the current one computes).
+bool pipelinedPass(const qkdev::PassParams& P);
+
 // NVRTC compile of a source to a cubin (used by tests on the CPU too).
 std::vector<char> compileToCubin(const std::string& src, const std::string& name);
 

@@ -246,7 +246,9 @@ struct qk_program {
     quokka::Program prog;
     std::mutex mu;
     std::map<int, std::shared_ptr<Compiled>> compiled;            // by nLocal
-    std::map<std::pair<int, int>, DeviceTables> tables;           // (nLocal, device)
+    // (schedule, device): each compiled schedule (slice size x layout x kernel
+    // family) has its own gtab / target tables
+    std::map<std::pair<const Compiled*, int>, DeviceTables> tables;
     ~qk_program() {
         for (auto& kv : tables) {
             int prev = 0;
@@ -617,7 +619,7 @@ std::shared_ptr<Compiled> compileFor(qk_program* p, int nLocal, bool fromBasis =
 
 DeviceTables tablesFor(qk_program* p, const Compiled& c, int device) {
     std::lock_guard<std::mutex> lk(p->mu);
-    auto key = std::make_pair(c.nLocal, device);
+    auto key = std::make_pair(&c, device);
     auto it = p->tables.find(key);
     if (it != p->tables.end()) return it->second;
     DeviceTables t;
@@ -787,6 +789,11 @@ void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_ru
                 s.tune->ms[v] = ms;
                 s.tune->runs[v]++;
                 rs.tuning_runs++;
+                if (std::getenv("QK_DEBUG_TUNE")) {
+                    const qkdev::PassParams& Q = v ? *s.alts[size_t(v - 1)] : *s.pass;
+                    std::fprintf(stderr, "pass variant %d (ct %d rb %d segs %d%s): %.3f ms\n", v, Q.ct, Q.rb, Q.nsegs,
+                                 qkjit::pipelinedPass(Q) ? ", TMA-pipelined" : "", double(ms));
+                }
             } else if (s.tune) {
                 std::lock_guard<std::mutex> lk(tuneMu());
                 s.tune->runs[v]++;

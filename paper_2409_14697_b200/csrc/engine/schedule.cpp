@@ -1128,13 +1128,15 @@ double passCodeBudget() {
 
 // Pass cost model of the DP (units: one HBM sweep of the slice).  Row
 // penalty by the number L of contiguous lowest memory bits in the tile
-// (QK_ROW_PEN="p0,p1,p2,p3"): measured on B200 at 2^33 amplitudes, a pass
-// with L = 0 (16-B rows, lanes 2^12 amplitudes apart) ran 2.7x a coalesced
-// one, L = 3 about 1.3x.  QK_XCHG_COST: cost of one extra segment (a smem
-// exchange of the whole tile, ~10 ms of a ~45 ms pass).
+// (QK_ROW_PEN="p0,p1,p2,p3", default 1.0,0.6,0.3,0) and the cost of each
+// extra segment (QK_XCHG_COST, default 0).  A steeper row penalty
+// (1.7,1.0,0.4,0.1) with 0.2 per exchange was measured on B200 at 33 qubits
+// (profiles/r2_dp_model_ab.txt): QFT 0.153 -> 0.161 s, QAOA / random / Grover
+// within 1 %, BV unchanged (its L = 0 pass has no cheaper cut) -- kept as
+// knobs, not defaults.
 const double* rowPenalty() {
     static const std::vector<double> v = [] {
-        std::vector<double> p = {1.7, 1.0, 0.4, 0.1};
+        std::vector<double> p = {1.0, 0.6, 0.3, 0.0};
         if (const char* e = std::getenv("QK_ROW_PEN")) {
             std::istringstream in(e);
             std::string tok;
@@ -1147,7 +1149,7 @@ const double* rowPenalty() {
 double exchangeCost() {
     static const double v = [] {
         const char* e = std::getenv("QK_XCHG_COST");
-        return e ? std::atof(e) : 0.2;
+        return e ? std::atof(e) : 0.0;
     }();
     return v;
 }
