@@ -80,6 +80,12 @@ typedef struct qk_run_stats {
     uint64_t full_pass_launches;
     double full_pass_bytes;
     double init_ms;
+    /* Passes of a run from a basis state whose input still has known zeros
+     * (they read only the support: algorithmic bytes 16 B/amp written + 16 B
+     * per amplitude not known to be zero). */
+    double sparse_pass_ms;
+    uint64_t sparse_pass_launches;
+    double sparse_pass_bytes;
 } qk_run_stats;
 
 typedef struct qk_state qk_state;      /* one rank slice in HBM + its stream */

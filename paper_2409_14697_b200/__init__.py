@@ -82,7 +82,8 @@ class _RunStats(C.Structure):
                 ("block_flops", C.c_double), ("ims_bytes", C.c_double), ("xrs_bytes", C.c_double),
                 ("tuning_runs", C.c_uint64), ("full_pass_ms", C.c_double),
                 ("full_pass_launches", C.c_uint64), ("full_pass_bytes", C.c_double),
-                ("init_ms", C.c_double)]
+                ("init_ms", C.c_double), ("sparse_pass_ms", C.c_double),
+                ("sparse_pass_launches", C.c_uint64), ("sparse_pass_bytes", C.c_double)]
 
 
 def build(quiet: bool = True) -> None:

@@ -229,7 +229,7 @@ public:
         o_ << kPrologue;
         ctaTables();
         o_ << "extern \"C\" __global__ void __launch_bounds__(" << nt_ << "," << minb << ") " << name
-           << "(double2* __restrict__ st, const double2* __restrict__ gt, const u32 ntiles, const u64 basis, const u32 tile0, double* __restrict__ np) {\n";
+           << "(double2* __restrict__ st, const double2* __restrict__ gt, const u32 ntiles, const u64 basis, const u32 tile0, double* __restrict__ np, const u64 smask, const u64 sval) {\n";
         o_ << "  extern __shared__ double2 sm[];\n  double2* const F = sm + " << (1 << ct_)
            << ";\n  const u32 tid = threadIdx.x;\n";
         o_ << "  for (u32 tile = blockIdx.x + tile0; tile < ntiles; tile += gridDim.x) {\n";
@@ -238,8 +238,15 @@ public:
         std::string decl = "  double2 ";
         for (int s = 0; s < na_; s++) decl += (s ? ", a" : "a") + std::to_string(s);
         o_ << decl << ";\n  double2 P = C2(1.0, 0.0);\n" << pendDecl();
-        // load (map_in[0], no flips)
-        o_ << "  { const u64 off = base | " << threadGlobal(P_.map_in[0]) << ";\n  if (basis == ~0ull) {\n";
+        // load (map_in[0], no flips).  smask != 0: the input is zero outside
+        // the coset {i : (i ^ sval) & smask == 0} (a run from a basis state,
+        // before its passes have touched every bit): only those amplitudes
+        // are read, the rest are zeros that need no memory.
+        o_ << "  { const u64 off = base | " << threadGlobal(P_.map_in[0]) << ";\n  if (smask != 0ull) {\n";
+        for (int s = 0; s < na_; s++)
+            o_ << "  { const u64 i_ = off | " << regGlobal(P_.map_in[0], s) << "ull; a" << s
+               << " = ((i_ ^ sval) & smask) == 0ull ? __ldcs(st + i_) : C2(0.0, 0.0); }\n";
+        o_ << "  } else if (basis == ~0ull) {\n";
         const int kl = slotOfMem0(P_.map_in[0]);
         for (int s = 0; s < na_; s++) {
             if (kl >= 0) {  // neighbours (slot kl = 0 / 1) in one 256-bit load
@@ -294,7 +301,7 @@ public:
         o_ << kPrologue;
         ctaTables();
         o_ << "extern \"C\" __global__ void __launch_bounds__(" << nt_ << ",1) " << name
-           << "(double2* __restrict__ st, const double2* __restrict__ gt, const u32 ntiles, const u64 basis, const u32 tile0, double* __restrict__ np) {\n"
+           << "(double2* __restrict__ st, const double2* __restrict__ gt, const u32 ntiles, const u64 basis, const u32 tile0, double* __restrict__ np, const u64 smask, const u64 sval) {\n"
            << "  extern __shared__ double2 sm[];  // PB: next tile (linear tile coordinates) | XS | F | mbarrier\n"
            << "  double2* const XS = sm + 8192;\n  double2* const F = sm + 12288;\n"
            << "  u64* const mbar = (u64*)(sm + " << (12288 + qkdev::kMaxCtaFactors) << ");\n  const u32 tid = threadIdx.x;\n"
@@ -348,11 +355,13 @@ private:
            << "    if ((tid & 31u) == 0u) np[(u64)tile * " << warps << "u + (tid >> 5)] = s_;\n  }\n";
     }
 
-    // First pass of a run (|basis> synthesized): a tile that does not hold the
-    // basis index is all zeros and stays all zeros under the pass's linear
-    // map -- write the zeros, skip the arithmetic.
+    // A tile whose input is all zeros -- the first pass of a run (|basis>
+    // synthesized) for every tile but the basis's, or any tile outside the
+    // support coset (smask / sval) -- stays all zeros under the pass's linear
+    // map: write the zeros, skip the loads and the arithmetic.
     void zeroTile() {
-        o_ << "  if (basis != ~0ull && ((basis ^ base) & " << (~P_.tile_mask) << "ull) != 0ull) {\n"
+        o_ << "  if ((basis != ~0ull && ((basis ^ base) & " << (~P_.tile_mask) << "ull) != 0ull) ||\n"
+           << "      ((base ^ sval) & smask & " << (~P_.tile_mask) << "ull) != 0ull) {\n"
            << "    const u64 zoff = base | " << threadGlobal(P_.map_in[0]) << ";\n";
         const int kl = slotOfMem0(P_.map_in[0]);
         for (int s = 0; s < na_; s++) {
@@ -362,6 +371,10 @@ private:
                 continue;
             }
             o_ << "    __stcs(st + (zoff | " << regGlobal(P_.map_in[0], s) << "ull), C2(0.0, 0.0));\n";
+        }
+        if (P_.norm_out) {  // this tile's share of sum |a|^2 is 0
+            const int warps = nt_ / 32 > 0 ? nt_ / 32 : 1;
+            o_ << "    if ((tid & 31u) == 0u) np[(u64)tile * " << warps << "u + (tid >> 5)] = 0.0;\n";
         }
         o_ << "    continue;\n  }\n";
     }
@@ -819,7 +832,7 @@ private:
 // ---- compile / load / launch -------------------------------------------------
 
 // Bump when the generated code changes for the same PassParams (on-disk cache key).
-constexpr uint64_t kGeneratorVersion = 22;
+constexpr uint64_t kGeneratorVersion = 23;
 
 uint64_t hashPass(const PassParams& P) {
     uint64_t h = 1469598103934665603ull ^ (kGeneratorVersion * 0x9E3779B97F4A7C15ull) ^ (usePrefetch() ? 1u : 0u) ^ (usePersistent() ? 2u : 0u) ^
@@ -1118,7 +1131,7 @@ void prepare(const std::vector<const PassParams*>& passes, int device) {
 }
 
 cudaError_t launch(const PassParams& P, double2* state, const double2* gtab, int nLocal, uint64_t basis,
-                   cudaStream_t stream, double* np) {
+                   cudaStream_t stream, double* np, uint64_t smask, uint64_t sval, bool zeroFill) {
     int dev = 0;
     cudaGetDevice(&dev);
     void* fn = functionFor(P, hashPass(P), dev);
@@ -1129,8 +1142,10 @@ cudaError_t launch(const PassParams& P, double2* state, const double2* gtab, int
     if (basis != ~uint64_t(0)) {
         // First pass of a run: every tile but the one holding |basis> is zeros
         // in and zeros out -- memset the slice, compute that one tile.
-        const cudaError_t e = cudaMemsetAsync(state, 0, sizeof(double2) << nLocal, stream);
-        if (e != cudaSuccess) return e;
+        if (zeroFill) {  // else the next pass writes every tile (launched with smask / sval)
+            const cudaError_t e = cudaMemsetAsync(state, 0, sizeof(double2) << nLocal, stream);
+            if (e != cudaSuccess) return e;
+        }
         if (basis >> nLocal) return cudaSuccess;  // the basis state lives on another rank
         uint32_t t = 0, q = 0;  // tile index = the basis's non-tile bits, compacted
         for (int b = 0; b < nLocal; b++)
@@ -1145,7 +1160,8 @@ cudaError_t launch(const PassParams& P, double2* state, const double2* gtab, int
     const unsigned nt = 1u << (P.ct - P.rb);
     const unsigned smem = pipe ? unsigned(sizeof(double2) * kPipeSmemAmps)
                                : unsigned((sizeof(double2) << P.ct) + sizeof(double2) * qkdev::kMaxCtaFactors + 256);
-    void* args[] = {&state, &gtab, &ntiles, &basis, &tile0, &np};
+    if (smask && pipe) return cudaErrorInvalidValue;  // the TMA-pipelined kernels read whole tiles
+    void* args[] = {&state, &gtab, &ntiles, &basis, &tile0, &np, &smask, &sval};
     if (driver().launchKernel(fn, ctas, 1, 1, nt, 1, 1, smem, stream, args, nullptr) != 0)
         return cudaErrorLaunchFailure;
     return cudaSuccess;

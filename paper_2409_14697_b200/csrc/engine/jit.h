@@ -27,8 +27,15 @@ void prepare(const std::vector<const qkdev::PassParams*>& passes, int device);
 // basis != ~0: synthesize the basis state |basis> (slice index) instead of
 // loading the slice (the first pass of a simulation needs no initState).
 // np: per-tile sums of |a|^2 when P.norm_out (one double per tile).
+// smask != 0: the slice is zero outside {i : (i ^ sval) & smask == 0} (a run
+// from a basis state whose passes have not yet touched every bit): tiles
+// outside it are written as zeros with no reads or arithmetic, and inside
+// only the in-support amplitudes are read -- the slice need not be valid
+// elsewhere.  zeroFill (basis passes): memset the slice first; false when
+// the next pass is launched with smask and so writes every tile itself.
 cudaError_t launch(const qkdev::PassParams& P, double2* state, const double2* gtab, int nLocal, uint64_t basis,
-                   cudaStream_t stream, double* np = nullptr);
+                   cudaStream_t stream, double* np = nullptr, uint64_t smask = 0, uint64_t sval = 0,
+                   bool zeroFill = true);
 
 // Slices with at least this many local qubits use specialized kernels
 // (QK_JIT_MIN_QUBITS, default 22; -1 disables).

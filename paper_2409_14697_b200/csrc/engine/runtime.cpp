@@ -638,7 +638,7 @@ DeviceTables tablesFor(qk_program* p, const Compiled& c, int device) {
 struct Timer {
     qk_state* st;
     // classes: 0 block items, 1 IMS, 2 XRS, 3 full-slice fused passes, 4 init (first pass / memset)
-    static constexpr int kClasses = 5;
+    static constexpr int kClasses = 6;  // + 5: passes with known zeros in their input
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[kClasses];
     explicit Timer(qk_state* s) : st(s) {}
     template <class F>
@@ -664,7 +664,7 @@ struct Timer {
                 cudaEventElapsedTime(&ms, a, b);
                 out[c] += ms;
                 static const bool perItem = std::getenv("QK_PROFILE_ITEMS") != nullptr;
-                static const char* names[kClasses] = {"block", "ims", "xrs", "pass", "init"};
+                static const char* names[kClasses] = {"block", "ims", "xrs", "pass", "init", "sparse pass"};
                 if (perItem) std::fprintf(stderr, "qk item %s %.3f ms\n", names[c], ms);
                 cudaEventDestroy(a);
                 cudaEventDestroy(b);
@@ -705,6 +705,17 @@ std::mutex& tuneMu() {
     return m;
 }
 
+// QK_SPARSE_START (default 1): passes of a run from a basis state skip the
+// reads (and whole tiles) known to be zero, and the basis pass skips the
+// memset when the next pass writes every tile.
+bool sparseStart() {
+    static const bool v = [] {
+        const char* e = std::getenv("QK_SPARSE_START");
+        return !e || std::atoi(e) != 0;
+    }();
+    return v;
+}
+
 // QK_DENSE_MODE: 0 = DFMA, 1 = DMMA (FP64 tensor cores) for the U5 tile
 // kernel; unset = time both on a step's first executions, keep the faster.
 std::atomic<int>& denseModeVar() {
@@ -729,23 +740,59 @@ int smCountOf(int device) {
 
 // basis != kNoBasis: the first step is a pass that synthesizes |basis> (slice
 // index) instead of reading the slice (replaces initState's memset + store).
+// Support of a run from a basis state (qk_simulate): the slice is zero
+// outside {i : (i ^ val) & mask == 0}.  Every pass, dense group and IMS
+// frees or permutes bits; mask == 0 means "no known zeros".  Specialized
+// passes use it to skip the reads (and, for whole tiles outside it, the
+// arithmetic) of amplitudes known to be zero.
+struct Support {
+    uint64_t mask = 0, val = 0;
+};
+
+// A pass step with a variant that is not TMA-pipelined (those stream whole
+// tiles, so they cannot run with known zeros).
+bool hasPlainVariant(const qkeng::Step& s) {
+    if (!qkjit::pipelinedPass(*s.pass)) return true;
+    for (const auto& a : s.alts)
+        if (!qkjit::pipelinedPass(*a)) return true;
+    return false;
+}
+
 void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_run_stats& rs,
-              uint64_t basis = kNoBasis, Timer* timer = nullptr) {
-    const bool synthesized = basis != kNoBasis;
-    for (const qkeng::Step& s : ci.steps) {
+              uint64_t basis = kNoBasis, Timer* timer = nullptr, Support* sup = nullptr) {
+    const double amps = double(st->count);
+    for (size_t si = 0; si < ci.steps.size(); si++) {
+        const qkeng::Step& s = ci.steps[si];
         st->normValid = false;
         if (s.kind == qkeng::Step::Pass) {
+            const bool jit = useJit(st->nLocal);
+            // known zeros in this pass's input (not for the basis-synthesizing pass)
+            const uint64_t smask = (jit && sup && basis == kNoBasis && hasPlainVariant(s)) ? sup->mask : 0;
             // Register-width autotune: the first two executions of a pass time
             // each variant (events, synchronous); later ones take the faster.
+            // A pass that runs with known zeros never uses the TMA-pipelined
+            // variant (it streams whole tiles).
             const int nv = 1 + int(s.alts.size());
             int v = 0;
             bool timing = false;
             if (s.tune) {
                 std::lock_guard<std::mutex> lk(tuneMu());
+                if (smask)
+                    for (int k = 0; k < nv; k++)
+                        if (qkjit::pipelinedPass(k ? *s.alts[size_t(k - 1)] : *s.pass)) {
+                            s.tune->ms[k] = 1e30f;
+                            s.tune->runs[k] = std::max(s.tune->runs[k], 1);
+                        }
                 v = s.tune->choice(nv);
                 timing = s.tune->runs[v] == 0;
             }
             const qkdev::PassParams& P = v ? *s.alts[size_t(v - 1)] : *s.pass;
+            // The basis pass computes one tile; the memset of the rest is
+            // skipped when the next step is a specialized pass that writes
+            // every tile itself (launched with the known zeros).
+            const bool zeroFill = !(sup && sup->mask && jit && basis != kNoBasis && (basis >> st->nLocal) == 0 &&
+                                    si + 1 < ci.steps.size() && ci.steps[si + 1].kind == qkeng::Step::Pass &&
+                                    hasPlainVariant(ci.steps[si + 1]));
             cudaEvent_t e0 = nullptr, e1 = nullptr;
             if (timing) {
                 cuda(cudaEventCreate(&e0), "event");
@@ -765,19 +812,29 @@ void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_ru
                 }
             }
             auto launchPass = [&] {
-                if (useJit(st->nLocal))
+                if (jit)
                     cuda(qkjit::launch(P, st->amps, t.gtab, st->nLocal, basis, st->stream,
-                                       P.norm_out ? st->normTiles : nullptr),
+                                       P.norm_out ? st->normTiles : nullptr, smask, smask ? sup->val : 0, zeroFill),
                          "specialized block pass");
                 else
                     cuda(qkdev::launchBlockPass(st->amps, t.gtab, P, st->nLocal, basis, st->stream), "block pass");
             };
-            if (timer) timer->time(basis == kNoBasis ? 3 : 4, launchPass);
+            if (timer) timer->time(basis != kNoBasis ? 4 : smask ? 5 : 3, launchPass);
             else launchPass();
-            if (basis == kNoBasis) {
+            // algorithmic bytes: write every amplitude; read those not known to be zero
+            if (basis != kNoBasis) {
+                rs.block_bytes += zeroFill ? 16.0 * amps : 16.0 * double(uint64_t(1) << P.ct);
+            } else if (smask) {
+                const double b = 16.0 * amps + 16.0 * std::ldexp(amps, -__builtin_popcountll(smask));
+                rs.sparse_pass_launches++;
+                rs.sparse_pass_bytes += b;
+                rs.block_bytes += b;
+            } else {
                 rs.full_pass_launches++;
-                rs.full_pass_bytes += 32.0 * double(st->count);
+                rs.full_pass_bytes += 32.0 * amps;
+                rs.block_bytes += 32.0 * amps;
             }
+            if (sup && jit) sup->mask &= ~P.tile_mask;  // the pass mixes every tile bit
             if (timing) {
                 float ms = 0;
                 cuda(cudaEventRecord(e1, st->stream), "event");
@@ -805,9 +862,13 @@ void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_ru
             }
             basis = kNoBasis;
         } else if (s.kind == qkeng::Step::DiagTable) {
+            rs.block_bytes += 32.0 * amps;
             cuda(qkdev::launchDiagTable(st->amps, t.gtab + s.matOff, st->count, s.targets.data() + 1, s.k, st->stream),
                  "diag table");
         } else if (s.k == 5 && st->nLocal >= 12 && denseMode() != 2) {
+            rs.block_bytes += 32.0 * amps;
+            if (sup)
+                for (size_t j = 1; j < s.targets.size(); j++) sup->mask &= ~(uint64_t(1) << s.targets[j]);
             // U5 tile kernel, DFMA or DMMA: the first two executions time
             // both (events, synchronous), later ones take the faster
             int v = denseMode();
@@ -846,6 +907,8 @@ void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_ru
         } else {
             uint64_t mask = 0;
             for (size_t j = 1; j < s.targets.size(); j++) mask |= uint64_t(1) << s.targets[j];
+            rs.block_bytes += 32.0 * amps;
+            if (sup) sup->mask &= ~mask;
             cuda(qkdev::launchDenseGroup(st->amps, t.gtab + s.matOff, s.k, t.targets + s.targets[0], mask, st->nLocal,
                                          st->stream),
                  "dense group");
@@ -853,14 +916,24 @@ void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_ru
         rs.kernel_launches++;
         rs.block_launches++;
     }
-    // algorithmic bytes: read + write every amplitude per step; a pass that
-    // synthesizes its input (folded initState) only writes
-    rs.block_bytes += 32.0 * double(st->count) * double(ci.steps.size()) - (synthesized ? 16.0 * double(st->count) : 0.0);
     rs.block_flops += ci.flopsPerAmp * double(st->count);
 }
 
-void runIms(qk_state* st, const std::vector<int>& outs, const std::vector<int>& ins, qk_run_stats& rs) {
+uint64_t swapBits(uint64_t x, const std::vector<int>& outs, const std::vector<int>& ins) {
+    for (size_t j = 0; j < outs.size(); j++) {
+        const uint64_t d = ((x >> outs[j]) ^ (x >> ins[j])) & 1u;
+        x ^= (d << outs[j]) | (d << ins[j]);
+    }
+    return x;
+}
+
+void runIms(qk_state* st, const std::vector<int>& outs, const std::vector<int>& ins, qk_run_stats& rs,
+            Support* sup = nullptr) {
     st->normValid = false;
+    if (sup) {  // a[bitswap(i)] <- a[i]: the known-zero coset moves with its bits
+        sup->mask = swapBits(sup->mask, outs, ins);
+        sup->val = swapBits(sup->val, outs, ins);
+    }
     if (outs.empty()) return;
     cuda(qkdev::launchIms(st->amps, st->nLocal, outs.data(), ins.data(), int(outs.size()), st->stream), "ims");
     rs.kernel_launches++;
@@ -1754,17 +1827,23 @@ int qk_simulate(qk_state* st, const qk_program* cp, const qk_config* cfg, uint64
         const bool synth = !comp->items.empty() && comp->items[0].kind == CompiledItem::Block &&
                            !comp->items[0].steps.empty() && comp->items[0].steps[0].kind == qkeng::Step::Pass;
         uint64_t basis = kNoBasis;
-        if (synth)
-            basis = (initial >> st->nLocal) == Index(st->rank) ? layoutIndex(initial & (st->count - 1), comp->mem0)
-                                                              : st->count;
-        else timer.time(4, [&] { setBasis(st, initial, &comp->mem0); });
+        Support sup;  // the run starts from |initial>: one nonzero amplitude (this rank) or none
+        if (synth) {
+            const bool here = (initial >> st->nLocal) == Index(st->rank);
+            basis = here ? layoutIndex(initial & (st->count - 1), comp->mem0) : st->count;
+            if (here) sup = Support{st->count - 1, basis};
+        } else {
+            timer.time(4, [&] { setBasis(st, initial, &comp->mem0); });
+        }
+        if (!sparseStart()) sup.mask = 0;
         auto runItem = [&](const CompiledItem& it) {
             if (it.kind == CompiledItem::Block) {
-                timer.time(0, [&] { runBlock(st, it, t, rs, basis, &timer); });
+                timer.time(0, [&] { runBlock(st, it, t, rs, basis, &timer, &sup); });
                 basis = kNoBasis;
             }
-            else if (it.kind == CompiledItem::Ims) timer.time(1, [&] { runIms(st, it.outs, it.ins, rs); });
+            else if (it.kind == CompiledItem::Ims) timer.time(1, [&] { runIms(st, it.outs, it.ins, rs, &sup); });
             else {
+                sup.mask = 0;
                 quokka::SwapOp op;
                 op.kind = quokka::SwapOp::CrossRank;
                 for (size_t j = 0; j < it.outs.size(); j++) op.pairs.emplace_back(it.outs[j], it.ins[j]);
@@ -1834,6 +1913,7 @@ int qk_simulate(qk_state* st, const qk_program* cp, const qk_config* cfg, uint64
         rs.xrs_ms = cls[2];
         rs.full_pass_ms = cls[3];
         rs.init_ms = cls[4];
+        rs.sparse_pass_ms = cls[5];
         rs.total_ms = ms;
         st->last = rs;
         if (stats) *stats = rs;

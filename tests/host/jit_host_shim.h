@@ -58,14 +58,17 @@ extern "C" double2 sm[1 << 14];
 
 // Launch: a persistent grid of min(ntiles, 3) CTAs run one after another
 // (each walks its tiles), nt threads each.
+// qk_host_launch2: tiles [tile0, ntiles) (0 = all) with the known-zero
+// coset (smask, sval), as the runtime launches the passes of a basis run.
 #define QK_HOST_LAUNCHER(KERNEL)                                                              \
     double2 sm[1 << 14];                                                                      \
-    extern "C" void qk_host_launch(double2* st, const double2* gt, int nLocal, int ct, int rb,    \
-                                   unsigned long long basis) {                              \
-        const unsigned ntiles = 1u << (nLocal - ct), nt = 1u << (ct - rb);                   \
+    extern "C" void qk_host_launch2(double2* st, const double2* gt, int nLocal, int ct, int rb,   \
+                                    unsigned long long basis, unsigned tile0, unsigned tiles,   \
+                                    unsigned long long smask, unsigned long long sval) {        \
+        const unsigned ntiles = tiles ? tiles : 1u << (nLocal - ct), nt = 1u << (ct - rb);   \
         std::vector<double> npv(size_t(ntiles) * (nt >= 32u ? nt / 32u : 1u)); /* norm partials */ \
         double* const np = npv.data();                                                        \
-        qk_grid = ntiles < 3u ? ntiles : 3u;                                                  \
+        qk_grid = ntiles - tile0 < 3u ? ntiles - tile0 : 3u;                                  \
         for (unsigned b = 0; b < qk_grid; b++) {                                              \
             std::barrier<> bar(nt);                                                           \
             qk_bar = &bar;                                                                    \
@@ -81,8 +84,12 @@ extern "C" double2 sm[1 << 14];
                 ts.emplace_back([=] {                                                         \
                     qk_tl_tid = t;                                                            \
                     qk_tl_bid = b;                                                            \
-                    KERNEL(st, gt, ntiles, basis, 0u, np);                                    \
+                    KERNEL(st, gt, ntiles, basis, tile0, np, smask, sval);                    \
                 });                                                                           \
             for (auto& th : ts) th.join();                                                    \
         }                                                                                     \
+    }                                                                                         \
+    extern "C" void qk_host_launch(double2* st, const double2* gt, int nLocal, int ct, int rb,    \
+                                   unsigned long long basis) {                              \
+        qk_host_launch2(st, gt, nLocal, ct, rb, basis, 0u, 0u, 0ull, 0ull);                    \
     }

@@ -29,7 +29,21 @@ def host_kernel(name: str, src: str):
         os.replace(so + ".tmp", so)
     lib = C.CDLL(so)
     lib.qk_host_launch.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_uint64]
-    return lib.qk_host_launch
+    lib.qk_host_launch2.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_uint,
+                                    C.c_uint, C.c_uint64, C.c_uint64]
+    return lib.qk_host_launch if not sparse_launch else lib.qk_host_launch2
+
+
+sparse_launch = False
+
+
+def host_kernel2(name: str, src: str):
+    global sparse_launch
+    sparse_launch = True
+    try:
+        return host_kernel(name, src)
+    finally:
+        sparse_launch = False
 
 
 NO_BASIS = (1 << 64) - 1
@@ -64,6 +78,63 @@ def run_program_jit(qk, port, prog, n_local, state, basis=None):
                     run_steps(state, n_local, {"gtab": blk["gtab"], "steps": [st]})
         elif it["kind"] == 1:
             port.ims_swap(state.view(np.float64), n_local, [tuple(p) for p in it["pairs"]])
+        else:
+            raise AssertionError("cross-rank item")
+    return state
+
+
+def run_program_jit_sparse(qk, port, prog, n_local, state, initial):
+    """As the runtime runs a program from |basis> with known zeros: the first
+    pass computes ONLY the tile holding |basis> (no memset: `state` may hold
+    garbage, e.g. NaN), later passes get the known-zero coset (smask, sval)
+    and skip what lies outside it.  Requires the program to start with a
+    block of >= 2 passes (else the runtime zero-fills)."""
+    os.environ["QK_DEBUG_FROM_BASIS"] = "1"  # the schedule qk_simulate runs (free initial layout)
+    qk.set_jit_min_qubits(0)
+    try:
+        d = prog.debug_compile(n_local)
+        srcs = iter(prog.debug_jit_sources(n_local))
+    finally:
+        qk.set_jit_min_qubits(22)
+        del os.environ["QK_DEBUG_FROM_BASIS"]
+    items = d["items"]
+    basis = sum(((initial >> p) & 1) << m for p, m in enumerate(d["mem0"]))  # initial in the start layout
+    full = (1 << n_local) - 1
+    smask, sval, first = full, basis, True
+    for it in items:
+        if it["kind"] == 0:
+            blk = it["block"]
+            gt = np.array(blk["gtab"] if blk["gtab"] else [0.0, 0.0], dtype=np.float64)
+            for st in blk["steps"]:
+                if st["kind"] != 0:
+                    run_steps(state, n_local, {"gtab": blk["gtab"], "steps": [st]})
+                    for q in st["targets"]:
+                        smask &= ~(1 << q)
+                    continue
+                name, src = next(srcs)
+                tmask = sum(1 << b for b in st["tile_phys"])
+                fn = host_kernel2(name, src)
+                if first:  # only the basis tile: compacted non-tile bits of basis
+                    t, q = 0, 0
+                    for b in range(n_local):
+                        if not (tmask >> b) & 1:
+                            t |= ((basis >> b) & 1) << q
+                            q += 1
+                    fn(state.ctypes.data, gt.ctypes.data, n_local, st["ct"], st["rb"], basis, t, t + 1, 0, 0)
+                    first = False
+                else:
+                    fn(state.ctypes.data, gt.ctypes.data, n_local, st["ct"], st["rb"], NO_BASIS, 0, 0, smask,
+                       sval if smask else 0)
+                smask &= ~tmask
+        elif it["kind"] == 1:
+            pairs = [tuple(p) for p in it["pairs"]]
+            port.ims_swap(state.view(np.float64), n_local, pairs)
+            def sw(x):
+                for o, i in pairs:
+                    d = ((x >> o) ^ (x >> i)) & 1
+                    x ^= (d << o) | (d << i)
+                return x
+            smask, sval = sw(smask), sw(sval)
         else:
             raise AssertionError("cross-rank item")
     return state

@@ -12,7 +12,7 @@ import pytest
 
 from conftest import ROOT
 
-from jit_host import run_program_jit
+from jit_host import run_program_jit, run_program_jit_sparse
 from oracle import config_text
 
 
@@ -47,7 +47,7 @@ import sys, numpy as np
 sys.path[:0] = [%r, %r, %r]
 import paper_2409_14697_b200 as qk
 from oracle import Ref, Port, config_text
-from jit_host import run_program_jit
+from jit_host import run_program_jit, run_program_jit_sparse
 ref, port = Ref(), Port()
 for kind, n, a in (("qft", 16, 0), ("random", 15, 150)):
     cfg_text = config_text(n, 0, 13, fusion=0, diag=0)
@@ -76,7 +76,7 @@ import sys, numpy as np
 sys.path[:0] = [%r, %r, %r]
 import paper_2409_14697_b200 as qk
 from oracle import Ref, Port, config_text
-from jit_host import run_program_jit
+from jit_host import run_program_jit, run_program_jit_sparse
 ref, port = Ref(), Port()
 for kind, n, a in (("qft", 16, 0), ("qaoa", 15, 1)):
     cfg_text = config_text(n, 0, 13, fusion=0, diag=0)
@@ -95,3 +95,20 @@ print("ok")
     env = dict(os.environ, QK_JIT_TMA="1")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("kind,n,a,seed", [("qft", 16, 0, 0), ("qaoa", 15, 1, 2), ("random", 15, 300, 4),
+                                           ("bvones", 15, 0, 0)])
+def test_sparse_start_on_host(ref, qk, port, kind, n, a, seed):
+    # A run from a basis state as qk_simulate launches it: the basis pass
+    # computes only its own tile (no memset -- the rest of the slice is NaN
+    # here), later passes get the known-zero coset and skip what lies outside
+    # it.  Any read of a never-written amplitude would show up as NaN.
+    cfg_text = config_text(n, 0, 13, fusion=0, diag=0)
+    prog_text = ref.optimize(ref.gen(kind, n, a, seed), cfg_text)
+    want, _, _, _ = ref.simulate(prog_text, cfg_text, n, 0, 0x1235 & ((1 << n) - 1), 2)
+    prog = qk.Program.parse(prog_text, qk.Config.parse(cfg_text))
+    st = np.full(1 << n, np.nan, dtype=np.complex128)
+    run_program_jit_sparse(qk, port, prog, n, st, 0x1235 & ((1 << n) - 1))
+    assert not np.isnan(st).any()
+    assert np.max(np.abs(st - want.view(np.complex128))) < 1e-10
