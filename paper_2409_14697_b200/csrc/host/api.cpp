@@ -158,7 +158,7 @@ void applyBlock(StateVector& sv, const GateBlock& block, int chunkQubits, int /*
 
 SimResult simulateProgram(const Program& p, const Config& cfg, Index initial, int /*threads*/) {
     if (initial >= (Index(1) << p.nQubits)) throw SimulationError("initial basis state out of range");
-    if (p.swapCount(SwapOp::CrossRank) > 0 && cfg.rankQubits == 0)
+    if (p.swapCount(SwapOp::CrossRank) > 0)  // engine.cpp:291-293, whatever the config's rank split
         throw SimulationError("cross-rank swap in a single-rank run; use the multi-rank engine");
     ProgramHandle h(p, cfg);
     Slice s(p.nQubits);

@@ -4,9 +4,8 @@ libqk_b200.so, with a doctest-subset shim) run and pass.
 
 Host-only suites (gates, circuit text, tools/generators) run on the CPU; the
 engine, distributed, optimizer (fidelity checks), CLI and acceptance suites
-need the B200.  The one expected failure is the reference's kernel-backend
-selection case (test_engine.cpp:322-331): this framework has no CPU backends
-to select (the north star forbids multi-backend dispatch)."""
+need the B200.  The expected failures are listed (and justified) in
+EXPECTED_FAILURES below."""
 import os
 import re
 import subprocess
@@ -16,7 +15,18 @@ import pytest
 from conftest import ROOT
 
 BIN = os.path.join(ROOT, "tests", "cpp", "_bin")
-EXPECTED_FAILURES = {"test_engine": {"kernel backend selection validates its argument"}}
+# Two reference cases test properties of its CPU kernels, not of the result:
+#  * backend selection (test_engine.cpp:322-331): there is no CPU backend to
+#    select here (the north star forbids multi-backend dispatch);
+#  * "applyBlock equals gate-by-gate application bit for bit"
+#    (test_engine.cpp:210-233): the reference applies each gate of a block
+#    with the same scalar kernel as applyGate, so the two agree bitwise; the
+#    fused pass kernels here reassociate (H scales folded into one power of
+#    two, diagonal phases deferred and batched), so blocks agree with
+#    gate-by-gate application to ~1e-16 per amplitude, not bitwise
+#    (tests/test_gpu_kernels.py holds blocks to 1e-12 against the reference).
+EXPECTED_FAILURES = {"test_engine": {"kernel backend selection validates its argument",
+                                     "applyBlock equals gate-by-gate application bit for bit"}}
 
 
 def run_suite(name, timeout=1200):
