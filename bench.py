@@ -309,20 +309,32 @@ def main():
     e2e_s, cold_s = float(et[0].item()), float(et[1].item())
 
     # Roofline of the dominant kernel, the fused block pass over the whole
-    # slice: algorithmic 32 B/amplitude per launch over its
-    # event-timed average launch.  The first pass of a run (memset + the one
-    # tile holding |initial>) is reported apart as init.
+    # slice: algorithmic bytes per launch (32 B/amplitude,
+    # read + write) over its event-timed average launch.  Passes of a run from
+    # a basis state that still have known zeros in their input ("sparse")
+    # write every amplitude but read only the support: their algorithmic
+    # bytes are 16 B/amp + 16 B per amplitude not known to be zero.  The first
+    # pass of a run (the one tile holding |initial>) is reported apart as init.
     amps = 1 << (n - R)
     peak, peak_src = measured_peaks()
     fp_launches = sum(x["full_pass_launches"] for x in stats)
     fp_ms = sum(x["full_pass_ms"] for x in stats)
     fp_bytes = sum(x["full_pass_bytes"] for x in stats)
-    pass_launch_ms = fp_ms / max(1, fp_launches)
-    pass_bytes_per_launch = fp_bytes / max(1, fp_launches)
-    pass_gbs = pass_bytes_per_launch / (pass_launch_ms * 1e-3) / 1e9 if fp_launches else 0.0
+    sp_launches = sum(x["sparse_pass_launches"] for x in stats)
+    sp_ms = sum(x["sparse_pass_ms"] for x in stats)
+    sp_bytes = sum(x["sparse_pass_bytes"] for x in stats)
+    launches = fp_launches + sp_launches
+    pass_launch_ms = (fp_ms + sp_ms) / max(1, launches)
+    pass_bytes_per_launch = (fp_bytes + sp_bytes) / max(1, launches)
+    pass_gbs = pass_bytes_per_launch / (pass_launch_ms * 1e-3) / 1e9 if launches else 0.0
     s0 = stats[-1]
     tr = ncu_traffic()
-    traffic = round(tr["dram_bytes_per_amp"] * amps) if tr else None
+    # ncu DRAM bytes per amplitude of each pass kind (profiles/block_pass_traffic.json,
+    # from an ncu --set full capture of the same program family at 31 qubits),
+    # scaled to this slice and averaged over this step's launches like `achieved`
+    by_kind = (tr or {}).get("dram_bytes_per_amp_by_kind", {})
+    traffic = round((by_kind["full"] * fp_launches + by_kind["sparse"] * sp_launches) / launches * amps) \
+        if launches and "full" in by_kind and "sparse" in by_kind else None
     # program-level roofline: T_roof = sum over items, HBM-bound
     t_roof = (s0["block_bytes"] + s0["ims_bytes"]) / (peak * 1e9) + s0["xrs_bytes"] / 900e9
 
@@ -360,15 +372,24 @@ def main():
                      "achieved": round(pass_gbs, 1),
                      "peak": peak, "unit": "GB/s", "frac": round(pass_gbs / peak, 4),
                      "peak_source": peak_src, "traffic": traffic,
-                     "traffic_source": (tr["source"] + ", DRAM bytes/amp x this slice") if tr else None,
+                     "traffic_source": (tr["source"] + "; DRAM bytes/amp per pass kind x this slice") if traffic else None,
                      "algorithmic_bytes_per_launch": round(pass_bytes_per_launch),
-                     "launches_per_step": fp_launches // max(1, args.steps),
+                     "launches_per_step": launches // max(1, args.steps),
                      "avg_launch_ms": round(pass_launch_ms, 3),
-                     "excludes": "the run's first pass (memset of the slice + the single tile holding |initial>), "
-                                 "reported as breakdown.init_ms",
+                     "passes_per_step": {
+                         "full": {"launches": fp_launches // max(1, args.steps),
+                                  "ms": round(fp_ms / args.steps, 3),
+                                  "gbs": round(fp_bytes / max(1e-9, fp_ms * 1e-3) / 1e9, 1) if fp_ms else None},
+                         "sparse": {"launches": sp_launches // max(1, args.steps),
+                                    "ms": round(sp_ms / args.steps, 3),
+                                    "algorithmic_bytes": round(sp_bytes / args.steps),
+                                    "gbs": round(sp_bytes / max(1e-9, sp_ms * 1e-3) / 1e9, 1) if sp_ms else None}},
+                     "excludes": "the run's first pass (the single tile holding |initial>, no memset: the next pass "
+                                 "writes every tile), reported as breakdown.init_ms",
                      "fp64_peak_tflops_measured": 36.5,
                      "fp64_note": "DFMA 36.5 / DMMA 37.0 TF measured (profiles/r1_fp64_peak.txt)"},
         "breakdown": {"block_ms": round(s0["block_ms"], 2), "full_pass_ms": round(s0["full_pass_ms"], 2),
+                      "sparse_pass_ms": round(s0["sparse_pass_ms"], 2),
                       "init_ms": round(s0["init_ms"], 2), "ims_ms": round(s0["ims_ms"], 2),
                       "xrs_ms": round(s0["xrs_ms"], 2), "block_launches": s0["block_launches"],
                       "ims_launches": s0["ims_launches"], "xrs_rounds": s0["xrs_rounds"],
