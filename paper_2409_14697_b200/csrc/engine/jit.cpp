@@ -138,6 +138,31 @@ static __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, u32 
     memcpy(dst, src, bytes);
 #endif
 }
+// TMA bulk store of a contiguous shared-memory row to global memory (async
+// proxy, bulk group of the issuing thread), and the group waits.
+static __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, u32 bytes) {
+#ifdef __CUDA_ARCH__
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
+                 : "memory");
+#else
+    memcpy(dst, src, bytes);
+#endif
+}
+static __device__ __forceinline__ void bulk_commit() {
+#ifdef __CUDA_ARCH__
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+#endif
+}
+static __device__ __forceinline__ void bulk_wait_read() {  // sources of committed stores may be reused
+#ifdef __CUDA_ARCH__
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+#endif
+}
+static __device__ __forceinline__ void bulk_wait_all() {
+#ifdef __CUDA_ARCH__
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+#endif
+}
 // TMA-engine prefetch of a contiguous row into L2 (no registers, no smem).
 static __device__ __forceinline__ void pf_l2(const void* p, u32 bytes) {
 #ifdef __CUDA_ARCH__
@@ -305,7 +330,7 @@ public:
            << "  extern __shared__ double2 sm[];  // PB: next tile (linear tile coordinates) | XS | F | mbarrier\n"
            << "  double2* const XS = sm + 8192;\n  double2* const F = sm + 12288;\n"
            << "  u64* const mbar = (u64*)(sm + " << (12288 + qkdev::kMaxCtaFactors) << ");\n  const u32 tid = threadIdx.x;\n"
-           << "  const bool tma = basis == ~0ull;\n  u32 phase = 0u;\n"
+           << "  const bool tma = basis == ~0ull && smask == 0ull;  // sparse runs: no whole-tile streaming\n  u32 phase = 0u;\n"
            << "  if (tid == 0) mbar_init(mbar);\n  __syncthreads();\n"
            << "  if (tma && blockIdx.x < ntiles) {\n";
         issueTile("blockIdx.x", L);
@@ -321,7 +346,12 @@ public:
         o_ << "    }\n    __syncthreads();  // PB drained: stream the next tile into it\n"
            << "    if (tile + gridDim.x < ntiles) {\n";
         issueTile("tile + gridDim.x", L);
-        o_ << "    }\n  } else {  // first pass of a run: synthesize |basis>\n"
+        o_ << "    }\n  } else if (smask != 0ull) {  // known zeros: read only the support\n"
+           << "    const u64 off = base | " << threadGlobal(P_.map_in[0]) << ";\n";
+        for (int s = 0; s < na_; s++)
+            o_ << "    { const u64 i_ = off | " << regGlobal(P_.map_in[0], s) << "ull; a" << s
+               << " = ((i_ ^ sval) & smask) == 0ull ? __ldcs(st + i_) : C2(0.0, 0.0); }\n";
+        o_ << "  } else {  // first pass of a run: synthesize |basis>\n"
            << "    const u64 off = base | " << threadGlobal(P_.map_in[0]) << ";\n";
         for (int s = 0; s < na_; s++)
             o_ << "    a" << s << " = C2((off | " << regGlobal(P_.map_in[0], s) << "ull) == basis ? 1.0 : 0.0, 0.0);\n";
@@ -333,12 +363,24 @@ public:
         for (int j = 0; j < ct_; j++)
             if ((P_.xmask_out[last] >> j) & 1) gx |= uint64_t(1) << P_.tile_phys[j];
         if (P_.norm_out) emitNorm();
+        // Sparse runs (PB is free: no tile streams in): stage the output tile
+        // in PB and let the TMA engine write its rows, so the HBM write of this
+        // tile drains while the CTA computes the next one.
+        o_ << "  if (smask != 0ull) {\n    bulk_wait_read();  // this thread's previous rows have left PB\n"
+           << "    __syncthreads();\n    { const u32 u = " << threadSmem(P_.map_out[last]) << " ^ "
+           << uint32_t(P_.xmask_out[last]) << "u;\n";
+        for (int s = 0; s < na_; s++)
+            o_ << "    sm[u ^ " << regCoord(P_.map_out[last], s) << "u] = a" << nm_[size_t(s)] << ";\n";
+        o_ << "    }\n    fence_async();\n    __syncthreads();\n";
+        storeTile(L);
+        o_ << "  } else {\n";
         o_ << "  { const u64 off = (base | " << threadGlobal(P_.map_out[last]) << ") ^ " << gx << "ull;\n";
         for (int s = 0; s < na_; s++)
             o_ << "  __stcs(st + (off ^ " << regGlobal(P_.map_out[last], s) << "ull), a" << nm_[size_t(s)] << ");\n";
         // (TMA tiles re-synchronize after draining PB; synthesized tiles must
         // not start writing F / XS while a slow thread still reads them.)
-        o_ << "  }\n  if (!tma && tile + gridDim.x < ntiles) __syncthreads();\n  }\n}\n";
+        o_ << "  }\n  }\n  if (!tma && tile + gridDim.x < ntiles) __syncthreads();\n  }\n"
+           << "  if (smask != 0ull) bulk_wait_all();\n}\n";
         return o_.str();
     }
 
@@ -377,6 +419,17 @@ private:
             o_ << "    if ((tid & 31u) == 0u) np[(u64)tile * " << warps << "u + (tid >> 5)] = 0.0;\n";
         }
         o_ << "    continue;\n  }\n";
+    }
+    // The staged output tile (PB, linear tile coordinates) to global memory:
+    // one bulk store per contiguous row, rows spread over all threads, each
+    // thread committing its own bulk group.
+    void storeTile(int Lrun) {
+        const int L = std::min(Lrun, 8);  // rows of <= 4 KB
+        const int rows = 1 << (ct_ - L);
+        o_ << "    for (u32 r = tid; r < " << rows << "u; r += " << nt_ << "u) {\n      u64 o = base;\n";
+        for (int j = L; j < ct_; j++)
+            o_ << "      o |= (u64)((r >> " << (j - L) << ") & 1u) << " << int(P_.tile_phys[j]) << ";\n";
+        o_ << "      bulk_s2g(st + o, sm + (r << " << L << "), " << (16u << L) << "u);\n    }\n    bulk_commit();\n";
     }
     // Warp 0 streams tile `t` into PB: one cp.async.bulk per contiguous row.
     void issueTile(const std::string& t, int Lrun) {
@@ -832,7 +885,7 @@ private:
 // ---- compile / load / launch -------------------------------------------------
 
 // Bump when the generated code changes for the same PassParams (on-disk cache key).
-constexpr uint64_t kGeneratorVersion = 23;
+constexpr uint64_t kGeneratorVersion = 24;
 
 uint64_t hashPass(const PassParams& P) {
     uint64_t h = 1469598103934665603ull ^ (kGeneratorVersion * 0x9E3779B97F4A7C15ull) ^ (usePrefetch() ? 1u : 0u) ^ (usePersistent() ? 2u : 0u) ^
@@ -1160,7 +1213,6 @@ cudaError_t launch(const PassParams& P, double2* state, const double2* gtab, int
     const unsigned nt = 1u << (P.ct - P.rb);
     const unsigned smem = pipe ? unsigned(sizeof(double2) * kPipeSmemAmps)
                                : unsigned((sizeof(double2) << P.ct) + sizeof(double2) * qkdev::kMaxCtaFactors + 256);
-    if (smask && pipe) return cudaErrorInvalidValue;  // the TMA-pipelined kernels read whole tiles
     void* args[] = {&state, &gtab, &ntiles, &basis, &tile0, &np, &smask, &sval};
     if (driver().launchKernel(fn, ctas, 1, 1, nt, 1, 1, smem, stream, args, nullptr) != 0)
         return cudaErrorLaunchFailure;

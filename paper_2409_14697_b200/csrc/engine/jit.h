@@ -31,7 +31,8 @@ void prepare(const std::vector<const qkdev::PassParams*>& passes, int device);
 // from a basis state whose passes have not yet touched every bit): tiles
 // outside it are written as zeros with no reads or arithmetic, and inside
 // only the in-support amplitudes are read -- the slice need not be valid
-// elsewhere.  zeroFill (basis passes): memset the slice first; false when
+// elsewhere.  The TMA-pipelined kernels then stage each output tile in
+// shared memory and write it with TMA bulk stores.  zeroFill (basis passes): memset the slice first; false when
 // the next pass is launched with smask and so writes every tile itself.
 cudaError_t launch(const qkdev::PassParams& P, double2* state, const double2* gtab, int nLocal, uint64_t basis,
                    cudaStream_t stream, double* np = nullptr, uint64_t smask = 0, uint64_t sval = 0,

@@ -749,15 +749,6 @@ struct Support {
     uint64_t mask = 0, val = 0;
 };
 
-// A pass step with a variant that is not TMA-pipelined (those stream whole
-// tiles, so they cannot run with known zeros).
-bool hasPlainVariant(const qkeng::Step& s) {
-    if (!qkjit::pipelinedPass(*s.pass)) return true;
-    for (const auto& a : s.alts)
-        if (!qkjit::pipelinedPass(*a)) return true;
-    return false;
-}
-
 void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_run_stats& rs,
               uint64_t basis = kNoBasis, Timer* timer = nullptr, Support* sup = nullptr) {
     const double amps = double(st->count);
@@ -767,22 +758,16 @@ void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_ru
         if (s.kind == qkeng::Step::Pass) {
             const bool jit = useJit(st->nLocal);
             // known zeros in this pass's input (not for the basis-synthesizing pass)
-            const uint64_t smask = (jit && sup && basis == kNoBasis && hasPlainVariant(s)) ? sup->mask : 0;
+            const uint64_t smask = (jit && sup && basis == kNoBasis) ? sup->mask : 0;
             // Register-width autotune: the first two executions of a pass time
             // each variant (events, synchronous); later ones take the faster.
-            // A pass that runs with known zeros never uses the TMA-pipelined
-            // variant (it streams whole tiles).
+            // (With known zeros the TMA-pipelined variant reads only the
+            // support and writes its tiles through TMA bulk stores.)
             const int nv = 1 + int(s.alts.size());
             int v = 0;
             bool timing = false;
             if (s.tune) {
                 std::lock_guard<std::mutex> lk(tuneMu());
-                if (smask)
-                    for (int k = 0; k < nv; k++)
-                        if (qkjit::pipelinedPass(k ? *s.alts[size_t(k - 1)] : *s.pass)) {
-                            s.tune->ms[k] = 1e30f;
-                            s.tune->runs[k] = std::max(s.tune->runs[k], 1);
-                        }
                 v = s.tune->choice(nv);
                 timing = s.tune->runs[v] == 0;
             }
@@ -791,8 +776,7 @@ void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_ru
             // skipped when the next step is a specialized pass that writes
             // every tile itself (launched with the known zeros).
             const bool zeroFill = !(sup && sup->mask && jit && basis != kNoBasis && (basis >> st->nLocal) == 0 &&
-                                    si + 1 < ci.steps.size() && ci.steps[si + 1].kind == qkeng::Step::Pass &&
-                                    hasPlainVariant(ci.steps[si + 1]));
+                                    si + 1 < ci.steps.size() && ci.steps[si + 1].kind == qkeng::Step::Pass);
             cudaEvent_t e0 = nullptr, e1 = nullptr;
             if (timing) {
                 cuda(cudaEventCreate(&e0), "event");

@@ -90,6 +90,10 @@ for kind, n, a in (("qft", 16, 0), ("qaoa", 15, 1)):
         st = np.zeros(1 << n, dtype=np.complex128); st[5] = 1
         run_program_jit(qk, port, prog, n, st, basis=basis)
         assert np.max(np.abs(st - want)) < 1e-10, (kind, basis)
+    # sparse start: support-only reads, output tiles through TMA bulk stores
+    st = np.full(1 << n, np.nan, dtype=np.complex128)
+    run_program_jit_sparse(qk, port, prog, n, st, 5)
+    assert not np.isnan(st).any() and np.max(np.abs(st - want)) < 1e-10, (kind, "sparse")
 print("ok")
 """ % (ROOT, os.path.join(ROOT, "oracle"), os.path.join(ROOT, "tests"))
     env = dict(os.environ, QK_JIT_TMA="1")
