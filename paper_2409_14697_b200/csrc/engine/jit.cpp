@@ -234,6 +234,7 @@ bool pipelined(const PassParams& P) {
 }
 }  // namespace
 bool pipelinedPass(const PassParams& P) { return pipelined(P); }
+int lowRunOf(const PassParams& P) { return lowRun(P); }
 namespace {
 constexpr int kPipeSmemAmps = (1 << 13) + (1 << 12) + qkdev::kMaxCtaFactors + 1;  // PB | XS | F | mbarrier
 
@@ -254,7 +255,7 @@ public:
         o_ << kPrologue;
         ctaTables();
         o_ << "extern \"C\" __global__ void __launch_bounds__(" << nt_ << "," << minb << ") " << name
-           << "(double2* __restrict__ st, const double2* __restrict__ gt, const u32 ntiles, const u64 basis, const u32 tile0, double* __restrict__ np, const u64 smask, const u64 sval) {\n";
+           << "(double2* __restrict__ st, const double2* __restrict__ gt, const u32 ntiles, const u64 basis, const u32 tile0, double* __restrict__ np, const u64 smask, const u64 sval, const u32 zskip) {\n";
         o_ << "  extern __shared__ double2 sm[];\n  double2* const F = sm + " << (1 << ct_)
            << ";\n  const u32 tid = threadIdx.x;\n";
         o_ << "  for (u32 tile = blockIdx.x + tile0; tile < ntiles; tile += gridDim.x) {\n";
@@ -326,7 +327,7 @@ public:
         o_ << kPrologue;
         ctaTables();
         o_ << "extern \"C\" __global__ void __launch_bounds__(" << nt_ << ",1) " << name
-           << "(double2* __restrict__ st, const double2* __restrict__ gt, const u32 ntiles, const u64 basis, const u32 tile0, double* __restrict__ np, const u64 smask, const u64 sval) {\n"
+           << "(double2* __restrict__ st, const double2* __restrict__ gt, const u32 ntiles, const u64 basis, const u32 tile0, double* __restrict__ np, const u64 smask, const u64 sval, const u32 zskip) {\n"
            << "  extern __shared__ double2 sm[];  // PB: next tile (linear tile coordinates) | XS | F | mbarrier\n"
            << "  double2* const XS = sm + 8192;\n  double2* const F = sm + 12288;\n"
            << "  u64* const mbar = (u64*)(sm + " << (12288 + qkdev::kMaxCtaFactors) << ");\n  const u32 tid = threadIdx.x;\n"
@@ -404,7 +405,8 @@ private:
     void zeroTile() {
         o_ << "  if ((basis != ~0ull && ((basis ^ base) & " << (~P_.tile_mask) << "ull) != 0ull) ||\n"
            << "      ((base ^ sval) & smask & " << (~P_.tile_mask) << "ull) != 0ull) {\n"
-           << "    const u64 zoff = base | " << threadGlobal(P_.map_in[0]) << ";\n";
+           << "    const u64 zoff = base | " << threadGlobal(P_.map_in[0]) << ";\n"
+           << "    if (!zskip) {  // else a coalesced zero-fill kernel writes the tiles outside the support\n";
         const int kl = slotOfMem0(P_.map_in[0]);
         for (int s = 0; s < na_; s++) {
             if (kl >= 0) {
@@ -414,6 +416,7 @@ private:
             }
             o_ << "    __stcs(st + (zoff | " << regGlobal(P_.map_in[0], s) << "ull), C2(0.0, 0.0));\n";
         }
+        o_ << "    }\n";
         if (P_.norm_out) {  // this tile's share of sum |a|^2 is 0
             const int warps = nt_ / 32 > 0 ? nt_ / 32 : 1;
             o_ << "    if ((tid & 31u) == 0u) np[(u64)tile * " << warps << "u + (tid >> 5)] = 0.0;\n";
@@ -885,7 +888,7 @@ private:
 // ---- compile / load / launch -------------------------------------------------
 
 // Bump when the generated code changes for the same PassParams (on-disk cache key).
-constexpr uint64_t kGeneratorVersion = 24;
+constexpr uint64_t kGeneratorVersion = 25;
 
 uint64_t hashPass(const PassParams& P) {
     uint64_t h = 1469598103934665603ull ^ (kGeneratorVersion * 0x9E3779B97F4A7C15ull) ^ (usePrefetch() ? 1u : 0u) ^ (usePersistent() ? 2u : 0u) ^
@@ -1184,7 +1187,7 @@ void prepare(const std::vector<const PassParams*>& passes, int device) {
 }
 
 cudaError_t launch(const PassParams& P, double2* state, const double2* gtab, int nLocal, uint64_t basis,
-                   cudaStream_t stream, double* np, uint64_t smask, uint64_t sval, bool zeroFill) {
+                   cudaStream_t stream, double* np, uint64_t smask, uint64_t sval, bool zeroFill, bool zeroSkip) {
     int dev = 0;
     cudaGetDevice(&dev);
     void* fn = functionFor(P, hashPass(P), dev);
@@ -1213,7 +1216,8 @@ cudaError_t launch(const PassParams& P, double2* state, const double2* gtab, int
     const unsigned nt = 1u << (P.ct - P.rb);
     const unsigned smem = pipe ? unsigned(sizeof(double2) * kPipeSmemAmps)
                                : unsigned((sizeof(double2) << P.ct) + sizeof(double2) * qkdev::kMaxCtaFactors + 256);
-    void* args[] = {&state, &gtab, &ntiles, &basis, &tile0, &np, &smask, &sval};
+    unsigned zskip = zeroSkip ? 1u : 0u;
+    void* args[] = {&state, &gtab, &ntiles, &basis, &tile0, &np, &smask, &sval, &zskip};
     if (driver().launchKernel(fn, ctas, 1, 1, nt, 1, 1, smem, stream, args, nullptr) != 0)
         return cudaErrorLaunchFailure;
     return cudaSuccess;

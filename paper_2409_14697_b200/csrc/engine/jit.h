@@ -36,7 +36,12 @@ void prepare(const std::vector<const qkdev::PassParams*>& passes, int device);
 // the next pass is launched with smask and so writes every tile itself.
 cudaError_t launch(const qkdev::PassParams& P, double2* state, const double2* gtab, int nLocal, uint64_t basis,
                    cudaStream_t stream, double* np = nullptr, uint64_t smask = 0, uint64_t sval = 0,
-                   bool zeroFill = true);
+                   bool zeroFill = true, bool zeroSkip = false);
+// zeroSkip: tiles outside the support are not written by the pass (a
+// separate coalesced zero-fill covers them: passes whose tiles have short
+// rows write zeros inefficiently).
+// Contiguous low memory bits of P's tile (row length 2^lowRun amplitudes).
+int lowRunOf(const qkdev::PassParams& P);
 
 // Slices with at least this many local qubits use specialized kernels
 // (QK_JIT_MIN_QUBITS, default 22; -1 disables).

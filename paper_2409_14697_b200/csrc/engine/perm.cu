@@ -362,6 +362,24 @@ __global__ void __launch_bounds__(256) k_sum_partial(const double* __restrict__ 
 
 __global__ void k_set_basis(double2* a, uint64_t idx) { a[idx] = make_double2(1.0, 0.0); }
 
+// Zeros at every i with ((i ^ val) & m) != 0: the tiles a sparse pass skips
+// (outside its input's support), written as one coalesced stream of 32-B
+// stores instead of tile by tile (tiles with short rows).
+__global__ void __launch_bounds__(256) k_zero_outside(double2* __restrict__ a, uint64_t n, uint64_t m, uint64_t val) {
+    const uint64_t stride = 2 * uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t i = 2 * (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x); i < n; i += stride) {
+        const bool z0 = ((i ^ val) & m) != 0, z1 = (((i | 1) ^ val) & m) != 0;
+        const double2 z = make_double2(0.0, 0.0);
+        if (z0 && z1) {
+            asm volatile("st.global.cs.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(a + i), "d"(0.0), "d"(0.0), "d"(0.0), "d"(0.0)
+                         : "memory");
+        } else {
+            if (z0) __stcs(a + i, z);
+            if (z1) __stcs(a + i + 1, z);
+        }
+    }
+}
+
 // Marginal probabilities over k <= 10 slice bits: part[block][v] = sum of
 // |a_i|^2 over this block's range with bits(i) = v (bit j of v = slice bit
 // bits[j]).  Shared-memory atomics within a block; blocks fold in order.
@@ -622,6 +640,11 @@ cudaError_t launchMarginal(const double2* a, uint64_t n, const int* bits, int k,
     for (int j = 0; j < k; j++) m.bits[j] = bits[j];
     k_marginal_partial<<<kMargBlocks, 256, 0, st>>>(a, n, m, scratch);
     k_marginal_final<<<((1 << k) + 255) / 256, 256, 0, st>>>(scratch, kMargBlocks, 1 << k, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launchZeroOutside(double2* a, uint64_t n, uint64_t m, uint64_t val, int smCount, cudaStream_t st) {
+    k_zero_outside<<<unsigned(smCount) * 8u, 256, 0, st>>>(a, n, m, val);
     return cudaGetLastError();
 }
 

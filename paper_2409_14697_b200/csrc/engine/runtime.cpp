@@ -44,6 +44,7 @@ cudaError_t launchNorm(const double2*, uint64_t, double*, double*, cudaStream_t)
 cudaError_t launchSumTiles(const double*, uint64_t, double*, double*, cudaStream_t);
 size_t normScratchDoubles();
 cudaError_t launchSetBasis(double2*, uint64_t, cudaStream_t);
+cudaError_t launchZeroOutside(double2*, uint64_t, uint64_t, uint64_t, int, cudaStream_t);
 cudaError_t launchMarginal(const double2*, uint64_t, const int*, int, double*, double*, cudaStream_t);
 size_t marginalScratchDoubles(int k);
 }  // namespace qkdev
@@ -795,16 +796,26 @@ void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_ru
                     st->normTilesCap = tiles;
                 }
             }
+            // Tiles with rows under 128 B write zeros inefficiently: a sparse
+            // pass over such tiles leaves the ones outside the support to one
+            // coalesced zero-fill (disjoint from the support, so any order).
+            const bool zeroSkip = smask && qkjit::lowRunOf(P) < 3;
             auto launchPass = [&] {
+                if (zeroSkip)
+                    cuda(qkdev::launchZeroOutside(st->amps, st->count, smask & ~P.tile_mask, sup->val,
+                                                  smCountOf(st->device), st->stream),
+                         "zero-fill outside the support");
                 if (jit)
                     cuda(qkjit::launch(P, st->amps, t.gtab, st->nLocal, basis, st->stream,
-                                       P.norm_out ? st->normTiles : nullptr, smask, smask ? sup->val : 0, zeroFill),
+                                       P.norm_out ? st->normTiles : nullptr, smask, smask ? sup->val : 0, zeroFill,
+                                       zeroSkip),
                          "specialized block pass");
                 else
                     cuda(qkdev::launchBlockPass(st->amps, t.gtab, P, st->nLocal, basis, st->stream), "block pass");
             };
             if (timer) timer->time(basis != kNoBasis ? 4 : smask ? 5 : 3, launchPass);
             else launchPass();
+            if (zeroSkip) rs.kernel_launches++;
             // algorithmic bytes: write every amplitude; read those not known to be zero
             if (basis != kNoBasis) {
                 rs.block_bytes += zeroFill ? 16.0 * amps : 16.0 * double(uint64_t(1) << P.ct);

@@ -84,7 +84,7 @@ extern "C" double2 sm[1 << 14];
                 ts.emplace_back([=] {                                                         \
                     qk_tl_tid = t;                                                            \
                     qk_tl_bid = b;                                                            \
-                    KERNEL(st, gt, ntiles, basis, tile0, np, smask, sval);                    \
+                    KERNEL(st, gt, ntiles, basis, tile0, np, smask, sval, 0u);                    \
                 });                                                                           \
             for (auto& th : ts) th.join();                                                    \
         }                                                                                     \
