@@ -16,6 +16,7 @@
 #include <nvrtc.h>
 
 #include <algorithm>
+#include <cmath>
 #include <atomic>
 #include <cerrno>
 #include <cstdio>
@@ -581,8 +582,18 @@ private:
     }
 
     std::string lc(uint32_t i) const { return c2(P_.coef[2 * i], P_.coef[2 * i + 1]); }
+    // Phase literals: a part below 2^-50 of a unit-modulus coefficient is the
+    // rounding residue of cos / sin at a multiple of pi/2 (cos(pi/2) =
+    // 6.1e-17); it is taken as 0 so the multiply specializes.  This moves
+    // results by < 1e-16 relative per multiply (the north star's bar is 1e-10).
+    static void snap(double& re, double& im) {
+        const double tiny = 0x1p-50;
+        if (std::fabs(re) < tiny && std::fabs(std::fabs(im) - 1.0) < tiny) re = 0.0, im = im > 0 ? 1.0 : -1.0;
+        if (std::fabs(im) < tiny && std::fabs(std::fabs(re) - 1.0) < tiny) im = 0.0, re = re > 0 ? 1.0 : -1.0;
+    }
     // x * (re + i im) for a literal coefficient, specialized when a part is 0.
     static std::string mulK(const std::string& x, double re, double im) {
+        snap(re, im);
         if (re == 0.0 && im == 0.0) return "C2(0.0, 0.0)";
         if (im == 0.0) return re == 1.0 ? x : "cmulr(" + x + ", " + lit(re) + ")";
         if (re == 0.0) return "cmuli(" + x + ", " + lit(im) + ")";
@@ -590,6 +601,7 @@ private:
     }
     // acc + (re + i im) * x
     static std::string macK(const std::string& acc, double re, double im, const std::string& x) {
+        snap(re, im);
         if (re == 0.0 && im == 0.0) return acc;
         if (im == 0.0) return "cmacr(" + acc + ", " + lit(re) + ", " + x + ")";
         if (re == 0.0) return "cmaci(" + acc + ", " + lit(im) + ", " + x + ")";
@@ -728,17 +740,21 @@ private:
                     if ((d.b >> k) & 1) bits.push_back(k);
                 const int ng = 1 << bits.size();
                 o_ << "  {\n";
-                for (int j = 0; j < ng; j++) {
-                    const std::string g = lc(d.c + uint32_t(j));
-                    o_ << "    const double2 h" << j << " = " << (dirtyR_[a] ? mulC("R" + std::to_string(a), d.c + uint32_t(j)) : g)
-                       << ";\n";
-                }
+                if (dirtyR_[a])
+                    for (int j = 0; j < ng; j++)
+                        o_ << "    const double2 h" << j << " = " << mulC("R" + std::to_string(a), d.c + uint32_t(j)) << ";\n";
                 for (int s = 0; s < na_; s++) {
                     if (!((s >> a) & 1)) continue;
                     int j = 0;
                     for (size_t q = 0; q < bits.size(); q++) j |= ((s >> bits[q]) & 1) << q;
-                    o_ << "  ";
-                    mulAmp(s, "h" + std::to_string(j));
+                    if (dirtyR_[a]) {
+                        o_ << "  ";
+                        mulAmp(s, "h" + std::to_string(j));
+                        continue;
+                    }
+                    // literal factor: specialized multiply (none at all for 1)
+                    const std::string m = mulC(A(s), d.c + uint32_t(j));
+                    if (m != A(s)) o_ << "  " << A(s) << " = " << m << ";\n";
                 }
                 o_ << "  }\n";
                 if (dirtyR_[a]) o_ << "  R" << a << " = C2(1.0, 0.0);\n";
@@ -888,7 +904,7 @@ private:
 // ---- compile / load / launch -------------------------------------------------
 
 // Bump when the generated code changes for the same PassParams (on-disk cache key).
-constexpr uint64_t kGeneratorVersion = 25;
+constexpr uint64_t kGeneratorVersion = 26;
 
 uint64_t hashPass(const PassParams& P) {
     uint64_t h = 1469598103934665603ull ^ (kGeneratorVersion * 0x9E3779B97F4A7C15ull) ^ (usePrefetch() ? 1u : 0u) ^ (usePersistent() ? 2u : 0u) ^
