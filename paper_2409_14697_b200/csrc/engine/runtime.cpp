@@ -717,6 +717,16 @@ bool sparseStart() {
     return v;
 }
 
+// QK_DEFER_ZEROS (default 1): a sparse pass followed by another sparse pass
+// leaves its zero tiles unwritten (the chain's last pass writes them).
+bool deferZeros() {
+    static const bool v = [] {
+        const char* e = std::getenv("QK_DEFER_ZEROS");
+        return !e || std::atoi(e) != 0;
+    }();
+    return v;
+}
+
 // QK_DENSE_MODE: 0 = DFMA, 1 = DMMA (FP64 tensor cores) for the U5 tile
 // kernel; unset = time both on a step's first executions, keep the faster.
 std::atomic<int>& denseModeVar() {
@@ -799,9 +809,19 @@ void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_ru
             // Tiles with rows under 128 B write zeros inefficiently: a sparse
             // pass over such tiles leaves the ones outside the support to one
             // coalesced zero-fill (disjoint from the support, so any order).
-            const bool zeroSkip = smask && qkjit::lowRunOf(P) < 3;
+            //
+            // Deferred zeros: when the support is still partial after this pass
+            // and the next step is a pass that runs with it, this pass need
+            // not write its zero tiles at all -- the next pass reads only
+            // inside the support (= this pass's written tiles), and the last
+            // pass of the chain writes every tile.  QFT-33's middle pass then
+            // computes only the tiles meeting the support.
+            const bool nextSparse = smask && (smask & ~P.tile_mask) && si + 1 < ci.steps.size() &&
+                                    ci.steps[si + 1].kind == qkeng::Step::Pass && deferZeros();
+            const bool fillShort = smask && !nextSparse && qkjit::lowRunOf(P) < 3;
+            const bool zeroSkip = nextSparse || fillShort;
             auto launchPass = [&] {
-                if (zeroSkip)
+                if (fillShort)
                     cuda(qkdev::launchZeroOutside(st->amps, st->count, smask & ~P.tile_mask, sup->val,
                                                   smCountOf(st->device), st->stream),
                          "zero-fill outside the support");
@@ -815,12 +835,13 @@ void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_ru
             };
             if (timer) timer->time(basis != kNoBasis ? 4 : smask ? 5 : 3, launchPass);
             else launchPass();
-            if (zeroSkip) rs.kernel_launches++;
+            if (fillShort) rs.kernel_launches++;
             // algorithmic bytes: write every amplitude; read those not known to be zero
             if (basis != kNoBasis) {
                 rs.block_bytes += zeroFill ? 16.0 * amps : 16.0 * double(uint64_t(1) << P.ct);
             } else if (smask) {
-                const double b = 16.0 * amps + 16.0 * std::ldexp(amps, -__builtin_popcountll(smask));
+                const double written = nextSparse ? std::ldexp(amps, -__builtin_popcountll(smask & ~P.tile_mask)) : amps;
+                const double b = 16.0 * written + 16.0 * std::ldexp(amps, -__builtin_popcountll(smask));
                 rs.sparse_pass_launches++;
                 rs.sparse_pass_bytes += b;
                 rs.block_bytes += b;

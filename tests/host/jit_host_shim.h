@@ -64,7 +64,8 @@ extern "C" double2 sm[1 << 14];
     double2 sm[1 << 14];                                                                      \
     extern "C" void qk_host_launch2(double2* st, const double2* gt, int nLocal, int ct, int rb,   \
                                     unsigned long long basis, unsigned tile0, unsigned tiles,   \
-                                    unsigned long long smask, unsigned long long sval) {        \
+                                    unsigned long long smask, unsigned long long sval,          \
+                                    unsigned zskip) {                                           \
         const unsigned ntiles = tiles ? tiles : 1u << (nLocal - ct), nt = 1u << (ct - rb);   \
         std::vector<double> npv(size_t(ntiles) * (nt >= 32u ? nt / 32u : 1u)); /* norm partials */ \
         double* const np = npv.data();                                                        \
@@ -84,12 +85,12 @@ extern "C" double2 sm[1 << 14];
                 ts.emplace_back([=] {                                                         \
                     qk_tl_tid = t;                                                            \
                     qk_tl_bid = b;                                                            \
-                    KERNEL(st, gt, ntiles, basis, tile0, np, smask, sval, 0u);                    \
+                    KERNEL(st, gt, ntiles, basis, tile0, np, smask, sval, zskip);                    \
                 });                                                                           \
             for (auto& th : ts) th.join();                                                    \
         }                                                                                     \
     }                                                                                         \
     extern "C" void qk_host_launch(double2* st, const double2* gt, int nLocal, int ct, int rb,    \
                                    unsigned long long basis) {                              \
-        qk_host_launch2(st, gt, nLocal, ct, rb, basis, 0u, 0u, 0ull, 0ull);                    \
+        qk_host_launch2(st, gt, nLocal, ct, rb, basis, 0u, 0u, 0ull, 0ull, 0u);                \
     }

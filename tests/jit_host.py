@@ -30,7 +30,7 @@ def host_kernel(name: str, src: str):
     lib = C.CDLL(so)
     lib.qk_host_launch.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_uint64]
     lib.qk_host_launch2.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_uint,
-                                    C.c_uint, C.c_uint64, C.c_uint64]
+                                    C.c_uint, C.c_uint64, C.c_uint64, C.c_uint]
     return lib.qk_host_launch if not sparse_launch else lib.qk_host_launch2
 
 
@@ -105,7 +105,8 @@ def run_program_jit_sparse(qk, port, prog, n_local, state, initial):
         if it["kind"] == 0:
             blk = it["block"]
             gt = np.array(blk["gtab"] if blk["gtab"] else [0.0, 0.0], dtype=np.float64)
-            for st in blk["steps"]:
+            steps = blk["steps"]
+            for si, st in enumerate(steps):
                 if st["kind"] != 0:
                     run_steps(state, n_local, {"gtab": blk["gtab"], "steps": [st]})
                     for q in st["targets"]:
@@ -120,11 +121,15 @@ def run_program_jit_sparse(qk, port, prog, n_local, state, initial):
                         if not (tmask >> b) & 1:
                             t |= ((basis >> b) & 1) << q
                             q += 1
-                    fn(state.ctypes.data, gt.ctypes.data, n_local, st["ct"], st["rb"], basis, t, t + 1, 0, 0)
+                    fn(state.ctypes.data, gt.ctypes.data, n_local, st["ct"], st["rb"], basis, t, t + 1, 0, 0, 0)
                     first = False
                 else:
+                    # deferred zeros (as the runtime): a sparse pass followed by a pass,
+                    # with the support still partial after it, leaves its zero tiles unwritten
+                    nxt = si + 1 < len(steps) and steps[si + 1]["kind"] == 0
+                    zskip = 1 if (smask and (smask & ~tmask) and nxt) else 0
                     fn(state.ctypes.data, gt.ctypes.data, n_local, st["ct"], st["rb"], NO_BASIS, 0, 0, smask,
-                       sval if smask else 0)
+                       sval if smask else 0, zskip)
                 smask &= ~tmask
         elif it["kind"] == 1:
             pairs = [tuple(p) for p in it["pairs"]]
