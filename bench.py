@@ -450,7 +450,22 @@ def cpu_baseline(args, kind, n, st, qk):
                       f"({items_t} items); a {n}-qubit host state needs {16 * 2**n / 2**30:.0f} GiB",
             "measured_pair": {"workload": f"{kind.upper()}-{ns}, same program, this box",
                               "cpu_s": round(sec, 3), "gpu_s": round(gpu_s, 5),
-                              "cpu_over_gpu": round(sec / gpu_s, 1) if gpu_s else None}}
+                              "cpu_over_gpu": round(sec / gpu_s, 1) if gpu_s else None},
+            "full_size_check": full_size_reference(kind, n)}
+
+
+def full_size_reference(kind, n):
+    """The one full-size reference run on record (not this run: it takes ~8 min
+    and 128 GiB of host RAM; profiles/r2_reference_cpu_full_size.json)."""
+    path = os.path.join(ROOT, "profiles", "r2_reference_cpu_full_size.json")
+    if not os.path.exists(path):
+        return None
+    d = json.load(open(path))
+    for r in d.get("runs", []):
+        if r.get("workload", "").startswith(f"{kind.upper()}-{n} "):
+            return {"workload": r["workload"], "cpu_s": r["simulate_s"], "threads": r["threads"],
+                    "source": "profiles/r2_reference_cpu_full_size.json (tools/ref_cpu_full.py, gpurun box host)"}
+    return None
 
 
 def run_reference(args, rank, n, R, kind):
