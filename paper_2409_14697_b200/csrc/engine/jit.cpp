@@ -260,7 +260,7 @@ public:
         o_ << "  extern __shared__ double2 sm[];\n  double2* const F = sm + " << (1 << ct_)
            << ";\n  const u32 tid = threadIdx.x;\n";
         o_ << "  for (u32 tile = blockIdx.x + tile0; tile < ntiles; tile += gridDim.x) {\n";
-        o_ << "  " << deposit("base", "(u64)tile") << "\n";
+        o_ << "  " << tileBase() << "\n";
         zeroTile();
         std::string decl = "  double2 ";
         for (int s = 0; s < na_; s++) decl += (s ? ", a" : "a") + std::to_string(s);
@@ -337,7 +337,7 @@ public:
            << "  if (tma && blockIdx.x < ntiles) {\n";
         issueTile("blockIdx.x", L);
         o_ << "  }\n  for (u32 tile = blockIdx.x + tile0; tile < ntiles; tile += gridDim.x) {\n"
-           << "  " << deposit("base", "(u64)tile") << "\n";
+           << "  " << tileBase() << "\n";
         zeroTile();
         std::string decl = "  double2 ";
         for (int s = 0; s < na_; s++) decl += (s ? ", a" : "a") + std::to_string(s);
@@ -458,6 +458,18 @@ private:
         for (int k = 0; k < rb_; k++)
             if ((s >> k) & 1) u |= 1u << m[k];
         return u;
+    }
+    // Base index of tile `tile`.  zskip == 2: only the tiles meeting the
+    // support {i : (i ^ sval) & smask == 0} are enumerated -- the tile index
+    // is deposited into the non-tile bits the support leaves free, and the
+    // fixed ones come from sval (the pass runs on 2^free tiles instead of
+    // launching every tile to skip most of them).
+    std::string tileBase() const {
+        const std::string all = deposit("base", "(u64)tile");
+        const std::string nt = std::to_string(~P_.tile_mask) + "ull";
+        return all + "\n  if (zskip == 2u) {\n    const u64 fixed_ = smask & " + nt + ";\n" +
+               "    u64 m_ = " + nt + " & ~fixed_, t_ = (u64)tile;\n    base = sval & fixed_;\n" +
+               "    while (t_) { const u64 low_ = m_ & (0ull - m_); if (t_ & 1ull) base |= low_; t_ >>= 1; m_ ^= low_; }\n  }";
     }
     // CTA index deposited into the non-tile bits of the slice index.
     // Statement block declaring `u64 var` = v deposited into the non-tile bits.
@@ -904,7 +916,7 @@ private:
 // ---- compile / load / launch -------------------------------------------------
 
 // Bump when the generated code changes for the same PassParams (on-disk cache key).
-constexpr uint64_t kGeneratorVersion = 26;
+constexpr uint64_t kGeneratorVersion = 27;
 
 uint64_t hashPass(const PassParams& P) {
     uint64_t h = 1469598103934665603ull ^ (kGeneratorVersion * 0x9E3779B97F4A7C15ull) ^ (usePrefetch() ? 1u : 0u) ^ (usePersistent() ? 2u : 0u) ^
@@ -1203,7 +1215,7 @@ void prepare(const std::vector<const PassParams*>& passes, int device) {
 }
 
 cudaError_t launch(const PassParams& P, double2* state, const double2* gtab, int nLocal, uint64_t basis,
-                   cudaStream_t stream, double* np, uint64_t smask, uint64_t sval, bool zeroFill, bool zeroSkip) {
+                   cudaStream_t stream, double* np, uint64_t smask, uint64_t sval, bool zeroFill, int zeroSkip) {
     int dev = 0;
     cudaGetDevice(&dev);
     void* fn = functionFor(P, hashPass(P), dev);
@@ -1226,13 +1238,15 @@ cudaError_t launch(const PassParams& P, double2* state, const double2* gtab, int
         ntiles = t + 1;
         ctas = 1;
     } else {
+        if (zeroSkip == 2)  // only the tiles meeting the support
+            ntiles = unsigned(uint64_t(1) << (nLocal - P.ct - __builtin_popcountll(smask & ~P.tile_mask)));
         const unsigned resident = unsigned(smCount(dev) * blocksPerSm(P.ct, P.rb));
         ctas = (ntiles < resident || !(usePersistent() || pipe)) ? ntiles : resident;
     }
     const unsigned nt = 1u << (P.ct - P.rb);
     const unsigned smem = pipe ? unsigned(sizeof(double2) * kPipeSmemAmps)
                                : unsigned((sizeof(double2) << P.ct) + sizeof(double2) * qkdev::kMaxCtaFactors + 256);
-    unsigned zskip = zeroSkip ? 1u : 0u;
+    unsigned zskip = unsigned(zeroSkip);
     void* args[] = {&state, &gtab, &ntiles, &basis, &tile0, &np, &smask, &sval, &zskip};
     if (driver().launchKernel(fn, ctas, 1, 1, nt, 1, 1, smem, stream, args, nullptr) != 0)
         return cudaErrorLaunchFailure;

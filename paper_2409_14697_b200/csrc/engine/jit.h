@@ -36,10 +36,12 @@ void prepare(const std::vector<const qkdev::PassParams*>& passes, int device);
 // the next pass is launched with smask and so writes every tile itself.
 cudaError_t launch(const qkdev::PassParams& P, double2* state, const double2* gtab, int nLocal, uint64_t basis,
                    cudaStream_t stream, double* np = nullptr, uint64_t smask = 0, uint64_t sval = 0,
-                   bool zeroFill = true, bool zeroSkip = false);
-// zeroSkip: tiles outside the support are not written by the pass (a
-// separate coalesced zero-fill covers them: passes whose tiles have short
-// rows write zeros inefficiently).
+                   bool zeroFill = true, int zeroSkip = 0);
+// zeroSkip (with smask): 0 = tiles outside the support are written as zeros;
+// 1 = they are not written (a separate coalesced zero-fill covers them:
+// passes whose tiles have short rows write zeros inefficiently); 2 = only the
+// tiles meeting the support are launched at all (deferred zeros: the next
+// pass reads only the support and a later pass writes every tile).
 // Contiguous low memory bits of P's tile (row length 2^lowRun amplitudes).
 int lowRunOf(const qkdev::PassParams& P);
 

@@ -828,7 +828,7 @@ void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_ru
                 if (jit)
                     cuda(qkjit::launch(P, st->amps, t.gtab, st->nLocal, basis, st->stream,
                                        P.norm_out ? st->normTiles : nullptr, smask, smask ? sup->val : 0, zeroFill,
-                                       zeroSkip),
+                                       nextSparse && !P.norm_out ? 2 : zeroSkip ? 1 : 0),
                          "specialized block pass");
                 else
                     cuda(qkdev::launchBlockPass(st->amps, t.gtab, P, st->nLocal, basis, st->stream), "block pass");

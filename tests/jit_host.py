@@ -127,9 +127,11 @@ def run_program_jit_sparse(qk, port, prog, n_local, state, initial):
                     # deferred zeros (as the runtime): a sparse pass followed by a pass,
                     # with the support still partial after it, leaves its zero tiles unwritten
                     nxt = si + 1 < len(steps) and steps[si + 1]["kind"] == 0
-                    zskip = 1 if (smask and (smask & ~tmask) and nxt) else 0
-                    fn(state.ctypes.data, gt.ctypes.data, n_local, st["ct"], st["rb"], NO_BASIS, 0, 0, smask,
-                       sval if smask else 0, zskip)
+                    defer = bool(smask and (smask & ~tmask) and nxt)
+                    # deferred zeros launch only the tiles meeting the support (zskip 2)
+                    tiles = 1 << (n_local - st["ct"] - bin(smask & ~tmask).count("1")) if defer else 0
+                    fn(state.ctypes.data, gt.ctypes.data, n_local, st["ct"], st["rb"], NO_BASIS, 0, tiles, smask,
+                       sval if smask else 0, 2 if defer else 0)
                 smask &= ~tmask
         elif it["kind"] == 1:
             pairs = [tuple(p) for p in it["pairs"]]
