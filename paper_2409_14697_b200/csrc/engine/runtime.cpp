@@ -780,7 +780,7 @@ void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_ru
             if (s.tune) {
                 std::lock_guard<std::mutex> lk(tuneMu());
                 v = s.tune->choice(nv);
-                timing = s.tune->runs[v] == 0;
+                timing = s.tune->needsTiming(v);
             }
             const qkdev::PassParams& P = v ? *s.alts[size_t(v - 1)] : *s.pass;
             // The basis pass computes one tile; the memset of the rest is
@@ -859,7 +859,7 @@ void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_ru
                 cudaEventDestroy(e0);
                 cudaEventDestroy(e1);
                 std::lock_guard<std::mutex> lk(tuneMu());
-                s.tune->ms[v] = ms;
+                s.tune->record(v, ms);
                 s.tune->runs[v]++;
                 rs.tuning_runs++;
                 if (std::getenv("QK_DEBUG_TUNE")) {
@@ -891,8 +891,8 @@ void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_ru
             bool timing = false;
             if (v < 0) {
                 std::lock_guard<std::mutex> lk(tuneMu());
-                timing = s.tune && s.tune->runs[s.tune->choice(2)] == 0;
                 v = s.tune ? s.tune->choice(2) : 0;
+                timing = s.tune && s.tune->needsTiming(v);
             }
             cudaEvent_t e0 = nullptr, e1 = nullptr;
             if (timing) {
@@ -911,7 +911,7 @@ void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_ru
                 cudaEventDestroy(e0);
                 cudaEventDestroy(e1);
                 std::lock_guard<std::mutex> lk(tuneMu());
-                s.tune->ms[v] = ms;
+                s.tune->record(v, ms);
                 rs.tuning_runs++;
                 if (std::getenv("QK_DEBUG_TUNE"))
                     std::fprintf(stderr, "dense U5 %s: %.3f ms\n", v ? "DMMA" : "DFMA", double(ms));
@@ -1808,7 +1808,7 @@ int chooseTileVariant(const Compiled& c, const Alternative& alt) {
             const int nv = 1 + int(s.alts.size());
             float best = s.tune->ms[0];
             for (int v = 0; v < nv; v++) {
-                if (s.tune->runs[v] == 0) return 0;  // A still tuning its register widths
+                if (s.tune->needsTiming(v)) return 0;  // A still tuning its register widths
                 best = std::min(best, s.tune->ms[v]);
             }
             est += double(best) - double(s.tune->ms[0]);

@@ -1,6 +1,7 @@
 // Host-side compiler: GateBlock (physical positions) -> device steps.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <memory>
 #include <vector>
@@ -18,16 +19,25 @@ struct Step {
     // first execution and keeps the fastest (`tune`, shared by copies).
     std::vector<std::shared_ptr<qkdev::PassParams>> alts;
     struct Tune {
-        static constexpr int kMax = 4;  // rb 5 / 4 / 3, rb 5 with half-splittable exchanges (TMA-pipelined)
+        static constexpr int kMax = 4;      // rb 5 / 4 / 3, rb 5 with half-splittable exchanges (TMA-pipelined)
+        static constexpr int kTimings = 2;  // each variant timed twice, round robin; its best time counts
         float ms[kMax] = {0, 0, 0, 0};
         int runs[kMax] = {0, 0, 0, 0};
+        int timed[kMax] = {0, 0, 0, 0};
+        // the variant to run next: an untimed one while any is left, else the fastest
         int choice(int n) const {  // n = 1 + alts
-            for (int v = 0; v < n; v++)
-                if (runs[v] == 0) return v;
+            for (int r = 0; r < kTimings; r++)
+                for (int v = 0; v < n; v++)
+                    if (timed[v] == r) return v;
             int best = 0;
             for (int v = 1; v < n; v++)
                 if (ms[v] < ms[best]) best = v;
             return best;
+        }
+        bool needsTiming(int v) const { return timed[v] < kTimings; }
+        void record(int v, float t) {
+            ms[v] = timed[v] ? std::min(ms[v], t) : t;
+            timed[v]++;
         }
     };
     std::shared_ptr<Tune> tune;
