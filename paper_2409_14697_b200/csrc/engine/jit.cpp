@@ -270,9 +270,7 @@ public:
         // before its passes have touched every bit): only those amplitudes
         // are read, the rest are zeros that need no memory.
         o_ << "  { const u64 off = base | " << threadGlobal(P_.map_in[0]) << ";\n  if (smask != 0ull) {\n";
-        for (int s = 0; s < na_; s++)
-            o_ << "  { const u64 i_ = off | " << regGlobal(P_.map_in[0], s) << "ull; a" << s
-               << " = ((i_ ^ sval) & smask) == 0ull ? __ldcs(st + i_) : C2(0.0, 0.0); }\n";
+        sparseLoads("  ");
         o_ << "  } else if (basis == ~0ull) {\n";
         const int kl = slotOfMem0(P_.map_in[0]);
         for (int s = 0; s < na_; s++) {
@@ -350,9 +348,7 @@ public:
         issueTile("tile + gridDim.x", L);
         o_ << "    }\n  } else if (smask != 0ull) {  // known zeros: read only the support\n"
            << "    const u64 off = base | " << threadGlobal(P_.map_in[0]) << ";\n";
-        for (int s = 0; s < na_; s++)
-            o_ << "    { const u64 i_ = off | " << regGlobal(P_.map_in[0], s) << "ull; a" << s
-               << " = ((i_ ^ sval) & smask) == 0ull ? __ldcs(st + i_) : C2(0.0, 0.0); }\n";
+        sparseLoads("    ");
         o_ << "  } else {  // first pass of a run: synthesize |basis>\n"
            << "    const u64 off = base | " << threadGlobal(P_.map_in[0]) << ";\n";
         for (int s = 0; s < na_; s++)
@@ -458,6 +454,23 @@ private:
         for (int k = 0; k < rb_; k++)
             if ((s >> k) & 1) u |= 1u << m[k];
         return u;
+    }
+    // Loads of a pass with known zeros (smask / sval): a thread whose own
+    // index bits already leave the support has only zeros (one test, no
+    // loads); otherwise each register slot is read only if its slot bits
+    // match the support.
+    void sparseLoads(const std::string& ind) {
+        uint64_t slots = 0;
+        for (int s = 0; s < na_; s++) slots |= regGlobal(P_.map_in[0], s);
+        o_ << ind << "if (((off ^ sval) & smask & " << (~slots) << "ull) != 0ull) {\n";
+        for (int s = 0; s < na_; s++) o_ << ind << "  a" << s << " = C2(0.0, 0.0);\n";
+        o_ << ind << "} else {\n";
+        for (int s = 0; s < na_; s++) {
+            const uint64_t r = regGlobal(P_.map_in[0], s);
+            o_ << ind << "  a" << s << " = ((" << r << "ull ^ sval) & smask & " << slots << "ull) == 0ull ? __ldcs(st + (off | "
+               << r << "ull)) : C2(0.0, 0.0);\n";
+        }
+        o_ << ind << "}\n";
     }
     // Base index of tile `tile`.  zskip == 2: only the tiles meeting the
     // support {i : (i ^ sval) & smask == 0} are enumerated -- the tile index
@@ -916,7 +929,7 @@ private:
 // ---- compile / load / launch -------------------------------------------------
 
 // Bump when the generated code changes for the same PassParams (on-disk cache key).
-constexpr uint64_t kGeneratorVersion = 27;
+constexpr uint64_t kGeneratorVersion = 28;
 
 uint64_t hashPass(const PassParams& P) {
     uint64_t h = 1469598103934665603ull ^ (kGeneratorVersion * 0x9E3779B97F4A7C15ull) ^ (usePrefetch() ? 1u : 0u) ^ (usePersistent() ? 2u : 0u) ^
