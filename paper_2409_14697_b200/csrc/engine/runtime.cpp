@@ -340,6 +340,16 @@ std::vector<std::vector<std::pair<int, int>>> materializePairs(const std::vector
 
 bool useJit(int nLocal);
 
+// QK_PARTIAL_MATERIALIZE (default 1): before a CSQS only its staged positions
+// are put in place (the rest of the lazy relabeling carries on).
+bool partialMaterialize() {
+    static const bool v = [] {
+        const char* e = std::getenv("QK_PARTIAL_MATERIALIZE");
+        return !e || std::atoi(e) != 0;
+    }();
+    return v;
+}
+
 // QK_BASIS_LAYOUT (default 1): see compileFor(fromBasis).
 bool basisLayout() {
     static const bool v = [] {
@@ -432,14 +442,30 @@ std::shared_ptr<Compiled> compileLayout(qk_program* p, int nLocal, const std::ve
     const bool lazy = lazyIms();
     c->mem0 = mem;
     std::vector<quokka::Gate> stream;
-    auto flushStream = [&](bool beforeMaterialize, int tileBits = 0) {
+    // keep == nullptr: materialize the whole layout (mem = identity: the end of
+    // the program).  Before a CSQS only its staged positions (`keep`, the
+    // outs) must sit at their own memory bits; the rest of the relabeling
+    // stays lazy (the XRS moves memory bits outs <-> rank bits and leaves mem
+    // valid), which takes at most as many IMS sweeps and often none.
+    auto flushStream = [&](bool beforeMaterialize, int tileBits = 0, const std::vector<int>* keep = nullptr) {
         if (stream.empty()) return;
         CompiledItem ci;
         ci.kind = CompiledItem::Block;
         if (lazy && beforeMaterialize) {
-            // route the data toward the program's physical order (mem = identity)
+            // route the data toward the program's physical order (mem = identity),
+            // or only the kept positions (the rest stays where it is)
             std::vector<int> dest(static_cast<size_t>(nLocal)), moved;
-            for (int q = 0; q < nLocal; q++) dest[size_t(mem[size_t(q)])] = q;
+            if (keep) {
+                for (int b = 0; b < nLocal; b++) dest[size_t(b)] = b;
+                std::vector<char> claimed(static_cast<size_t>(nLocal), 0);
+                for (int o : *keep) claimed[size_t(o)] = 1;
+                for (int o : *keep) dest[size_t(mem[size_t(o)])] = o;
+                // a bit displaced from a kept target goes to the source the target's data leaves
+                for (int o : *keep)
+                    if (!claimed[size_t(mem[size_t(o)])] && mem[size_t(o)] != o) dest[size_t(o)] = mem[size_t(o)];
+            } else {
+                for (int q = 0; q < nLocal; q++) dest[size_t(mem[size_t(q)])] = q;
+            }
             ci.steps = qkeng::compileBlock(stream, nLocal, c->gtab, &dest, &moved, tileBits, synthFirst && c->items.empty(),
                                            interp);
             for (int q = 0; q < nLocal; q++) mem[size_t(q)] = moved[size_t(mem[size_t(q)])];
@@ -457,8 +483,33 @@ std::shared_ptr<Compiled> compileLayout(qk_program* p, int nLocal, const std::ve
         }
         c->items.push_back(std::move(ci));
     };
-    auto materialize = [&] {
-        for (const auto& pairs : materializePairs(mem)) {
+    auto materialize = [&](const std::vector<int>* keep = nullptr) {
+        // tau: memory bit b's data goes to tau[b]; full: mem -> identity;
+        // partial: transpositions (mem[o], o) for the kept positions only
+        std::vector<int> tau(static_cast<size_t>(nLocal));
+        if (!keep) {
+            for (int q = 0; q < nLocal; q++) tau[size_t(mem[size_t(q)])] = q;
+        } else {
+            for (int b = 0; b < nLocal; b++) tau[size_t(b)] = b;
+            std::vector<int> cur = mem;  // cur[p] = memory bit of position p after the moves so far
+            std::vector<int> at(static_cast<size_t>(nLocal));  // at[b] = position held by memory bit b
+            for (int q = 0; q < nLocal; q++) at[size_t(cur[size_t(q)])] = q;
+            for (int o : *keep) {
+                const int x = cur[size_t(o)];
+                if (x == o) continue;
+                const int p2 = at[size_t(o)];  // the position now at memory bit o moves to x
+                for (int b = 0; b < nLocal; b++) {  // compose: data headed for x goes to o and vice versa
+                    if (tau[size_t(b)] == x) tau[size_t(b)] = o;
+                    else if (tau[size_t(b)] == o) tau[size_t(b)] = x;
+                }
+                std::swap(cur[size_t(o)], cur[size_t(p2)]);
+                at[size_t(o)] = o;
+                at[size_t(x)] = p2;
+            }
+        }
+        std::vector<int> inv(static_cast<size_t>(nLocal));  // materializePairs moves memory bit inv[q] -> q
+        for (int b = 0; b < nLocal; b++) inv[size_t(tau[size_t(b)])] = b;
+        for (const auto& pairs : materializePairs(inv)) {
             CompiledItem ci;
             ci.kind = CompiledItem::Ims;
             for (const auto& [o, i] : pairs) {
@@ -467,15 +518,17 @@ std::shared_ptr<Compiled> compileLayout(qk_program* p, int nLocal, const std::ve
             }
             c->items.push_back(std::move(ci));
         }
-        for (int b = 0; b < nLocal; b++) mem[size_t(b)] = b;
+        for (int q = 0; q < nLocal; q++) mem[size_t(q)] = tau[size_t(mem[size_t(q)])];
     };
-    // A stream, routed and materialized (mem ends as the identity); with tile
-    // autotune also the 2^12-tile alternative of the same range.
-    auto flushAndMaterialize = [&] {
+    // A stream, routed and materialized (mem ends as the identity, or with the
+    // kept positions in place); with tile autotune also the 2^12-tile
+    // alternative of the same range.
+    auto flushAndMaterialize = [&](const std::vector<int>* keep = nullptr) {
         const size_t first = c->items.size();
         const std::vector<int> mem0 = mem;
-        flushStream(true);
-        materialize();
+        flushStream(true, 0, keep);
+        materialize(keep);
+        const std::vector<int> memA = mem;
         if (lazy && !stream.empty() && qkdev::tileTune() && !interp && nLocal > 13) {
             const size_t last = c->items.size();
             std::vector<CompiledItem> a(std::make_move_iterator(c->items.begin() + long(first)),
@@ -483,8 +536,9 @@ std::shared_ptr<Compiled> compileLayout(qk_program* p, int nLocal, const std::ve
             c->items.resize(first);
             mem = mem0;
             try {
-                flushStream(true, 12);
-                materialize();
+                flushStream(true, 12, keep);
+                materialize(keep);
+                if (mem != memA) throw SimulationError("alternative ends in another layout");
                 Alternative alt;
                 alt.first = first;
                 alt.last = last;
@@ -499,7 +553,7 @@ std::shared_ptr<Compiled> compileLayout(qk_program* p, int nLocal, const std::ve
             }
             c->items.resize(first);
             for (auto& x : a) c->items.push_back(std::move(x));
-            for (int b = 0; b < nLocal; b++) mem[size_t(b)] = b;
+            mem = memA;
         }
         stream.clear();
     };
@@ -526,7 +580,10 @@ std::shared_ptr<Compiled> compileLayout(qk_program* p, int nLocal, const std::ve
         }
         const bool cross = item.swap.kind == quokka::SwapOp::CrossRank;
         if (cross) {
-            flushAndMaterialize();
+            std::vector<int> outs;
+            for (const auto& [o, i] : item.swap.pairs) outs.push_back(o);
+            if (partialMaterialize()) flushAndMaterialize(&outs);
+            else flushAndMaterialize();
         } else {
             flushStream(false);
             stream.clear();
