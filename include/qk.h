@@ -197,6 +197,14 @@ int qk_config_serialize(const qk_config* cfg, char** text);
 int qk_program_parse(const char* text, const qk_config* cfg, int lenient, qk_program** out);
 int qk_program_optimize(const char* circuit_text, const qk_config* cfg, qk_program** out);
 int qk_program_serialize(const qk_program* p, char** text);
+/* GPU-aware AIO configuration: among chunk_qbit 12/13, fusion
+ * off / fusion_qbit 4 / 5 and diagonal fusion on/off, the Config whose
+ * reference-optimizer Program this engine's scheduler prices cheapest (slice
+ * sweeps: passes, IMS, U5 tiles, XRS over NVLink), with buffer_qbit sized to
+ * the HBM left beside the slice (hbm_bytes <= 0: 180 GB).  report (optional):
+ * the candidates and their costs, one per line. */
+int qk_config_tune(const char* circuit_text, int n_qubits, int rank_qubits, double hbm_bytes, qk_config* out,
+                   char** report);
 int qk_program_counts(const qk_program* p, int64_t* blocks, int64_t* sqs, int64_t* csqs,
                       int64_t* gates);
 int qk_program_final_layout(const qk_program* p, int* phys_to_log);

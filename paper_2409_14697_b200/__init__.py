@@ -143,6 +143,7 @@ def lib():
         "qk_program_parse": ([C.c_char_p, C.POINTER(_Config), I, C.POINTER(P)], I),
         "qk_program_optimize": ([C.c_char_p, C.POINTER(_Config), C.POINTER(P)], I),
         "qk_program_serialize": ([P, C.POINTER(P)], I),
+        "qk_config_tune": ([C.c_char_p, I, I, D, C.POINTER(_Config), C.POINTER(P)], I),
         "qk_program_counts": ([P] + [C.POINTER(C.c_int64)] * 4, I),
         "qk_program_final_layout": ([P, C.POINTER(I)], I),
         "qk_program_destroy": ([P], I),
@@ -201,6 +202,17 @@ class Config:
         c = _Config(n, r, buffer, chunk, fusion_qubits, cache_line, ims, xrs, fusion, diag)
         _check(lib().qk_config_finalize(C.byref(c)))
         return cls(c)
+
+    @classmethod
+    def tune(cls, circuit_text: str, n: int, r: int = 0, hbm_bytes: float = 0.0):
+        """GPU-aware configuration: (Config, report) -- the candidate whose
+        reference-optimizer Program this engine runs cheapest (qk_config_tune)."""
+        c = _Config()
+        rep = C.c_void_p()
+        _check(lib().qk_config_tune(circuit_text.encode(), n, r, hbm_bytes, C.byref(c), C.byref(rep)))
+        text = C.cast(rep, C.c_char_p).value.decode()
+        lib().qk_free(rep)
+        return cls(c), text
 
     def __getattr__(self, k):
         if k in Config.FIELDS:

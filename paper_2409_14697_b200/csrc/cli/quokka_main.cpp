@@ -5,6 +5,7 @@
 //   quokka_b200 optimize circuit chunk inrank total ims xrs fusion_qbit fusion
 //   quokka_b200 simulate -i cfg.ini -c program [--raw] [--dump-state] [--initial K]
 //   quokka_b200 validate circuit program [-i cfg.ini]
+//   quokka_b200 tune -i circuit -n N [-r R] [-o cfg.ini]        (GPU-aware config, this framework's addition)
 //   quokka_b200 gen qft|qaoa|bv|gate|random|grover -n N [-o file] [-l L] [-g G]
 //                   [--seed S] [--secret X] [--kind K]
 //   quokka_b200 bench [-n N] [-g G] [--seed S] [--engine blockwise|gate_by_gate]
@@ -332,8 +333,34 @@ int runBench(const Args& a) {
     return 0;
 }
 
+// tune -i circuit -n N [-r R] [-o cfg.ini]: the GPU-aware configuration
+// (qk_config_tune) as an INI file; the candidates and costs on stderr.  Then
+// `optimize --config cfg.ini` produces the Program with the reference's
+// optimizer, unchanged.
+int runTune(const Args& a) {
+    if (!a.opts.count("--input") && a.positional.empty()) throw ConfigError("tune needs -i <circuit>");
+    if (!a.opts.count("--qubits")) throw ConfigError("tune needs -n <qubits>");
+    const std::string path = a.opts.count("--input") ? a.opts.at("--input") : a.positional.front();
+    const int n = int(toInt(a.opts.at("--qubits"), "-n"));
+    const int r = a.opts.count("--rank-qubits") ? int(toInt(a.opts.at("--rank-qubits"), "-r")) : 0;
+    std::ifstream in(path);
+    if (!in) throw ParseError("cannot open circuit file: " + path);
+    std::stringstream ss;
+    ss << in.rdbuf();
+    qk_config c;
+    char* report = nullptr;
+    if (qk_config_tune(ss.str().c_str(), n, r, 0.0, &c, &report) != QK_OK) throw ConfigError(qk_last_error());
+    std::cerr << report;
+    qk_free(report);
+    char* ini = nullptr;
+    if (qk_config_serialize(&c, &ini) != QK_OK) throw ConfigError(qk_last_error());
+    writeText(a.opts.count("--output") ? a.opts.at("--output") : "", ini);
+    qk_free(ini);
+    return 0;
+}
+
 int usage() {
-    std::cerr << "usage: quokka_b200 optimize|simulate|validate|gen|bench ... (see the header of "
+    std::cerr << "usage: quokka_b200 optimize|simulate|validate|gen|bench|tune ... (see the header of "
                  "csrc/cli/quokka_main.cpp)\n";
     return 2;
 }
@@ -356,6 +383,13 @@ int main(int argc, char** argv) {
                                           {"--dump-state", "--dump-state"}, {"--initial", "--initial"},
                                           {"--threads", "--threads"}},
                                          {"--raw", "--dump-state"}));
+        if (cmd == "tune")
+            return runTune(parseArgs(argc, argv, 2,
+                                     {{"-i", "--input"}, {"--input", "--input"}, {"-n", "--qubits"},
+                                      {"--qubits", "--qubits"}, {"-r", "--rank-qubits"},
+                                      {"--rank-qubits", "--rank-qubits"}, {"-o", "--output"},
+                                      {"--output", "--output"}},
+                                     {}));
         if (cmd == "validate")
             return runValidate(parseArgs(argc, argv, 2, {{"-i", "--config"}, {"--config", "--config"}}, {}));
         if (cmd == "bench")

@@ -1796,6 +1796,73 @@ int qk_program_optimize(const char* circuit, const qk_config* cfg, qk_program** 
     });
 }
 
+// GPU-aware AIO configuration: the Config under which the
+// reference's own optimizer (aioOptimize, unchanged) produces the Program this
+// engine runs fastest.  Candidates: chunk_qbit 12 / 13 (2^12-2^13-amplitude
+// tiles), fusion off / fusion_qbit 4 (dense gates the register window holds)
+// / 5 (U5 tile kernel), diagonal fusion on / off.  Each candidate Program is
+// compiled by this engine's scheduler and priced in slice sweeps: a pass or
+// an IMS 1, a fused U5 2.7 (FP64-bound, measured 115 ms vs a 42 ms sweep at 33
+// qubits), another dense / diagonal-table step 1 + its flops over the FP64
+// rate, an XRS 16 B/amp (1 - 2^-S) over NVLink against 32 B/amp over HBM.
+// buffer_qbit: the largest 2^B receive buffer (double-buffered: 2 x 2^B x 16
+// B) that fits the HBM left beside the slice.
+int qk_config_tune(const char* circuitText, int n, int R, double hbmBytes, qk_config* out, char** report) {
+    return guard([&] {
+        if (n < 1 || R < 0 || R >= n) throw ConfigError("bad qubit split");
+        std::istringstream in(circuitText);
+        const quokka::Circuit circ = quokka::parseCircuit(in, n);
+        const int region = n - R;
+        const double slice = 16.0 * std::ldexp(1.0, region);
+        const double headroom = (hbmBytes > 0 ? hbmBytes : 180e9) - slice - 2e9;  // tables, norm, NCCL
+        int B = region;
+        while (B > 0 && 32.0 * std::ldexp(1.0, B) > headroom) B--;
+        if (B < R) B = R;
+        std::ostringstream rep;
+        double best = 1e300;
+        quokka::Config bestCfg;
+        for (int C : {13, 12})
+            for (int F : {0, 4, 5})
+                for (int diag : {0, 1}) {
+                    quokka::Config cfg;
+                    cfg.totalQubits = n;
+                    cfg.rankQubits = R;
+                    cfg.chunkQubits = std::min(C, region);
+                    cfg.bufferQubits = B;
+                    cfg.fusionEnabled = F > 0;
+                    cfg.fusionQubits = F > 0 ? std::min(F, cfg.chunkQubits) : -1;
+                    cfg.diagonalFusionEnabled = diag != 0;
+                    cfg.finalize();
+                    qk_program prog;
+                    prog.prog = quokka::aioOptimize(circ, cfg);
+                    auto comp = compileFor(&prog, region, true, 1);
+                    double cost = 0;
+                    for (const CompiledItem& it : comp->items) {
+                        if (it.kind == CompiledItem::Ims) cost += 1;
+                        else if (it.kind == CompiledItem::Xrs)
+                            cost += (16.0 / 900.0) / (32.0 / 6500.0) * (1.0 - std::ldexp(1.0, -int(it.outs.size())));
+                        else
+                            for (const qkeng::Step& st : it.steps) {
+                                if (st.kind == qkeng::Step::Pass) cost += 1;
+                                else if (st.kind == qkeng::Step::DenseGroup && st.k == 5) cost += 2.7;
+                                else cost += 1 + st.flopsPerAmp * 6500e9 / 32.0 / 36.5e12;
+                            }
+                    }
+                    rep << "chunk " << cfg.chunkQubits << " fusion " << F << " diagonal_fusion " << diag << ": "
+                        << prog.prog.blockCount() << " blocks, " << comp->items.size() << " device items, cost "
+                        << cost << " sweeps\n";
+                    if (cost < best - 1e-9) {
+                        best = cost;
+                        bestCfg = cfg;
+                    }
+                }
+        rep << "chosen: chunk " << bestCfg.chunkQubits << " fusion " << (bestCfg.fusionEnabled ? bestCfg.fusionQubits : 0)
+            << " diagonal_fusion " << bestCfg.diagonalFusionEnabled << " buffer_qbit " << bestCfg.bufferQubits << "\n";
+        *out = fromConfig(bestCfg);
+        if (report) *report = dupText(rep.str());
+    });
+}
+
 int qk_program_serialize(const qk_program* p, char** text) {
     return guard([&] { *text = dupText(quokka::serializeProgram(p->prog)); });
 }
