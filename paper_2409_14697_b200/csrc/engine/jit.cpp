@@ -460,6 +460,14 @@ private:
     // loads); otherwise each register slot is read only if its slot bits
     // match the support.
     void sparseLoads(const std::string& ind) {
+        // QK_SPARSE_EARLY_OUT=1: a per-thread test first.  Measured slower
+        // and bimodal on QFT-33 (50-64 ms vs 47.8 ms for per-slot tests).
+        if (!knob("QK_SPARSE_EARLY_OUT", 0)) {
+            for (int s = 0; s < na_; s++)
+                o_ << ind << "{ const u64 i_ = off | " << regGlobal(P_.map_in[0], s) << "ull; a" << s
+                   << " = ((i_ ^ sval) & smask) == 0ull ? __ldcs(st + i_) : C2(0.0, 0.0); }\n";
+            return;
+        }
         uint64_t slots = 0;
         for (int s = 0; s < na_; s++) slots |= regGlobal(P_.map_in[0], s);
         o_ << ind << "if (((off ^ sval) & smask & " << (~slots) << "ull) != 0ull) {\n";
