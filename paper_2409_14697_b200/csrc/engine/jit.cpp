@@ -259,6 +259,7 @@ public:
            << "(double2* __restrict__ st, const double2* __restrict__ gt, const u32 ntiles, const u64 basis, const u32 tile0, double* __restrict__ np, const u64 smask, const u64 sval, const u32 zskip) {\n";
         o_ << "  extern __shared__ double2 sm[];\n  double2* const F = sm + " << (1 << ct_)
            << ";\n  const u32 tid = threadIdx.x;\n";
+        hoistTables();
         o_ << "  for (u32 tile = blockIdx.x + tile0; tile < ntiles; tile += gridDim.x) {\n";
         o_ << "  " << tileBase() << "\n";
         zeroTile();
@@ -331,7 +332,9 @@ public:
            << "  double2* const XS = sm + 8192;\n  double2* const F = sm + 12288;\n"
            << "  u64* const mbar = (u64*)(sm + " << (12288 + qkdev::kMaxCtaFactors) << ");\n  const u32 tid = threadIdx.x;\n"
            << "  const bool tma = basis == ~0ull && smask == 0ull;  // sparse runs: no whole-tile streaming\n  u32 phase = 0u;\n"
-           << "  if (tid == 0) mbar_init(mbar);\n  __syncthreads();\n"
+           << "  if (tid == 0) mbar_init(mbar);\n  __syncthreads();\n";
+        hoistTables();
+        o_ << ""
            << "  if (tma && blockIdx.x < ntiles) {\n";
         issueTile("blockIdx.x", L);
         o_ << "  }\n  for (u32 tile = blockIdx.x + tile0; tile < ntiles; tile += gridDim.x) {\n"
@@ -480,6 +483,28 @@ private:
         }
         o_ << ind << "}\n";
     }
+    // Per-thread table factors (OP_SCAL_TAB / OP_PEND_TAB) depend only on the
+    // thread index: with QK_HOIST_TAB (default 1) they are all loaded at the
+    // kernel's start, before the tile loop, so their latency hides behind the
+    // amplitude loads instead of stalling the op that uses them.
+    void hoistTables() {
+        tabName_.clear();
+        if (!knob("QK_HOIST_TAB", 1)) return;
+        int k = 0;
+        for (int i = 0; i < P_.nops; i++) {
+            const DevOp& d = P_.ops[i];
+            if (d.type != qkdev::OP_SCAL_TAB && d.type != qkdev::OP_PEND_TAB) continue;
+            const std::string nm = "T" + std::to_string(k++);
+            o_ << "  const double2 " << nm << " = __ldg(gt + " << d.c << "u + " << pext(d.x16) << ");\n";
+            tabName_[i] = nm;
+        }
+    }
+    std::string tabLoad(const DevOp& d) {
+        const auto it = tabName_.find(int(&d - P_.ops));
+        if (it != tabName_.end()) return it->second;
+        return "__ldg(gt + " + std::to_string(d.c) + "u + " + pext(d.x16) + ")";
+    }
+    std::map<int, std::string> tabName_;
     // Base index of tile `tile`.  zskip == 2: only the tiles meeting the
     // support {i : (i ^ sval) & smask == 0} are enumerated -- the tile index
     // is deposited into the non-tile bits the support leaves free, and the
@@ -724,11 +749,11 @@ private:
                 dirtyP_ = true;
                 return;
             case qkdev::OP_SCAL_TAB:
-                o_ << "  P = cmul(P, __ldg(gt + " << d.c << "u + " << pext(d.x16) << "));\n";
+                o_ << "  P = cmul(P, " << tabLoad(d) << ");\n";
                 dirtyP_ = true;
                 return;
             case qkdev::OP_PEND_TAB:
-                o_ << "  R" << a << " = cmul(R" << a << ", __ldg(gt + " << d.c << "u + " << pext(d.x16) << "));\n";
+                o_ << "  R" << a << " = cmul(R" << a << ", " << tabLoad(d) << ");\n";
                 dirtyR_[a] = true;
                 return;
             case qkdev::OP_CX_PEND:
@@ -937,7 +962,7 @@ private:
 // ---- compile / load / launch -------------------------------------------------
 
 // Bump when the generated code changes for the same PassParams (on-disk cache key).
-constexpr uint64_t kGeneratorVersion = 28;
+constexpr uint64_t kGeneratorVersion = 29;
 
 uint64_t hashPass(const PassParams& P) {
     uint64_t h = 1469598103934665603ull ^ (kGeneratorVersion * 0x9E3779B97F4A7C15ull) ^ (usePrefetch() ? 1u : 0u) ^ (usePersistent() ? 2u : 0u) ^
