@@ -261,7 +261,7 @@ def main():
     # settles over the first few runs of a program; finish it before the
     # warm-up so the timed steps run the tuned schedule.
     tune_runs = 1
-    while tune_runs < 16 and tuning:
+    while tune_runs < 24 and tuning:
         tuning = st.simulate(prog, 0)["tuning_runs"]
         tune_runs += 1
     for _ in range(args.warmup):
@@ -423,7 +423,7 @@ def gpu_time_program(qk, kind, n, chunk, reps=5):
     prog = qk.Program.optimize(qk.generate(kind, n, a, seed), cfg)
     st = qk.State(n)
     try:
-        for _ in range(16):
+        for _ in range(24):
             if not st.simulate(prog, 0)["tuning_runs"]:
                 break
         ts = sorted(st.simulate(prog, 0)["total_ms"] for _ in range(reps))

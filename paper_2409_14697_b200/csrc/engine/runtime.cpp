@@ -215,7 +215,8 @@ struct CompiledItem {
 struct ChoiceTune {
     int runs = 0;
     float msA = -1, msB = -1;  // group device time: A's first run, B's fastest run
-    int runsB = 0;             // B is timed twice (a first run can be slow)
+    float msA2 = -1;           // A's fastest run once its passes' register widths are tuned
+    int runsB = 0, runsA2 = 0; // B and tuned A are timed twice each (a first run can be slow)
     int choice = -1;
 };
 
@@ -1920,28 +1921,30 @@ int qk_circuit_generate(const char* kind, int n, int64_t a, uint64_t seed, char*
 // then A until its passes' register-width variants are all timed, then B
 // once more; then the faster of B (its better run) and A's best estimate
 // (A's first run with every pass replaced by its fastest variant).
-int chooseTileVariant(const Compiled& c, const Alternative& alt) {
+// Tile-size choice for one alternative range: A (2^13 tiles) once, B (2^12)
+// once, A until its passes' register-width variants are all timed, B again,
+// then A twice with its tuned variants; the faster of tuned A and B (each its
+// best run) is kept.  phase: which timing this run records (0 none, 1 A's
+// first run, 2 B, 3 tuned A).
+int chooseTileVariant(const Compiled& c, const Alternative& alt, int& phase) {
     ChoiceTune& t = *alt.tune;
+    phase = 0;
     if (t.choice >= 0) return t.choice;
-    if (t.msA < 0) return 0;
-    if (t.runsB == 0) return 1;
-    double est = t.msA;
+    if (t.msA < 0) return phase = 1, 0;
+    if (t.runsB == 0) return phase = 2, 1;
     for (size_t k = alt.first; k < alt.last; k++)
         for (const qkeng::Step& s : c.items[k].steps) {
             if (!s.tune) continue;
             const int nv = 1 + int(s.alts.size());
-            float best = s.tune->ms[0];
-            for (int v = 0; v < nv; v++) {
+            for (int v = 0; v < nv; v++)
                 if (s.tune->needsTiming(v)) return 0;  // A still tuning its register widths
-                best = std::min(best, s.tune->ms[v]);
-            }
-            est += double(best) - double(s.tune->ms[0]);
         }
-    if (t.runsB < 2) return 1;
-    t.choice = t.msB < est ? 1 : 0;
+    if (t.runsB < 2) return phase = 2, 1;
+    if (t.runsA2 < 2) return phase = 3, 0;
+    t.choice = t.msB < t.msA2 ? 1 : 0;
     if (std::getenv("QK_DEBUG_TUNE"))
-        std::fprintf(stderr, "tile tune [%zu,%zu): A first run %.2f ms, A best estimate %.2f ms, B (2^12) %.2f ms -> %s\n",
-                     alt.first, alt.last, double(t.msA), est, double(t.msB), t.choice ? "B" : "A");
+        std::fprintf(stderr, "tile tune [%zu,%zu): A first run %.2f ms, A tuned %.2f ms, B (2^12) %.2f ms -> %s\n",
+                     alt.first, alt.last, double(t.msA), double(t.msA2), double(t.msB), t.choice ? "B" : "A");
     return t.choice;
 }
 
@@ -1998,12 +2001,12 @@ int qk_simulate(qk_state* st, const qk_program* cp, const qk_config* cfg, uint64
         for (size_t i = 0; i < comp->items.size();) {
             if (nextAlt < comp->alts.size() && comp->alts[nextAlt].first == i) {
                 const Alternative& alt = comp->alts[nextAlt++];
-                int v;
+                int v, phase;
                 bool timing;
                 {
                     std::lock_guard<std::mutex> lk(tuneMu());
-                    v = chooseTileVariant(*comp, alt);
-                    timing = alt.tune->choice < 0 && ((v == 0 && alt.tune->msA < 0) || v == 1);
+                    v = chooseTileVariant(*comp, alt, phase);
+                    timing = phase != 0;
                 }
                 cudaEvent_t a0 = nullptr, a1 = nullptr;
                 if (timing) {
@@ -2024,9 +2027,12 @@ int qk_simulate(qk_state* st, const qk_program* cp, const qk_config* cfg, uint64
                     cudaEventDestroy(a0);
                     cudaEventDestroy(a1);
                     std::lock_guard<std::mutex> lk(tuneMu());
-                    if (v == 1) {
+                    if (phase == 2) {
                         alt.tune->msB = alt.tune->runsB ? std::min(alt.tune->msB, ms) : ms;
                         alt.tune->runsB++;
+                    } else if (phase == 3) {
+                        alt.tune->msA2 = alt.tune->runsA2 ? std::min(alt.tune->msA2, ms) : ms;
+                        alt.tune->runsA2++;
                     } else {
                         alt.tune->msA = ms;
                     }

@@ -163,7 +163,7 @@ def test_autotune_variants_agree(ref, qk):
         prog = qk.Program.parse(prog_text, qk.Config.parse(cfg_text))
         st = qk.State(n)
         tuning = []
-        for _ in range(14):
+        for _ in range(18):
             tuning.append(st.simulate(prog, 3)["tuning_runs"])
             assert np.max(np.abs(st.download() - want.view(np.complex128))) < TOL, kind
         assert not any(tuning[-3:]), tuning

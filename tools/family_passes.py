@@ -12,7 +12,7 @@ a, seed = {"qft": (0, 0), "bvones": (0, 0), "qaoa": (1, 1), "random": (400, 7), 
 cfg = qk.Config.make(n, 0, chunk=13, fusion=0, diag=0)
 prog = qk.Program.optimize(qk.generate(kind, n, a, seed), cfg)
 st = qk.State(n)
-for _ in range(16):
+for _ in range(24):
     if not st.simulate(prog, 0)["tuning_runs"]:
         break
 st.set_profiling(True)
