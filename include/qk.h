@@ -102,6 +102,14 @@ int qk_destroy(qk_state* st);
 int qk_set_basis(qk_state* st, uint64_t global_index);          /* initState */
 int qk_upload(qk_state* st, uint64_t offset, uint64_t count, const double* host);
 int qk_download(qk_state* st, uint64_t offset, uint64_t count, double* host);
+/* Streamed download for states larger than host RAM (33-36 qubits): the range
+ * [offset, offset + count) goes through two pinned host buffers of chunk_amps
+ * amplitudes each; sink(data, n, user) receives every chunk in order while the
+ * next one is already copying (D2H overlapped with the consumer).  A nonzero
+ * return from sink stops the stream (QK_ERR_SIM). */
+typedef int (*qk_chunk_sink)(const double* amps, uint64_t count, void* user);
+int qk_download_stream(qk_state* st, uint64_t offset, uint64_t count, uint64_t chunk_amps, qk_chunk_sink sink,
+                       void* user);
 int qk_norm(qk_state* st, double* out);                          /* StateVector::norm */
 /* Marginal probabilities of this slice over k <= 10 of its bits (physical
  * positions): out[v] = sum |a_i|^2 over i whose bits[j] equal bit j of v

@@ -74,6 +74,9 @@ class _XrsMsg(C.Structure):
                 ("section", C.c_int32), ("w0", C.c_uint64), ("count", C.c_uint64)]
 
 
+_SINK = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.c_uint64, C.c_void_p)
+
+
 class _RunStats(C.Structure):
     _fields_ = [("block_ms", C.c_double), ("ims_ms", C.c_double), ("xrs_ms", C.c_double),
                 ("total_ms", C.c_double), ("block_launches", C.c_uint64),
@@ -112,6 +115,7 @@ def lib():
         "qk_set_basis": ([P, U64], I),
         "qk_upload": ([P, U64, U64, P], I),
         "qk_download": ([P, U64, U64, P], I),
+        "qk_download_stream": ([P, U64, U64, U64, _SINK, P], I),
         "qk_norm": ([P, C.POINTER(D)], I),
         "qk_marginal": ([P, C.POINTER(I), I, C.POINTER(D)], I),
         "qk_synchronize": ([P], I),
@@ -321,6 +325,30 @@ class State:
             out = np.empty(count, dtype=np.complex128)
         _check(lib().qk_download(self._h, offset, count, out.ctypes.data))
         return out
+
+    def stream_chunks(self, fn, offset: int = 0, count: int | None = None, chunk: int = 1 << 22) -> None:
+        """Stream [offset, offset + count) to fn(ndarray complex128 chunk) through
+        two pinned buffers (qk_download_stream): for states larger than host RAM."""
+        count = self.count - offset if count is None else count
+        err = []
+
+        def sink(ptr, n, _user):
+            try:
+                fn(np.ctypeslib.as_array(ptr, shape=(2 * n,)).view(np.complex128))
+                return 0
+            except Exception as e:  # noqa: BLE001
+                err.append(e)
+                return 1
+        cb = _SINK(sink)
+        rc = lib().qk_download_stream(self._h, offset, count, chunk, cb, None)
+        if err:
+            raise err[0]
+        _check(rc)
+
+    def save(self, path: str, chunk: int = 1 << 22) -> None:
+        """Write the slice (physical order, interleaved complex128) to a file, streamed."""
+        with open(path, "wb") as f:
+            self.stream_chunks(lambda a: f.write(a.tobytes()), chunk=chunk)
 
     def norm(self) -> float:
         v = C.c_double()

@@ -1469,6 +1469,52 @@ int qk_download(qk_state* st, uint64_t off, uint64_t cnt, double* host) {
     });
 }
 
+int qk_download_stream(qk_state* st, uint64_t off, uint64_t cnt, uint64_t chunk, qk_chunk_sink sink, void* user) {
+    return guard([&] {
+        if (off + cnt > st->count) throw SimulationError("download range outside the slice");
+        if (!sink) throw SimulationError("no chunk sink");
+        if (chunk == 0) chunk = uint64_t(1) << 22;  // 64 MiB per buffer
+        chunk = std::min(chunk, std::max<uint64_t>(cnt, 1));
+        DeviceGuard g(st->device);
+        double2* buf[2] = {nullptr, nullptr};
+        cudaEvent_t done[2] = {nullptr, nullptr};
+        auto cleanup = [&] {
+            for (int h = 0; h < 2; h++) {
+                if (buf[h]) cudaFreeHost(buf[h]);
+                if (done[h]) cudaEventDestroy(done[h]);
+            }
+        };
+        try {
+            for (int h = 0; h < 2; h++) {
+                cuda(cudaMallocHost(&buf[h], chunk * sizeof(double2)), "cudaMallocHost(stream buffer)");
+                cuda(cudaEventCreateWithFlags(&done[h], cudaEventDisableTiming), "event");
+            }
+            const uint64_t n = (cnt + chunk - 1) / chunk;
+            auto issue = [&](uint64_t k) {
+                const uint64_t o = off + k * chunk, m = std::min(chunk, cnt - k * chunk);
+                const int h = int(k & 1);
+                cuda(cudaMemcpyAsync(buf[h], st->amps + o, m * sizeof(double2), cudaMemcpyDeviceToHost, st->stream),
+                     "stream chunk");
+                cuda(cudaEventRecord(done[h], st->stream), "event");
+            };
+            if (n) issue(0);
+            for (uint64_t k = 0; k < n; k++) {
+                const int h = int(k & 1);
+                cuda(cudaEventSynchronize(done[h]), "stream chunk");
+                if (k + 1 < n) issue(k + 1);  // the other buffer: its sink call has returned
+                const uint64_t m = std::min(chunk, cnt - k * chunk);
+                if (sink(reinterpret_cast<const double*>(buf[h]), m, user) != 0)
+                    throw SimulationError("download stream stopped by its sink");
+            }
+        } catch (...) {
+            cudaStreamSynchronize(st->stream);
+            cleanup();
+            throw;
+        }
+        cleanup();
+    });
+}
+
 int qk_norm(qk_state* st, double* out) {
     return guard([&] {
         DeviceGuard g(st->device);

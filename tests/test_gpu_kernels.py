@@ -273,3 +273,28 @@ def test_u5_tile_kernel_vs_reference(ref, qk, mode):
                 assert np.max(np.abs(got - cx(want))) < TOL, (tg, mode)
     finally:
         qk.set_dense_mode(-1)
+
+
+def test_download_stream_matches_download(qk, tmp_path):
+    # qk_download_stream: two pinned buffers, D2H overlapped with the consumer
+    n = 22
+    st = qk.State(n)
+    try:
+        host = (np.random.default_rng(4).standard_normal(1 << n)
+                + 1j * np.random.default_rng(5).standard_normal(1 << n))
+        st.upload(host)
+        chunks = []
+        st.stream_chunks(lambda a: chunks.append(a.copy()), offset=12345, count=(1 << n) - 20000, chunk=1 << 18)
+        got = np.concatenate(chunks)
+        assert np.array_equal(got, host[12345:12345 + (1 << n) - 20000])
+        assert len(chunks) == -(-((1 << n) - 20000) // (1 << 18))
+        path = tmp_path / "state.bin"
+        st.save(str(path), chunk=1 << 20)
+        assert np.array_equal(np.fromfile(path, dtype=np.complex128), host)
+
+        def stop(a):
+            raise RuntimeError("consumer full")
+        with pytest.raises(RuntimeError):
+            st.stream_chunks(stop, chunk=1 << 18)
+    finally:
+        st.close()
