@@ -38,6 +38,8 @@ struct DenseSpec {
     int vslot[kDctMax];  // tile index bit j -> plane offset contribution (s row or g column)
     int nfree;           // memory bits outside the tile (ascending)
     int fbit[40];
+    uint64_t tileMask;   // memory bits of the tile
+    uint64_t smask, sval;  // known zeros: the slice is zero outside {i : (i ^ sval) & smask == 0}
 };
 
 __device__ __forceinline__ double2 cmacD(double2 acc, double2 m, double2 x) {
@@ -118,6 +120,18 @@ __global__ void __launch_bounds__(MMA ? 256 : 128, MMA ? 3 : 2) k_dense_tile(dou
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         uint64_t base = 0;
         for (int j = 0; j < sp.nfree; j++) base |= ((tile >> j) & 1) << sp.fbit[j];
+        if (((base ^ sp.sval) & sp.smask & ~sp.tileMask) != 0) {  // outside the support: zeros in, zeros out
+            const uint64_t b = base | depLo;
+#pragma unroll 1
+            for (int i = 0; i < PER; i++) {
+                uint64_t a = b;
+#pragma unroll
+                for (int j = 0; j < HI; j++)
+                    if ((i >> j) & 1) a |= depHi[j];
+                __stcs(st + a, make_double2(0.0, 0.0));
+            }
+            continue;
+        }
         __syncthreads();  // the previous tile's stores read the planes
         base |= depLo;
 #pragma unroll 1
@@ -130,7 +144,7 @@ __global__ void __launch_bounds__(MMA ? 256 : 128, MMA ? 3 : 2) k_dense_tile(dou
 #pragma unroll
                 for (int j = 0; j < HI; j++)
                     if ((ii >> j) & 1) a |= depHi[j];
-                v[i] = __ldcs(st + a);
+                v[i] = ((a ^ sp.sval) & sp.smask) == 0 ? __ldcs(st + a) : make_double2(0.0, 0.0);
             }
 #pragma unroll
             for (int i = 0; i < 8; i++) {
@@ -214,9 +228,11 @@ __global__ void __launch_bounds__(MMA ? 256 : 128, MMA ? 3 : 2) k_dense_tile(dou
 }  // namespace
 
 // U5 over a slice of 2^nLocal >= 2^12 amplitudes; targets[j] = memory bit of
-// sub-index bit (4 - j).  mode 0 = DFMA, 1 = DMMA.
+// sub-index bit (4 - j).  mode 0 = DFMA, 1 = DMMA.  smask != 0: the slice is
+// zero outside {i : (i ^ sval) & smask == 0} (a run from a basis state): tiles
+// outside it are written as zeros, inside only the support is read.
 cudaError_t launchDenseTile(double2* state, const double2* M, const int* targets, int k, int nLocal, int mode,
-                            int smCount, cudaStream_t stream) {
+                            int smCount, cudaStream_t stream, uint64_t smask, uint64_t sval) {
     const int kDct = mode ? 11 : 12;
     if (k != kDk || nLocal < kDct) return cudaErrorInvalidValue;
     const int kDstride = mode ? TileShape<11>::stride : TileShape<12>::stride;
@@ -239,6 +255,9 @@ cudaError_t launchDenseTile(double2* state, const double2* M, const int* targets
         sp.vslot[j] = q >= 0 ? (1 << (k - 1 - q)) * kDstride : (1 << gbit++);
         j++;
     }
+    sp.tileMask = tile;
+    sp.smask = smask;
+    sp.sval = sval;
     const uint64_t ntiles = uint64_t(1) << (nLocal - kDct);
     const size_t smem = sizeof(double) * 2 * kDplane + (mode ? sizeof(double) * 64 * 64 : sizeof(double2) * 32 * 32);
     const uint64_t resident = uint64_t(smCount) * (mode ? 3 : 2);

@@ -32,7 +32,8 @@
 namespace qkdev {
 cudaError_t launchBlockPass(double2*, const double2*, const PassParams&, int, uint64_t, cudaStream_t);
 cudaError_t launchDenseGroup(double2*, const double2*, int, const int*, uint64_t, int, cudaStream_t);
-cudaError_t launchDenseTile(double2*, const double2*, const int*, int, int, int, int, cudaStream_t);
+cudaError_t launchDenseTile(double2*, const double2*, const int*, int, int, int, int, cudaStream_t, uint64_t,
+                            uint64_t);
 cudaError_t launchIms(double2*, int, const int*, const int*, int, cudaStream_t);
 void setImsMode(int);
 cudaError_t launchSlabSwap(int, double2* const*, double2* const*, const uint64_t*, const uint64_t*, const int*, int,
@@ -941,6 +942,7 @@ void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_ru
                  "diag table");
         } else if (s.k == 5 && st->nLocal >= 12 && denseMode() != 2) {
             rs.block_bytes += 32.0 * amps;
+            const uint64_t dmask = (sup && useJit(st->nLocal)) ? sup->mask : 0;  // known zeros of this step's input
             if (sup)
                 for (size_t j = 1; j < s.targets.size(); j++) sup->mask &= ~(uint64_t(1) << s.targets[j]);
             // U5 tile kernel, DFMA or DMMA: the first two executions time
@@ -959,7 +961,7 @@ void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_ru
                 cuda(cudaEventRecord(e0, st->stream), "event");
             }
             cuda(qkdev::launchDenseTile(st->amps, t.gtab + s.matOff, s.targets.data() + 1, s.k, st->nLocal, v,
-                                        smCountOf(st->device), st->stream),
+                                        smCountOf(st->device), st->stream, dmask, dmask ? sup->val : 0),
                  "dense U5 tile");
             if (timing) {
                 float ms = 0;
