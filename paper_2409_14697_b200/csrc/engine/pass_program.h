@@ -46,6 +46,7 @@ constexpr int kMaxCtaTerms = 640;
 // QK_RB13 = 4|5 register bits at ct = 13 (default 5).
 int maxTileBits();
 int regBitsFor(int ct);
+bool storeWide();
 bool tileTune();
 bool halfExchanges();
 bool wideAccess();

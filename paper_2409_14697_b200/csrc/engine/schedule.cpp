@@ -65,6 +65,13 @@ bool wideAccess() {
 
 // QK_GTERMS (default 1): register-pair phases are deferred and applied with
 // the slot flush of whichever of their bits is touched first.
+// QK_STORE_WIDE (default 1): later segments prefer memory bit 0 in a free
+// register slot (256-bit stores at the end of the pass).
+bool storeWide() {
+    static const bool v = envInt("QK_STORE_WIDE", 1, 0, 1) != 0;
+    return v;
+}
+
 bool deferPairPhases() {
     static const bool v = envInt("QK_GTERMS", 1, 0, 1) != 0;
     return v;
@@ -212,9 +219,9 @@ Amp ratio(Amp num, Amp den) {
 class PassBuilder {
 public:
     PassBuilder(const std::vector<Gate>& tg, const std::vector<Gate>& orig, const std::vector<int>& tilePhys,
-                std::vector<double>& gtab, int rb = -1, bool halfX = false)
+                std::vector<double>& gtab, int rb = -1, bool halfX = false, bool sparseIn = false)
         : tg_(tg), orig_(orig), gtab_(gtab), ct_(int(tilePhys.size())),
-          rb_(rb > 0 ? rb : regBitsFor(int(tilePhys.size()))), halfX_(halfX || halfExchanges()) {
+          rb_(rb > 0 ? rb : regBitsFor(int(tilePhys.size()))), halfX_(halfX || halfExchanges()), sparseIn_(sparseIn) {
         tilePhys_ = tilePhys;
     }
 
@@ -272,7 +279,7 @@ public:
                 flushAll(true);
                 closeSegment();
                 seg_++;
-                chooseMap(i, halfX_ ? &P_->xsplit[seg_] : nullptr);
+                chooseMap(i, halfX_ ? &P_->xsplit[seg_] : nullptr, false, storeBit0());
                 if (!halfX_) P_->xsplit[seg_] = 255;
                 std::memcpy(P_->map_in[seg_], map_, sizeof map_);
                 emit(OP_EXCHANGE, 0, 0, 0, uint32_t(seg_));
@@ -339,7 +346,14 @@ private:
     // halves split on that bit, through a half-tile shared-memory buffer.
     // wantBit0: hold tile bit 0 (= memory bit 0) in a register slot, so each
     // thread's amplitudes pair up into 32-B neighbours (one 256-bit load each).
-    void chooseMap(size_t i, uint8_t* split = nullptr, bool wantBit0 = false) {
+    // preferBit0: a later segment holds memory bit 0 in a register slot when
+    // one is free, so that if it is the pass's last segment the tile is
+    // stored with 256-bit stores (half the store instructions).  Only for
+    // passes of a basis run that still have known zeros in their input: they
+    // read almost nothing, so their stores are the memory stream (QFT-33 pass 3
+    // 48.6 -> 47.6 ms); on full passes it moved QAOA-33 297 -> 312 ms.
+    bool storeBit0() const { return sparseIn_ && wideAccess() && tilePhys_[0] == 0 && qkdev::storeWide(); }
+    void chooseMap(size_t i, uint8_t* split = nullptr, bool wantBit0 = false, bool preferBit0 = false) {
         int prev[kMaxRegBits];
         for (int s = 0; s < rb_; s++) prev[s] = map_[s];
         int slotBit[kMaxRegBits];
@@ -377,6 +391,9 @@ private:
                 regs.push_back(origin[size_t(b)]);
             }
         }
+        if (preferBit0 && !wantBit0 && int(regs.size()) < rb_ &&
+            std::find(regs.begin(), regs.end(), 0) == regs.end())
+            regs.push_back(0);
         if (wantBit0 && std::find(regs.begin(), regs.end(), 0) == regs.end()) {
             if (int(regs.size()) < rb_) {
                 regs.push_back(0);
@@ -1039,6 +1056,7 @@ private:
     std::vector<int> tilePhys_;
     int ct_, rb_;
     bool halfX_;
+    bool sparseIn_;  // the pass's input has known zeros (a basis run before every bit was touched)
     PassParams* P_ = nullptr;
     int nops_ = 0, ncoef_ = 0, ncontrib_ = 0, seg_ = 0, hcount_ = 0;
     bool pendScalar_ = false;
@@ -1085,7 +1103,7 @@ Gate remapQubits(const Gate& g, const int* tileOf) {
 }
 
 void compileGroup(const std::vector<Gate>& gates, uint64_t used, int ct, int nLocal, std::vector<double>& gtab,
-                  std::vector<Step>& out, int rb = -1, bool halfX = false) {
+                  std::vector<Step>& out, int rb = -1, bool halfX = false, bool sparseIn = false) {
     // Tile bits: every bit the group touches, padded with the lowest others.
     uint64_t tile = used;
     for (int b = 0; b < nLocal && __builtin_popcountll(tile) < ct; b++) tile |= uint64_t(1) << b;
@@ -1099,7 +1117,7 @@ void compileGroup(const std::vector<Gate>& gates, uint64_t used, int ct, int nLo
         }
     std::vector<Gate> tg;
     for (const Gate& g : gates) tg.push_back(remapQubits(g, tileOf));
-    PassBuilder pb(tg, gates, phys, gtab, rb, halfX);
+    PassBuilder pb(tg, gates, phys, gtab, rb, halfX, sparseIn);
     size_t i = 0;
     while (i < gates.size()) {
         Step st;
@@ -1277,6 +1295,9 @@ std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::
         c += exchangeCost() * double(std::max(0, (u + rb - 1) / rb - 1));
         return c;
     };
+    // support of a run from a basis state, as the runtime will track it: every
+    // pass frees its tile bits, every dense step its targets
+    uint64_t sparseMask = synthFirst ? (nLocal >= 64 ? ~uint64_t(0) : (uint64_t(1) << nLocal) - 1) : 0;
     std::vector<Gate> run;
     auto cutRun = [&] {
         const size_t m = run.size();
@@ -1316,16 +1337,20 @@ std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::
                 if (mask[k]) used |= group.back().depMask();
             }
             const size_t first = steps.size();
-            compileGroup(group, used, ct, nLocal, gtab, steps, interp ? rb : -1);
+            // a run from a basis state: the support grows by each pass's tile
+            const bool sparseIn = sparseMask != 0;
+            compileGroup(group, used, ct, nLocal, gtab, steps, interp ? rb : -1, false, sparseIn);
+            for (size_t k = first; k < steps.size(); k++)
+                if (steps[k].kind == Step::Pass) sparseMask &= ~steps[k].pass->tile_mask;
             if (!interp && ct == 13 && tuneRegBits() && steps.size() == first + 1 && steps[first].kind == Step::Pass) {
                 for (int rbAlt : {4, 3}) {  // 16 and 8 amplitudes per thread (512 / 1024 threads)
                     std::vector<Step> alt;
-                    compileGroup(group, used, ct, nLocal, gtab, alt, rbAlt);
+                    compileGroup(group, used, ct, nLocal, gtab, alt, rbAlt, false, sparseIn);
                     if (alt.size() == 1 && alt[0].kind == Step::Pass) steps[first].alts.push_back(alt[0].pass);
                 }
                 if (!halfExchanges()) {  // 32 per thread, half-splittable exchanges: the TMA-pipelined kernel
                     std::vector<Step> alt;
-                    compileGroup(group, used, ct, nLocal, gtab, alt, 5, true);
+                    compileGroup(group, used, ct, nLocal, gtab, alt, 5, true, sparseIn);
                     if (alt.size() == 1 && alt[0].kind == Step::Pass) steps[first].alts.push_back(alt[0].pass);
                 }
                 if (!steps[first].alts.empty()) steps[first].tune = std::make_shared<Step::Tune>();
@@ -1341,6 +1366,7 @@ std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::
             cutRun();
             const Gate m = relabelGate(g);
             denseStep(m.payload, m.targets, referenceFlopsPerAmp(m));
+            for (int q : m.targets) sparseMask &= ~(uint64_t(1) << q);
             continue;
         }
         run.push_back(g);
