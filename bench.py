@@ -231,7 +231,11 @@ def main():
     prog_text = prog.text()
 
     st = qk.State(n, R, rank, cfg.buffer_qubits, local_rank)
-    transport = os.environ.get("QK_XRS", "nccl")
+    # Cross-rank transport: the peer-memory rank group (qk_ipc_init: one
+    # in-place swap kernel per CSQS over NVLink P2P, no buffer, no copy-back)
+    # is the default -- it is the path exercised on hardware (multi-process
+    # tests on the B200); QK_XRS=nccl selects grouped ncclSend/ncclRecv.
+    transport = os.environ.get("QK_XRS", "ipc")
     if world > 1 and transport == "ipc":
         # peer-memory rank group: in-place swap kernels over NVLink, no buffer
         job = [f"bench{os.getpid()}_{time.time_ns()}" if rank == 0 else None]
