@@ -217,9 +217,17 @@ def main():
     import torch.distributed as dist
     import paper_2409_14697_b200 as qk
 
-    torch.cuda.set_device(local_rank)
+    # QK_BENCH_SHARE_GPU=1 (test hook): every rank on cuda:0 with a gloo
+    # process group -- the multi-rank path (peer-memory XRS) on a 1-GPU box.
+    share = os.environ.get("QK_BENCH_SHARE_GPU") == "1"
+    device = 0 if share else local_rank
+    torch.cuda.set_device(device)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    tdev = "cpu" if share else "cuda"
 
     a, seed = circuit_args(kind, n)
     circ = qk.generate(kind, n, a, seed)
@@ -230,7 +238,7 @@ def main():
     counts = prog.counts()
     prog_text = prog.text()
 
-    st = qk.State(n, R, rank, cfg.buffer_qubits, local_rank)
+    st = qk.State(n, R, rank, cfg.buffer_qubits, device)
     # Cross-rank transport: the peer-memory rank group (qk_ipc_init: one
     # in-place swap kernel per CSQS over NVLink P2P, no buffer, no copy-back)
     # is the default -- it is the path exercised on hardware (multi-process
@@ -242,7 +250,7 @@ def main():
         dist.broadcast_object_list(job, 0)
         st.ipc_init(job[0], world, rank)
     elif world > 1:
-        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        uid = torch.zeros(128, dtype=torch.uint8, device=tdev)
         if rank == 0:
             uid.copy_(torch.frombuffer(bytearray(qk.comm_unique_id()), dtype=torch.uint8))
         dist.broadcast(uid, 0)
@@ -275,7 +283,7 @@ def main():
     st.set_profiling(True)
     stats = []
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(device) as clk:
         barrier()
         ev0.record(ext)
         for _ in range(args.steps):
@@ -284,7 +292,7 @@ def main():
         barrier()
     st.set_profiling(False)
     dev_ms = ev0.elapsed_time(ev1)
-    t = torch.tensor([dev_ms], dtype=torch.float64, device="cuda")
+    t = torch.tensor([dev_ms], dtype=torch.float64, device=tdev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
@@ -307,7 +315,7 @@ def main():
         e2e.append(time.perf_counter() - t1)
         del p2
     e2e_s = sorted(e2e)[len(e2e) // 2]
-    et = torch.tensor([e2e_s, cold_s], dtype=torch.float64, device="cuda")
+    et = torch.tensor([e2e_s, cold_s], dtype=torch.float64, device=tdev)
     if world > 1:
         dist.all_reduce(et, op=dist.ReduceOp.MAX)
     e2e_s, cold_s = float(et[0].item()), float(et[1].item())
