@@ -315,6 +315,10 @@ def main():
         e2e.append(time.perf_counter() - t1)
         del p2
     e2e_s = sorted(e2e)[len(e2e) // 2]
+    if world > 1:  # the norm of the whole state: sum of the slices' sum |a|^2
+        nt = torch.tensor([nrm], dtype=torch.float64, device=tdev)
+        dist.all_reduce(nt, op=dist.ReduceOp.SUM)
+        nrm = float(nt.item())
     et = torch.tensor([e2e_s, cold_s], dtype=torch.float64, device=tdev)
     if world > 1:
         dist.all_reduce(et, op=dist.ReduceOp.MAX)
