@@ -179,29 +179,39 @@ __global__ void __launch_bounds__(MMA ? 256 : 128, MMA ? 3 : 2) k_dense_tile(dou
                 }
             }
         } else {
-            constexpr int CTILES = kDgroups / 8;  // 8 column tiles of Y per warp
-            double acc[CTILES][2];
+            // warp w: row tiles 2 (w & 3) .. +1, column tiles 4 (w >> 2) .. +3
+            // (Y = 8 row tiles x 8 column tiles of 8 x 8): per k-step 2 A and
+            // 4 B fragment loads feed 8 DMMAs
+            const int rp = w & 3, ch = w >> 2;
+            double acc[2][4][2];
 #pragma unroll
-            for (int c = 0; c < CTILES; c++) acc[c][0] = acc[c][1] = 0.0;
-#pragma unroll 1
+            for (int r = 0; r < 2; r++)
+#pragma unroll
+                for (int c = 0; c < 4; c++) acc[r][c][0] = acc[r][c][1] = 0.0;
+#pragma unroll 2
             for (int kk = 0; kk < 16; kk++) {
                 const int k = 4 * kk + (lane & 3);
-                const double afr = As[(w * 16 + kk) * 32 + lane];
-                const double* const row = (k < 32 ? Xr : Xi) + (k & 31) * kDstride + (lane >> 2);
-                double b[CTILES];
+                const double a0 = As[((2 * rp) * 16 + kk) * 32 + lane];
+                const double a1 = As[((2 * rp + 1) * 16 + kk) * 32 + lane];
+                const double* const row = (k < 32 ? Xr : Xi) + (k & 31) * kDstride + 32 * ch + (lane >> 2);
+                double b[4];
 #pragma unroll
-                for (int c = 0; c < CTILES; c++) b[c] = row[8 * c];
+                for (int c = 0; c < 4; c++) b[c] = row[8 * c];
 #pragma unroll
-                for (int c = 0; c < CTILES; c++) dmma(acc[c][0], acc[c][1], afr, b[c]);
+                for (int c = 0; c < 4; c++) {
+                    dmma(acc[0][c][0], acc[0][c][1], a0, b[c]);
+                    dmma(acc[1][c][0], acc[1][c][1], a1, b[c]);
+                }
             }
             __syncthreads();  // every warp has read X before Y overwrites it
-            {
-                const int i = 8 * w + (lane >> 2);
-                double* const plane = (i < 32 ? Xr : Xi) + (i & 31) * kDstride + 2 * (lane & 3);
 #pragma unroll
-                for (int c = 0; c < CTILES; c++) {
-                    plane[8 * c] = acc[c][0];
-                    plane[8 * c + 1] = acc[c][1];
+            for (int r = 0; r < 2; r++) {
+                const int i = 8 * (2 * rp + r) + (lane >> 2);
+                double* const plane = (i < 32 ? Xr : Xi) + (i & 31) * kDstride + 32 * ch + 2 * (lane & 3);
+#pragma unroll
+                for (int c = 0; c < 4; c++) {
+                    plane[8 * c] = acc[r][c][0];
+                    plane[8 * c + 1] = acc[r][c][1];
                 }
             }
         }
