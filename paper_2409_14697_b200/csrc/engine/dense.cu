@@ -76,6 +76,7 @@ __global__ void __launch_bounds__(MMA ? 256 : 128, MMA ? 3 : 2) k_dense_tile(dou
     constexpr int kDstride = TileShape<CT>::stride;
     constexpr int kDplane = TileShape<CT>::plane;
     constexpr int kDgroups = TileShape<CT>::groups;
+    static_assert(kDgroups == 64 || kDgroups == 128, "tile shapes: 2^11 (DMMA) or 2^12 (DFMA) amplitudes");
     constexpr int LOGNT = MMA ? 8 : 7;
     constexpr int NT = 1 << LOGNT;
     constexpr int PER = (1 << CT) / NT;  // amplitudes per thread in the load / store phases
