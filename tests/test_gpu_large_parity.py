@@ -11,6 +11,8 @@
 * IMS at 27 qubits, where both IMS kernels take several trips per thread /
   warp (the incremental GF(2) walks): bit-exact against bitswap on an
   index-encoded state (engine.cpp:86-101).
+* The reference optimizer's fused programs at 26 qubits (U5 tiles, D_k
+  tables, IMS) from a nonzero basis state vs its simulateProgram.
 
 Tolerance: 1e-10 max abs per amplitude, |norm - 1| < 1e-12 (north star);
 permutations bit-exact.
@@ -135,4 +137,32 @@ def test_ims_multi_trip_bitexact(qk, mode):
             assert np.array_equal(got.imag, -src.astype(np.float64)), pairs
     finally:
         qk.set_ims_mode(1)
+        st.close()
+
+
+@pytest.mark.parametrize("kind,a,seed,flags", [("random", 300, 11, dict()),                     # reference defaults: U5 + D_k
+                                               ("qaoa", 2, 4, dict(c=12)),                      # D_k fusion, chunk 12
+                                               ("qft", 0, 0, dict(c=11, fusion=0, diag=1))])   # D_k only
+def test_26q_reference_default_flags(ref, qk, kind, a, seed, flags):
+    # the reference optimizer's fused programs (U5 tile kernel, D_k tables,
+    # IMS materializations) from a nonzero basis state, amplitude by
+    # amplitude against the reference's simulateProgram
+    n = 26
+    flags = dict(flags)
+    c = flags.pop("c", None)
+    cfg_text = config_text(n, 0, c, **flags)
+    prog_text = ref.optimize(ref.gen(kind, n, a, seed), cfg_text)
+    initial = 0x2B3C4D5 & ((1 << n) - 1)
+    want, wl, _, _ = ref.simulate(prog_text, cfg_text, n, 0, initial, 0)
+    want = want.view(np.complex128)
+    prog = qk.Program.parse(prog_text, qk.Config.parse(cfg_text))
+    st = qk.State(n)
+    try:
+        for run in range(2):
+            st.simulate(prog, initial)
+            got = st.download()
+            assert np.max(np.abs(got - want)) < TOL, run
+        assert prog.final_layout() == wl
+        assert abs(st.norm() - 1.0) < 1e-12
+    finally:
         st.close()
