@@ -625,14 +625,17 @@ std::shared_ptr<Compiled> compileLayout(qk_program* p, int nLocal, const std::ve
 // jit: schedule for the specialized kernels (1), the interpreter (0), or
 // whichever runs a 2^nLocal slice (-1).  The two get different schedules
 // (interpreter: rb = 3, tiles <= 2^12).
-std::shared_ptr<Compiled> compileFor(qk_program* p, int nLocal, bool fromBasis = true, int jit = -1) {
+// share = false: neither read nor fill the process-wide cache (throwaway
+// compilations, e.g. qk_config_tune's candidates, must not evict live ones).
+std::shared_ptr<Compiled> compileFor(qk_program* p, int nLocal, bool fromBasis = true, int jit = -1,
+                                     bool share = true) {
     std::lock_guard<std::mutex> lk(p->mu);
     const bool interp = jit < 0 ? !useJit(nLocal) : jit == 0;
     const int slot = (fromBasis ? nLocal : -1 - nLocal) * 2 + (interp ? 1 : 0);
     auto it = p->compiled.find(slot);
     if (it != p->compiled.end()) return it->second;
-    const std::string key = scheduleKey(p->prog, slot);
-    {
+    const std::string key = share ? scheduleKey(p->prog, slot) : std::string();
+    if (share) {
         ScheduleCache& sc = scheduleCache();
         std::lock_guard<std::mutex> g(sc.mu);
         auto hit = sc.byKey.find(key);
@@ -663,7 +666,7 @@ std::shared_ptr<Compiled> compileFor(qk_program* p, int nLocal, bool fromBasis =
         }
     }
     p->compiled[slot] = c;
-    {
+    if (share) {
         ScheduleCache& sc = scheduleCache();
         std::lock_guard<std::mutex> g(sc.mu);
         if (sc.byKey.emplace(key, c).second) {
@@ -1884,7 +1887,7 @@ int qk_config_tune(const char* circuitText, int n, int R, double hbmBytes, qk_co
                     cfg.finalize();
                     qk_program prog;
                     prog.prog = quokka::aioOptimize(circ, cfg);
-                    auto comp = compileFor(&prog, region, true, 1);
+                    auto comp = compileFor(&prog, region, true, 1, false);
                     double cost = 0;
                     for (const CompiledItem& it : comp->items) {
                         if (it.kind == CompiledItem::Ims) cost += 1;
