@@ -820,6 +820,11 @@ int smCountOf(int device) {
 // arithmetic) of amplitudes known to be zero.
 struct Support {
     uint64_t mask = 0, val = 0;
+    // the whole slice is zero (a rank that does not hold |initial>, before its
+    // first cross-rank swap): every block and IMS step is skipped -- zeros in,
+    // zeros out -- instead of sweeping HBM for nothing (on 2^R GPUs these
+    // ranks would otherwise be the critical path to the first XRS barrier)
+    bool empty = false;
 };
 
 void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_run_stats& rs,
@@ -828,6 +833,7 @@ void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_ru
     for (size_t si = 0; si < ci.steps.size(); si++) {
         const qkeng::Step& s = ci.steps[si];
         st->normValid = false;
+        if (sup && sup->empty && !(s.kind == qkeng::Step::Pass && basis != kNoBasis)) continue;  // zeros stay zeros
         if (s.kind == qkeng::Step::Pass) {
             const bool jit = useJit(st->nLocal);
             // known zeros in this pass's input (not for the basis-synthesizing pass)
@@ -1009,6 +1015,7 @@ uint64_t swapBits(uint64_t x, const std::vector<int>& outs, const std::vector<in
 void runIms(qk_state* st, const std::vector<int>& outs, const std::vector<int>& ins, qk_run_stats& rs,
             Support* sup = nullptr) {
     st->normValid = false;
+    if (sup && sup->empty) return;  // a permutation of zeros
     if (sup) {  // a[bitswap(i)] <- a[i]: the known-zero coset moves with its bits
         sup->mask = swapBits(sup->mask, outs, ins);
         sup->val = swapBits(sup->val, outs, ins);
@@ -2025,11 +2032,13 @@ int qk_simulate(qk_state* st, const qk_program* cp, const qk_config* cfg, uint64
         if (synth) {
             const bool here = (initial >> st->nLocal) == Index(st->rank);
             basis = here ? layoutIndex(initial & (st->count - 1), comp->mem0) : st->count;
-            if (here) sup = Support{st->count - 1, basis};
+            if (here) sup = Support{st->count - 1, basis, false};
+            else sup.empty = true;  // the basis pass only zero-fills this slice
         } else {
             timer.time(4, [&] { setBasis(st, initial, &comp->mem0); });
+            sup.empty = (initial >> st->nLocal) != Index(st->rank);
         }
-        if (!sparseStart()) sup.mask = 0;
+        if (!sparseStart()) sup = Support{};
         auto runItem = [&](const CompiledItem& it) {
             if (it.kind == CompiledItem::Block) {
                 timer.time(0, [&] { runBlock(st, it, t, rs, basis, &timer, &sup); });
@@ -2037,7 +2046,7 @@ int qk_simulate(qk_state* st, const qk_program* cp, const qk_config* cfg, uint64
             }
             else if (it.kind == CompiledItem::Ims) timer.time(1, [&] { runIms(st, it.outs, it.ins, rs, &sup); });
             else {
-                sup.mask = 0;
+                sup = Support{};  // data arrives from the other ranks
                 quokka::SwapOp op;
                 op.kind = quokka::SwapOp::CrossRank;
                 for (size_t j = 0; j < it.outs.size(); j++) op.pairs.emplace_back(it.outs[j], it.ins[j]);
