@@ -159,9 +159,20 @@ static __device__ __forceinline__ void bulk_wait_read() {  // sources of committ
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 #endif
 }
+// The tile as one box of a tensor view of the slice (cuTensorMapEncodeTiled,
+// built by launch()); passed to the TMA-pipelined kernels by value.
+struct __align__(64) QkTmap {
+    unsigned long long v[16];
+};
 static __device__ __forceinline__ void bulk_wait_all() {
 #ifdef __CUDA_ARCH__
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+#endif
+}
+// One line of the next tile's support into L2 (sparse runs, persistent grid).
+static __device__ __forceinline__ void pf_line(const void* p) {
+#ifdef __CUDA_ARCH__
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 #endif
 }
 // TMA-engine prefetch of a contiguous row into L2 (no registers, no smem).
@@ -188,11 +199,26 @@ bool usePrefetch() {
     static const bool v = usePersistent() && knob("QK_JIT_PF", 1) != 0;
     return v;
 }
+// QK_JIT_PF_SPARSE (default 1; persistent grids: the TMA-pipelined form, and
+// the plain form under QK_JIT_PERSIST=1): in a run with known zeros, each
+// thread prefetches into L2 the support amplitudes its slots will read in the
+// CTA's next tile, so the next tile's loads do not wait on HBM.
+bool useSparsePrefetch() {
+    static const bool v = knob("QK_JIT_PF_SPARSE", 1) != 0;
+    return v;
+}
 
 // QK_CTA_LITERAL (default 1): per-CTA factors as straight-line code with
 // literal terms; 0: a loop over device term tables.
 bool literalFactors() {
     static const bool v = knob("QK_CTA_LITERAL", 1) != 0;
+    return v;
+}
+
+// QK_JIT_TMAP (default 1): the TMA-pipelined kernels move a tile with one
+// tensor-map op (cuTensorMapEncodeTiled) instead of one bulk copy per row.
+bool useTensorMaps() {
+    static const bool v = knob("QK_JIT_TMAP", 1) != 0;
     return v;
 }
 
@@ -218,13 +244,41 @@ int lowRun(const PassParams& P) {
     return L;
 }
 
-// TMA-pipelined form (QK_JIT_TMA=1; off by default: issuing one bulk copy per
-// <= 4 KB row costs more than the overlap gains on B200): a persistent CTA per SM keeps
-// the NEXT tile streaming into a 128 KB shared-memory buffer (cp.async.bulk
-// rows, mbarrier) while the current tile computes in registers; exchanges
-// run in two halves through a 64 KB buffer, split on a tile bit that stays in
-// the same register slot (schedule.cpp guarantees one).  Needs 2^13 tiles, 32
-// amplitudes per thread and >= 128-B rows.
+// The tile as a box of a <= 5-D tensor view of the slice in doubles:
+// dimension d spans memory bits [lo[d], lo[d+1]) (the last one up to the
+// slice's top bit) and the box its low tb[d] bits, which are tile bits (<= 8
+// per dimension, <= cap0 <= 7 in dimension 0 whose elements are the two
+// halves of an amplitude).  Returns the rank, 0 when the tile needs more than 5
+// dimensions or does not hold memory bits 0-2 (rows under 128 B).
+int tensorDims(const PassParams& P, int lo[5], int tb[5], int cap0 = 7) {
+    if (lowRun(P) < 3) return 0;
+    int nd = 0;
+    for (int j = 0; j < P.ct;) {
+        const int start = P.tile_phys[j], cap = nd == 0 ? cap0 : 8;
+        int len = 1;
+        while (j + len < P.ct && P.tile_phys[j + len] == start + len && len < cap) len++;
+        if (nd == 5) return 0;
+        lo[nd] = start;
+        tb[nd] = len;
+        nd++;
+        j += len;
+    }
+    for (int d = 0; d + 1 < nd; d++)
+        if (lo[d + 1] - lo[d] + (d == 0 ? 1 : 0) > 32) return 0;  // extents <= 2^32
+    return nd;
+}
+
+// TMA-pipelined form (an autotune variant of every 2^13-tile pass; the default
+// for all passes under QK_JIT_TMA=1): a persistent CTA per SM keeps the NEXT
+// tile streaming into a 128 KB shared-memory buffer PB (one tensor-map TMA
+// load per tile, swizzled, mbarrier) while the current tile computes in
+// registers, and in runs with known zeros stages its output tile in PB for
+// one TMA store that drains while the next tile computes; exchanges run in
+// two halves through a 64 KB buffer, split on a tile bit that stays in the
+// same register slot (schedule.cpp guarantees one).  Needs 2^13 tiles, 32
+// amplitudes per thread and >= 128-B rows.  Measured on B200 (QFT / QAOA /
+// Grover at 33 qubits) it loses to the plain kernel by 5-30 %: the
+// half-splittable exchanges cost extra segments (QFT pass 3: 3 instead of 2).
 bool pipelined(const PassParams& P) {
     if (!P.half_x || P.ct != 13 || P.rb != 5 || lowRun(P) < 3) return false;
     for (int c = 1; c < P.nsegs; c++) {
@@ -235,6 +289,66 @@ bool pipelined(const PassParams& P) {
 }
 }  // namespace
 bool pipelinedPass(const PassParams& P) { return pipelined(P); }
+
+// Shared-memory wavefronts of one tile's warp-wide 16-byte accesses to PB
+// (every register slot, warp 0; other warps differ by a constant XOR) when
+// the amplitude at tile coordinate u sits at chunk u ^ ((u >> 3) & (2^mode -
+// 1)): a phase is 8 consecutive lanes and costs the largest number of
+// distinct chunks sharing a bank group.
+int pbWavefronts(const PassParams& P, const uint8_t* m, int mode) {
+    const uint32_t msk = (1u << mode) - 1;
+    int total = 0;
+    for (int s = 0; s < (1 << P.rb); s++) {
+        uint32_t us = 0;
+        for (int k = 0; k < P.rb; k++)
+            if ((s >> k) & 1) us |= 1u << m[k];
+        for (int ph = 0; ph < 4; ph++) {
+            uint32_t chunk[8];
+            for (int l = 0; l < 8; l++) {
+                const uint32_t lane = uint32_t(ph * 8 + l);
+                uint32_t u = us;
+                for (int j = 0; j < 5 && j < P.ct - P.rb; j++) u |= ((lane >> j) & 1u) << m[P.rb + j];
+                chunk[l] = u ^ ((u >> 3) & msk);
+            }
+            int worst = 0;
+            for (int g = 0; g < 8; g++) {
+                int distinct = 0;
+                for (int l = 0; l < 8; l++) {
+                    if ((chunk[l] & 7u) != uint32_t(g)) continue;
+                    bool seen = false;
+                    for (int e = 0; e < l; e++) seen = seen || chunk[e] == chunk[l];
+                    distinct += seen ? 0 : 1;
+                }
+                worst = std::max(worst, distinct);
+            }
+            total += worst;
+        }
+    }
+    return total;
+}
+
+// The TMA-pipelined kernel's tensor view: rank (0: rows only) and the PB
+// swizzle (0 none, 1 / 2 / 3: the 32 / 64 / 128-byte hardware patterns) with
+// the fewest shared-memory wavefronts for the tile's reads (dense runs) and
+// staged writes (sparse runs).  A swizzle limits dimension 0 to its span.
+int tensorLayout(const PassParams& P, int lo[5], int tb[5], int* swizzle) {
+    *swizzle = 0;
+    if (!pipelined(P)) return 0;
+    int best = -1, bestNd = 0;
+    for (int mode = 0; mode <= 3; mode++) {
+        int l[5], t[5];
+        const int nd = tensorDims(P, l, t, mode ? mode : 7);
+        if (!nd) continue;
+        const int cost = pbWavefronts(P, P.map_in[0], mode) + pbWavefronts(P, P.map_out[P.nsegs - 1], mode);
+        if (best >= 0 && cost >= best) continue;
+        best = cost;
+        bestNd = nd;
+        *swizzle = mode;
+        std::memcpy(lo, l, sizeof l);
+        std::memcpy(tb, t, sizeof t);
+    }
+    return bestNd;
+}
 int lowRunOf(const PassParams& P) { return lowRun(P); }
 namespace {
 constexpr int kPipeSmemAmps = (1 << 13) + (1 << 12) + qkdev::kMaxCtaFactors + 1;  // PB | XS | F | mbarrier
@@ -324,10 +438,11 @@ public:
 
     std::string runPipelined(const std::string& name) {
         const int L = lowRun(P_);
+        tensorView();
         o_ << kPrologue;
         ctaTables();
         o_ << "extern \"C\" __global__ void __launch_bounds__(" << nt_ << ",1) " << name
-           << "(double2* __restrict__ st, const double2* __restrict__ gt, const u32 ntiles, const u64 basis, const u32 tile0, double* __restrict__ np, const u64 smask, const u64 sval, const u32 zskip) {\n"
+           << "(double2* __restrict__ st, const double2* __restrict__ gt, const u32 ntiles, const u64 basis, const u32 tile0, double* __restrict__ np, const u64 smask, const u64 sval, const u32 zskip, const __grid_constant__ QkTmap tm, const u32 tmv) {\n"
            << "  extern __shared__ double2 sm[];  // PB: next tile (linear tile coordinates) | XS | F | mbarrier\n"
            << "  double2* const XS = sm + 8192;\n  double2* const F = sm + 12288;\n"
            << "  u64* const mbar = (u64*)(sm + " << (12288 + qkdev::kMaxCtaFactors) << ");\n  const u32 tid = threadIdx.x;\n"
@@ -344,14 +459,15 @@ public:
         for (int s = 0; s < na_; s++) decl += (s ? ", a" : "a") + std::to_string(s);
         o_ << decl << ";\n  double2 P = C2(1.0, 0.0);\n" << pendDecl();
         o_ << "  if (tma) {\n    mbar_wait(mbar, phase);\n    phase ^= 1u;\n    { const u32 u = "
-           << threadSmem(P_.map_in[0]) << ";\n";
-        for (int s = 0; s < na_; s++) o_ << "    a" << s << " = sm[u | " << regCoord(P_.map_in[0], s) << "u];\n";
+           << pbSwExpr(threadSmem(P_.map_in[0])) << ";\n";
+        for (int s = 0; s < na_; s++) o_ << "    a" << s << " = sm[u ^ " << pbSw(regCoord(P_.map_in[0], s)) << "u];\n";
         o_ << "    }\n    __syncthreads();  // PB drained: stream the next tile into it\n"
            << "    if (tile + gridDim.x < ntiles) {\n";
         issueTile("tile + gridDim.x", L);
         o_ << "    }\n  } else if (smask != 0ull) {  // known zeros: read only the support\n"
            << "    const u64 off = base | " << threadGlobal(P_.map_in[0]) << ";\n";
         sparseLoads("    ");
+        prefetchSupportNext();
         o_ << "  } else {  // first pass of a run: synthesize |basis>\n"
            << "    const u64 off = base | " << threadGlobal(P_.map_in[0]) << ";\n";
         for (int s = 0; s < na_; s++)
@@ -368,10 +484,10 @@ public:
         // in PB and let the TMA engine write its rows, so the HBM write of this
         // tile drains while the CTA computes the next one.
         o_ << "  if (smask != 0ull) {\n    bulk_wait_read();  // this thread's previous rows have left PB\n"
-           << "    __syncthreads();\n    { const u32 u = " << threadSmem(P_.map_out[last]) << " ^ "
-           << uint32_t(P_.xmask_out[last]) << "u;\n";
+           << "    __syncthreads();\n    { const u32 u = "
+           << pbSwExpr(threadSmem(P_.map_out[last]) + " ^ " + std::to_string(uint32_t(P_.xmask_out[last])) + "u") << ";\n";
         for (int s = 0; s < na_; s++)
-            o_ << "    sm[u ^ " << regCoord(P_.map_out[last], s) << "u] = a" << nm_[size_t(s)] << ";\n";
+            o_ << "    sm[u ^ " << pbSw(regCoord(P_.map_out[last], s)) << "u] = a" << nm_[size_t(s)] << ";\n";
         o_ << "    }\n    fence_async();\n    __syncthreads();\n";
         storeTile(L);
         o_ << "  } else {\n";
@@ -423,10 +539,62 @@ private:
         }
         o_ << "    continue;\n  }\n";
     }
-    // The staged output tile (PB, linear tile coordinates) to global memory:
-    // one bulk store per contiguous row, rows spread over all threads, each
-    // thread committing its own bulk group.
+    // Tensor view of the tile (tensorLayout): rank, dimensions, PB swizzle.
+    int tmNd_ = 0, tmLo_[5] = {}, tmTb_[5] = {}, tmSwz_ = 0;
+    void tensorView() { tmNd_ = tensorLayout(P_, tmLo_, tmTb_, &tmSwz_); }
+    // PB chunk of tile coordinate u under the swizzle (GF(2)-linear: the
+    // thread part and each slot's part are swizzled separately).
+    uint32_t pbSw(uint32_t u) const { return u ^ ((u >> 3) & ((1u << tmSwz_) - 1)); }
+    std::string pbSwExpr(const std::string& u) const {
+        if (!tmSwz_) return u;
+        return "((" + u + ") ^ (((" + u + ") >> 3) & " + std::to_string((1u << tmSwz_) - 1) + "u))";
+    }
+    // Box coordinates of the tile at `b` ("r" operands).
+    std::string tmCoords(const std::string& b) const {
+        std::string c;
+        for (int d = 0; d < tmNd_; d++) {
+            std::string e = d ? "(" + b + " >> " + std::to_string(tmLo_[d]) + ")" : "(" + b + " << 1)";
+            if (d + 1 < tmNd_)
+                e = "(" + e + " & " + std::to_string((uint64_t(1) << (tmLo_[d + 1] - tmLo_[d] + (d ? 0 : 1))) - 1) + "ull)";
+            c += std::string(d ? ", " : "") + "\"r\"((int)" + e + ")";
+        }
+        return c;
+    }
+    std::string tmOperands(int first) const {
+        std::string s = "{";
+        for (int d = 0; d < tmNd_; d++) s += (d ? ", %" : "%") + std::to_string(first + d);
+        return s + "}";
+    }
+    // Host builds (tests/host/jit_host_shim.h) replay a tensor-map copy of the
+    // tile at `b` element by element, swizzle included.
+    void hostTileCopy(const std::string& b, bool toGlobal) {
+        o_ << "#else\n    if (tid == 0u) {\n      static const unsigned char tp_[] = {";
+        for (int j = 0; j < ct_; j++) o_ << (j ? "," : "") << int(P_.tile_phys[j]);
+        o_ << "};\n      for (u32 v = 0; v < " << (1u << ct_) << "u; v++) {\n        u64 o = " << b
+           << ";\n        for (int j = 0; j < " << ct_ << "; j++) o |= (u64)((v >> j) & 1u) << tp_[j];\n        const u32 c = "
+           << pbSwExpr("v") << ";\n        " << (toGlobal ? "st[o] = sm[c];" : "sm[c] = st[o];") << "\n      }\n    }\n#endif\n";
+    }
+    // The staged tile (PB) to global memory: one tensor-map TMA store (tmv:
+    // launch() encoded the map), else one bulk store per row (unswizzled PB
+    // only).
     void storeTile(int Lrun) {
+        if (!tmNd_) {
+            storeRows(Lrun);
+            return;
+        }
+        o_ << "#ifdef __CUDA_ARCH__\n    if (tmv) {\n      if (tid == 0u) {\n        asm volatile(\"cp.async.bulk.tensor." << tmNd_
+           << "d.global.shared::cta.bulk_group [%0, " << tmOperands(2) << "], [%1];\" :: \"l\"(&tm), \"r\"(smem_u32(sm)), "
+           << tmCoords("base") << " : \"memory\");\n        bulk_commit();\n      }\n    } else {\n";
+        if (tmSwz_)
+            o_ << "      __trap();  // a swizzled PB has no row form\n";
+        else
+            storeRows(Lrun);
+        o_ << "    }\n";
+        hostTileCopy("base", true);
+    }
+    // One bulk store per contiguous row, rows spread over all threads, each
+    // thread committing its own bulk group.
+    void storeRows(int Lrun) {
         const int L = std::min(Lrun, 8);  // rows of <= 4 KB
         const int rows = 1 << (ct_ - L);
         o_ << "    for (u32 r = tid; r < " << rows << "u; r += " << nt_ << "u) {\n      u64 o = base;\n";
@@ -434,16 +602,36 @@ private:
             o_ << "      o |= (u64)((r >> " << (j - L) << ") & 1u) << " << int(P_.tile_phys[j]) << ";\n";
         o_ << "      bulk_s2g(st + o, sm + (r << " << L << "), " << (16u << L) << "u);\n    }\n    bulk_commit();\n";
     }
-    // Warp 0 streams tile `t` into PB: one cp.async.bulk per contiguous row.
+    // Stream tile `t` into PB: one tensor-map TMA load, else one bulk copy per
+    // contiguous row.
     void issueTile(const std::string& t, int Lrun) {
         const int L = std::min(Lrun, 8);  // rows of <= 4 KB, spread over all threads
         const int rows = 1 << (ct_ - L);
         o_ << "    {\n      " << deposit("nb", "(u64)(" + t + ")") << "\n"
            << "      fence_async();\n      if (tid == 0u) mbar_expect_tx(mbar, " << (16u << ct_) << "u);\n"
-           << "      __syncthreads();\n      for (u32 r = tid; r < " << rows << "u; r += " << nt_ << "u) {\n        u64 o = nb;\n";
-        for (int j = L; j < ct_; j++)
-            o_ << "        o |= (u64)((r >> " << (j - L) << ") & 1u) << " << int(P_.tile_phys[j]) << ";\n";
-        o_ << "        bulk_g2s(sm + (r << " << L << "), st + o, " << (16u << L) << "u, mbar);\n      }\n    }\n";
+           << "      __syncthreads();\n";
+        auto rowsLoop = [&]() {
+            o_ << "      for (u32 r = tid; r < " << rows << "u; r += " << nt_ << "u) {\n        u64 o = nb;\n";
+            for (int j = L; j < ct_; j++)
+                o_ << "        o |= (u64)((r >> " << (j - L) << ") & 1u) << " << int(P_.tile_phys[j]) << ";\n";
+            o_ << "        bulk_g2s(sm + (r << " << L << "), st + o, " << (16u << L) << "u, mbar);\n      }\n";
+        };
+        if (!tmNd_) {
+            rowsLoop();
+            o_ << "    }\n";
+            return;
+        }
+        o_ << "#ifdef __CUDA_ARCH__\n      if (tmv) {\n        if (tid == 0u)\n          asm volatile(\"cp.async.bulk.tensor." << tmNd_
+           << "d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, " << tmOperands(3)
+           << "], [%2];\" :: \"r\"(smem_u32(sm)), \"l\"(&tm), \"r\"(smem_u32(mbar)), " << tmCoords("nb")
+           << " : \"memory\");\n      } else {\n";
+        if (tmSwz_)
+            o_ << "      __trap();  // a swizzled PB has no row form\n";
+        else
+            rowsLoop();
+        o_ << "      }\n";
+        hostTileCopy("nb", false);
+        o_ << "    }\n";
     }
     // Register slot whose tile bit is memory bit 0 (-1: none / wide access off).
     int slotOfMem0(const uint8_t* m) const {
@@ -511,12 +699,13 @@ private:
     // is deposited into the non-tile bits the support leaves free, and the
     // fixed ones come from sval (the pass runs on 2^free tiles instead of
     // launching every tile to skip most of them).
-    std::string tileBase() const {
-        const std::string all = deposit("base", "(u64)tile");
+    std::string tileBase(const std::string& var = "base", const std::string& t = "tile") const {
+        const std::string all = deposit(var, "(u64)(" + t + ")");
         const std::string nt = std::to_string(~P_.tile_mask) + "ull";
         return all + "\n  if (zskip == 2u) {\n    const u64 fixed_ = smask & " + nt + ";\n" +
-               "    u64 m_ = " + nt + " & ~fixed_, t_ = (u64)tile;\n    base = sval & fixed_;\n" +
-               "    while (t_) { const u64 low_ = m_ & (0ull - m_); if (t_ & 1ull) base |= low_; t_ >>= 1; m_ ^= low_; }\n  }";
+               "    u64 m_ = " + nt + " & ~fixed_, t_ = (u64)(" + t + ");\n    " + var + " = sval & fixed_;\n" +
+               "    while (t_) { const u64 low_ = m_ & (0ull - m_); if (t_ & 1ull) " + var +
+               " |= low_; t_ >>= 1; m_ ^= low_; }\n  }";
     }
     // CTA index deposited into the non-tile bits of the slice index.
     // Statement block declaring `u64 var` = v deposited into the non-tile bits.
@@ -532,12 +721,13 @@ private:
     // Rows of the tile: the run of tile bits that are the lowest memory bits is
     // contiguous; the remaining tile bits enumerate rows.
     void prefetchNext() {
+        if (usePersistent()) prefetchSupportNext();
         int L = 0;
         while (L < ct_ && P_.tile_phys[L] == L) L++;
         if (L < 3 || !usePrefetch()) return;  // rows under 128 B: not worth a TMA op each
         const int rows = 1 << (ct_ - L);
         const unsigned bytes = 16u << L;
-        o_ << "  if (tile + gridDim.x < ntiles) {\n    u64 nb = (u64)(tile + gridDim.x);\n";
+        o_ << "  if (smask == 0ull && basis == ~0ull && tile + gridDim.x < ntiles) {\n    u64 nb = (u64)(tile + gridDim.x);\n";
         for (int j = 0; j < ct_; j++) {
             const int p = P_.tile_phys[j];
             o_ << "    nb = ((nb >> " << p << ") << " << (p + 1) << ") | (nb & " << ((uint64_t(1) << p) - 1) << "ull);\n";
@@ -546,6 +736,23 @@ private:
         for (int j = L; j < ct_; j++)
             o_ << "      o |= (u64)((r >> " << (j - L) << ") & 1u) << " << int(P_.tile_phys[j]) << ";\n";
         o_ << "      pf_l2(st + o, " << bytes << "u);\n    }\n  }\n";
+    }
+    // Each thread prefetches into L2 the support amplitudes its slots read in
+    // the CTA's next tile (a run with known zeros, persistent grid).
+    void prefetchSupportNext() {
+        if (useSparsePrefetch()) {
+            uint64_t slots = 0;
+            for (int s = 0; s < na_; s++) slots |= regGlobal(P_.map_in[0], s);
+            o_ << "  if (smask != 0ull && tile + gridDim.x < ntiles) {\n  " << tileBase("nb_", "tile + gridDim.x") << "\n"
+               << "    const u64 noff_ = nb_ | " << threadGlobal(P_.map_in[0]) << ";\n"
+               << "    if (((noff_ ^ sval) & smask & " << (~slots) << "ull) == 0ull) {\n";
+            for (int s = 0; s < na_; s++) {
+                const uint64_t r = regGlobal(P_.map_in[0], s);
+                o_ << "      if (((" << r << "ull ^ sval) & smask & " << slots << "ull) == 0ull) pf_line(st + (noff_ | " << r
+                   << "ull));\n";
+            }
+            o_ << "    }\n  }\n";
+        }
     }
     // Factor f is computed by warp f mod #warps: lane j takes term j (mod 32)
     // with its condition and value as literals (no table loads), then the
@@ -963,10 +1170,10 @@ private:
 // ---- compile / load / launch -------------------------------------------------
 
 // Bump when the generated code changes for the same PassParams (on-disk cache key).
-constexpr uint64_t kGeneratorVersion = 29;
+constexpr uint64_t kGeneratorVersion = 32;
 
 uint64_t hashPass(const PassParams& P) {
-    uint64_t h = 1469598103934665603ull ^ (kGeneratorVersion * 0x9E3779B97F4A7C15ull) ^ (usePrefetch() ? 1u : 0u) ^ (usePersistent() ? 2u : 0u) ^
+    uint64_t h = 1469598103934665603ull ^ (kGeneratorVersion * 0x9E3779B97F4A7C15ull) ^ (usePrefetch() ? 1u : 0u) ^ (usePersistent() ? 2u : 0u) ^ (useSparsePrefetch() ? 8u : 0u) ^
                  (qkdev::halfExchanges() ? 4u : 0u);
     const unsigned char* p = reinterpret_cast<const unsigned char*>(&P);
     for (size_t i = 0; i < sizeof(PassParams); i++) {
@@ -984,6 +1191,8 @@ struct Driver {
     Res (*funcSetAttribute)(void*, int, int) = nullptr;
     Res (*launchKernel)(void*, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, void*, void**,
                         void**) = nullptr;
+    Res (*tensorMapEncodeTiled)(void*, int, unsigned, void*, const uint64_t*, const uint64_t*, const unsigned*,
+                                const unsigned*, int, int, int, int) = nullptr;  // optional
     bool ok = false;
     Driver() {
         void* h = dlopen("libcuda.so.1", RTLD_NOW | RTLD_GLOBAL);
@@ -992,6 +1201,7 @@ struct Driver {
         moduleGetFunction = reinterpret_cast<decltype(moduleGetFunction)>(dlsym(h, "cuModuleGetFunction"));
         funcSetAttribute = reinterpret_cast<decltype(funcSetAttribute)>(dlsym(h, "cuFuncSetAttribute"));
         launchKernel = reinterpret_cast<decltype(launchKernel)>(dlsym(h, "cuLaunchKernel"));
+        tensorMapEncodeTiled = reinterpret_cast<decltype(tensorMapEncodeTiled)>(dlsym(h, "cuTensorMapEncodeTiled"));
         ok = moduleLoadData && moduleGetFunction && funcSetAttribute && launchKernel;
     }
 };
@@ -1294,7 +1504,29 @@ cudaError_t launch(const PassParams& P, double2* state, const double2* gtab, int
     const unsigned smem = pipe ? unsigned(sizeof(double2) * kPipeSmemAmps)
                                : unsigned((sizeof(double2) << P.ct) + sizeof(double2) * qkdev::kMaxCtaFactors + 256);
     unsigned zskip = unsigned(zeroSkip);
-    void* args[] = {&state, &gtab, &ntiles, &basis, &tile0, &np, &smask, &sval, &zskip};
+    // TMA-pipelined kernels: the tile as one box of a tensor view of the
+    // slice (tensorDims), so a tile moves in one TMA op instead of one per row.
+    alignas(64) uint64_t tmap[16] = {};
+    unsigned tmv = 0;
+    int lo[5], tb[5], swizzle = 0;
+    const int nd = pipe ? tensorLayout(P, lo, tb, &swizzle) : 0;
+    if (nd && (useTensorMaps() || swizzle) && driver().tensorMapEncodeTiled && nLocal - lo[nd - 1] <= 32) {
+        uint64_t dim[5], stride[4];
+        unsigned box[5], es[5];
+        for (int d = 0; d < nd; d++) {
+            const int hi = d + 1 < nd ? lo[d + 1] : nLocal;
+            dim[d] = uint64_t(1) << (hi - lo[d] + (d ? 0 : 1));
+            box[d] = 1u << (tb[d] + (d ? 0 : 1));
+            es[d] = 1u;
+            if (d) stride[d - 1] = uint64_t(16) << lo[d];
+        }
+        constexpr int kFloat64 = 8, kL2Promote256 = 3;  // CU_TENSOR_MAP_DATA_TYPE_FLOAT64, ..._L2_PROMOTION_L2_256B
+        if (driver().tensorMapEncodeTiled(tmap, kFloat64, unsigned(nd), state, dim, stride, box, es, 0, swizzle,
+                                          kL2Promote256, 0) == 0)
+            tmv = 1;
+    }
+    if (nd && swizzle && !tmv) return cudaErrorInvalidValue;  // a swizzled PB needs the tensor map
+    void* args[] = {&state, &gtab, &ntiles, &basis, &tile0, &np, &smask, &sval, &zskip, tmap, &tmv};
     if (driver().launchKernel(fn, ctas, 1, 1, nt, 1, 1, smem, stream, args, nullptr) != 0)
         return cudaErrorLaunchFailure;
     return cudaSuccess;

@@ -9,6 +9,7 @@
 #include <memory>
 #include <cstdint>
 #include <thread>
+#include <type_traits>
 #include <vector>
 
 struct double2 {
@@ -53,6 +54,8 @@ static inline void __stcs(T* p, T v) { *p = v; }
 #define __launch_bounds__(a, b)
 #define __restrict__
 #define __shared__
+#define __grid_constant__
+#define __align__(n) alignas(n)
 // `extern __shared__ double2 sm[];` in the kernel binds to this array.
 extern "C" double2 sm[1 << 14];
 
@@ -85,7 +88,16 @@ extern "C" double2 sm[1 << 14];
                 ts.emplace_back([=] {                                                         \
                     qk_tl_tid = t;                                                            \
                     qk_tl_bid = b;                                                            \
-                    KERNEL(st, gt, ntiles, basis, tile0, np, smask, sval, zskip);                    \
+                    auto call = [&](auto k) { /* TMA-pipelined kernels: no tensor map (rows) */ \
+                        if constexpr (std::is_invocable_v<decltype(k), double2*, const double2*,    \
+                                          unsigned, unsigned long long, unsigned, double*,          \
+                                          unsigned long long, unsigned long long, unsigned,         \
+                                          QkTmap, unsigned>)                                        \
+                            k(st, gt, ntiles, basis, tile0, np, smask, sval, zskip, QkTmap{}, 0u);  \
+                        else                                                                        \
+                            k(st, gt, ntiles, basis, tile0, np, smask, sval, zskip);                \
+                    };                                                                              \
+                    call(KERNEL);                                                                   \
                 });                                                                           \
             for (auto& th : ts) th.join();                                                    \
         }                                                                                     \
