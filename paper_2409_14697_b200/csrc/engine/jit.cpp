@@ -164,6 +164,11 @@ static __device__ __forceinline__ void bulk_wait_read() {  // sources of committ
 struct __align__(64) QkTmap {
     unsigned long long v[16];
 };
+static __device__ __forceinline__ void bulk_wait_read1() {  // all but the newest group have left shared memory
+#ifdef __CUDA_ARCH__
+    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+#endif
+}
 static __device__ __forceinline__ void bulk_wait_all() {
 #ifdef __CUDA_ARCH__
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -327,6 +332,45 @@ int pbWavefronts(const PassParams& P, const uint8_t* m, int mode) {
     return total;
 }
 
+// QK_STAGED_STORES (default 1): in runs with known zeros the plain kernel
+// writes its output tile through shared memory and the TMA engine instead of
+// register stores (stagedLayout).
+bool stagedStores() {
+    static const bool v = knob("QK_STAGED_STORES", 1) != 0;
+    return v;
+}
+
+// The plain kernel's staged output: the tile leaves as two half boxes of a
+// tensor view of the slice, split on its top tile bit -- half 0 staged in a
+// half-tile buffer S and drained across the whole next tile, half 1 in the
+// exchange buffer and drained before the next tile's first exchange -- so the
+// SM computes the next tile while the TMA engine writes this one (register
+// stores serialize with the compute: profiles/r2_store_path_probe.txt).
+// Rank 0: register stores only.  The swizzle minimizes the staging writes'
+// bank conflicts.
+int stagedLayout(const PassParams& P, int lo[5], int tb[5], int* swizzle) {
+    *swizzle = 0;
+    if (!stagedStores() || !P.stage_out || pipelined(P) || P.ct != 13) return 0;  // 2^12 tiles: two CTAs per SM overlap already
+    int best = -1, bestNd = 0;
+    for (int mode = 0; mode <= 3; mode++) {
+        int l[5], t[5];
+        const int nd = tensorDims(P, l, t, mode ? mode : 7);
+        if (!nd) continue;
+        const int cost = pbWavefronts(P, P.map_out[P.nsegs - 1], mode);
+        if (best >= 0 && cost >= best) continue;
+        best = cost;
+        bestNd = nd;
+        *swizzle = mode;
+        std::memcpy(lo, l, sizeof l);
+        std::memcpy(tb, t, sizeof t);
+    }
+    return bestNd;
+}
+bool stagedPass(const PassParams& P) {
+    int lo[5], tb[5], swizzle;
+    return stagedLayout(P, lo, tb, &swizzle) > 0;
+}
+
 // The TMA-pipelined kernel's tensor view: rank (0: rows only) and the PB
 // swizzle (0 none, 1 / 2 / 3: the 32 / 64 / 128-byte hardware patterns) with
 // the fewest shared-memory wavefronts for the tile's reads (dense runs) and
@@ -353,6 +397,16 @@ int lowRunOf(const PassParams& P) { return lowRun(P); }
 namespace {
 constexpr int kPipeSmemAmps = (1 << 13) + (1 << 12) + qkdev::kMaxCtaFactors + 1;  // PB | XS | F | mbarrier
 
+// Dynamic shared memory of a pass kernel: PB | XS | F | mbarrier (pipelined),
+// exchange buffer [| S] | F (plain).
+unsigned kernelSmem(const PassParams& P) {
+    if (pipelined(P)) return unsigned(sizeof(double2) * kPipeSmemAmps);
+    int lo[5], tb[5], swizzle;
+    const bool staged = stagedLayout(P, lo, tb, &swizzle) > 0;
+    return unsigned((sizeof(double2) << P.ct) + (staged ? sizeof(double2) << (P.ct - 1) : 0) +
+                    sizeof(double2) * qkdev::kMaxCtaFactors + 256);
+}
+
 class Gen {
 public:
     explicit Gen(const PassParams& P)
@@ -370,9 +424,16 @@ public:
         o_ << kPrologue;
         ctaTables();
         o_ << "extern \"C\" __global__ void __launch_bounds__(" << nt_ << "," << minb << ") " << name
-           << "(double2* __restrict__ st, const double2* __restrict__ gt, const u32 ntiles, const u64 basis, const u32 tile0, double* __restrict__ np, const u64 smask, const u64 sval, const u32 zskip) {\n";
-        o_ << "  extern __shared__ double2 sm[];\n  double2* const F = sm + " << (1 << ct_)
-           << ";\n  const u32 tid = threadIdx.x;\n";
+           << "(double2* __restrict__ st, const double2* __restrict__ gt, const u32 ntiles, const u64 basis, const u32 tile0, double* __restrict__ np, const u64 smask, const u64 sval, const u32 zskip, const __grid_constant__ QkTmap tm, const u32 tmv) {\n";
+        tmNd_ = stagedLayout(P_, tmLo_, tmTb_, &tmSwz_);
+        staged_ = tmNd_ > 0;
+        if (staged_)  // exchange buffer | S (half tile) | F
+            o_ << "  extern __shared__ double2 sm[];\n  double2* const S = sm + " << (1 << ct_) << ";\n  double2* const F = sm + "
+               << (3 << (ct_ - 1)) << ";\n  const u32 tid = threadIdx.x;\n"
+               << "#ifdef __CUDA_ARCH__\n  const bool stg_ = smask != 0ull && tmv != 0u;\n#else\n  const bool stg_ = smask != 0ull;\n#endif\n";
+        else
+            o_ << "  extern __shared__ double2 sm[];\n  double2* const F = sm + " << (1 << ct_)
+               << ";\n  const u32 tid = threadIdx.x;\n";
         hoistTables();
         o_ << "  for (u32 tile = blockIdx.x + tile0; tile < ntiles; tile += gridDim.x) {\n";
         o_ << "  " << tileBase() << "\n";
@@ -416,6 +477,10 @@ public:
         if (P_.nsegs == 1 && (std::memcmp(P_.map_in[0], P_.map_out[0], sizeof P_.map_in[0]) != 0 || P_.xmask_out[0]))
             o_ << "  __syncthreads();\n";
         if (P_.norm_out) emitNorm();
+        if (staged_) {
+            stageHalves(last);
+            o_ << "  } else\n";
+        }
         o_ << "  { const u64 off = (base | " << threadGlobal(P_.map_out[last]) << ") ^ " << gx << "ull;\n";
         const int ks = slotOfMem0(P_.map_out[last]);
         for (int s = 0; s < na_; s++) {
@@ -432,7 +497,9 @@ public:
         o_ << "  }\n";
         // The next iteration's first shared-memory write must not overtake a
         // slow thread still reading this tile's last exchange.
-        o_ << "  if (tile + gridDim.x < ntiles) __syncthreads();\n  }\n}\n";
+        o_ << "  if (tile + gridDim.x < ntiles) __syncthreads();\n  }\n";
+        if (staged_) o_ << "  if (tid == 0u) bulk_wait_all();\n";
+        o_ << "}\n";
         return o_.str();
     }
 
@@ -538,6 +605,44 @@ private:
             o_ << "    if ((tid & 31u) == 0u) np[(u64)tile * " << warps << "u + (tid >> 5)] = 0.0;\n";
         }
         o_ << "    continue;\n  }\n";
+    }
+    bool staged_ = false;
+    // Staged store of the output tile (stagedLayout), opening the `if (stg_)`
+    // branch: half 0 (top tile bit 0) into S, half 1 into the exchange buffer,
+    // then one TMA store per half (half 1 first: it must drain sooner).
+    void stageHalves(int last) {
+        const uint32_t half = 1u << (ct_ - 1);
+        const int d = tmNd_ - 1;
+        o_ << "  if (stg_) {\n    if (tid == 0u) bulk_wait_read();  // both halves of the previous tile have left\n"
+           << "    __syncthreads();\n    { const u32 u = "
+           << pbSwExpr(threadSmem(P_.map_out[last]) + " ^ " + std::to_string(uint32_t(P_.xmask_out[last])) + "u") << ";\n"
+           << "    double2* const H0 = (u & " << half << "u) ? sm : S;\n    double2* const H1 = (u & " << half
+           << "u) ? S : sm;\n";
+        for (int s = 0; s < na_; s++) {
+            const uint32_t w = pbSw(regCoord(P_.map_out[last], s));
+            o_ << "    " << ((w & half) ? "H1" : "H0") << "[(u ^ " << w << "u) & " << (half - 1) << "u] = a" << nm_[size_t(s)]
+               << ";\n";
+        }
+        o_ << "    }\n    fence_async();\n    __syncthreads();\n";
+        const std::string hiCoords = [&] {
+            std::string c = tmCoords("base");
+            // the top dimension's coordinate of half 1: + half its box
+            const std::string key = "\"r\"((int)(base >> " + std::to_string(tmLo_[d]) + ")";
+            const size_t at = c.rfind(key);
+            c.insert(at + key.size(), " + " + std::to_string(1 << (tmTb_[d] - 1)));
+            return c;
+        }();
+        o_ << "#ifdef __CUDA_ARCH__\n    if (tid == 0u) {\n"
+           << "      asm volatile(\"cp.async.bulk.tensor." << tmNd_ << "d.global.shared::cta.bulk_group [%0, " << tmOperands(2)
+           << "], [%1];\" :: \"l\"(&tm), \"r\"(smem_u32(sm)), " << hiCoords << " : \"memory\");\n      bulk_commit();\n"
+           << "      asm volatile(\"cp.async.bulk.tensor." << tmNd_ << "d.global.shared::cta.bulk_group [%0, " << tmOperands(2)
+           << "], [%1];\" :: \"l\"(&tm), \"r\"(smem_u32(S)), " << tmCoords("base") << " : \"memory\");\n      bulk_commit();\n"
+           << "    }\n#else\n    if (tid == 0u) {\n      static const unsigned char tp_[] = {";
+        for (int j = 0; j < ct_; j++) o_ << (j ? "," : "") << int(P_.tile_phys[j]);
+        o_ << "};\n      for (u32 h = 0; h < 2u; h++)\n        for (u32 v = 0; v < " << half << "u; v++) {\n"
+           << "          u64 o = base | ((u64)h << tp_[" << (ct_ - 1) << "]);\n"
+           << "          for (int j = 0; j < " << (ct_ - 1) << "; j++) o |= (u64)((v >> j) & 1u) << tp_[j];\n"
+           << "          st[o] = (h ? sm : S)[" << pbSwExpr("v") << "];\n        }\n    }\n#endif\n";
     }
     // Tensor view of the tile (tensorLayout): rank, dimensions, PB swizzle.
     int tmNd_ = 0, tmLo_[5] = {}, tmTb_[5] = {}, tmSwz_ = 0;
@@ -1065,6 +1170,8 @@ private:
                 const uint8_t* mo = P_.map_out[d.c - 1];
                 const uint8_t* mi = P_.map_in[d.c];
                 if (pipe_) return halfExchange(d.c, mo, mi);
+                if (staged_)  // the previous tile's half 1 must have left the exchange buffer
+                    o_ << "  if (stg_ && tid == 0u) bulk_wait_read1();\n";
                 o_ << "  __syncthreads();\n  { const u32 u = swz(" << threadSmem(mo) << ") ^ "
                    << swzHost(P_.xmask_out[d.c - 1]) << "u;\n";
                 for (int s = 0; s < na_; s++) o_ << "  sm[u ^ " << regSmem(mo, s) << "u] = " << A(s) << ";\n";
@@ -1170,7 +1277,7 @@ private:
 // ---- compile / load / launch -------------------------------------------------
 
 // Bump when the generated code changes for the same PassParams (on-disk cache key).
-constexpr uint64_t kGeneratorVersion = 32;
+constexpr uint64_t kGeneratorVersion = 33;
 
 uint64_t hashPass(const PassParams& P) {
     uint64_t h = 1469598103934665603ull ^ (kGeneratorVersion * 0x9E3779B97F4A7C15ull) ^ (usePrefetch() ? 1u : 0u) ^ (usePersistent() ? 2u : 0u) ^ (useSparsePrefetch() ? 8u : 0u) ^
@@ -1321,8 +1428,7 @@ void* functionFor(const PassParams& P, uint64_t h, int device) {
     void* fn = nullptr;
     if (d.moduleLoadData(&mod, e.cubin.data()) != 0) throw SimulationError("jit: cuModuleLoadData failed");
     if (d.moduleGetFunction(&fn, mod, kernelName(h).c_str()) != 0) throw SimulationError("jit: cuModuleGetFunction failed");
-    const int smem = pipelined(P) ? int(sizeof(double2) * kPipeSmemAmps)
-                                  : int((sizeof(double2) << P.ct) + sizeof(double2) * qkdev::kMaxCtaFactors + 256);
+    const int smem = int(kernelSmem(P));
     if (smem > 48 * 1024 && d.funcSetAttribute(fn, 8 /*CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES*/, smem) != 0)
         throw SimulationError("jit: cuFuncSetAttribute failed");
     e.func[device] = fn;
@@ -1500,23 +1606,23 @@ cudaError_t launch(const PassParams& P, double2* state, const double2* gtab, int
         const unsigned resident = unsigned(smCount(dev) * blocksPerSm(P.ct, P.rb));
         ctas = (ntiles < resident || !(usePersistent() || pipe)) ? ntiles : resident;
     }
+    int lo[5], tb[5], swizzle = 0;
+    const int nd = pipe ? tensorLayout(P, lo, tb, &swizzle) : stagedLayout(P, lo, tb, &swizzle);
+    const bool staged = !pipe && nd > 0;
     const unsigned nt = 1u << (P.ct - P.rb);
-    const unsigned smem = pipe ? unsigned(sizeof(double2) * kPipeSmemAmps)
-                               : unsigned((sizeof(double2) << P.ct) + sizeof(double2) * qkdev::kMaxCtaFactors + 256);
+    const unsigned smem = kernelSmem(P);
     unsigned zskip = unsigned(zeroSkip);
     // TMA-pipelined kernels: the tile as one box of a tensor view of the
     // slice (tensorDims), so a tile moves in one TMA op instead of one per row.
     alignas(64) uint64_t tmap[16] = {};
     unsigned tmv = 0;
-    int lo[5], tb[5], swizzle = 0;
-    const int nd = pipe ? tensorLayout(P, lo, tb, &swizzle) : 0;
-    if (nd && (useTensorMaps() || swizzle) && driver().tensorMapEncodeTiled && nLocal - lo[nd - 1] <= 32) {
+    if (nd && (useTensorMaps() || swizzle || staged) && driver().tensorMapEncodeTiled && nLocal - lo[nd - 1] <= 32) {
         uint64_t dim[5], stride[4];
         unsigned box[5], es[5];
         for (int d = 0; d < nd; d++) {
             const int hi = d + 1 < nd ? lo[d + 1] : nLocal;
             dim[d] = uint64_t(1) << (hi - lo[d] + (d ? 0 : 1));
-            box[d] = 1u << (tb[d] + (d ? 0 : 1));
+            box[d] = 1u << (tb[d] + (d ? 0 : 1) - (staged && d == nd - 1 ? 1 : 0));  // staged: half boxes
             es[d] = 1u;
             if (d) stride[d - 1] = uint64_t(16) << lo[d];
         }
@@ -1525,7 +1631,12 @@ cudaError_t launch(const PassParams& P, double2* state, const double2* gtab, int
                                           kL2Promote256, 0) == 0)
             tmv = 1;
     }
-    if (nd && swizzle && !tmv) return cudaErrorInvalidValue;  // a swizzled PB needs the tensor map
+    if (pipe && nd && swizzle && !tmv) return cudaErrorInvalidValue;  // a swizzled PB needs the tensor map
+    // staged stores drain while the CTA's next tile computes: a persistent grid
+    if (staged && tmv && smask != 0 && basis == ~uint64_t(0)) {
+        const unsigned resident = unsigned(smCount(dev) * blocksPerSm(P.ct, P.rb));
+        ctas = std::min(ntiles - tile0, resident);
+    }
     void* args[] = {&state, &gtab, &ntiles, &basis, &tile0, &np, &smask, &sval, &zskip, tmap, &tmv};
     if (driver().launchKernel(fn, ctas, 1, 1, nt, 1, 1, smem, stream, args, nullptr) != 0)
         return cudaErrorLaunchFailure;

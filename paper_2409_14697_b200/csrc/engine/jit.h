@@ -54,6 +54,10 @@ void setMinQubits(int v);
 // shared memory while the current one computes).
 bool pipelinedPass(const qkdev::PassParams& P);
 
+// P's specialized kernel writes its output through shared memory and the
+// TMA engine in runs with known zeros (staged stores; P.stage_out).
+bool stagedPass(const qkdev::PassParams& P);
+
 // NVRTC compile of a source to a cubin (used by tests on the CPU too).
 std::vector<char> compileToCubin(const std::string& src, const std::string& name);
 

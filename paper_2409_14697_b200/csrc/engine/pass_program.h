@@ -118,6 +118,8 @@ struct PassParams {
     CtaTerm cta_terms[kMaxCtaTerms];
     int32_t norm_out;  // specialized kernels: also write sum |a|^2 of each output tile to np[tile]
     int32_t half_x;    // exchanges scheduled splittable in halves (xsplit): TMA-pipelined kernel eligible
+    int32_t stage_out;  // specialized kernels: in runs with known zeros, the output tile leaves through shared
+                        // memory and the TMA engine (set for passes whose input is sparse in a basis run)
 };
 
 static_assert(sizeof(PassParams) <= 32000, "kernel parameter limit");

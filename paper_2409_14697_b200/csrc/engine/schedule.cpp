@@ -21,6 +21,7 @@
 // the same factor, so the product is folded into one exact power-of-two (x
 // 1/sqrt2) scale applied with the next full flush.
 #include "schedule.h"
+#include "jit.h"
 
 #include <algorithm>
 #include <sstream>
@@ -231,6 +232,7 @@ public:
         std::memset(P.get(), 0, sizeof(PassParams));
         P_ = P.get();
         P_->half_x = halfX_ ? 1 : 0;
+        P_->stage_out = sparseIn_ ? 1 : 0;
         P_->ct = ct_;
         P_->rb = rb_;
         for (int j = 0; j < ct_; j++) {
@@ -1348,11 +1350,17 @@ std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::
                     compileGroup(group, used, ct, nLocal, gtab, alt, rbAlt, false, sparseIn);
                     if (alt.size() == 1 && alt[0].kind == Step::Pass) steps[first].alts.push_back(alt[0].pass);
                 }
+                if (sparseIn && qkjit::stagedPass(*steps[first].pass)) {  // register stores instead of staged TMA stores
+                    auto p = std::make_shared<qkdev::PassParams>(*steps[first].pass);
+                    p->stage_out = 0;
+                    steps[first].alts.push_back(p);
+                }
                 if (!halfExchanges()) {  // 32 per thread, half-splittable exchanges: the TMA-pipelined kernel
                     std::vector<Step> alt;
                     compileGroup(group, used, ct, nLocal, gtab, alt, 5, true, sparseIn);
                     if (alt.size() == 1 && alt[0].kind == Step::Pass) steps[first].alts.push_back(alt[0].pass);
                 }
+                if (steps[first].alts.size() >= size_t(Step::Tune::kMax)) steps[first].alts.resize(Step::Tune::kMax - 1);
                 if (!steps[first].alts.empty()) steps[first].tune = std::make_shared<Step::Tune>();
             }
             route(first);

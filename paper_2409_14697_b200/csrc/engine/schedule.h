@@ -19,11 +19,13 @@ struct Step {
     // first execution and keeps the fastest (`tune`, shared by copies).
     std::vector<std::shared_ptr<qkdev::PassParams>> alts;
     struct Tune {
-        static constexpr int kMax = 4;      // rb 5 / 4 / 3, rb 5 with half-splittable exchanges (TMA-pipelined)
+        // rb 5 / 4 / 3, rb 5 with register stores in runs with known zeros
+        // (stage_out = 0), rb 5 with half-splittable exchanges (TMA-pipelined)
+        static constexpr int kMax = 5;
         static constexpr int kTimings = 2;  // each variant timed twice, round robin; its best time counts
-        float ms[kMax] = {0, 0, 0, 0};
-        int runs[kMax] = {0, 0, 0, 0};
-        int timed[kMax] = {0, 0, 0, 0};
+        float ms[kMax] = {};
+        int runs[kMax] = {};
+        int timed[kMax] = {};
         // the variant to run next: an untimed one while any is left, else the fastest
         int choice(int n) const {  // n = 1 + alts
             for (int r = 0; r < kTimings; r++)
