@@ -430,7 +430,8 @@ public:
         if (staged_)  // exchange buffer | S (half tile) | F
             o_ << "  extern __shared__ double2 sm[];\n  double2* const S = sm + " << (1 << ct_) << ";\n  double2* const F = sm + "
                << (3 << (ct_ - 1)) << ";\n  const u32 tid = threadIdx.x;\n"
-               << "#ifdef __CUDA_ARCH__\n  const bool stg_ = smask != 0ull && tmv != 0u;\n#else\n  const bool stg_ = smask != 0ull;\n#endif\n";
+               << "#ifdef __CUDA_ARCH__\n  const bool stg_ = " << (P_.stage_out == 2 ? "" : "smask != 0ull && ")
+               << "tmv != 0u;\n#else\n  const bool stg_ = " << (P_.stage_out == 2 ? "true" : "smask != 0ull") << ";\n#endif\n";
         else
             o_ << "  extern __shared__ double2 sm[];\n  double2* const F = sm + " << (1 << ct_)
                << ";\n  const u32 tid = threadIdx.x;\n";
@@ -1633,7 +1634,7 @@ cudaError_t launch(const PassParams& P, double2* state, const double2* gtab, int
     }
     if (pipe && nd && swizzle && !tmv) return cudaErrorInvalidValue;  // a swizzled PB needs the tensor map
     // staged stores drain while the CTA's next tile computes: a persistent grid
-    if (staged && tmv && smask != 0 && basis == ~uint64_t(0)) {
+    if (staged && tmv && (smask != 0 || P.stage_out == 2) && basis == ~uint64_t(0)) {
         const unsigned resident = unsigned(smCount(dev) * blocksPerSm(P.ct, P.rb));
         ctas = std::min(ntiles - tile0, resident);
     }

@@ -49,6 +49,7 @@ int regBitsFor(int ct);
 bool storeWide();
 bool tileTune();
 bool halfExchanges();
+bool stageDense();
 bool wideAccess();
 
 enum OpType : uint8_t {

@@ -94,6 +94,15 @@ bool carryPending() {
     return v;
 }
 
+// QK_STAGE_DENSE=1: passes whose input is dense stage their output tiles
+// through shared memory and TMA stores too (stage_out = 2; see jit.cpp).
+// Off: measured on B200 at 33 qubits, QAOA 283 -> 302 ms, random 632 -> 628
+// ms (the tile's register loads, not its stores, hold a dense pass back).
+bool stageDense() {
+    static const bool v = envInt("QK_STAGE_DENSE", 0, 0, 1) != 0;
+    return v;
+}
+
 bool halfExchanges() {
     static const bool v = envInt("QK_JIT_TMA", 0, 0, 1) != 0;
     return v;
@@ -232,7 +241,7 @@ public:
         std::memset(P.get(), 0, sizeof(PassParams));
         P_ = P.get();
         P_->half_x = halfX_ ? 1 : 0;
-        P_->stage_out = sparseIn_ ? 1 : 0;
+        P_->stage_out = sparseIn_ ? 1 : stageDense() ? 2 : 0;
         P_->ct = ct_;
         P_->rb = rb_;
         for (int j = 0; j < ct_; j++) {
@@ -1350,7 +1359,7 @@ std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::
                     compileGroup(group, used, ct, nLocal, gtab, alt, rbAlt, false, sparseIn);
                     if (alt.size() == 1 && alt[0].kind == Step::Pass) steps[first].alts.push_back(alt[0].pass);
                 }
-                if (sparseIn && qkjit::stagedPass(*steps[first].pass)) {  // register stores instead of staged TMA stores
+                if (qkjit::stagedPass(*steps[first].pass)) {  // register stores instead of staged TMA stores
                     auto p = std::make_shared<qkdev::PassParams>(*steps[first].pass);
                     p->stage_out = 0;
                     steps[first].alts.push_back(p);
