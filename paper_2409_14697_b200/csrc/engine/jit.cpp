@@ -366,6 +366,12 @@ int stagedLayout(const PassParams& P, int lo[5], int tb[5], int* swizzle) {
     }
     return bestNd;
 }
+// QK_JIT_PERSIST=1 with QK_JIT_PF (default 1): a dense-input 2^13-tile pass
+// runs on a persistent grid and prefetches its CTA's next tile into L2 with
+// two tensor-map TMA prefetches.  Off by default: measured at 33 qubits,
+// random 638 -> 615 ms but QAOA 285 -> 326 ms; as a per-pass autotune
+// variant (rb 5 only) it gained nothing (random 640, QAOA 287 ms).
+bool prefetchTiles(const PassParams& P) { return usePrefetch() && P.ct == 13 && !pipelined(P); }
 bool stagedPass(const PassParams& P) {
     int lo[5], tb[5], swizzle;
     return stagedLayout(P, lo, tb, &swizzle) > 0;
@@ -427,6 +433,7 @@ public:
            << "(double2* __restrict__ st, const double2* __restrict__ gt, const u32 ntiles, const u64 basis, const u32 tile0, double* __restrict__ np, const u64 smask, const u64 sval, const u32 zskip, const __grid_constant__ QkTmap tm, const u32 tmv) {\n";
         tmNd_ = stagedLayout(P_, tmLo_, tmTb_, &tmSwz_);
         staged_ = tmNd_ > 0;
+        if (!staged_ && prefetchTiles(P_)) tmNd_ = tensorDims(P_, tmLo_, tmTb_);  // the next tile's L2 prefetch only
         if (staged_)  // exchange buffer | S (half tile) | F
             o_ << "  extern __shared__ double2 sm[];\n  double2* const S = sm + " << (1 << ct_) << ";\n  double2* const F = sm + "
                << (3 << (ct_ - 1)) << ";\n  const u32 tid = threadIdx.x;\n"
@@ -828,6 +835,19 @@ private:
     // contiguous; the remaining tile bits enumerate rows.
     void prefetchNext() {
         if (usePersistent()) prefetchSupportNext();
+        if (tmNd_ && prefetchTiles(P_)) {  // one tensor prefetch per half tile
+            const int d = tmNd_ - 1;
+            std::string hi = tmCoords("nb_");
+            const std::string key = "\"r\"((int)(nb_ >> " + std::to_string(tmLo_[d]) + ")";
+            hi.insert(hi.rfind(key) + key.size(), " + " + std::to_string(1 << (tmTb_[d] - 1)));
+            o_ << "#ifdef __CUDA_ARCH__\n  if (basis == ~0ull && smask == 0ull && tmv && tid == 0u && tile + gridDim.x < ntiles) {\n  "
+               << tileBase("nb_", "tile + gridDim.x") << "\n"
+               << "    asm volatile(\"cp.async.bulk.prefetch.tensor." << tmNd_ << "d.L2.global.tile [%0, " << tmOperands(1)
+               << "];\" :: \"l\"(&tm), " << tmCoords("nb_") << " : \"memory\");\n"
+               << "    asm volatile(\"cp.async.bulk.prefetch.tensor." << tmNd_ << "d.L2.global.tile [%0, " << tmOperands(1)
+               << "];\" :: \"l\"(&tm), " << hi << " : \"memory\");\n  }\n#endif\n";
+            return;
+        }
         int L = 0;
         while (L < ct_ && P_.tile_phys[L] == L) L++;
         if (L < 3 || !usePrefetch()) return;  // rows under 128 B: not worth a TMA op each
@@ -1278,7 +1298,7 @@ private:
 // ---- compile / load / launch -------------------------------------------------
 
 // Bump when the generated code changes for the same PassParams (on-disk cache key).
-constexpr uint64_t kGeneratorVersion = 33;
+constexpr uint64_t kGeneratorVersion = 34;
 
 uint64_t hashPass(const PassParams& P) {
     uint64_t h = 1469598103934665603ull ^ (kGeneratorVersion * 0x9E3779B97F4A7C15ull) ^ (usePrefetch() ? 1u : 0u) ^ (usePersistent() ? 2u : 0u) ^ (useSparsePrefetch() ? 8u : 0u) ^
@@ -1608,8 +1628,9 @@ cudaError_t launch(const PassParams& P, double2* state, const double2* gtab, int
         ctas = (ntiles < resident || !(usePersistent() || pipe)) ? ntiles : resident;
     }
     int lo[5], tb[5], swizzle = 0;
-    const int nd = pipe ? tensorLayout(P, lo, tb, &swizzle) : stagedLayout(P, lo, tb, &swizzle);
+    int nd = pipe ? tensorLayout(P, lo, tb, &swizzle) : stagedLayout(P, lo, tb, &swizzle);
     const bool staged = !pipe && nd > 0;
+    if (!pipe && !staged && prefetchTiles(P)) nd = tensorDims(P, lo, tb);
     const unsigned nt = 1u << (P.ct - P.rb);
     const unsigned smem = kernelSmem(P);
     unsigned zskip = unsigned(zeroSkip);
@@ -1617,13 +1638,13 @@ cudaError_t launch(const PassParams& P, double2* state, const double2* gtab, int
     // slice (tensorDims), so a tile moves in one TMA op instead of one per row.
     alignas(64) uint64_t tmap[16] = {};
     unsigned tmv = 0;
-    if (nd && (useTensorMaps() || swizzle || staged) && driver().tensorMapEncodeTiled && nLocal - lo[nd - 1] <= 32) {
+    if (nd && (useTensorMaps() || swizzle || !pipe) && driver().tensorMapEncodeTiled && nLocal - lo[nd - 1] <= 32) {
         uint64_t dim[5], stride[4];
         unsigned box[5], es[5];
         for (int d = 0; d < nd; d++) {
             const int hi = d + 1 < nd ? lo[d + 1] : nLocal;
             dim[d] = uint64_t(1) << (hi - lo[d] + (d ? 0 : 1));
-            box[d] = 1u << (tb[d] + (d ? 0 : 1) - (staged && d == nd - 1 ? 1 : 0));  // staged: half boxes
+            box[d] = 1u << (tb[d] + (d ? 0 : 1) - (!pipe && d == nd - 1 ? 1 : 0));  // plain kernels: half boxes
             es[d] = 1u;
             if (d) stride[d - 1] = uint64_t(16) << lo[d];
         }
