@@ -213,11 +213,16 @@ bool useSparsePrefetch() {
     return v;
 }
 
-// QK_CTA_LITERAL (default 1): per-CTA factors as straight-line code with
-// literal terms; 0: a loop over device term tables.
-bool literalFactors() {
-    static const bool v = knob("QK_CTA_LITERAL", 1) != 0;
-    return v;
+// Per-CTA factors as straight-line code with literal terms, or as a loop over
+// device term tables.  QK_CTA_LITERAL=1 / 0 forces one form; by default a
+// pass with more than QK_CTA_LITERAL_MAX (128) terms takes the tables: the
+// literal code of QAOA's passes (92-473 terms) misses the instruction cache
+// (ncu: no_instructions 24 %).  Measured at 33 qubits: all-table QAOA 284 ->
+// 273 ms but random (<= 28 terms per pass) 639 -> 660 ms.
+bool literalFactors(const PassParams& P) {
+    static const int force = knob("QK_CTA_LITERAL", -1), cap = knob("QK_CTA_LITERAL_MAX", 128);
+    if (force >= 0) return force != 0;
+    return !P.ncta || P.cta_end[P.ncta - 1] <= cap;
 }
 
 // QK_JIT_TMAP (default 1): the TMA-pipelined kernels move a tile with one
@@ -883,9 +888,9 @@ private:
     // Factor f is computed by warp f mod #warps: lane j takes term j (mod 32)
     // with its condition and value as literals (no table loads), then the
     // partial products meet in a shuffle tree.
-    // Per-CTA factor terms as device tables (QK_CTA_LITERAL=0 form).
+    // Per-CTA factor terms as device tables (literalFactors false).
     void ctaTables() {
-        if (!P_.ncta || literalFactors()) return;
+        if (!P_.ncta || literalFactors(P_)) return;
         const int nt = P_.cta_end[P_.ncta - 1];
         o_ << "static __device__ const unsigned char qk_tb[] = {";
         for (int t = 0; t < nt; t++) o_ << (t ? "," : "") << int(P_.cta_terms[t].b1) << "," << int(P_.cta_terms[t].b2);
@@ -913,7 +918,7 @@ private:
     }
     void ctaFactors() {
         if (!P_.ncta) return;
-        if (!literalFactors()) return ctaFactorsTable();
+        if (!literalFactors(P_)) return ctaFactorsTable();
         const int nw = std::max(1, nt_ / 32);
         o_ << "  { const u32 w = tid >> 5, l = tid & 31u;\n";
         for (int f = 0; f < P_.ncta; f++) {
@@ -1298,7 +1303,7 @@ private:
 // ---- compile / load / launch -------------------------------------------------
 
 // Bump when the generated code changes for the same PassParams (on-disk cache key).
-constexpr uint64_t kGeneratorVersion = 34;
+constexpr uint64_t kGeneratorVersion = 35;
 
 uint64_t hashPass(const PassParams& P) {
     uint64_t h = 1469598103934665603ull ^ (kGeneratorVersion * 0x9E3779B97F4A7C15ull) ^ (usePrefetch() ? 1u : 0u) ^ (usePersistent() ? 2u : 0u) ^ (useSparsePrefetch() ? 8u : 0u) ^
