@@ -398,6 +398,23 @@ __global__ void __launch_bounds__(1 << (CT - RB), MINB)
                     QK_SLOT1(o.a, opCx, NA, a, cm, cv, thr)
                     break;
                 }
+                case OP_CCX: {
+                    uint32_t cm = 0, cv = 0;
+                    bool thr = true;
+                    const uint32_t p1 = (o.k >> 1) & 1u, p2 = (o.k >> 3) & 1u;
+                    if (o.k & 1u) thr = (((tid >> o.b) & 1u) ^ p1) != 0;
+                    else {
+                        cm |= 1u << o.b;
+                        cv |= (1u ^ p1) << o.b;
+                    }
+                    if (o.k & 4u) thr = thr && ((((tid >> o.c) & 1u) ^ p2) != 0);
+                    else {
+                        cm |= 1u << o.c;
+                        cv |= (1u ^ p2) << o.c;
+                    }
+                    QK_SLOT1(o.a, opCx, NA, a, cm, cv, thr)
+                    break;
+                }
                 case OP_DIAG1_R: {
                     const double2 d0 = coefAt(P, o.c), d1 = coefAt(P, o.c + 1);
                     QK_SLOT1(o.a, opDiag1, NA, a, d0, d1)

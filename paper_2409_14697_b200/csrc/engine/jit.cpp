@@ -1051,6 +1051,28 @@ private:
                 }
                 return;
             }
+            case qkdev::OP_CCX: {  // register controls: rename; thread controls: selects
+                const int b2 = int(d.c);
+                const bool t1 = d.k & 1, t2 = (d.k >> 2) & 1;
+                const int p1 = (d.k >> 1) & 1, p2 = (d.k >> 3) & 1;
+                std::string cond;
+                if (t1) cond = "(" + tb(b) + " ^ " + std::to_string(p1) + "u) != 0u";
+                if (t2) cond += (cond.empty() ? "" : " && ") + std::string("(") + tb(b2) + " ^ " + std::to_string(p2) + "u) != 0u";
+                if (!cond.empty()) o_ << "  { const bool c = " << cond << ";\n";
+                for (int s = 0; s < na_; s++) {
+                    if (s & K) continue;
+                    if (!t1 && ((s >> b) & 1) != (1 ^ p1)) continue;
+                    if (!t2 && ((s >> b2) & 1) != (1 ^ p2)) continue;
+                    if (cond.empty()) {
+                        std::swap(nm_[size_t(s)], nm_[size_t(s | K)]);
+                        continue;
+                    }
+                    o_ << "    { const double2 x = " << A(s) << ", y = " << A(s | K) << "; " << A(s)
+                       << " = csel(c, y, x); " << A(s | K) << " = csel(c, x, y); }\n";
+                }
+                if (!cond.empty()) o_ << "  }\n";
+                return;
+            }
             case qkdev::OP_DIAG1_R:
                 for (int s = 0; s < na_; s++) {
                     const std::string e = mulC(A(s), d.c + ((s >> a) & 1));

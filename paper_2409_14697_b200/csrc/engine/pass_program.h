@@ -78,6 +78,8 @@ enum OpType : uint8_t {
     OP_RESET,         // P = 1, R[*] = 1 (the pending factors are re-issued for the next segment)
     OP_CX_PEND,       // before a thread-controlled CX on slot a (control thread bit b, k bit1 = polarity):
                       // where it fires, P *= R[a]; R[a] = 1 / R[a]  (the pending phase follows the swap)
+    OP_CCX,           // Toffoli on target slot a: control 1 = b (k bit0: thread bit, else slot; k bit1: polarity),
+                      // control 2 = c (k bit2: thread bit, else slot; k bit3: polarity)
 };
 
 // Diagonal gates never need their qubits inside the tile: a bit outside the

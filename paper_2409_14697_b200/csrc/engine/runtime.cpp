@@ -884,7 +884,10 @@ void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_ru
             // inside the support (= this pass's written tiles), and the last
             // pass of the chain writes every tile.  QFT-33's middle pass then
             // computes only the tiles meeting the support.
-            const bool nextSparse = smask && (smask & ~P.tile_mask) && si + 1 < ci.steps.size() &&
+            // known zeros after this pass (bits no non-diagonal gate touched stay known)
+            uint64_t afterMask = smask, afterVal = smask ? sup->val : 0;
+            if (smask) qkeng::supportAfter(s, P.tile_mask, afterMask, afterVal);
+            const bool nextSparse = afterMask && si + 1 < ci.steps.size() &&
                                     ci.steps[si + 1].kind == qkeng::Step::Pass && deferZeros();
             const bool fillShort = smask && !nextSparse && qkjit::lowRunOf(P) < 3;
             const bool zeroSkip = nextSparse || fillShort;
@@ -908,7 +911,7 @@ void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_ru
             if (basis != kNoBasis) {
                 rs.block_bytes += zeroFill ? 16.0 * amps : 16.0 * double(uint64_t(1) << P.ct);
             } else if (smask) {
-                const double written = nextSparse ? std::ldexp(amps, -__builtin_popcountll(smask & ~P.tile_mask)) : amps;
+                const double written = nextSparse ? std::ldexp(amps, -__builtin_popcountll(afterMask)) : amps;
                 const double b = 16.0 * written + 16.0 * std::ldexp(amps, -__builtin_popcountll(smask));
                 rs.sparse_pass_launches++;
                 rs.sparse_pass_bytes += b;
@@ -918,7 +921,7 @@ void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_ru
                 rs.full_pass_bytes += 32.0 * amps;
                 rs.block_bytes += 32.0 * amps;
             }
-            if (sup && jit) sup->mask &= ~P.tile_mask;  // the pass mixes every tile bit
+            if (sup && jit) qkeng::supportAfter(s, P.tile_mask, sup->mask, sup->val);  // frees the bits it mixes
             if (timing) {
                 float ms = 0;
                 cuda(cudaEventRecord(e1, st->stream), "event");
@@ -1312,6 +1315,10 @@ std::string stepsJson(const std::vector<qkeng::Step>& steps, const std::vector<d
         o << "]";
         if (s.kind == qkeng::Step::Pass) {
             const qkdev::PassParams& P = *s.pass;
+            o << ",\"keep\":[";
+            for (size_t j = 0; j < s.keep.size(); j++)
+                o << (j ? "," : "") << "[" << s.keep[j].first << "," << s.keep[j].second << "]";
+            o << "]";
             o << ",\"ct\":" << P.ct << ",\"rb\":" << P.rb << ",\"nsegs\":" << P.nsegs << ",\"tile_phys\":[";
             for (int j = 0; j < P.ct; j++) o << (j ? "," : "") << int(P.tile_phys[j]);
             o << "],\"map_in\":[";

@@ -24,6 +24,7 @@
 #include "jit.h"
 
 #include <algorithm>
+#include <array>
 #include <sstream>
 #include <cmath>
 #include <cstdio>
@@ -973,6 +974,16 @@ private:
                 return mat1(g.targets[0], m);
             }
             case GateKind::CX: {
+                if (g.controls.size() == 2) {  // fused Toffoli (fuseToffolis): rename / selects, no arithmetic
+                    const int t = inv_[g.targets[0]], c1 = inv_[g.controls[0]], c2 = inv_[g.controls[1]];
+                    emitBatch();
+                    flushSlot(t);
+                    int k = flip(c1) << 1 | flip(c2) << 3;  // physical control values meaning logical 1: 1 ^ pol
+                    if (!isReg(c1)) k |= 1;
+                    if (!isReg(c2)) k |= 4;
+                    emit(OP_CCX, t, isReg(c1) ? c1 : c1 - rb_, k, uint32_t(isReg(c2) ? c2 : c2 - rb_));
+                    return;
+                }
                 const int t = inv_[g.targets[0]], c = inv_[g.controls[0]];
                 emitBatch();
                 const int pol = flip(c);  // physical control value that means logical 1 is (1 ^ pol)
@@ -1188,6 +1199,165 @@ int lowTileBits() {
     return v;
 }
 
+// Support-aware pricing of runs from a basis state (QK_SPARSE_DP, default 1):
+// a pass whose output support is still partial reads and writes only that
+// support (sparse loads, deferred zeros), so it costs its support fraction of
+// a sweep; the pass that first fills the slice writes it all and reads only
+// its input support.  Work (reference flops/amp) is priced at QK_DP_FLOP
+// sweeps per 10^4 flops (default 2.5) on the amplitudes it touches, so the DP
+// moves gates into the cheap sparse passes and leaves the full-output pass as
+// little arithmetic as the tile allows (QFT-33: 13 + 11 + 9 -> 13 + 13 + 7
+// H levels).  0 restores the support-blind model.
+// QK_TIGHT_SUPPORT (default 1): a pass frees only the tile bits its
+// non-diagonal gates touch; padding bits of a run from a basis state stay
+// known (Step::keep), so later passes read and write less.
+bool tightSupport() {
+    static const bool v = envInt("QK_TIGHT_SUPPORT", 1, 0, 1) != 0;
+    return v;
+}
+
+bool sparseDp() {
+    static const bool v = envInt("QK_SPARSE_DP", 1, 0, 1) != 0;
+    return v;
+}
+double dpFlopWeight() {
+    static const double v = envInt("QK_DP_FLOP", 25, 0, 100000) * 1e-5;
+    return v;
+}
+
+// QK_FUSE_CCX (default 1): a run of 1-qubit gates and CX on three qubits
+// whose product is exactly a Toffoli (entries within 1e-12 of the
+// permutation: the 15-gate H / T / CX decomposition Grover's AND chain uses)
+// is applied as one CCX -- a register rename or a select, no arithmetic --
+// instead of two butterflies, seven phases and six CX.  Gates on other qubits
+// that sit between them commute with the run (disjoint qubits) and keep
+// their order.
+bool fuseCcx() {
+    static const bool v = envInt("QK_FUSE_CCX", 1, 0, 1) != 0;
+    return v;
+}
+
+namespace {
+using Mat8 = std::array<Amp, 64>;  // row-major over 3 local bits
+
+bool windowGate(const Gate& g) {
+    switch (g.kind) {
+        case GateKind::H:
+        case GateKind::U:
+        case GateKind::X:
+        case GateKind::RX:
+        case GateKind::RY:
+        case GateKind::RZ:
+            return g.targets.size() == 1 && g.controls.empty();
+        case GateKind::CX:
+            return g.targets.size() == 1 && g.controls.size() == 1;
+        default:
+            return false;
+    }
+}
+
+void applyToMat(Mat8& M, const Gate& g, const int* local) {
+    if (g.kind == GateKind::CX) {
+        const int c = local[0], t = local[1];
+        for (int r = 0; r < 8; r++)
+            if (((r >> c) & 1) && !((r >> t) & 1))
+                for (int col = 0; col < 8; col++) std::swap(M[size_t(r * 8 + col)], M[size_t((r | (1 << t)) * 8 + col)]);
+        return;
+    }
+    const std::vector<Amp> m = quokka::gateMatrix(g);
+    const int j = local[0];
+    for (int r = 0; r < 8; r++) {
+        if ((r >> j) & 1) continue;
+        const int r1 = r | (1 << j);
+        for (int col = 0; col < 8; col++) {
+            const Amp x = M[size_t(r * 8 + col)], y = M[size_t(r1 * 8 + col)];
+            M[size_t(r * 8 + col)] = m[0] * x + m[1] * y;
+            M[size_t(r1 * 8 + col)] = m[2] * x + m[3] * y;
+        }
+    }
+}
+
+// Local target bit of the Toffoli M equals, else -1.
+int toffoliTarget(const Mat8& M) {
+    for (int t = 0; t < 3; t++) {
+        const int c1 = (t + 1) % 3, c2 = (t + 2) % 3;
+        bool ok = true;
+        for (int r = 0; r < 8 && ok; r++) {
+            const int want = (((r >> c1) & 1) && ((r >> c2) & 1)) ? (r ^ (1 << t)) : r;
+            for (int col = 0; col < 8 && ok; col++)
+                ok = std::abs(M[size_t(want * 8 + col)] - Amp(col == r ? 1.0 : 0.0, 0.0)) < 1e-12;
+        }
+        if (ok) return t;
+    }
+    return -1;
+}
+}  // namespace
+
+std::vector<Gate> fuseToffolis(const std::vector<Gate>& gates) {
+    const size_t n = gates.size();
+    std::vector<char> drop(n, 0);
+    std::vector<Gate> at(n);  // replacement placed at a window's last gate
+    std::vector<char> has(n, 0);
+    for (size_t i = 0; i < n; i++) {
+        if (drop[i] || has[i] || gates[i].kind != GateKind::H) continue;
+        std::vector<int> Q;
+        uint64_t skipped = 0;  // qubits of gates skipped over (they must stay outside Q)
+        Mat8 M{};
+        for (int r = 0; r < 8; r++) M[size_t(r * 9)] = Amp(1.0, 0.0);
+        std::vector<size_t> taken;
+        for (size_t j = i; j < n && j < i + 64 && taken.size() < 32; j++) {
+            if (drop[j] || has[j]) break;
+            const Gate& g = gates[j];
+            const std::vector<int> qs = g.qubits();
+            bool anyIn = false;
+            for (int q : qs) anyIn |= std::find(Q.begin(), Q.end(), q) != Q.end();
+            if (!anyIn && j != i) {  // disjoint: commutes with the window, stays where it is
+                for (int q : qs) skipped |= uint64_t(1) << q;
+                continue;
+            }
+            if (!windowGate(g)) break;
+            bool fits = true;
+            std::vector<int> add;
+            for (int q : qs)
+                if (std::find(Q.begin(), Q.end(), q) == Q.end()) {
+                    if ((skipped >> q) & 1) fits = false;
+                    add.push_back(q);
+                }
+            if (!fits || Q.size() + add.size() > 3) break;
+            Q.insert(Q.end(), add.begin(), add.end());
+            int local[2];
+            for (size_t k = 0; k < qs.size(); k++)
+                local[k] = int(std::find(Q.begin(), Q.end(), qs[k]) - Q.begin());
+            applyToMat(M, g, local);
+            taken.push_back(j);
+            if (Q.size() == 3 && taken.size() >= 3) {
+                const int t = toffoliTarget(M);
+                if (t >= 0) {
+                    Gate f = gates[i];
+                    f.kind = GateKind::CX;
+                    f.targets = {Q[size_t(t)]};
+                    f.controls = {Q[size_t((t + 1) % 3)], Q[size_t((t + 2) % 3)]};
+                    f.params.clear();
+                    f.payload.clear();
+                    f.constituents.clear();
+                    for (size_t k : taken) drop[k] = 1;
+                    drop[j] = 0;
+                    at[j] = f;
+                    has[j] = 1;
+                    break;
+                }
+            }
+        }
+    }
+    std::vector<Gate> out;
+    out.reserve(n);
+    for (size_t k = 0; k < n; k++) {
+        if (has[k]) out.push_back(at[k]);
+        else if (!drop[k]) out.push_back(gates[k]);
+    }
+    return out;
+}
+
 // Gates (memory-bit positions, program order) -> steps.  Consecutive gates
 // share a pass while the bits their NON-diagonal gates touch fit in one tile
 // (padded with the lowest memory bits for coalesced rows): diagonal gates
@@ -1254,6 +1424,7 @@ std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::
                 }
             applyStorePermutation(P, sigma);
             for (auto& a : steps[k].alts) applyStorePermutation(*a, sigma);  // same tile, same sigma
+            for (auto& kp : steps[k].keep) kp.second = P.tile_phys[sigma[size_t(where[size_t(kp.second)])]];
             std::vector<int> moved(static_cast<size_t>(nLocal));
             for (int b = 0; b < nLocal; b++) moved[size_t(b)] = b;
             for (int j = 0; j < ct; j++) moved[size_t(P.tile_phys[j])] = P.tile_phys[sigma[size_t(j)]];
@@ -1280,6 +1451,13 @@ std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::
         steps.push_back(std::move(s));
     };
 
+    std::vector<Gate> fusedGates;
+    if (fuseCcx() && nLocal >= 4) {
+        fusedGates = fuseToffolis(gates);
+        if (std::getenv("QK_DEBUG_CCX")) std::fprintf(stderr, "ccx fusion: %zu -> %zu gates\n", gates.size(), fusedGates.size());
+        if (fusedGates.size() != gates.size())
+            return compileBlock(fusedGates, nLocal, gtab, dest, relabel, tileBits, synthFirst, interp);
+    }
     if (relabel) *relabel = R;  // identity unless passes route data (below)
     if (nLocal < 4) {  // too small for a register tile: every gate as a dense group
         for (const Gate& g : gates) denseStep(quokka::gateMatrix(g), g.qubits(), referenceFlopsPerAmp(g));
@@ -1318,6 +1496,25 @@ std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::
         for (size_t k = 0; k < m; k++) mask[k] = isDiagonalGate(run[k]) ? 0 : run[k].depMask();
         std::vector<double> work(m);  // reference-formula flops/amp: bounds a pass's straight-line code
         for (size_t k = 0; k < m; k++) work[k] = referenceFlopsPerAmp(run[k]);
+        // support-aware model: free[k] = bits the support spans before gate k
+        // (the run's fixed bits minus every bit a non-diagonal gate touched;
+        // earlier passes' padding bits are not counted)
+        const bool sparseModel = sparseDp() && sparseMask != 0;
+        const uint64_t all = nLocal >= 64 ? ~uint64_t(0) : (uint64_t(1) << nLocal) - 1;
+        std::vector<uint64_t> freeAt(m + 1, all & ~sparseMask);
+        for (size_t k = 0; k < m; k++) freeAt[k + 1] = freeAt[k] | mask[k];
+        auto sparseCost = [&](size_t j, uint64_t used, double w) {
+            uint64_t tile = used;
+            for (int b = 0; b < nLocal && __builtin_popcountll(tile) < ct; b++) tile |= uint64_t(1) << b;
+            int L = 0;
+            while (L < ct && ((tile >> L) & 1)) L++;
+            const double pen = rowPenalty()[std::min(L, lowTileBits())];
+            const double fin = std::ldexp(1.0, __builtin_popcountll(freeAt[j]) - nLocal);
+            const double fout = std::ldexp(1.0, __builtin_popcountll(freeAt[j] | tile) - nLocal);
+            const double comp = dpFlopWeight() * w;
+            if (fout < 1.0) return fout * (1.0 + pen + comp);  // deferred zeros: support in, support out
+            return 0.5 * (1.0 + pen) * (1.0 + fin) + comp;      // every tile written, support read
+        };
         std::vector<double> best(m + 1, 1e300);
         std::vector<size_t> from(m + 1, 0);
         best[0] = 0;
@@ -1329,7 +1526,9 @@ std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::
                 w += work[j];
                 if (__builtin_popcountll(used) > ct) break;
                 if (w > passWorkBudget() && j + 1 < i) break;
-                const double c = best[j] + ((synthRun && j == 0) ? 1.0 : passCost(used));
+                const double c = best[j] + (sparseModel           ? sparseCost(j, used, w)
+                                            : (synthRun && j == 0) ? 1.0
+                                                                   : passCost(used));
                 if (c < best[i] - 1e-9) {
                     best[i] = c;
                     from[i] = j;
@@ -1352,7 +1551,11 @@ std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::
             const bool sparseIn = sparseMask != 0;
             compileGroup(group, used, ct, nLocal, gtab, steps, interp ? rb : -1, false, sparseIn);
             for (size_t k = first; k < steps.size(); k++)
-                if (steps[k].kind == Step::Pass) sparseMask &= ~steps[k].pass->tile_mask;
+                if (steps[k].kind == Step::Pass && tightSupport())
+                    for (int j = 0; j < steps[k].pass->ct; j++) {
+                        const int b = steps[k].pass->tile_phys[j];
+                        if (!((used >> b) & 1)) steps[k].keep.emplace_back(b, b);
+                    }
             if (!interp && ct == 13 && tuneRegBits() && steps.size() == first + 1 && steps[first].kind == Step::Pass) {
                 for (int rbAlt : {4, 3}) {  // 16 and 8 amplitudes per thread (512 / 1024 threads)
                     std::vector<Step> alt;
@@ -1373,6 +1576,11 @@ std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::
                 if (!steps[first].alts.empty()) steps[first].tune = std::make_shared<Step::Tune>();
             }
             route(first);
+            for (size_t k = first; k < steps.size(); k++)
+                if (steps[k].kind == Step::Pass) {
+                    uint64_t v = 0;
+                    supportAfter(steps[k], steps[k].pass->tile_mask, sparseMask, v);
+                }
         }
         run.clear();
     };

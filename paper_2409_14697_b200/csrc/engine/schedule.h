@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <memory>
+#include <utility>
 #include <vector>
 
 #include "pass_program.h"
@@ -43,6 +44,10 @@ struct Step {
         }
     };
     std::shared_ptr<Tune> tune;
+    // Kind::Pass: tile bits no non-diagonal gate of the pass touches, as
+    // (memory bit before, memory bit after the store permutation): a bit known
+    // to be fixed in the input support stays fixed (same value) in the output.
+    std::vector<std::pair<int, int>> keep;
     // Kind::DenseGroup / DiagTable: matrix (or diagonal) at gtab offset `matOff`,
     // targets (j -> sub-index bit k-1-j)
     int k = 0;
@@ -70,6 +75,19 @@ struct Step {
 std::vector<Step> compileBlock(const std::vector<quokka::Gate>& gates, int nLocal, std::vector<double>& gtab,
                                const std::vector<int>* dest = nullptr, std::vector<int>* relabel = nullptr,
                                int tileBits = 0, bool synthFirst = false, bool interp = false);
+
+// Support mask after pass `s` (bits of `mask` stay fixed only where the pass
+// keeps them; `val` moves with them).
+inline void supportAfter(const Step& s, uint64_t tileMask, uint64_t& mask, uint64_t& val) {
+    uint64_t m = mask & ~tileMask, v = val & ~tileMask;
+    for (const auto& [from, to] : s.keep)
+        if ((mask >> from) & 1) {
+            m |= uint64_t(1) << to;
+            v |= ((val >> from) & 1) << to;
+        }
+    mask = m;
+    val = v;
+}
 
 // Reference-formula flops per amplitude for one gate.
 double referenceFlopsPerAmp(const quokka::Gate& g);

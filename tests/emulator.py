@@ -7,7 +7,7 @@ import numpy as np
 
 OPS = ["MAT1", "H", "CX", "DIAG1_R", "DIAG2_RR", "CPHASE_RR", "PEND_R", "PEND_RT", "SCAL", "SCAL_T",
        "SCAL_TT", "FLUSH_SLOT", "FLUSH", "DTABLE", "DENSE", "EXCHANGE", "SCAL_TAB", "PEND_TAB", "SCAL_CTA",
-       "PEND_CTA", "SCAL_TCTA", "FLUSH_SLOT_G", "RESET", "CX_PEND"]
+       "PEND_CTA", "SCAL_TCTA", "FLUSH_SLOT_G", "RESET", "CX_PEND", "CCX"]
 
 
 def pext8(t, m):
@@ -136,6 +136,18 @@ def _run_pass(state, n, P, gt):
                     cond = ((bit(tid, ob) ^ pol) == 1)[:, None] & np.ones(len(lo), bool)[None, :]
                 else:
                     cond = np.broadcast_to(((bit(lo, ob) ^ pol) == 1)[None, :], (nt, len(lo)))
+                x, y = a[:, lo].copy(), a[:, hi].copy()
+                a[:, lo] = np.where(cond, y, x)
+                a[:, hi] = np.where(cond, x, y)
+            elif name == "CCX":
+                lo = s_idx[(s_idx >> oa) & 1 == 0]
+                hi = lo | (1 << oa)
+                cond = np.ones((nt, len(lo)), bool)
+                for (thr, idx, pol) in (((ok & 1), ob, (ok >> 1) & 1), ((ok >> 2) & 1, oc, (ok >> 3) & 1)):
+                    if thr:
+                        cond &= ((bit(tid, idx) ^ pol) == 1)[:, None]
+                    else:
+                        cond &= ((bit(lo, idx) ^ pol) == 1)[None, :]
                 x, y = a[:, lo].copy(), a[:, hi].copy()
                 a[:, lo] = np.where(cond, y, x)
                 a[:, hi] = np.where(cond, x, y)

@@ -83,6 +83,17 @@ def run_program_jit(qk, port, prog, n_local, state, basis=None):
     return state
 
 
+def support_after(st, tmask, smask, sval):
+    """Known-zero coset after a pass (schedule.h supportAfter): tile bits that
+    no non-diagonal gate touched stay fixed, moved by the store permutation."""
+    m, v = smask & ~tmask, sval & ~tmask
+    for frm, to in st.get("keep", []):
+        if (smask >> frm) & 1:
+            m |= 1 << to
+            v |= ((sval >> frm) & 1) << to
+    return m, v
+
+
 def run_program_jit_sparse(qk, port, prog, n_local, state, initial):
     """As the runtime runs a program from |basis> with known zeros: the first
     pass computes ONLY the tile holding |basis> (no memset: `state` may hold
@@ -127,12 +138,13 @@ def run_program_jit_sparse(qk, port, prog, n_local, state, initial):
                     # deferred zeros (as the runtime): a sparse pass followed by a pass,
                     # with the support still partial after it, leaves its zero tiles unwritten
                     nxt = si + 1 < len(steps) and steps[si + 1]["kind"] == 0
-                    defer = bool(smask and (smask & ~tmask) and nxt)
+                    amask, _ = support_after(st, tmask, smask, sval)
+                    defer = bool(smask and amask and nxt)
                     # deferred zeros launch only the tiles meeting the support (zskip 2)
                     tiles = 1 << (n_local - st["ct"] - bin(smask & ~tmask).count("1")) if defer else 0
                     fn(state.ctypes.data, gt.ctypes.data, n_local, st["ct"], st["rb"], NO_BASIS, 0, tiles, smask,
                        sval if smask else 0, 2 if defer else 0)
-                smask &= ~tmask
+                smask, sval = support_after(st, tmask, smask, sval)
         elif it["kind"] == 1:
             pairs = [tuple(p) for p in it["pairs"]]
             port.ims_swap(state.view(np.float64), n_local, pairs)

@@ -116,3 +116,22 @@ def test_sparse_start_on_host(ref, qk, port, kind, n, a, seed):
     run_program_jit_sparse(qk, port, prog, n, st, 0x1235 & ((1 << n) - 1))
     assert not np.isnan(st).any()
     assert np.max(np.abs(st - want.view(np.complex128))) < 1e-10
+
+
+@pytest.mark.parametrize("n,chunk,seed", [(14, 13, 3), (15, 11, 5)])
+def test_toffoli_fusion_kernels_on_host(ref, qk, port, n, chunk, seed):
+    # generated OP_CCX code (register renames and thread-bit selects) in the
+    # specialized kernels, full and sparse-start runs, vs the reference
+    from test_scheduler import toffoli_circuit
+    cfg_text = config_text(n, 0, chunk, fusion=0, diag=0)
+    prog_text = ref.optimize(toffoli_circuit(n, 14, seed), cfg_text)
+    want, _, _, _ = ref.simulate(prog_text, cfg_text, n, 0, 5, 2)
+    prog = qk.Program.parse(prog_text, qk.Config.parse(cfg_text))
+    assert any("csel(c, y, x)" in src for _, src in prog.debug_jit_sources(n))
+    st = np.zeros(1 << n, dtype=np.complex128)
+    st[5] = 1
+    run_program_jit(qk, port, prog, n, st)
+    assert np.max(np.abs(st - want.view(np.complex128))) < 1e-10
+    st = np.full(1 << n, np.nan, dtype=np.complex128)
+    run_program_jit_sparse(qk, port, prog, n, st, 5)
+    assert not np.isnan(st).any() and np.max(np.abs(st - want.view(np.complex128))) < 1e-10

@@ -214,3 +214,71 @@ def test_tiny_programs_compile(qk, port, ref, n):
     want, _, _, _ = ref.simulate(prog_text, cfg_text, n, 0, 1, 1)
     got = run_compiled(qk, port, prog, n, 1)
     assert np.max(np.abs(got - want.view(np.complex128))) < 1e-12
+
+
+def toffoli_lines(a, b, t, gid):
+    """The 15-gate H / T / CX Toffoli (Grover's AND chain, csrc/host/tools.cpp)."""
+    q = 0.78539816339744828
+    seq = [("H", t), ("CX", b, t), ("U", t, -q), ("CX", a, t), ("U", t, q), ("CX", b, t), ("U", t, -q),
+           ("CX", a, t), ("U", b, q), ("U", t, q), ("H", t), ("CX", a, b), ("U", a, q), ("U", b, -q), ("CX", a, b)]
+    out = []
+    for g in seq:
+        if g[0] == "H":
+            out.append(f"H {g[1]} {gid}")
+        elif g[0] == "CX":
+            out.append(f"CX {g[1]} {g[2]} {gid}")
+        else:
+            out.append(f"U {g[1]} {gid} 0 0 {g[2]!r}")
+        gid += 1
+    return out, gid
+
+
+def toffoli_circuit(n, count, seed):
+    """Toffolis on random triples, X flips (control polarities), H and RZ
+    between them (partial overlaps end a fusion window), as circuit text."""
+    rng = np.random.default_rng(seed)
+    lines, gid = [f"H {q} {q}" for q in range(n)], n
+    for _ in range(count):
+        a, b, t = (int(x) for x in rng.choice(n, 3, replace=False))
+        for q in rng.choice(n, 2, replace=False):
+            lines.append(f"X {int(q)} {gid}")
+            gid += 1
+        tl, gid = toffoli_lines(a, b, t, gid)
+        lines += tl
+        if rng.random() < 0.5:
+            lines.append(f"RZ {int(rng.integers(n))} {gid} {rng.normal():.6f}")
+            gid += 1
+        if rng.random() < 0.3:
+            lines.append(f"H {int(rng.integers(n))} {gid}")
+            gid += 1
+    return "\n".join(lines) + "\n"
+
+
+@pytest.mark.parametrize("n,chunk,seed", [(6, 6, 0), (9, 5, 1), (11, 8, 2), (14, 13, 3), (15, 9, 4)])
+def test_toffoli_fusion(qk, port, ref, n, chunk, seed):
+    # fuseToffolis: each 15-gate Toffoli becomes one OP_CCX (controls in
+    # register slots or thread bits, either polarity) -- results vs the
+    # reference's gate-by-gate simulateProgram
+    cfg_text = config_text(n, 0, chunk, fusion=0, diag=0)
+    prog_text = ref.optimize(toffoli_circuit(n, 12, seed), cfg_text)
+    want, _, _, _ = ref.simulate(prog_text, cfg_text, n, 0, 3, 1)
+    prog = qk.Program.parse(prog_text, qk.Config.parse(cfg_text))
+    ops = [o[0] for it in prog.debug_compile(n)["items"] if it["kind"] == 0
+           for s in it["block"]["steps"] if s["kind"] == 0 for o in s["ops"]]
+    assert ops.count(24) >= 6  # OP_CCX
+    got = run_compiled(qk, port, prog, n, 3)
+    assert np.max(np.abs(got - want.view(np.complex128))) < 1e-10
+
+
+def test_toffoli_fusion_grover(qk, port):
+    # Grover's oracle + diffusion (AND chain of Toffolis into ancillas) vs the
+    # plain-C oracle replaying the same program gate by gate
+    n = 14
+    cfg = qk.Config.make(n, 0, chunk=10, fusion=0, diag=0)
+    prog = qk.Program.optimize(qk.generate("grover", n, 2, 5), cfg)
+    ops = [o[0] for it in prog.debug_compile(n)["items"] if it["kind"] == 0
+           for s in it["block"]["steps"] if s["kind"] == 0 for o in s["ops"]]
+    assert ops.count(24) >= 20
+    got = run_compiled(qk, port, prog, n, 6)
+    want = port.run_program(prog.text(), n, 10, 6).view(np.complex128)
+    assert np.max(np.abs(got - want)) < 1e-10
