@@ -473,7 +473,7 @@ public:
         }
         o_ << "  } else {  // first pass of a run: synthesize |basis> instead of reading it\n";
         for (int s = 0; s < na_; s++)
-            o_ << "  a" << s << " = C2((off | " << regGlobal(P_.map_in[0], s) << "ull) == basis ? 1.0 : 0.0, 0.0);\n";
+            o_ << "  a" << s << " = C2((off | " << regGlobal(P_.map_in[0], s) << "ull) == basis ? " << lit(P_.synth_amp ? P_.synth_amp : 1.0) << " : 0.0, 0.0);\n";
         o_ << "  }\n  }\n";
         prefetchNext();
         ctaFactors();
@@ -551,7 +551,7 @@ public:
         o_ << "  } else {  // first pass of a run: synthesize |basis>\n"
            << "    const u64 off = base | " << threadGlobal(P_.map_in[0]) << ";\n";
         for (int s = 0; s < na_; s++)
-            o_ << "    a" << s << " = C2((off | " << regGlobal(P_.map_in[0], s) << "ull) == basis ? 1.0 : 0.0, 0.0);\n";
+            o_ << "    a" << s << " = C2((off | " << regGlobal(P_.map_in[0], s) << "ull) == basis ? " << lit(P_.synth_amp ? P_.synth_amp : 1.0) << " : 0.0, 0.0);\n";
         o_ << "  }\n";
         ctaFactors();
         for (int i = 0; i < P_.nops; i++) op(P_.ops[i]);

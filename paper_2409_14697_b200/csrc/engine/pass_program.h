@@ -123,6 +123,8 @@ struct PassParams {
     int32_t half_x;    // exchanges scheduled splittable in halves (xsplit): TMA-pipelined kernel eligible
     int32_t stage_out;  // specialized kernels: in runs with known zeros, the output tile leaves through shared
                         // memory and the TMA engine (set for passes whose input is sparse in a basis run)
+    double synth_amp;   // specialized basis pass: value of the synthesized |basis> amplitude (0: 1.0); the
+                        // run's deferred H normalization (qkeng::DeferHScales)
 };
 
 static_assert(sizeof(PassParams) <= 32000, "kernel parameter limit");

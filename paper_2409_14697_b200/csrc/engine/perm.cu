@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(256) k_sum_partial(const double* __restrict__ 
     }
 }
 
-__global__ void k_set_basis(double2* a, uint64_t idx) { a[idx] = make_double2(1.0, 0.0); }
+__global__ void k_set_basis(double2* a, uint64_t idx, double v) { a[idx] = make_double2(v, 0.0); }
 
 // Zeros at every i with ((i ^ val) & m) != 0: the tiles a sparse pass skips
 // (outside its input's support), written as one coalesced stream of 32-B
@@ -648,8 +648,8 @@ cudaError_t launchZeroOutside(double2* a, uint64_t n, uint64_t m, uint64_t val, 
     return cudaGetLastError();
 }
 
-cudaError_t launchSetBasis(double2* a, uint64_t idx, cudaStream_t st) {
-    k_set_basis<<<1, 1, 0, st>>>(a, idx);
+cudaError_t launchSetBasis(double2* a, uint64_t idx, cudaStream_t st, double v) {
+    k_set_basis<<<1, 1, 0, st>>>(a, idx, v);
     return cudaGetLastError();
 }
 

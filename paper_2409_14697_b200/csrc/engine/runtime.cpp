@@ -44,7 +44,7 @@ cudaError_t launchDiagTable(double2*, const double2*, uint64_t, const int*, int,
 cudaError_t launchNorm(const double2*, uint64_t, double*, double*, cudaStream_t);
 cudaError_t launchSumTiles(const double*, uint64_t, double*, double*, cudaStream_t);
 size_t normScratchDoubles();
-cudaError_t launchSetBasis(double2*, uint64_t, cudaStream_t);
+cudaError_t launchSetBasis(double2*, uint64_t, cudaStream_t, double);
 cudaError_t launchZeroOutside(double2*, uint64_t, uint64_t, uint64_t, int, cudaStream_t);
 cudaError_t launchMarginal(const double2*, uint64_t, const int*, int, double*, double*, cudaStream_t);
 size_t marginalScratchDoubles(int k);
@@ -236,6 +236,7 @@ struct Compiled {
     std::vector<Alternative> alts;  // sorted by first
     std::vector<double> gtab;     // host copy of device tables
     std::vector<int> targets;     // dense-group target lists
+    double basisAmp = 1.0;        // |initial> amplitude the run starts from (deferred H normalization)
 };
 
 struct DeviceTables {
@@ -352,6 +353,15 @@ bool partialMaterialize() {
     return v;
 }
 
+// QK_DEFER_H (default 1): see compileLayout.
+bool deferHScales() {
+    static const bool v = [] {
+        const char* e = std::getenv("QK_DEFER_H");
+        return !e || std::atoi(e) != 0;
+    }();
+    return v;
+}
+
 // QK_BASIS_LAYOUT (default 1): see compileFor(fromBasis).
 bool basisLayout() {
     static const bool v = [] {
@@ -432,6 +442,20 @@ std::shared_ptr<Compiled> compileLayout(qk_program* p, int nLocal, const std::ve
                                         bool interp) {
     auto c = std::make_shared<Compiled>();
     c->nLocal = nLocal;
+    // Runs from a basis state on the specialized kernels: Hadamard butterflies
+    // skip their 1/sqrt2 and the initial amplitude carries the product (one
+    // fewer multiply per amplitude in passes that would scale on their own,
+    // e.g. QFT's last pass).  Not beyond 1000 H (the start value would leave
+    // the double range).
+    int deferH = 0;
+    std::unique_ptr<qkeng::DeferHScales> deferScope;
+    if (synthFirst && !interp && nLocal >= 4 && deferHScales()) {
+        long nh = 0;
+        for (const quokka::ProgramItem& item : p->prog.items)
+            if (item.type == quokka::ProgramItem::Block)
+                for (const quokka::Gate& g : item.block.gates) nh += g.kind == quokka::GateKind::H;
+        if (nh <= 1000) deferScope = std::make_unique<qkeng::DeferHScales>(&deferH);
+    }
     // Lazy in-memory swaps: an SQS (and a SWAP gate) only relabels which
     // memory bit holds which program position (mem[p]); later gates address
     // their qubits through `mem`, so it costs no HBM pass.  Gates between
@@ -531,6 +555,7 @@ std::shared_ptr<Compiled> compileLayout(qk_program* p, int nLocal, const std::ve
         flushStream(true, 0, keep);
         materialize(keep);
         const std::vector<int> memA = mem;
+        const int deferA = deferH;  // the alternative applies the same H gates
         if (lazy && !stream.empty() && qkdev::tileTune() && !interp && nLocal > 13) {
             const size_t last = c->items.size();
             std::vector<CompiledItem> a(std::make_move_iterator(c->items.begin() + long(first)),
@@ -556,6 +581,7 @@ std::shared_ptr<Compiled> compileLayout(qk_program* p, int nLocal, const std::ve
             c->items.resize(first);
             for (auto& x : a) c->items.push_back(std::move(x));
             mem = memA;
+            deferH = deferA;
         }
         stream.clear();
     };
@@ -613,6 +639,20 @@ std::shared_ptr<Compiled> compileLayout(qk_program* p, int nLocal, const std::ve
     for (Alternative& alt : c->alts)
         if (alt.last == c->items.size()) markNorm(alt.b, synthFirst && alt.first == 0);
     markNorm(c->items, synthFirst);
+    if (deferScope) {
+        deferScope.reset();
+        c->basisAmp = qkeng::deferredHScale(deferH);
+        auto stamp = [&](std::vector<CompiledItem>& items) {  // the synthesized basis pass
+            if (items.empty() || items[0].kind != CompiledItem::Block || items[0].steps.empty()) return;
+            qkeng::Step& s0 = items[0].steps[0];
+            if (s0.kind != qkeng::Step::Pass) return;
+            s0.pass->synth_amp = c->basisAmp;
+            for (auto& a : s0.alts) a->synth_amp = c->basisAmp;
+        };
+        stamp(c->items);
+        for (Alternative& alt : c->alts)
+            if (alt.first == 0) stamp(alt.b);
+    }
     return c;
 }
 
@@ -1391,13 +1431,13 @@ uint64_t layoutIndex(uint64_t local, const std::vector<int>& mem0) {
     return x;
 }
 
-void setBasis(qk_state* st, Index global, const std::vector<int>* mem0 = nullptr) {
+void setBasis(qk_state* st, Index global, const std::vector<int>* mem0 = nullptr, double amp = 1.0) {
     st->normValid = false;
     if (global >= (Index(1) << st->n)) throw SimulationError("initial basis state out of range");
     cuda(cudaMemsetAsync(st->amps, 0, st->count * sizeof(double2), st->stream), "memset");
     uint64_t local = global & (st->count - 1);
     if (mem0) local = layoutIndex(local, *mem0);
-    if ((global >> st->nLocal) == Index(st->rank)) cuda(qkdev::launchSetBasis(st->amps, local, st->stream), "set basis");
+    if ((global >> st->nLocal) == Index(st->rank)) cuda(qkdev::launchSetBasis(st->amps, local, st->stream, amp), "set basis");
 }
 
 }  // namespace
@@ -2042,7 +2082,7 @@ int qk_simulate(qk_state* st, const qk_program* cp, const qk_config* cfg, uint64
             if (here) sup = Support{st->count - 1, basis, false};
             else sup.empty = true;  // the basis pass only zero-fills this slice
         } else {
-            timer.time(4, [&] { setBasis(st, initial, &comp->mem0); });
+            timer.time(4, [&] { setBasis(st, initial, &comp->mem0, comp->basisAmp); });
             sup.empty = (initial >> st->nLocal) != Index(st->rank);
         }
         if (!sparseStart()) sup = Support{};
@@ -2152,7 +2192,7 @@ int qk_simulate_local(qk_state** sl, int ns, const qk_program* cp, const qk_conf
             tabs.push_back(tablesFor(p, *comp, sl[k]->device));
             DeviceGuard g(sl[k]->device);
             prepareJit(*comp, sl[k]->device);
-            setBasis(sl[k], initial, &comp->mem0);
+            setBasis(sl[k], initial, &comp->mem0, comp->basisAmp);
         }
         if (stats)
             for (int k = 0; k < ns; k++) stats[k] = qk_xrs_stats{};

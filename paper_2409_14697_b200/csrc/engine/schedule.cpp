@@ -206,6 +206,10 @@ bool isDiagonalGate(const Gate& g) {
 
 double passCodeBudget();
 
+thread_local int* tlDeferH = nullptr;
+DeferHScales::DeferHScales(int* count) : prev(tlDeferH) { tlDeferH = count; }
+DeferHScales::~DeferHScales() { tlDeferH = prev; }
+
 namespace {
 
 // Tile bits that must sit in register slots when `g` runs.
@@ -589,6 +593,10 @@ private:
         pendConst_ = Amp(1.0, 0.0);
         carryOk_ = true;
         emitBatch();
+        if (tlDeferH) {  // the run's initial amplitude carries the normalization
+            *tlDeferH += hcount_;
+            hcount_ = 0;
+        }
         bool any = hcount_ > 0 || pendScalar_;
         for (int s = 0; s < rb_; s++) any |= pendSlot_[s];
         uint16_t dtab = 0;  // 1 + coef index of a 2^rb pair-phase table, 0: none
@@ -1557,6 +1565,10 @@ std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::
                         if (!((used >> b) & 1)) steps[k].keep.emplace_back(b, b);
                     }
             if (!interp && ct == 13 && tuneRegBits() && steps.size() == first + 1 && steps[first].kind == Step::Pass) {
+                // the variants apply the same gates: their deferred H are not counted again
+                int variantH = 0;
+                int* const countH = tlDeferH;
+                if (countH) tlDeferH = &variantH;
                 for (int rbAlt : {4, 3}) {  // 16 and 8 amplitudes per thread (512 / 1024 threads)
                     std::vector<Step> alt;
                     compileGroup(group, used, ct, nLocal, gtab, alt, rbAlt, false, sparseIn);
@@ -1572,6 +1584,7 @@ std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::
                     compileGroup(group, used, ct, nLocal, gtab, alt, 5, true, sparseIn);
                     if (alt.size() == 1 && alt[0].kind == Step::Pass) steps[first].alts.push_back(alt[0].pass);
                 }
+                tlDeferH = countH;
                 if (steps[first].alts.size() >= size_t(Step::Tune::kMax)) steps[first].alts.resize(Step::Tune::kMax - 1);
                 if (!steps[first].alts.empty()) steps[first].tune = std::make_shared<Step::Tune>();
             }

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <memory>
 #include <utility>
@@ -88,6 +89,20 @@ inline void supportAfter(const Step& s, uint64_t tileMask, uint64_t& mask, uint6
     mask = m;
     val = v;
 }
+
+// While alive (one per compilation, this thread): passes leave the 1/sqrt2
+// of their Hadamard butterflies out (no scaling multiplies) and add their
+// count to *count; the run then starts from |basis> scaled by
+// (1/sqrt2)^count instead (linear, so the final state is the same up to
+// rounding).  Only for runs that start from a basis state.
+struct DeferHScales {
+    explicit DeferHScales(int* count);
+    ~DeferHScales();
+    DeferHScales(const DeferHScales&) = delete;
+    DeferHScales& operator=(const DeferHScales&) = delete;
+    int* prev;
+};
+inline double deferredHScale(int h) { return std::ldexp(h % 2 ? 0.70710678118654752440 : 1.0, -(h / 2)); }
 
 // Reference-formula flops per amplitude for one gate.
 double referenceFlopsPerAmp(const quokka::Gate& g);
