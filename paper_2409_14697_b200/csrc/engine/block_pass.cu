@@ -390,7 +390,8 @@ __global__ void __launch_bounds__(1 << (CT - RB), MINB)
                     const uint32_t pol = (o.k >> 1) & 1u;
                     uint32_t cm = 0, cv = 0;
                     bool thr = true;
-                    if (o.k & 1u) thr = (((tid >> o.b) & 1u) ^ pol) != 0;
+                    if (o.k & 4u) thr = ((base >> o.b) & 1u) != 0;  // CTA-bit control
+                    else if (o.k & 1u) thr = (((tid >> o.b) & 1u) ^ pol) != 0;
                     else {
                         cm = 1u << o.b;
                         cv = (1u ^ pol) << o.b;
@@ -402,12 +403,14 @@ __global__ void __launch_bounds__(1 << (CT - RB), MINB)
                     uint32_t cm = 0, cv = 0;
                     bool thr = true;
                     const uint32_t p1 = (o.k >> 1) & 1u, p2 = (o.k >> 3) & 1u;
-                    if (o.k & 1u) thr = (((tid >> o.b) & 1u) ^ p1) != 0;
+                    if (o.k & 16u) thr = ((base >> o.b) & 1u) != 0;  // CTA-bit control
+                    else if (o.k & 1u) thr = (((tid >> o.b) & 1u) ^ p1) != 0;
                     else {
                         cm |= 1u << o.b;
                         cv |= (1u ^ p1) << o.b;
                     }
-                    if (o.k & 4u) thr = thr && ((((tid >> o.c) & 1u) ^ p2) != 0);
+                    if (o.k & 32u) thr = thr && (((base >> o.c) & 1u) != 0);
+                    else if (o.k & 4u) thr = thr && ((((tid >> o.c) & 1u) ^ p2) != 0);
                     else {
                         cm |= 1u << o.c;
                         cv |= (1u ^ p2) << o.c;

@@ -1038,8 +1038,9 @@ private:
                 return;
             case qkdev::OP_CX: {
                 const int pol = (d.k >> 1) & 1;
-                if (d.k & 1) {  // thread-bit control: selects
-                    o_ << "  { const bool c = (" << tb(b) << " ^ " << pol << "u) != 0u;\n";
+                if (d.k & 5) {  // thread-bit or CTA-bit control: selects
+                    if (d.k & 4) o_ << "  { const bool c = ((base >> " << b << ") & 1ull) != 0ull;\n";
+                    else o_ << "  { const bool c = (" << tb(b) << " ^ " << pol << "u) != 0u;\n";
                     for (int s = 0; s < na_; s++)
                         if (!(s & K))
                             o_ << "    { const double2 x = " << A(s) << ", y = " << A(s | K) << "; " << A(s)
@@ -1053,11 +1054,16 @@ private:
             }
             case qkdev::OP_CCX: {  // register controls: rename; thread controls: selects
                 const int b2 = int(d.c);
-                const bool t1 = d.k & 1, t2 = (d.k >> 2) & 1;
+                const bool x1 = (d.k >> 4) & 1, x2 = (d.k >> 5) & 1;  // CTA-bit controls
+                const bool t1 = (d.k & 1) || x1, t2 = ((d.k >> 2) & 1) || x2;  // runtime conditions
                 const int p1 = (d.k >> 1) & 1, p2 = (d.k >> 3) & 1;
+                auto term = [&](bool x, int bit, int pol) {
+                    return x ? "((base >> " + std::to_string(bit) + ") & 1ull) != 0ull"
+                             : "(" + tb(bit) + " ^ " + std::to_string(pol) + "u) != 0u";
+                };
                 std::string cond;
-                if (t1) cond = "(" + tb(b) + " ^ " + std::to_string(p1) + "u) != 0u";
-                if (t2) cond += (cond.empty() ? "" : " && ") + std::string("(") + tb(b2) + " ^ " + std::to_string(p2) + "u) != 0u";
+                if (t1) cond = term(x1, b, p1);
+                if (t2) cond += (cond.empty() ? "" : " && ") + term(x2, b2, p2);
                 if (!cond.empty()) o_ << "  { const bool c = " << cond << ";\n";
                 for (int s = 0; s < na_; s++) {
                     if (s & K) continue;

@@ -55,7 +55,8 @@ bool wideAccess();
 enum OpType : uint8_t {
     OP_MAT1 = 0,      // a = slot; coef[c..c+3] = 2x2 row-major
     OP_H,             // a = slot; butterfly without 1/sqrt2 (folded into the final scale)
-    OP_CX,            // a = target slot; k bit0: control is thread bit b (else slot b); k bit1: control polarity
+    OP_CX,            // a = target slot; k bit0: control is thread bit b (else slot b); k bit1: control polarity;
+                      // k bit2: control is memory bit b outside the tile (a constant of the CTA)
     OP_DIAG1_R,       // a = slot; coef[c], coef[c+1] applied directly
     OP_DIAG2_RR,      // a = MSB slot, b = LSB slot; coef[c..c+3] applied directly
     OP_CPHASE_RR,     // a = MSB slot, b = LSB slot; coef[c] where (bit a, bit b) == pattern k
@@ -79,7 +80,8 @@ enum OpType : uint8_t {
     OP_CX_PEND,       // before a thread-controlled CX on slot a (control thread bit b, k bit1 = polarity):
                       // where it fires, P *= R[a]; R[a] = 1 / R[a]  (the pending phase follows the swap)
     OP_CCX,           // Toffoli on target slot a: control 1 = b (k bit0: thread bit, else slot; k bit1: polarity),
-                      // control 2 = c (k bit2: thread bit, else slot; k bit3: polarity)
+                      // control 2 = c (k bit2: thread bit, else slot; k bit3: polarity); k bit4 / bit5: control
+                      // 1 / 2 is memory bit b / c outside the tile (CTA constant)
 };
 
 // Diagonal gates never need their qubits inside the tile: a bit outside the

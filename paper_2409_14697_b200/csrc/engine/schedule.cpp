@@ -982,14 +982,33 @@ private:
                 return mat1(g.targets[0], m);
             }
             case GateKind::CX: {
+                // controls outside the tile are constants of the CTA (selects on its base index)
+                auto ctl = [&](int q, int& idx, int& pol, int& thr, int& cta) {
+                    if (isCtaBit(q)) {
+                        idx = q - kCta, pol = 0, thr = 0, cta = 1;
+                        return;
+                    }
+                    const int sl = inv_[q];
+                    pol = flip(sl);  // physical control value meaning logical 1: 1 ^ pol
+                    thr = isReg(sl) ? 0 : 1;
+                    idx = isReg(sl) ? sl : sl - rb_;
+                    cta = 0;
+                };
                 if (g.controls.size() == 2) {  // fused Toffoli (fuseToffolis): rename / selects, no arithmetic
-                    const int t = inv_[g.targets[0]], c1 = inv_[g.controls[0]], c2 = inv_[g.controls[1]];
+                    const int t = inv_[g.targets[0]];
+                    int i1, p1, t1, x1, i2, p2, t2, x2;
+                    ctl(g.controls[0], i1, p1, t1, x1);
+                    ctl(g.controls[1], i2, p2, t2, x2);
                     emitBatch();
                     flushSlot(t);
-                    int k = flip(c1) << 1 | flip(c2) << 3;  // physical control values meaning logical 1: 1 ^ pol
-                    if (!isReg(c1)) k |= 1;
-                    if (!isReg(c2)) k |= 4;
-                    emit(OP_CCX, t, isReg(c1) ? c1 : c1 - rb_, k, uint32_t(isReg(c2) ? c2 : c2 - rb_));
+                    emit(OP_CCX, t, i1, t1 | p1 << 1 | t2 << 2 | p2 << 3 | x1 << 4 | x2 << 5, uint32_t(i2));
+                    return;
+                }
+                if (isCtaBit(g.controls[0])) {
+                    const int t = inv_[g.targets[0]];
+                    emitBatch();
+                    flushSlot(t);
+                    emit(OP_CX, t, g.controls[0] - kCta, 4);
                     return;
                 }
                 const int t = inv_[g.targets[0]], c = inv_[g.controls[0]];
@@ -1231,6 +1250,21 @@ bool sparseDp() {
 double dpFlopWeight() {
     static const double v = envInt("QK_DP_FLOP", 25, 0, 100000) * 1e-5;
     return v;
+}
+
+// QK_CTA_CONTROLS (default 1): CX / CCX controls may lie outside the tile
+// (constants of the CTA, applied as selects on its base index), so a gate of
+// the X family needs only its target in the tile: Grover's AND chain and
+// BV's oracle fit many more gates per pass.
+bool ctaControls() {
+    static const bool v = envInt("QK_CTA_CONTROLS", 1, 0, 1) != 0;
+    return v;
+}
+// Memory bits a gate needs inside a pass's tile.
+uint64_t tileMaskOf(const Gate& g) {
+    if (isDiagonalGate(g)) return 0;
+    if (g.kind == GateKind::CX && ctaControls()) return uint64_t(1) << g.targets[0];
+    return g.depMask();
 }
 
 // QK_FUSE_CCX (default 1): a run of 1-qubit gates and CX on three qubits
@@ -1501,7 +1535,7 @@ std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::
         if (!m) return;
         const bool synthRun = synthFirst && steps.empty();
         std::vector<uint64_t> mask(m);
-        for (size_t k = 0; k < m; k++) mask[k] = isDiagonalGate(run[k]) ? 0 : run[k].depMask();
+        for (size_t k = 0; k < m; k++) mask[k] = tileMaskOf(run[k]);
         std::vector<double> work(m);  // reference-formula flops/amp: bounds a pass's straight-line code
         for (size_t k = 0; k < m; k++) work[k] = referenceFlopsPerAmp(run[k]);
         // support-aware model: free[k] = bits the support spans before gate k
@@ -1552,7 +1586,7 @@ std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::
             uint64_t used = 0;
             for (size_t k = cuts[c]; k < cuts[c + 1]; k++) {
                 group.push_back(relabelGate(run[k]));
-                if (mask[k]) used |= group.back().depMask();
+                used |= tileMaskOf(group.back());
             }
             const size_t first = steps.size();
             // a run from a basis state: the support grows by each pass's tile

@@ -132,7 +132,9 @@ def _run_pass(state, n, P, gt):
                 pol = (ok >> 1) & 1
                 lo = s_idx[(s_idx >> oa) & 1 == 0]
                 hi = lo | (1 << oa)
-                if ok & 1:
+                if ok & 4:  # control outside the tile: a bit of the CTA's base index
+                    cond = np.full((nt, len(lo)), bool((base >> ob) & 1))
+                elif ok & 1:
                     cond = ((bit(tid, ob) ^ pol) == 1)[:, None] & np.ones(len(lo), bool)[None, :]
                 else:
                     cond = np.broadcast_to(((bit(lo, ob) ^ pol) == 1)[None, :], (nt, len(lo)))
@@ -143,8 +145,11 @@ def _run_pass(state, n, P, gt):
                 lo = s_idx[(s_idx >> oa) & 1 == 0]
                 hi = lo | (1 << oa)
                 cond = np.ones((nt, len(lo)), bool)
-                for (thr, idx, pol) in (((ok & 1), ob, (ok >> 1) & 1), ((ok >> 2) & 1, oc, (ok >> 3) & 1)):
-                    if thr:
+                for (thr, idx, pol, cta) in (((ok & 1), ob, (ok >> 1) & 1, (ok >> 4) & 1),
+                                             ((ok >> 2) & 1, oc, (ok >> 3) & 1, (ok >> 5) & 1)):
+                    if cta:
+                        cond &= bool((base >> idx) & 1)
+                    elif thr:
                         cond &= ((bit(tid, idx) ^ pol) == 1)[:, None]
                     else:
                         cond &= ((bit(lo, idx) ^ pol) == 1)[None, :]

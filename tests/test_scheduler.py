@@ -282,3 +282,19 @@ def test_toffoli_fusion_grover(qk, port):
     got = run_compiled(qk, port, prog, n, 6)
     want = port.run_program(prog.text(), n, 10, 6).view(np.complex128)
     assert np.max(np.abs(got - want)) < 1e-10
+
+
+@pytest.mark.parametrize("kind,n,seed", [("toffoli", 16, 11), ("toffoli", 17, 12), ("bvones", 17, 0), ("random", 16, 13)])
+def test_cta_bit_controls(qk, port, ref, kind, n, seed):
+    # CX / CCX controls outside the pass's tile (QK_CTA_CONTROLS): selects on
+    # the CTA's base index; only the target must be in the tile
+    cfg_text = config_text(n, 0, 6, fusion=0, diag=0)
+    circ = toffoli_circuit(n, 16, seed) if kind == "toffoli" else ref.gen(kind, n, 200 if kind == "random" else 0, seed)
+    prog_text = ref.optimize(circ, cfg_text)
+    want, _, _, _ = ref.simulate(prog_text, cfg_text, n, 0, 9, 1)
+    prog = qk.Program.parse(prog_text, qk.Config.parse(cfg_text))
+    ops = [o for it in prog.debug_compile(n)["items"] if it["kind"] == 0
+           for s in it["block"]["steps"] if s["kind"] == 0 for o in s["ops"]]
+    assert sum(1 for o in ops if (o[0] == 2 and o[3] & 4) or (o[0] == 24 and o[3] & 48)) >= (2 if kind == "toffoli" else 0)
+    got = run_compiled(qk, port, prog, n, 9)
+    assert np.max(np.abs(got - want.view(np.complex128))) < 1e-10
