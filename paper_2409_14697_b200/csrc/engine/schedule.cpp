@@ -1231,10 +1231,13 @@ int lowTileBits() {
 // support (sparse loads, deferred zeros), so it costs its support fraction of
 // a sweep; the pass that first fills the slice writes it all and reads only
 // its input support.  Work (reference flops/amp) is priced at QK_DP_FLOP
-// sweeps per 10^4 flops (default 2.5) on the amplitudes it touches, so the DP
-// moves gates into the cheap sparse passes and leaves the full-output pass as
-// little arithmetic as the tile allows (QFT-33: 13 + 11 + 9 -> 13 + 13 + 7
-// H levels).  0 restores the support-blind model.
+// sweeps per 10^5 flops (default 250: a 14-flop butterfly level ~ 0.035 of a
+// sweep, as the filling passes measure) on the amplitudes it touches, so the
+// DP moves gates into the cheap sparse passes and leaves the full-output pass
+// as little arithmetic as the tile allows (QFT-33: 13 + 11 + 9 -> 2 + 13 + 13
+// + 5 H levels, the last pass without an exchange; sweep 25 / 60 / 120 / 250
+// in profiles/r2_families_ab.txt).  QK_SPARSE_DP=0 restores the
+// support-blind model.
 // QK_TIGHT_SUPPORT (default 1): a pass frees only the tile bits its
 // non-diagonal gates touch; padding bits of a run from a basis state stay
 // known (Step::keep), so later passes read and write less.
@@ -1248,7 +1251,7 @@ bool sparseDp() {
     return v;
 }
 double dpFlopWeight() {
-    static const double v = envInt("QK_DP_FLOP", 25, 0, 100000) * 1e-5;
+    static const double v = envInt("QK_DP_FLOP", 250, 0, 100000) * 1e-5;
     return v;
 }
 
