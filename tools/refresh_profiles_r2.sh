@@ -18,8 +18,8 @@ cp $O/launches.csv profiles/r2_bench_qft33_launches.csv
   python tools/launch_tail.py $O/launches.csv 6 2>/dev/null || true
 } > profiles/r2_bench_qft33_launches.txt
 {
-  echo "# ncu --set full --clock-control none of QFT-31 (tools/run_qft.py 31): the two passes after the basis tile, commit '$C'"
-  echo "# support-aware DP (13 + 13 + 7 H levels), tight support, deferred H scales; pass 3 reads the 2^24-amp support, writes every tile (staged TMA stores)"
+  echo "# ncu --set full --clock-control none of QFT-31 (tools/run_qft.py 31): the passes after the basis tile, commit '$C'"
+  echo "# support-aware DP (work weight 250), tight support, Toffoli fusion, CTA-bit controls, deferred H scales; the last (filling) pass reads the support and writes every tile (staged TMA stores)"
   python tools/ncu_summary.py $O/prof_qft31.ncu-rep --sass
 } > profiles/r2_qft31_sparse_dp_ncu_full.txt
 {
