@@ -1250,6 +1250,10 @@ bool sparseDp() {
     static const bool v = envInt("QK_SPARSE_DP", 1, 0, 1) != 0;
     return v;
 }
+double sparsePen0() {
+    static const double v = envInt("QK_SPARSE_PEN0", 8, 0, 1000);
+    return v;
+}
 double dpFlopWeight() {
     static const double v = envInt("QK_DP_FLOP", 250, 0, 100000) * 1e-5;
     return v;
@@ -1557,7 +1561,11 @@ std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::
             const double fin = std::ldexp(1.0, __builtin_popcountll(freeAt[j]) - nLocal);
             const double fout = std::ldexp(1.0, __builtin_popcountll(freeAt[j] | tile) - nLocal);
             const double comp = dpFlopWeight() * w;
-            if (fout < 1.0) return fout * (1.0 + pen + comp);  // deferred zeros: support in, support out
+            // deferred zeros: support in, support out.  A partial pass whose tile
+            // has no memory bit 0 writes 16-B fragments (a TMA box one amplitude
+            // wide): QFT-30's middle pass took ~3x its 32-B-row time, so L = 0
+            // costs QK_SPARSE_PEN0 (default 8) there
+            if (fout < 1.0) return fout * (1.0 + (L == 0 ? std::max(pen, sparsePen0()) : pen) + comp);
             return 0.5 * (1.0 + pen) * (1.0 + fin) + comp;      // every tile written, support read
         };
         std::vector<double> best(m + 1, 1e300);
