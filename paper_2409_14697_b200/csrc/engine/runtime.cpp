@@ -430,9 +430,37 @@ ScheduleCache& scheduleCache() {
 // block and every IMS / XRS item reads and writes the slice once; a block
 // step runs at ~1.5x the time of an IMS (B200: ~73 vs ~44 ms at 2^33), so
 // steps weigh 3 and permutations 2.
-size_t sweeps(const Compiled& c) {
+uint64_t swapBitsOf(uint64_t x, const std::vector<int>& outs, const std::vector<int>& ins) {
+    for (size_t j = 0; j < outs.size(); j++) {
+        const uint64_t d = ((x >> outs[j]) ^ (x >> ins[j])) & 1u;
+        x ^= (d << outs[j]) | (d << ins[j]);
+    }
+    return x;
+}
+
+// In a run from a basis state a pass whose input still has known zeros reads
+// almost nothing and its output stays partial or is the one filling write:
+// it weighs 1 (support tracked as the runtime does, schedule.h supportAfter).
+size_t sweeps(const Compiled& c, bool fromBasis = false) {
     size_t n = 0;
-    for (const CompiledItem& it : c.items) n += it.kind == CompiledItem::Block ? 3 * it.steps.size() : 2;
+    uint64_t mask = fromBasis ? (c.nLocal >= 64 ? ~uint64_t(0) : (uint64_t(1) << c.nLocal) - 1) : 0, val = 0;
+    for (const CompiledItem& it : c.items) {
+        if (it.kind != CompiledItem::Block) {
+            n += 2;
+            if (it.kind == CompiledItem::Xrs) mask = 0;
+            else mask = swapBitsOf(mask, it.outs, it.ins);
+            continue;
+        }
+        for (const qkeng::Step& s : it.steps) {
+            if (s.kind != qkeng::Step::Pass) {
+                n += 3;
+                for (size_t j = 1; j < s.targets.size(); j++) mask &= ~(uint64_t(1) << s.targets[j]);
+                continue;
+            }
+            n += mask ? 1 : 3;
+            qkeng::supportAfter(s, s.pass->tile_mask, mask, val);
+        }
+    }
     return n;
 }
 
@@ -702,7 +730,7 @@ std::shared_ptr<Compiled> compileFor(qk_program* p, int nLocal, bool fromBasis =
         for (int q = 0; q < nLocal; q++) mem0[size_t(sim[size_t(q)])] = q;
         if (mem0 != ident) {
             std::shared_ptr<Compiled> b = compileLayout(p, nLocal, mem0, fromBasis, interp);
-            if (sweeps(*b) <= sweeps(*c)) c = b;
+            if (sweeps(*b, fromBasis) <= sweeps(*c, fromBasis)) c = b;
         }
     }
     p->compiled[slot] = c;
