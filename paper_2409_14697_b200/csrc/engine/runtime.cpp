@@ -1013,6 +1013,7 @@ void runBlock(qk_state* st, const CompiledItem& ci, const DeviceTables& t, qk_ru
             if (fusedNorm) {
                 cuda(qkdev::launchSumTiles(st->normTiles, normParts, st->normScratch, st->normOut, st->stream),
                      "norm fold");
+                rs.kernel_launches += 2;  // k_sum_partial + k_norm_final
                 st->normValid = true;
             }
             basis = kNoBasis;
