@@ -1503,7 +1503,6 @@ std::vector<Step> compileBlock(const std::vector<Gate>& gates, int nLocal, std::
     std::vector<Gate> fusedGates;
     if (fuseCcx() && nLocal >= 4) {
         fusedGates = fuseToffolis(gates);
-        if (std::getenv("QK_DEBUG_CCX")) std::fprintf(stderr, "ccx fusion: %zu -> %zu gates\n", gates.size(), fusedGates.size());
         if (fusedGates.size() != gates.size())
             return compileBlock(fusedGates, nLocal, gtab, dest, relabel, tileBits, synthFirst, interp);
     }
