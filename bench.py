@@ -284,9 +284,20 @@ def main():
     # Schedule autotune (register widths per pass, tile size per gate stream)
     # settles over the first few runs of a program; finish it before the
     # warm-up so the timed steps run the tuned schedule.
+    # Every rank must call simulate equally often (each CSQS is a collective):
+    # a rank keeps going while ANY rank is still tuning (the rank holding
+    # |initial> times passes the others skip).
+    def any_tuning(x):
+        if world == 1:
+            return bool(x)
+        f = torch.tensor([float(x)], dtype=torch.float64, device=tdev)
+        dist.all_reduce(f, op=dist.ReduceOp.MAX)
+        return bool(f.item())
+
     tune_runs = 1
+    tuning = any_tuning(tuning)
     while tune_runs < 24 and tuning:
-        tuning = st.simulate(prog, 0)["tuning_runs"]
+        tuning = any_tuning(st.simulate(prog, 0)["tuning_runs"])
         tune_runs += 1
     for _ in range(args.warmup):
         st.simulate(prog, 0)
